@@ -1,0 +1,380 @@
+"""CPU ORACLE loader — TEST INFRASTRUCTURE ONLY.
+
+ctypes bindings for
+  * ``liboracle.so``         — the plain-C fp64 restatement (cmax_oracle.c), and
+  * ``_ref/libevcm_ref.so``  — the UNMODIFIED reference compiled from
+                               /root/reference by ``make ref`` (ref_capi.cpp).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s reference /
+cpu_baseline legs import this module. The product package never does.
+
+Array conventions match oracle/cmax_oracle.h: flows [B,2,H,W] f64,
+stack [B+1,2,H,W] f64, grads [B,2,H,W] f64, poses [B,6] f64, K [4] f64.
+Events are numpy structured arrays with the 16-byte evcm::Event layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libevcm_ref.so")
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+
+# evcm::Event (types.hpp:106-113), 16 bytes.
+EVENT_DTYPE = np.dtype(
+    {"names": ["t_us", "x", "y", "p"], "formats": ["<u8", "<u2", "<u2", "i1"],
+     "offsets": [0, 8, 10, 12], "itemsize": 16})
+
+ERR_NAMES = {1: "ConfigError", 2: "DimensionMismatchError", 3: "CoordinateRangeError",
+             4: "InvalidPolarityError", 5: "UnsortedEventsError", 6: "TimeRangeError",
+             7: "EmptySliceError", 99: "Error"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        self.code = code
+        self.kind = ERR_NAMES.get(code, "Error")
+        super().__init__(f"{self.kind}: {msg}")
+
+
+def build(ref: bool = True) -> None:
+    """Compile liboracle.so (always) and _ref/libevcm_ref.so (when the reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
+    if ref and os.path.isdir("/root/reference/proj/include"):
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build(ref=False)
+        L = C.CDLL(ORACLE_SO)
+        vp, i32, sz, u64 = C.c_void_p, C.c_int, C.c_size_t, C.c_uint64
+        L.orc_forward.argtypes = [i32, i32, i32, vp, vp, sz, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_backward.argtypes = [i32, i32, i32, vp, vp, sz, vp, vp, vp, vp, vp, vp, i32, vp]
+        L.orc_depth_pose_to_flows.argtypes = [i32, i32, vp, vp, i32, vp, vp, u64, u64, vp, vp]
+        L.orc_depth_pose_to_flows_backward.argtypes = [i32, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.orc_make_edges.argtypes = [u64, u64, i32, vp]
+        L.orc_make_edges.restype = None
+        L.orc_rodrigues.argtypes = [vp, vp]
+        L.orc_rodrigues.restype = None
+        L.orc_rodrigues_jacobian.argtypes = [vp, vp]
+        L.orc_rodrigues_jacobian.restype = None
+        L.orc_validate_window.argtypes = [i32, i32, i32, vp, u64, u64, vp, sz, vp]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            build(ref=True)
+        L = C.CDLL(REF_SO)
+        vp, i32, sz, u64, f64 = C.c_void_p, C.c_int, C.c_size_t, C.c_uint64, C.c_double
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_hardware_concurrency.restype = C.c_uint
+        L.ref_loss_and_grad.argtypes = [i32, i32, i32, vp, vp, sz, vp, i32, i32, i32, i32,
+                                        vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_warp_event.argtypes = [i32, i32, i32, vp, vp, f64, f64, f64, f64, vp]
+        L.ref_rsat.argtypes = [i32, i32, i32, vp, vp, sz, vp, vp]
+        L.ref_depth_pose_to_flows.argtypes = [i32, i32, vp, vp, i32, vp, vp, u64, u64, vp, vp, vp]
+        L.ref_depth_pose_to_flows_backward.argtypes = [i32, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.ref_random_fd_instance.argtypes = [u64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_bench_window.argtypes = [i32, i32, i32, f64, u64, sz, vp, vp, vp]
+        L.ref_generate_scene.argtypes = [i32, i32, i32, vp, vp, f64, u64, vp, vp, vp, vp]
+        L.ref_chain_instance.argtypes = [u64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.ref_chain_batch.argtypes = [i32, i32, i32, i32, vp, vp, vp, u64, u64, vp, vp, i32,
+                                      vp, vp, vp, vp]
+        _ref = L
+    return _ref
+
+
+def _check(rc, L, which="oracle"):
+    if rc != 0:
+        msg = L.ref_last_error().decode() if which == "ref" else ""
+        raise OracleError(rc, msg)
+
+
+# ---------------------------------------------------------------------------
+# Window containers
+
+
+class Window:
+    """One event window + flows: the (EventSlice, FlowSequence) pair."""
+
+    def __init__(self, W, H, edges, events, flows):
+        self.W, self.H = int(W), int(H)
+        self.edges = np.ascontiguousarray(edges, dtype=np.uint64)
+        self.B = len(self.edges) - 1
+        self.events = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+        self.flows = np.ascontiguousarray(flows, dtype=np.float64).reshape(self.B, 2, self.H, self.W)
+
+    @property
+    def n(self):
+        return len(self.events)
+
+
+def make_edges(t0, t1, B):
+    e = np.zeros(B + 1, np.uint64)
+    lib().orc_make_edges(t0, t1, B, _p(e))
+    return e
+
+
+def make_events(t, x, y, p):
+    ev = np.zeros(len(t), EVENT_DTYPE)
+    ev["t_us"], ev["x"], ev["y"], ev["p"] = t, x, y, p
+    return ev
+
+
+# ---------------------------------------------------------------------------
+# C restatement
+
+
+def forward(w: Window, want_pos=False):
+    R = w.B + 1
+    HW = w.W * w.H
+    out = dict(count=np.zeros((R, 2, w.H, w.W)), tsum=np.zeros((R, 2, w.H, w.W)),
+               n_active=np.zeros(R, np.int64), alive=np.zeros(w.n, np.uint8),
+               bin=np.zeros(w.n, np.int32))
+    pos = np.zeros((w.n, R, 2)) if want_pos else None
+    loss = C.c_double()
+    ns = C.c_int()
+    rc = lib().orc_forward(w.W, w.H, w.B, _p(w.edges), _p(w.events), w.n, _p(w.flows),
+                           _p(out["count"]), _p(out["tsum"]), _p(out["n_active"]),
+                           _p(out["alive"]), _p(out["bin"]), _p(pos), C.byref(loss), C.byref(ns))
+    _check(rc, lib())
+    out["loss"] = loss.value
+    out["no_survivors"] = bool(ns.value)
+    out["n_alive"] = int(out["alive"].sum())
+    if want_pos:
+        out["pos"] = pos
+    del HW
+    return out
+
+
+def backward(w: Window, fwd=None):
+    if fwd is None:
+        fwd = forward(w)
+    g = np.zeros((w.B, 2, w.H, w.W))
+    rc = lib().orc_backward(w.W, w.H, w.B, _p(w.edges), _p(w.events), w.n, _p(w.flows),
+                            _p(fwd["count"]), _p(fwd["tsum"]), _p(fwd["n_active"]),
+                            _p(fwd["alive"]), _p(fwd["bin"]), int(fwd["no_survivors"]), _p(g))
+    _check(rc, lib())
+    return g
+
+
+def depth_pose_to_flows(depth, poses, K, t0, t1, mask=None):
+    depth = np.ascontiguousarray(depth, np.float64)
+    H, W = depth.shape
+    poses = np.ascontiguousarray(poses, np.float64).reshape(-1, 6)
+    B = poses.shape[0]
+    K = np.ascontiguousarray(K, np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    flows = np.zeros((B, 2, H, W))
+    valid = np.zeros((B, H, W), np.uint8)
+    rc = lib().orc_depth_pose_to_flows(W, H, _p(depth), _p(m), B, _p(poses), _p(K), t0, t1,
+                                       _p(flows), _p(valid))
+    _check(rc, lib())
+    return flows, valid
+
+
+def depth_pose_to_flows_backward(depth, poses, K, edges, grad, mask=None):
+    depth = np.ascontiguousarray(depth, np.float64)
+    H, W = depth.shape
+    poses = np.ascontiguousarray(poses, np.float64).reshape(-1, 6)
+    B = poses.shape[0]
+    K = np.ascontiguousarray(K, np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    edges = np.ascontiguousarray(edges, np.uint64)
+    grad = np.ascontiguousarray(grad, np.float64)
+    dd = np.zeros((H, W))
+    dp = np.zeros((B, 6))
+    rc = lib().orc_depth_pose_to_flows_backward(W, H, _p(depth), _p(m), B, _p(poses), _p(K),
+                                                _p(edges), _p(grad), _p(dd), _p(dp))
+    _check(rc, lib())
+    return dd, dp
+
+
+def rodrigues(omega):
+    o = np.ascontiguousarray(omega, np.float64)
+    R = np.zeros(9)
+    lib().orc_rodrigues(_p(o), _p(R))
+    return R.reshape(3, 3)
+
+
+def rodrigues_jacobian(omega):
+    o = np.ascontiguousarray(omega, np.float64)
+    dR = np.zeros(27)
+    lib().orc_rodrigues_jacobian(_p(o), _p(dR))
+    return dR.reshape(3, 3, 3)
+
+
+# ---------------------------------------------------------------------------
+# The reference itself (oracle/_ref)
+
+
+def ref_loss_and_grad(w: Window, backend="parallel", n_workers=0, deterministic=True,
+                      backward=True, want_pos=False):
+    L = ref()
+    R = w.B + 1
+    be = {"naive": 0, "padded": 1, "parallel": 2}[backend]
+    out = dict(count=np.zeros((R, 2, w.H, w.W)), tsum=np.zeros((R, 2, w.H, w.W)),
+               n_active=np.zeros(R, np.int64), alive=np.zeros(w.n, np.uint8),
+               bin=np.zeros(w.n, np.int32))
+    pos = np.zeros((w.n, R, 2)) if want_pos else None
+    g = np.zeros((w.B, 2, w.H, w.W)) if backward else None
+    loss = C.c_double()
+    ns = C.c_int()
+    rc = L.ref_loss_and_grad(w.W, w.H, w.B, _p(w.edges), _p(w.events), w.n, _p(w.flows), be,
+                             n_workers, int(deterministic), int(backward), _p(out["count"]),
+                             _p(out["tsum"]), _p(out["n_active"]), _p(out["alive"]),
+                             _p(out["bin"]), _p(pos), C.byref(loss), C.byref(ns), _p(g))
+    _check(rc, L, "ref")
+    out["loss"] = loss.value
+    out["no_survivors"] = bool(ns.value)
+    out["n_alive"] = int(out["alive"].sum())
+    if want_pos:
+        out["pos"] = pos
+    if backward:
+        out["grad"] = g
+    return out
+
+
+def ref_warp_event(w: Window, x, y, t_from, t_to):
+    o = np.zeros(2)
+    _check(ref().ref_warp_event(w.W, w.H, w.B, _p(w.edges), _p(w.flows), x, y, t_from, t_to,
+                                _p(o)), ref(), "ref")
+    return o
+
+
+def ref_rsat(w: Window):
+    o = C.c_double()
+    _check(ref().ref_rsat(w.W, w.H, w.B, _p(w.edges), _p(w.events), w.n, _p(w.flows),
+                          C.byref(o)), ref(), "ref")
+    return o.value
+
+
+def ref_depth_pose_to_flows(depth, poses, K, t0, t1, mask=None):
+    depth = np.ascontiguousarray(depth, np.float64)
+    H, W = depth.shape
+    poses = np.ascontiguousarray(poses, np.float64).reshape(-1, 6)
+    B = poses.shape[0]
+    K = np.ascontiguousarray(K, np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    flows = np.zeros((B, 2, H, W))
+    valid = np.zeros((B, H, W), np.uint8)
+    edges = np.zeros(B + 1, np.uint64)
+    _check(ref().ref_depth_pose_to_flows(W, H, _p(depth), _p(m), B, _p(poses), _p(K), t0, t1,
+                                         _p(flows), _p(valid), _p(edges)), ref(), "ref")
+    return flows, valid, edges
+
+
+def ref_depth_pose_to_flows_backward(depth, poses, K, edges, grad, mask=None):
+    depth = np.ascontiguousarray(depth, np.float64)
+    H, W = depth.shape
+    poses = np.ascontiguousarray(poses, np.float64).reshape(-1, 6)
+    B = poses.shape[0]
+    K = np.ascontiguousarray(K, np.float64)
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    edges = np.ascontiguousarray(edges, np.uint64)
+    grad = np.ascontiguousarray(grad, np.float64)
+    dd = np.zeros((H, W))
+    dp = np.zeros((B, 6))
+    _check(ref().ref_depth_pose_to_flows_backward(W, H, _p(depth), _p(m), B, _p(poses), _p(K),
+                                                  _p(edges), _p(grad), _p(dd), _p(dp)),
+           ref(), "ref")
+    return dd, dp
+
+
+def ref_fd_instance(seed, max_events=0, max_dim=0, want_masked=False) -> Window:
+    L = ref()
+    W, H, B = C.c_int(), C.c_int(), C.c_int()
+    n, nm = C.c_size_t(), C.c_size_t()
+    _check(L.ref_random_fd_instance(seed, max_events, max_dim, int(want_masked), C.byref(W),
+                                    C.byref(H), C.byref(B), C.byref(n), None, None, None,
+                                    C.byref(nm)), L, "ref")
+    edges = np.zeros(B.value + 1, np.uint64)
+    ev = np.zeros(n.value, EVENT_DTYPE)
+    flows = np.zeros((B.value, 2, H.value, W.value))
+    _check(L.ref_random_fd_instance(seed, max_events, max_dim, int(want_masked), C.byref(W),
+                                    C.byref(H), C.byref(B), C.byref(n), _p(edges), _p(ev),
+                                    _p(flows), C.byref(nm)), L, "ref")
+    w = Window(W.value, H.value, edges, ev, flows)
+    w.n_masked = nm.value
+    return w
+
+
+def ref_bench_window(W, H, B, n_events, seed=1, window_s=0.1) -> Window:
+    edges = np.zeros(B + 1, np.uint64)
+    ev = np.zeros(n_events, EVENT_DTYPE)
+    flows = np.zeros((B, 2, H, W))
+    _check(ref().ref_bench_window(W, H, B, window_s, seed, n_events, _p(edges), _p(ev),
+                                  _p(flows)), ref(), "ref")
+    return Window(W, H, edges, ev, flows)
+
+
+def ref_generate_scene(W, H, poses, K, event_rate, seed):
+    L = ref()
+    poses = np.ascontiguousarray(poses, np.float64).reshape(-1, 6)
+    B = poses.shape[0]
+    K = np.ascontiguousarray(K, np.float64)
+    n = C.c_size_t()
+    _check(L.ref_generate_scene(W, H, B, _p(poses), _p(K), event_rate, seed, C.byref(n), None,
+                                None, None), L, "ref")
+    ev = np.zeros(n.value, EVENT_DTYPE)
+    depth = np.zeros((H, W))
+    mask = np.zeros((H, W), np.uint8)
+    _check(L.ref_generate_scene(W, H, B, _p(poses), _p(K), event_rate, seed, C.byref(n),
+                                _p(ev), _p(depth), _p(mask)), L, "ref")
+    return ev, depth, mask
+
+
+def ref_chain_instance(seed, sensor_w=16, sensor_h=12, factor=4, n_bins=2, n_events=24):
+    L = ref()
+    n = C.c_size_t()
+    _check(L.ref_chain_instance(seed, sensor_w, sensor_h, factor, n_bins, n_events, C.byref(n),
+                                None, None, None, None), L, "ref")
+    ev = np.zeros(n.value, EVENT_DTYPE)
+    depth = np.zeros((sensor_h, sensor_w))
+    poses = np.zeros((n_bins, 6))
+    K = np.zeros(4)
+    _check(L.ref_chain_instance(seed, sensor_w, sensor_h, factor, n_bins, n_events, C.byref(n),
+                                _p(ev), _p(depth), _p(poses), _p(K)), L, "ref")
+    return ev, depth, poses, K
+
+
+def ref_chain_batch(depth, poses, K, t0, t1, events, ev_off, n_workers=0, want_grads=False):
+    """Reference chain (flows → loss_and_grad → flows backward), window by window."""
+    L = ref()
+    depth = np.ascontiguousarray(depth, np.float64)
+    nw, H, W = depth.shape
+    poses = np.ascontiguousarray(poses, np.float64)
+    B = poses.shape[1]
+    K = np.ascontiguousarray(K, np.float64)
+    events = np.ascontiguousarray(events, EVENT_DTYPE)
+    ev_off = np.ascontiguousarray(ev_off, np.uint64)
+    dd = np.zeros((nw, H, W)) if want_grads else None
+    dp = np.zeros((nw, B, 6)) if want_grads else None
+    ls, sec = C.c_double(), C.c_double()
+    _check(L.ref_chain_batch(W, H, B, nw, _p(depth), _p(poses), _p(K), t0, t1, _p(events),
+                             _p(ev_off), n_workers, C.byref(ls), _p(dd), _p(dp), C.byref(sec)),
+           L, "ref")
+    return dict(loss_sum=ls.value, seconds=sec.value, d_depth=dd, d_poses=dp)

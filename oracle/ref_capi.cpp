@@ -1,0 +1,376 @@
+// TEST INFRASTRUCTURE ONLY — builds the UNMODIFIED reference (evcm, header-only
+// C++20, /root/reference/proj/include) into oracle/_ref/libevcm_ref.so behind a
+// small C-ABI so the Python tests and bench.py's reference arm can drive it.
+// Nothing here re-implements the algorithm: every entry point calls the
+// reference's own functions (engine.hpp, geometry.hpp, fdcheck.hpp, bench.hpp,
+// synth.hpp, tests/chain_support.hpp). Built with -fvisibility=hidden so only
+// the ref_* symbols leave the library (no ODR clash with anything else).
+//
+// Layouts are the ones documented in oracle/cmax_oracle.h.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "evcm/bench.hpp"
+#include "evcm/engine.hpp"
+#include "evcm/fdcheck.hpp"
+#include "evcm/geometry.hpp"
+#include "evcm/synth.hpp"
+#include "chain_support.hpp"
+
+#define REF_API extern "C" __attribute__((visibility("default")))
+
+using namespace evcm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int code_of(const std::exception& ex) {
+  // Order: most-derived first. Codes match oracle/cmax_oracle.h ORC_*.
+  if (dynamic_cast<const ConfigError*>(&ex)) return 1;
+  if (dynamic_cast<const DimensionMismatchError*>(&ex)) return 2;
+  if (dynamic_cast<const CoordinateRangeError*>(&ex)) return 3;
+  if (dynamic_cast<const InvalidPolarityError*>(&ex)) return 4;
+  if (dynamic_cast<const UnsortedEventsError*>(&ex)) return 5;
+  if (dynamic_cast<const TimeRangeError*>(&ex)) return 6;
+  if (dynamic_cast<const EmptySliceError*>(&ex)) return 7;
+  return 99;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return code_of(ex);
+  }
+}
+
+struct RefEvent {  // byte-identical to evcm::Event
+  std::uint64_t t_us;
+  std::uint16_t x, y;
+  std::int8_t p;
+  std::uint8_t pad[3];
+};
+static_assert(sizeof(RefEvent) == sizeof(Event), "event layout");
+
+EventSlice make_slice(int W, int H, std::uint64_t t0, std::uint64_t t1, const void* ev,
+                      std::size_t n) {
+  EventSlice s;
+  s.width = static_cast<std::uint16_t>(W);
+  s.height = static_cast<std::uint16_t>(H);
+  s.t_start_us = t0;
+  s.t_end_us = t1;
+  s.events.resize(n);
+  if (n) std::memcpy(s.events.data(), ev, n * sizeof(Event));
+  return s;
+}
+
+FlowSequence make_flows(int W, int H, int B, const std::uint64_t* edges, const double* flows) {
+  FlowSequence f;
+  f.edges_us.assign(edges, edges + B + 1);
+  const std::size_t HW = static_cast<std::size_t>(W) * H;
+  for (int b = 0; b < B; ++b) {
+    const double d = (static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6;
+    FlowField ff(W, H, d);
+    for (std::size_t i = 0; i < HW; ++i) {
+      ff.u[i] = flows[(static_cast<std::size_t>(b) * 2) * HW + i];
+      ff.v[i] = flows[(static_cast<std::size_t>(b) * 2 + 1) * HW + i];
+    }
+    f.fields.push_back(std::move(ff));
+  }
+  return f;
+}
+
+void dump_flows(const FlowSequence& f, double* out) {
+  const std::size_t HW = f.fields.empty() ? 0 : f.fields[0].u.size();
+  for (int b = 0; b < f.n_bins(); ++b)
+    for (std::size_t i = 0; i < HW; ++i) {
+      out[(static_cast<std::size_t>(b) * 2) * HW + i] = f.fields[static_cast<std::size_t>(b)].u[i];
+      out[(static_cast<std::size_t>(b) * 2 + 1) * HW + i] = f.fields[static_cast<std::size_t>(b)].v[i];
+    }
+}
+
+EngineOptions make_opts(int backend, int n_workers, int deterministic) {
+  EngineOptions o;
+  o.backend = backend == 0 ? Backend::naive : backend == 1 ? Backend::padded : Backend::parallel;
+  o.n_workers = n_workers;
+  o.deterministic = deterministic != 0;
+  if (backend == 1) o.batch_size = 16;
+  return o;
+}
+
+std::vector<PoseStep> make_poses(int B, const double* p) {
+  std::vector<PoseStep> v(static_cast<std::size_t>(B));
+  for (int i = 0; i < B; ++i)
+    v[static_cast<std::size_t>(i)] = PoseStep{{p[6 * i], p[6 * i + 1], p[6 * i + 2]},
+                                              {p[6 * i + 3], p[6 * i + 4], p[6 * i + 5]}};
+  return v;
+}
+
+DepthMap make_depth(int W, int H, const double* d, const std::uint8_t* mask) {
+  Image<double> img(W, H, 0.0);
+  for (std::size_t i = 0; i < img.size(); ++i) img[i] = d[i];
+  if (!mask) return DepthMap(std::move(img));
+  Image<std::uint8_t> m(W, H, 0);
+  for (std::size_t i = 0; i < m.size(); ++i) m[i] = mask[i];
+  return DepthMap(std::move(img), std::move(m));
+}
+
+}  // namespace
+
+REF_API const char* ref_last_error() { return g_err.c_str(); }
+
+REF_API unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// Engine::forward + optional Engine::backward through the reference's own
+// backends. Any output pointer may be NULL.
+REF_API int ref_loss_and_grad(int W, int H, int B, const std::uint64_t* edges, const void* ev,
+                              std::size_t n, const double* flows, int backend, int n_workers,
+                              int deterministic, int do_backward, double* count, double* tsum,
+                              std::int64_t* n_active, std::uint8_t* alive, std::int32_t* bin,
+                              double* pos, double* loss, int* no_survivors, double* grad) {
+  return guarded([&] {
+    const EventSlice s = make_slice(W, H, edges[0], edges[B], ev, n);
+    const FlowSequence f = make_flows(W, H, B, edges, flows);
+    const Engine eng(make_opts(backend, n_workers, deterministic));
+    const ForwardResult fw = eng.forward(s, f);
+    const std::size_t HW = static_cast<std::size_t>(W) * H;
+    const int R = B + 1;
+    for (int r = 0; r < R; ++r)
+      for (int c = 0; c < 2; ++c) {
+        const std::size_t o = (static_cast<std::size_t>(r) * 2 + c) * HW;
+        if (count)
+          std::memcpy(count + o, &fw.stack.count[r][c][0], HW * sizeof(double));
+        if (tsum) std::memcpy(tsum + o, &fw.stack.tsum[r][c][0], HW * sizeof(double));
+      }
+    if (n_active) std::memcpy(n_active, fw.stack.n_active.data(), R * sizeof(std::int64_t));
+    if (alive && n) std::memcpy(alive, fw.traj.alive.data(), n);
+    if (bin && n) std::memcpy(bin, fw.traj.bin.data(), n * sizeof(std::int32_t));
+    if (pos && n) std::memcpy(pos, fw.traj.pos.data(), n * R * 2 * sizeof(double));
+    if (loss) *loss = fw.loss.value;
+    if (no_survivors) *no_survivors = fw.loss.no_survivors ? 1 : 0;
+    if (do_backward && grad) {
+      const BackwardResult bw = eng.backward(s, f, fw);
+      for (int b = 0; b < B; ++b) {
+        std::memcpy(grad + (static_cast<std::size_t>(b) * 2) * HW, &bw.grad.gu[b][0],
+                    HW * sizeof(double));
+        std::memcpy(grad + (static_cast<std::size_t>(b) * 2 + 1) * HW, &bw.grad.gv[b][0],
+                    HW * sizeof(double));
+      }
+    }
+  });
+}
+
+REF_API int ref_warp_event(int W, int H, int B, const std::uint64_t* edges, const double* flows,
+                           double x, double y, double t_from, double t_to, double* out) {
+  return guarded([&] {
+    const FlowSequence f = make_flows(W, H, B, edges, flows);
+    const Vec2 p = warp_event({x, y}, t_from, t_to, f);
+    out[0] = p.x;
+    out[1] = p.y;
+  });
+}
+
+REF_API int ref_rsat(int W, int H, int B, const std::uint64_t* edges, const void* ev,
+                     std::size_t n, const double* flows, double* out) {
+  return guarded([&] {
+    const EventSlice s = make_slice(W, H, edges[0], edges[B], ev, n);
+    const FlowSequence f = make_flows(W, H, B, edges, flows);
+    *out = rsat(s, f);
+  });
+}
+
+REF_API int ref_depth_pose_to_flows(int W, int H, const double* depth, const std::uint8_t* mask,
+                                    int B, const double* poses, const double* K,
+                                    std::uint64_t t0, std::uint64_t t1, double* flows,
+                                    std::uint8_t* valid, std::uint64_t* edges_out) {
+  return guarded([&] {
+    const DepthMap d = make_depth(W, H, depth, mask);
+    const CameraIntrinsics k{K[0], K[1], K[2], K[3]};
+    const GeometryFlows g = depth_pose_to_flows(d, make_poses(B, poses), k, t0, t1);
+    dump_flows(g.flows, flows);
+    const std::size_t HW = static_cast<std::size_t>(W) * H;
+    if (valid)
+      for (int b = 0; b < B; ++b) std::memcpy(valid + b * HW, &g.valid[b][0], HW);
+    if (edges_out) std::memcpy(edges_out, g.flows.edges_us.data(), (B + 1) * sizeof(std::uint64_t));
+  });
+}
+
+REF_API int ref_depth_pose_to_flows_backward(int W, int H, const double* depth,
+                                             const std::uint8_t* mask, int B, const double* poses,
+                                             const double* K, const std::uint64_t* edges,
+                                             const double* grad, double* d_depth,
+                                             double* d_poses) {
+  return guarded([&] {
+    const DepthMap d = make_depth(W, H, depth, mask);
+    const CameraIntrinsics k{K[0], K[1], K[2], K[3]};
+    std::vector<double> zero(static_cast<std::size_t>(B) * 2 * W * H, 0.0);
+    const FlowSequence f = make_flows(W, H, B, edges, zero.data());
+    GradientBuffer g(W, H, B);
+    const std::size_t HW = static_cast<std::size_t>(W) * H;
+    for (int b = 0; b < B; ++b)
+      for (std::size_t i = 0; i < HW; ++i) {
+        g.gu[b][i] = grad[(static_cast<std::size_t>(b) * 2) * HW + i];
+        g.gv[b][i] = grad[(static_cast<std::size_t>(b) * 2 + 1) * HW + i];
+      }
+    const FlowsBackwardResult r = depth_pose_to_flows_backward(d, make_poses(B, poses), k, f, g);
+    std::memcpy(d_depth, &r.d_depth[0], HW * sizeof(double));
+    for (int b = 0; b < B; ++b) {
+      const PoseGrad& pg = r.d_poses[b];
+      const double v[6] = {pg.omega.x, pg.omega.y, pg.omega.z, pg.trans.x, pg.trans.y, pg.trans.z};
+      std::memcpy(d_poses + 6 * b, v, sizeof v);
+    }
+  });
+}
+
+// ---- the reference's own fixture generators ---------------------------------
+
+// random_fd_instance (fdcheck.hpp:94-146). Two-call protocol: with ev == NULL
+// only the shape is reported.
+REF_API int ref_random_fd_instance(std::uint64_t seed, int max_events, int max_dim,
+                                   int want_masked, int* W, int* H, int* B, std::size_t* n,
+                                   std::uint64_t* edges, void* ev, double* flows,
+                                   std::size_t* n_masked) {
+  return guarded([&] {
+    FdInstanceParams p;
+    if (max_events > 0) p.max_events = max_events;
+    if (max_dim > 0) p.max_dim = max_dim;
+    p.want_masked = want_masked != 0;
+    const FdInstance inst = random_fd_instance(seed, p);
+    *W = inst.slice.width;
+    *H = inst.slice.height;
+    *B = inst.flows.n_bins();
+    *n = inst.slice.events.size();
+    if (n_masked) *n_masked = inst.n_masked;
+    if (!ev) return;
+    std::memcpy(edges, inst.flows.edges_us.data(), (*B + 1) * sizeof(std::uint64_t));
+    if (*n) std::memcpy(ev, inst.slice.events.data(), *n * sizeof(Event));
+    dump_flows(inst.flows, flows);
+  });
+}
+
+// detail::bench_window (bench.hpp:112-141): constant per-bin flows.
+REF_API int ref_bench_window(int W, int H, int B, double window_s, std::uint64_t seed,
+                             std::size_t n_events, std::uint64_t* edges, void* ev,
+                             double* flows) {
+  return guarded([&] {
+    BenchConfig cfg;
+    cfg.width = W;
+    cfg.height = H;
+    cfg.bins = B;
+    cfg.window_s = window_s;
+    cfg.seed = seed;
+    FlowSequence f;
+    const EventSlice s = detail::bench_window(cfg, n_events, f);
+    std::memcpy(edges, f.edges_us.data(), (B + 1) * sizeof(std::uint64_t));
+    if (n_events) std::memcpy(ev, s.events.data(), n_events * sizeof(Event));
+    dump_flows(f, flows);
+  });
+}
+
+// generate_scene (synth.hpp:81-135) with the two-plane chain config of
+// SURVEY.md §8(d). Two-call protocol on the event count.
+REF_API int ref_generate_scene(int W, int H, int B, const double* poses, const double* K,
+                               double event_rate, std::uint64_t seed, std::size_t* n,
+                               void* ev, double* depth, std::uint8_t* mask) {
+  return guarded([&] {
+    SceneSpec spec;
+    spec.width = W;
+    spec.height = H;
+    spec.k = CameraIntrinsics{K[0], K[1], K[2], K[3]};
+    spec.event_rate = event_rate;
+    spec.seed = seed;
+    spec.trajectory = make_poses(B, poses);
+    spec.planes.push_back(PlaneSpec{1.0, 0, 0, W / 2, H, 0.05});
+    spec.planes.push_back(PlaneSpec{3.0, W / 2, 0, W, H, 0.05});
+    const SceneData sd = generate_scene(spec);
+    *n = sd.events.events.size();
+    if (!ev) return;
+    if (*n) std::memcpy(ev, sd.events.events.data(), *n * sizeof(Event));
+    for (std::size_t i = 0; i < sd.depth.d.size(); ++i) {
+      depth[i] = sd.depth.d[i];
+      mask[i] = sd.depth.valid[i];
+    }
+  });
+}
+
+// make_chain_instance (tests/chain_support.hpp:119-184) decoded to full
+// resolution: depth (all valid), poses, intrinsics, events.
+REF_API int ref_chain_instance(std::uint64_t seed, int sensor_w, int sensor_h, int factor,
+                               int n_bins, int n_events, std::size_t* n, void* ev, double* depth,
+                               double* poses, double* K) {
+  return guarded([&] {
+    evcm_test::ChainParams cp;
+    cp.sensor_w = sensor_w;
+    cp.sensor_h = sensor_h;
+    cp.factor = factor;
+    cp.n_bins = n_bins;
+    cp.n_events = n_events;
+    const evcm_test::ChainInstance inst = evcm_test::make_chain_instance(seed, cp);
+    *n = inst.slice.events.size();
+    if (!ev) return;
+    if (*n) std::memcpy(ev, inst.slice.events.data(), *n * sizeof(Event));
+    const DecodedPredictor dec = decode(inst.pred);
+    for (std::size_t i = 0; i < dec.depth.d.size(); ++i) depth[i] = dec.depth.d[i];
+    for (int b = 0; b < n_bins; ++b) {
+      const PoseStep& p = dec.poses[b];
+      const double v[6] = {p.omega.x, p.omega.y, p.omega.z, p.trans.x, p.trans.y, p.trans.z};
+      std::memcpy(poses + 6 * b, v, sizeof v);
+    }
+    K[0] = inst.k.fx;
+    K[1] = inst.k.fy;
+    K[2] = inst.k.cx;
+    K[3] = inst.k.cy;
+  });
+}
+
+// ---- CPU baseline: the reference's own chain, window by window -------------
+// Per window: depth_pose_to_flows (geometry.hpp:229) → Engine::loss_and_grad
+// (engine.hpp:208, default EngineOptions except n_workers) →
+// depth_pose_to_flows_backward (geometry.hpp:279); the composition of
+// predictor_loss_and_gradients (optimize.hpp:205-241) minus decode and L_geo.
+// Events are concatenated across windows; ev_off has n_windows+1 entries.
+// Returns wall seconds in *seconds and the summed loss in *loss_sum.
+REF_API int ref_chain_batch(int W, int H, int B, int n_windows, const double* depth,
+                            const double* poses, const double* K, std::uint64_t t0,
+                            std::uint64_t t1, const void* ev, const std::size_t* ev_off,
+                            int n_workers, double* loss_sum, double* d_depth_out,
+                            double* d_poses_out, double* seconds) {
+  return guarded([&] {
+    const CameraIntrinsics k{K[0], K[1], K[2], K[3]};
+    const std::size_t HW = static_cast<std::size_t>(W) * H;
+    EngineOptions o;
+    o.n_workers = n_workers;
+    const Engine eng(o);
+    double ls = 0.0;
+    const auto start = std::chrono::steady_clock::now();
+    for (int w = 0; w < n_windows; ++w) {
+      const DepthMap d = make_depth(W, H, depth + static_cast<std::size_t>(w) * HW, nullptr);
+      const std::vector<PoseStep> ps = make_poses(B, poses + static_cast<std::size_t>(w) * 6 * B);
+      const GeometryFlows g = depth_pose_to_flows(d, ps, k, t0, t1);
+      const EventSlice s =
+          make_slice(W, H, t0, t1, static_cast<const Event*>(ev) + ev_off[w], ev_off[w + 1] - ev_off[w]);
+      const auto [fw, bw] = eng.loss_and_grad(s, g.flows);
+      const FlowsBackwardResult r = depth_pose_to_flows_backward(d, ps, k, g.flows, bw.grad);
+      ls += fw.loss.value;
+      if (d_depth_out)
+        std::memcpy(d_depth_out + static_cast<std::size_t>(w) * HW, &r.d_depth[0], HW * sizeof(double));
+      if (d_poses_out)
+        for (int b = 0; b < B; ++b) {
+          const PoseGrad& pg = r.d_poses[b];
+          const double v[6] = {pg.omega.x, pg.omega.y, pg.omega.z, pg.trans.x, pg.trans.y, pg.trans.z};
+          std::memcpy(d_poses_out + (static_cast<std::size_t>(w) * B + b) * 6, v, sizeof v);
+        }
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+    *loss_sum = ls;
+  });
+}
