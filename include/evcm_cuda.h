@@ -1,0 +1,227 @@
+/*
+ * evcm_cuda.h — C-ABI of the B200 (sm_100a) CMax loss path.
+ *
+ * This is the drop-in boundary a maintainer of the reference (evcm, a
+ * header-only C++20 library) binds to add a `cuda` execution backend next to
+ * naive/padded/parallel (engine.hpp:37). Plain C: opaque handle, plain
+ * pointers and sizes, int status codes, no CUDA or torch types.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/include/evcm):
+ *   evcm_cuda_create / destroy          Engine(EngineOptions)           engine.hpp:136-141, 54-61
+ *   evcm_cuda_forward                   Engine::forward                 engine.hpp:145-183
+ *   evcm_cuda_forward_products          ForwardResult members           engine.hpp:99-105
+ *                                       (IweStack, Trajectories)        warp.hpp:167-220
+ *   evcm_cuda_backward                  Engine::backward                engine.hpp:185-205
+ *   evcm_cuda_loss_and_grad             Engine::loss_and_grad           engine.hpp:208-213
+ *   evcm_cuda_depth_pose_to_flows       depth_pose_to_flows             geometry.hpp:229-264
+ *   evcm_cuda_depth_pose_to_flows_backward
+ *                                       depth_pose_to_flows_backward    geometry.hpp:279-325
+ *   evcm_cuda_chain_batch               predictor_loss_and_gradients's  optimize.hpp:205-241
+ *                                       flows→forward→backward→flows-backward composition, over a
+ *                                       batch of windows (the reference runs them one at a time,
+ *                                       optimize.hpp:327-371)
+ *   evcm_cuda_last_error / error_name   evcm::Error taxonomy            types.hpp:18-76
+ *
+ * Memory: every call states where its array arguments live (EVCM_MEM_HOST or
+ * EVCM_MEM_DEVICE, device = the engine's CUDA device). Host inputs are staged
+ * through pinned buffers owned by the engine. Calls are synchronous with
+ * respect to the host unless documented otherwise.
+ *
+ * Layouts are the reference's own, flattened row-major (idx = y*W + x,
+ * Image<T>::idx, types.hpp:199-202):
+ *   events   evcm_event[n]          == evcm::Event, 16 B, time-sorted (types.hpp:106-113)
+ *   flows    f64 [B][2][H][W]       == FlowSequence.fields[b].{u,v}   (types.hpp:228-253)
+ *   stack    f64 [B+1][2][H][W]     == IweStack.count / tsum [ref][pol] (warp.hpp:167-172)
+ *   grad     f64 [B][2][H][W]       == GradientBuffer.gu[b] / gv[b]  (warp.hpp:223-224)
+ *   pos      f64 [n][B+1][2]        == Trajectories.pos              (warp.hpp:196-199)
+ *   poses    f64 [B][6]             == PoseStep {omega.xyz, trans.xyz} (types.hpp:356-358)
+ *   K        f64 [4]                == CameraIntrinsics {fx, fy, cx, cy} (types.hpp:164-168)
+ */
+#ifndef EVCM_CUDA_H
+#define EVCM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define EVCM_API __attribute__((visibility("default")))
+#else
+#define EVCM_API
+#endif
+
+#define EVCM_CUDA_ABI_VERSION 1
+#define EVCM_CUDA_MAX_BINS 32
+
+/* Status codes; the C++ adapter maps them onto the evcm::Error subclasses. */
+enum evcm_status {
+  EVCM_OK = 0,
+  EVCM_ERR_CONFIG = 1,      /* ConfigError */
+  EVCM_ERR_DIMENSION = 2,   /* DimensionMismatchError */
+  EVCM_ERR_COORDINATE = 3,  /* CoordinateRangeError */
+  EVCM_ERR_POLARITY = 4,    /* InvalidPolarityError */
+  EVCM_ERR_UNSORTED = 5,    /* UnsortedEventsError */
+  EVCM_ERR_TIME_RANGE = 6,  /* TimeRangeError */
+  EVCM_ERR_EMPTY = 7,       /* EmptySliceError */
+  EVCM_ERR_CUDA = 20,       /* device / driver failure (evcm::Error) */
+  EVCM_ERR_STATE = 21       /* backward without a matching forward (ConfigError analog,
+                               engine.hpp:191-193) */
+};
+
+enum evcm_mem { EVCM_MEM_HOST = 0, EVCM_MEM_DEVICE = 1 };
+
+/* Byte-identical to evcm::Event. */
+typedef struct {
+  uint64_t t_us;
+  uint16_t x;
+  uint16_t y;
+  int8_t p;
+  uint8_t pad_[3];
+} evcm_event;
+
+/* EngineOptions (engine.hpp:54-61) for the cuda backend. Fields the cuda
+ * backend does not need (n_workers, batch_size, padding_fraction) have no
+ * counterpart; `deterministic` keeps its meaning (run-to-run bit-stable
+ * gradients, engine.hpp:60). */
+typedef struct {
+  int device;          /* CUDA device ordinal */
+  int deterministic;   /* 1: fixed-order accumulation, bit-stable run to run */
+  int stack_f64;       /* 1 (default, parity): fp64 IWE stack + loss coefficients;
+                          0: fp32 ("fast": loss/IWE within 1e-6, gradients NOT within
+                          1e-5 on sparse windows — see DESIGN.md "Numerics") */
+  int grad_f64;        /* 1: fp64 flow-gradient accumulators (default 0: fp32, which
+                          keeps gradients within ~1e-7 of the reference) */
+  void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
+} evcm_cuda_options;
+
+/* EventSlice (types.hpp:121-126). */
+typedef struct {
+  uint16_t width;
+  uint16_t height;
+  uint64_t t_start_us;
+  uint64_t t_end_us; /* exclusive */
+  const evcm_event* events;
+  size_t n_events;
+} evcm_slice;
+
+/* FlowSequence (types.hpp:251-253): B+1 edges and B fields. */
+typedef struct {
+  int n_bins;
+  const uint64_t* edges_us; /* host pointer, B+1 entries */
+  const double* uv;         /* [B][2][H][W] */
+} evcm_flows;
+
+/* LossResult (warp.hpp:292-295). */
+typedef struct {
+  double value;
+  int no_survivors;
+} evcm_loss;
+
+typedef struct evcm_cuda_engine evcm_cuda_engine;
+
+/* ---- lifecycle / errors -------------------------------------------------- */
+EVCM_API void evcm_cuda_default_options(evcm_cuda_options* opts);
+EVCM_API int evcm_cuda_create(const evcm_cuda_options* opts, evcm_cuda_engine** out);
+EVCM_API void evcm_cuda_destroy(evcm_cuda_engine* e);
+/* Message of the last failing call on this thread ("" if none). */
+EVCM_API const char* evcm_cuda_last_error(void);
+/* "ConfigError", "DimensionMismatchError", ... for a status code. */
+EVCM_API const char* evcm_cuda_error_name(int status);
+EVCM_API int evcm_cuda_abi_version(void);
+
+/* ---- Engine ---------------------------------------------------------------- */
+
+/* Engine::forward. Validates the window exactly like Engine::validate_window
+ * (engine.hpp:215-222) and keeps the IWE stack on the device for a following
+ * backward. `mem` applies to slice->events and flows->uv. */
+EVCM_API int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* slice, const evcm_flows* flows,
+                      int mem, evcm_loss* loss);
+
+/* Copies ForwardResult members of the last forward to HOST buffers; any
+ * pointer may be NULL. count/tsum [B+1][2][H][W] f64; n_active [B+1];
+ * alive u8 [n]; bin i32 [n]; pos f64 [n][B+1][2]; n_alive scalar. */
+EVCM_API int evcm_cuda_forward_products(evcm_cuda_engine* e, double* count, double* tsum,
+                               int64_t* n_active, uint8_t* alive, int32_t* bin, double* pos,
+                               size_t* n_alive);
+
+/* Engine::backward for the window of the last forward (same slice/flows).
+ * grad: [B][2][H][W] f64, in `mem` space. */
+EVCM_API int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* slice, const evcm_flows* flows,
+                       int mem, double* grad);
+
+/* Engine::loss_and_grad. */
+EVCM_API int evcm_cuda_loss_and_grad(evcm_cuda_engine* e, const evcm_slice* slice,
+                            const evcm_flows* flows, int mem, evcm_loss* loss, double* grad);
+
+/* ---- motion field ------------------------------------------------------------- */
+
+/* depth_pose_to_flows: depth f64 [H][W], mask u8 [H][W] or NULL (all valid),
+ * poses [B][6], K [4]. Writes flows [B][2][H][W], valid u8 [B][H][W] (may be
+ * NULL) and, if edges_out != NULL (host), the B+1 FlowSequence::zeros edges. */
+EVCM_API int evcm_cuda_depth_pose_to_flows(evcm_cuda_engine* e, int width, int height,
+                                  const double* depth, const uint8_t* mask, int n_bins,
+                                  const double* poses, const double* K, uint64_t t_start_us,
+                                  uint64_t t_end_us, int mem, double* flows, uint8_t* valid,
+                                  uint64_t* edges_out);
+
+/* depth_pose_to_flows_backward: grad [B][2][H][W] -> d_depth [H][W], d_poses [B][6]. */
+EVCM_API int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int width, int height,
+                                           const double* depth, const uint8_t* mask, int n_bins,
+                                           const double* poses, const double* K,
+                                           const uint64_t* edges_us, const double* grad,
+                                           int mem, double* d_depth, double* d_poses);
+
+/* ---- batched chain (the hot path, one call per batch of windows) ---------------- */
+
+/* n_windows windows sharing sensor size, intrinsics and time window
+ * [t_start_us, t_end_us) split into n_bins FlowSequence::zeros bins. For each
+ * window w: depth_pose_to_flows(depth[w], poses[w]) -> Engine::forward ->
+ * Engine::backward -> depth_pose_to_flows_backward, i.e. the
+ * predictor_loss_and_gradients composition without decode / L_geo.
+ *   events   concatenated, window w = events[ev_offsets[w] .. ev_offsets[w+1])
+ *   depth    f64 [n_windows][H][W] (all pixels valid, as DecodedPredictor)
+ *   poses    f64 [n_windows][B][6]
+ * Outputs (in `mem` space): loss f64 [n_windows], no_survivors i32 [n_windows]
+ * (may be NULL), d_depth f64 [n_windows][H][W], d_poses f64 [n_windows][B][6].
+ * ev_offsets is always a HOST array of n_windows+1 entries. */
+typedef struct {
+  int n_windows;
+  int width, height, n_bins;
+  uint64_t t_start_us, t_end_us;
+  double K[4];
+  const evcm_event* events;
+  const uint64_t* ev_offsets;
+  const double* depth;
+  const double* poses;
+} evcm_chain_batch;
+
+typedef struct {
+  double* loss;
+  int32_t* no_survivors;
+  double* d_depth;
+  double* d_poses;
+} evcm_chain_out;
+
+EVCM_API int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* batch, int mem,
+                          evcm_chain_out* out);
+
+/* ---- instrumentation (PhaseStats analog, engine.hpp:63-66,226-242) --------------- */
+
+/* Per-stage device times (ms, CUDA events) of the last chain/forward/backward
+ * call when timing is enabled: stage order = stage, motion, sort, splat, loss,
+ * backward, flows_backward. Returns the number of stages written. */
+EVCM_API int evcm_cuda_set_timing(evcm_cuda_engine* e, int enabled);
+EVCM_API int evcm_cuda_stage_times(evcm_cuda_engine* e, double* ms, int max_stages);
+/* Number of kernels launched by the last API call (for bench gpu_launches). */
+EVCM_API int evcm_cuda_last_launch_count(evcm_cuda_engine* e);
+/* Device memory currently held by the engine's workspaces, in bytes (the
+ * PhaseStats.peak_bytes analog, memtrack.hpp:72-102). */
+EVCM_API size_t evcm_cuda_workspace_bytes(evcm_cuda_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVCM_CUDA_H */

@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) CMax loss path of arXiv 2412.06359 behind the reference's
+operator API (evcm::Engine, depth_pose_to_flows[_backward]).
+
+See DESIGN.md for the kernels, the HBM layout and the roofline; include/evcm_cuda.h
+for the C-ABI; INTEGRATION.md for the reference-side binding.
+"""
+from .engine import (  # noqa: F401
+    BACKENDS, EVENT_DTYPE, BackwardResult, CameraIntrinsics, ConfigError, CoordinateRangeError,
+    DimensionMismatchError, EmptySliceError, Engine, EngineOptions, Error, EventSlice,
+    FlowSequence, ForwardResult, GeometryFlows, InvalidPolarityError, IweStack, LossResult,
+    TimeRangeError, Trajectories, UnsortedEventsError, backend_from_name, build_iwe_stack,
+    contrast_loss_backward, default_engine, depth_pose_to_flows, depth_pose_to_flows_backward,
+    load_library, make_edges, rsat)

@@ -1,0 +1,673 @@
+// CUDA kernels of the CMax loss path for B200 (sm_100a).
+//
+// Stage map:
+//   k_stage          events AoS (evcm::Event) -> packed 8 B records + window
+//                    validation (EventSlice::validate, types.hpp:135-159)
+//   k_motion_field   K1  depth_pose_to_flows          geometry.hpp:229-264
+//   k_fwd_splat      K2+K3 build_trajectory + splat   warp.hpp:257-281, engine.hpp:365-374
+//   k_loss_reduce    K3b refresh_active + reference_loss + coefficient planes
+//                    warp.hpp:186-192, 299-312, 345-350
+//   k_loss_finalize  reduce_loss                      engine.hpp:442-468
+//   k_bwd            K4  backward_event               engine.hpp:475-504
+//   k_flows_bwd      K5  depth_pose_to_flows_backward geometry.hpp:279-325
+//
+// Data layout in HBM (per window w of a batch; HW = W*H, R = B+1):
+//   packed events  uint2 [n]                         8 B / event
+//   flows          double2 [w][B][HW]   (u, v) interleaved, 16 B / px / bin
+//   stack          S2 [w][R][2][HW]     (count, tsum) interleaved, S2 = float2|double2
+//   coef           S2 [w][R][2][HW]     (a = S/(C+eps), q = a/(C+eps))
+//   grad           G2 [w][B][HW]        (gu, gv) interleaved, G2 = float2|double2
+#include <cstdint>
+#include <cstdio>
+
+#include "cmax_device.cuh"
+#include "cmax_kernels.h"
+
+namespace evcm_b200 {
+
+static thread_local int g_launches = 0;
+void reset_launch_count() { g_launches = 0; }
+int launch_count() { return g_launches; }
+
+// --------------------------------------------------------------------------
+// helpers
+
+template <typename T> struct Vec2Of;
+template <> struct Vec2Of<float> { using type = float2; };
+template <> struct Vec2Of<double> { using type = double2; };
+
+__device__ __forceinline__ void red_add2(float2* p, double a, double b) {
+  atomicAdd(p, make_float2((float)a, (float)b));  // REDG.E.ADD.F32x2
+}
+__device__ __forceinline__ void red_add2(double2* p, double a, double b) {
+  atomicAdd(&p->x, a);  // REDG.E.ADD.F64
+  atomicAdd(&p->y, b);
+}
+__device__ __forceinline__ double2 ld2(const float2* p) {
+  const float2 v = __ldg(p);
+  return make_double2(v.x, v.y);
+}
+__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ void store2(float2* p, double a, double b) {
+  *p = make_float2((float)a, (float)b);
+}
+__device__ __forceinline__ void store2(double2* p, double a, double b) { *p = make_double2(a, b); }
+
+__device__ __forceinline__ void load_edges(const WinParams& P, double* es, uint32_t* erel) {
+  for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
+    es[i] = P.es[i];
+    erel[i] = P.erel[i];
+  }
+}
+
+// --------------------------------------------------------------------------
+// K0: staging + validation
+
+// Error key per window: (index << 4 | code), minimum wins = first violation in
+// event order, and for that event the first failing check in the order of
+// EventSlice::validate (types.hpp:143-155).
+__global__ void k_stage(const evcm_event* __restrict__ ev, const uint64_t* __restrict__ ev_off,
+                        WinParams P, uint2* __restrict__ packed,
+                        unsigned long long* __restrict__ err) {
+  const int w = blockIdx.y;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const evcm_event e = ev[base + k];
+    unsigned code = 0;
+    if (e.x >= P.W || e.y >= P.H) code = 3;
+    else if (e.p != 1 && e.p != -1) code = 4;
+    else if (k > 0 && e.t_us < ev[base + k - 1].t_us) code = 5;
+    else if (e.t_us < P.t0 || e.t_us >= P.t_end) code = 6;
+    if (code) {
+      atomicMin(err + w, ((unsigned long long)k << 4) | code);
+      continue;
+    }
+    const uint32_t dt = (uint32_t)(e.t_us - P.t0);
+    packed[base + k] = make_uint2(dt | (e.p > 0 ? 0u : 0x80000000u),
+                                  (uint32_t)e.x | ((uint32_t)e.y << 16));
+  }
+}
+
+// flows [B][2][HW] f64 planes -> interleaved double2 [B][HW]
+__global__ void k_interleave_flows(const double* __restrict__ uv, int B, int HW,
+                                   double2* __restrict__ out) {
+  const size_t total = (size_t)B * HW;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / HW, p = i % HW;
+    out[i] = make_double2(uv[(2 * b) * HW + p], uv[(2 * b + 1) * HW + p]);
+  }
+}
+
+// --------------------------------------------------------------------------
+// K1: motion field (depth_pose_to_flows, geometry.hpp:229-264)
+
+// pose table per (window, bin): R[9], dR[27], t[3], inv_dt  -> 40 doubles
+__global__ void k_motion_field(const double* __restrict__ depth, const uint8_t* __restrict__ mask,
+                               const double* __restrict__ pose_tab, WinParams P, double fx,
+                               double fy, double cx, double cy, double2* __restrict__ flows,
+                               uint8_t* __restrict__ valid) {
+  const int w = blockIdx.z, b = blockIdx.y;
+  const int HW = P.HW;
+  const double* pt = pose_tab + ((size_t)w * P.B + b) * kPoseTab;
+  const double* Rm = pt;
+  const double* tr = pt + 36;
+  const double inv_dt = pt[39];
+  const double* dep = depth + (size_t)w * HW;
+  double2* out = flows + ((size_t)w * P.B + b) * HW;
+  uint8_t* vout = valid ? valid + ((size_t)w * P.B + b) * HW : nullptr;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < HW; q += gridDim.x * blockDim.x) {
+    double2 f = make_double2(0.0, 0.0);
+    uint8_t ok = 0;
+    const double d = dep[q];
+    if ((!mask || mask[(size_t)w * HW + q]) && d > 0.0) {
+      const int y = q / P.W, x = q - y * P.W;
+      // backproject (geometry.hpp:147-149)
+      const double bx = dd(dm(d, ds((double)x, cx)), fx);
+      const double by = dd(dm(d, ds((double)y, cy)), fy);
+      const double bz = d;
+      // rot * v + trans (geometry.hpp:77-81, 159)
+      const double px = da(da(da(dm(Rm[0], bx), dm(Rm[1], by)), dm(Rm[2], bz)), tr[0]);
+      const double py = da(da(da(dm(Rm[3], bx), dm(Rm[4], by)), dm(Rm[5], bz)), tr[1]);
+      const double pz = da(da(da(dm(Rm[6], bx), dm(Rm[7], by)), dm(Rm[8], bz)), tr[2]);
+      if (pz > 0.0) {
+        const double ux = da(dd(dm(fx, px), pz), cx);
+        const double uy = da(dd(dm(fy, py), pz), cy);
+        f = make_double2(dm(ds(ux, (double)x), inv_dt), dm(ds(uy, (double)y), inv_dt));
+        ok = 1;
+      }
+    }
+    out[q] = f;
+    if (vout) vout[q] = ok;
+  }
+}
+
+// --------------------------------------------------------------------------
+// K2+K3: per-event trajectory + bilinear splat into the per-reference stack
+
+template <typename S2>
+__global__ void __launch_bounds__(kEvBlock) k_fwd_splat(const uint2* __restrict__ packed,
+                                                        const uint64_t* __restrict__ ev_off,
+                                                        WinParams P,
+                                                        const double2* __restrict__ flows,
+                                                        S2* __restrict__ stack) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* es = reinterpret_cast<double*>(smem);
+  uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
+  double2* pos = reinterpret_cast<double2*>(smem + kEvSmemHeader) + threadIdx.x;
+  load_edges(P, es, erel);
+  __syncthreads();
+  const int w = blockIdx.y;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint2 e = packed[base + k];
+  const uint32_t dt = ev_dt(e);
+  const double t = dm((double)dt, 1e-6);  // engine.hpp:270
+  const int j = bin_of(dt, erel, P.B);
+  const double2* fl = flows + (size_t)w * P.B * P.HW;
+  if (!trajectory((double)ev_x(e), (double)ev_y(e), t, j, fl, P, es, pos, blockDim.x)) return;
+  const int pol = ev_pol(e);
+  S2* st = stack + (size_t)w * (P.B + 1) * 2 * P.HW;
+  for (int r = 0; r <= P.B; ++r) {
+    const double2 p = pos[r * blockDim.x];
+    const Cell c = bilin_cell(p.x, p.y, P.W, P.H);
+    const Weights wt = weights(c);
+    const double tb = dd(fabs(ds(t, es[r])), P.window_s);  // engine.hpp:370
+    S2* plane = st + (size_t)(r * 2 + pol) * P.HW + c.i00;
+    red_add2(plane, wt.w00, dm(wt.w00, tb));
+    red_add2(plane + c.ox, wt.w10, dm(wt.w10, tb));
+    red_add2(plane + c.oy, wt.w01, dm(wt.w01, tb));
+    red_add2(plane + c.oy + c.ox, wt.w11, dm(wt.w11, tb));
+  }
+}
+
+// --------------------------------------------------------------------------
+// K3b: n_active + per-reference loss partial sums + coefficient planes
+
+template <typename S2>
+__global__ void __launch_bounds__(kPxBlock) k_loss_reduce(const S2* __restrict__ stack,
+                                                          WinParams P,
+                                                          S2* __restrict__ coef,
+                                                          double* __restrict__ part_acc,
+                                                          unsigned long long* __restrict__ part_act) {
+  const int w = blockIdx.z, r = blockIdx.y;
+  const int HW = P.HW;
+  const size_t plane0 = ((size_t)w * (P.B + 1) + r) * 2 * HW;
+  double acc = 0.0;
+  unsigned act = 0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < HW; q += gridDim.x * blockDim.x) {
+    const double2 v0 = ld2(stack + plane0 + q);
+    const double2 v1 = ld2(stack + plane0 + HW + q);
+    act += (v0.x + v1.x > 0.0) ? 1u : 0u;  // refresh_active (warp.hpp:190)
+    // reference_loss (warp.hpp:306-309)
+    const double a0 = v0.y / (v0.x + kLossEps), a1 = v1.y / (v1.x + kLossEps);
+    acc += a0 * a0 + a1 * a1;
+    // splat_position_grad's per-pixel factors (warp.hpp:346-349)
+    const double i0 = 1.0 / (v0.x + kLossEps), i1 = 1.0 / (v1.x + kLossEps);
+    const double b0 = v0.y * i0, b1 = v1.y * i1;
+    store2(coef + plane0 + q, b0, b0 * i0);
+    store2(coef + plane0 + HW + q, b1, b1 * i1);
+  }
+  // block reduction
+  __shared__ double s_acc[kPxBlock / 32];
+  __shared__ unsigned s_act[kPxBlock / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    act += __shfl_xor_sync(0xffffffffu, act, o);
+  }
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_acc[wid] = acc;
+    s_act[wid] = act;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    unsigned long long c = 0;
+    for (int i = 0; i < kPxBlock / 32; ++i) {
+      a += s_acc[i];
+      c += s_act[i];
+    }
+    const size_t slot = ((size_t)w * (P.B + 1) + r) * gridDim.x + blockIdx.x;
+    part_acc[slot] = a;
+    part_act[slot] = c;
+  }
+}
+
+// reduce_loss (engine.hpp:442-468): fixed-order sum of the block partials.
+// out per window: loss, no_survivors, n_active[R], scale[R] = 2/((n_a+eps) R)
+__global__ void k_loss_finalize(const double* __restrict__ part_acc,
+                                const unsigned long long* __restrict__ part_act, int n_parts,
+                                WinParams P, double* __restrict__ loss,
+                                int* __restrict__ no_surv, long long* __restrict__ n_active,
+                                double* __restrict__ scale) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= P.n_windows) return;
+  const int R = P.B + 1;
+  long long total = 0;
+  double sum = 0.0;
+  for (int r = 0; r < R; ++r) {
+    double acc = 0.0;
+    unsigned long long na = 0;
+    const size_t s0 = ((size_t)w * R + r) * n_parts;
+    for (int i = 0; i < n_parts; ++i) {
+      acc += part_acc[s0 + i];
+      na += part_act[s0 + i];
+    }
+    n_active[(size_t)w * R + r] = (long long)na;
+    scale[(size_t)w * R + r] = 2.0 / (((double)na + kLossEps) * (double)R);
+    total += (long long)na;
+    sum += acc / ((double)na + kLossEps);
+  }
+  no_surv[w] = total == 0 ? 1 : 0;
+  loss[w] = total == 0 ? 0.0 : sum / (double)R;
+}
+
+// --------------------------------------------------------------------------
+// K4: per-event backward (backward_event, engine.hpp:475-504)
+
+// dL/dpos at reference r (splat_position_grad, warp.hpp:334-358), from the
+// coefficient planes: corner g = scale * q * (tb - a).
+template <typename C2>
+__device__ __forceinline__ double2 pos_grad(const C2* __restrict__ cp, const Cell& c,
+                                            double tb, double scale) {
+  const double2 k00 = ld2(cp + c.i00), k10 = ld2(cp + c.i00 + c.ox);
+  const double2 k01 = ld2(cp + c.i00 + c.oy), k11 = ld2(cp + c.i00 + c.oy + c.ox);
+  const double g00 = scale * k00.y * (tb - k00.x);
+  const double g10 = scale * k10.y * (tb - k10.x);
+  const double g01 = scale * k01.y * (tb - k01.x);
+  const double g11 = scale * k11.y * (tb - k11.x);
+  const double ax = 1.0 - c.wx, ay = 1.0 - c.wy;
+  return make_double2(-ay * g00 + ay * g10 - c.wy * g01 + c.wy * g11,
+                      -ax * g00 - c.wx * g10 + ax * g01 + c.wx * g11);
+}
+
+// BufferGradSink::add (warp.hpp:394-406) as vector atomics.
+template <typename G2>
+__device__ __forceinline__ void sink_add(G2* __restrict__ g, const Cell& c, double gx, double gy) {
+  const Weights w = weights(c);
+  red_add2(g + c.i00, w.w00 * gx, w.w00 * gy);
+  red_add2(g + c.i00 + c.ox, w.w10 * gx, w.w10 * gy);
+  red_add2(g + c.i00 + c.oy, w.w01 * gx, w.w01 * gy);
+  red_add2(g + c.i00 + c.oy + c.ox, w.w11 * gx, w.w11 * gy);
+}
+
+template <typename C2, typename G2>
+__global__ void __launch_bounds__(kEvBlock) k_bwd(const uint2* __restrict__ packed,
+                                                  const uint64_t* __restrict__ ev_off,
+                                                  WinParams P, const double2* __restrict__ flows,
+                                                  const C2* __restrict__ coef,
+                                                  const double* __restrict__ scale_tab,
+                                                  const int* __restrict__ no_surv,
+                                                  G2* __restrict__ grad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* es = reinterpret_cast<double*>(smem);
+  uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
+  double2* pos = reinterpret_cast<double2*>(smem + kEvSmemHeader) + threadIdx.x;
+  load_edges(P, es, erel);
+  __syncthreads();
+  const int w = blockIdx.y;
+  if (no_surv[w]) return;  // engine.hpp:196
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int B = P.B, R = B + 1, HW = P.HW, W = P.W, H = P.H;
+  const uint2 e = packed[base + k];
+  const uint32_t dt_us = ev_dt(e);
+  const double t = dm((double)dt_us, 1e-6);
+  const int j = bin_of(dt_us, erel, B);
+  const double2* fl = flows + (size_t)w * B * HW;
+  const double x0 = (double)ev_x(e), y0 = (double)ev_y(e);
+  const int stride = blockDim.x;
+  if (!trajectory(x0, y0, t, j, fl, P, es, pos, stride)) return;
+  const int pol = ev_pol(e);
+  const C2* cw = coef + (size_t)w * R * 2 * HW + (size_t)pol * HW;  // + r*2*HW
+  const double* sc = scale_tab + (size_t)w * R;
+  G2* gw = grad + (size_t)w * B * HW;
+  const double inv_win = 1.0 / P.window_s;
+  (void)inv_win;
+
+  // d[0] and d[B] start the two adjoint legs.
+  double2 gb, gf;
+  {
+    const double2 p = pos[0];
+    const Cell c = bilin_cell(p.x, p.y, W, H);
+    gb = pos_grad(cw, c, fabs(t - es[0]) / P.window_s, sc[0]);
+  }
+  {
+    const double2 p = pos[B * stride];
+    const Cell c = bilin_cell(p.x, p.y, W, H);
+    gf = pos_grad(cw + (size_t)B * 2 * HW, c, fabs(t - es[B]) / P.window_s, sc[B]);
+  }
+  // Interleaved reverse sweep: step s < j is backward-leg step i = s (position
+  // r = i+1); otherwise forward-leg step i = B-1-(s-j) (position r = i).
+  for (int s = 0; s < B - 1; ++s) {
+    const bool back = s < j;
+    const int i = back ? s : B - 1 - (s - j);
+    const int r = back ? i + 1 : i;
+    const double dt = back ? es[i] - es[i + 1] : es[i + 1] - es[i];
+    const double2 p = pos[r * stride];
+    const Cell c = bilin_cell(p.x, p.y, W, H);
+    double2 g = back ? gb : gf;
+    sink_add(gw + (size_t)i * HW, c, dt * g.x, dt * g.y);
+    const Jac J = sample_jacobian(fl + (size_t)i * HW, c);
+    // apply_step_transpose (warp.hpp:91-94), then + d[r]
+    const double2 d = pos_grad(cw + (size_t)r * 2 * HW, c, fabs(t - es[r]) / P.window_s, sc[r]);
+    const double nx = g.x * (1.0 + dt * J.dux) + g.y * dt * J.dvx + d.x;
+    const double ny = g.y * (1.0 + dt * J.dvy) + g.x * dt * J.duy + d.y;
+    if (back) gb = make_double2(nx, ny); else gf = make_double2(nx, ny);
+  }
+  // Both legs end with a partial step sampled at the source pixel in bin j;
+  // x0 is integral, so its cell has a single nonzero weight (= 1).
+  const double cb = es[j] - t, cf = es[j + 1] - t;
+  const Cell c = bilin_cell(x0, y0, W, H);
+  const int q = c.i00 + (c.wx > 0.5 ? c.ox : 0) + (c.wy > 0.5 ? c.oy : 0);
+  red_add2(gw + (size_t)j * HW + q, cb * gb.x + cf * gf.x, cb * gb.y + cf * gf.y);
+}
+
+// --------------------------------------------------------------------------
+// K5: flows backward (depth_pose_to_flows_backward, geometry.hpp:279-325)
+
+template <typename G2>
+__global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict__ depth,
+                                                        const uint8_t* __restrict__ mask,
+                                                        const double* __restrict__ pose_tab,
+                                                        WinParams P, double fx, double fy,
+                                                        double cx, double cy,
+                                                        const G2* __restrict__ grad,
+                                                        double* __restrict__ d_depth,
+                                                        double* __restrict__ pose_part) {
+  __shared__ double s_pose[kMaxBins * kPoseTab];
+  __shared__ double s_red[kPxBlock / 32][6];
+  const int w = blockIdx.y;
+  const int B = P.B, HW = P.HW;
+  for (int i = threadIdx.x; i < B * kPoseTab; i += blockDim.x)
+    s_pose[i] = pose_tab[(size_t)w * B * kPoseTab + i];
+  __syncthreads();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = q < HW;
+  double d = 0.0;
+  bool px_ok = false;
+  double rx = 0.0, ry = 0.0;
+  if (in) {
+    d = depth[(size_t)w * HW + q];
+    px_ok = (!mask || mask[(size_t)w * HW + q]) && d > 0.0;
+    const int y = q / P.W, x = q - y * P.W;
+    rx = 1.0 * ((double)x - cx) / fx;  // backproject(x, 1.0, k)
+    ry = 1.0 * ((double)y - cy) / fy;
+  }
+  double dd_acc = 0.0;
+  const G2* gw = grad + (size_t)w * B * HW;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = 0; b < B; ++b) {
+    const double* pt = s_pose + b * kPoseTab;
+    double c6[6] = {0, 0, 0, 0, 0, 0};
+    if (px_ok) {
+      const auto gg = gw[(size_t)b * HW + q];
+      const double gu = gg.x, gv = gg.y;
+      if (gu != 0.0 || gv != 0.0) {
+        const double* Rm = pt;
+        const double rr0 = Rm[0] * rx + Rm[1] * ry + Rm[2];
+        const double rr1 = Rm[3] * rx + Rm[4] * ry + Rm[5];
+        const double rr2 = Rm[6] * rx + Rm[7] * ry + Rm[8];
+        const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
+        if (p2 > 0.0) {
+          const double inv_dt = pt[39];
+          const double iz = 1.0 / p2;
+          const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+          const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+          dd_acc += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+          c6[3] = gu * ju0 * inv_dt;
+          c6[4] = gv * jv1 * inv_dt;
+          c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const double* dR = pt + 9 + 9 * a;
+            const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
+            const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
+            const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
+            const double qx = d * m0, qy = d * m1, qz = d * m2;
+            c6[a] = (gu * (ju0 * qx + ju2 * qz) + gv * (jv1 * qy + jv2 * qz)) * inv_dt;
+          }
+        }
+      }
+    }
+    // warp + block reduction of the 6 pose partials for bin b
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      double v = c6[a];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s_red[wid][a] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      double v = 0.0;
+      for (int i = 0; i < kPxBlock / 32; ++i) v += s_red[i][threadIdx.x];
+      pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * 6 + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+  if (in) d_depth[(size_t)w * HW + q] = dd_acc;
+}
+
+__global__ void k_pose_finalize(const double* __restrict__ pose_part, int n_parts, int B,
+                                int n_windows, double* __restrict__ d_poses) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over windows * B * 6
+  if (i >= n_windows * B * 6) return;
+  const int w = i / (B * 6), rem = i % (B * 6);
+  double v = 0.0;
+  for (int p = 0; p < n_parts; ++p) v += pose_part[((size_t)w * n_parts + p) * B * 6 + rem];
+  d_poses[i] = v;
+}
+
+// --------------------------------------------------------------------------
+// products / format conversion
+
+template <typename S2>
+__global__ void k_unpack_stack(const S2* __restrict__ stack, size_t planes, int HW,
+                               double* __restrict__ count, double* __restrict__ tsum) {
+  const size_t total = planes * HW;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = ld2(stack + i);
+    count[i] = v.x;
+    tsum[i] = v.y;
+  }
+}
+
+template <typename G2>
+__global__ void k_unpack_grad(const G2* __restrict__ g, int B, int HW, double* __restrict__ out) {
+  const size_t total = (size_t)B * HW;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / HW, p = i % HW;
+    const double2 v = ld2(g + i);
+    out[(2 * b) * HW + p] = v.x;
+    out[(2 * b + 1) * HW + p] = v.y;
+  }
+}
+
+// Trajectories products in original event order (pos optional).
+__global__ void __launch_bounds__(kEvBlock) k_traj_products(const uint2* __restrict__ packed,
+                                                            uint64_t n, WinParams P,
+                                                            const double2* __restrict__ flows,
+                                                            uint8_t* __restrict__ alive,
+                                                            int32_t* __restrict__ bin,
+                                                            double* __restrict__ pos_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* es = reinterpret_cast<double*>(smem);
+  uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
+  double2* pos = reinterpret_cast<double2*>(smem + kEvSmemHeader) + threadIdx.x;
+  load_edges(P, es, erel);
+  __syncthreads();
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint2 e = packed[k];
+  const uint32_t dt = ev_dt(e);
+  const double t = dm((double)dt, 1e-6);
+  const int j = bin_of(dt, erel, P.B);
+  const bool ok = trajectory((double)ev_x(e), (double)ev_y(e), t, j, flows, P, es, pos, blockDim.x);
+  alive[k] = ok ? 1 : 0;
+  bin[k] = j;
+  if (pos_out)
+    for (int r = 0; r <= P.B; ++r) {
+      const double2 p = pos[r * blockDim.x];
+      pos_out[(k * (P.B + 1) + r) * 2] = p.x;
+      pos_out[(k * (P.B + 1) + r) * 2 + 1] = p.y;
+    }
+}
+
+// --------------------------------------------------------------------------
+// host launchers
+
+size_t ev_smem_bytes(const WinParams& P) {
+  return kEvSmemHeader + sizeof(double2) * (size_t)(P.B + 1) * kEvBlock;
+}
+
+// Opt every per-event kernel into the dynamic shared memory its largest
+// window (B = kMaxBins) needs; done once per process.
+static void ensure_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  const int bytes = (int)(kEvSmemHeader + sizeof(double2) * (size_t)kMaxRefs * kEvBlock);
+  cudaFuncSetAttribute(k_fwd_splat<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_fwd_splat<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bwd<float2, float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bwd<float2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bwd<double2, float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_bwd<double2, double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_traj_products, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = true;
+}
+
+void launch_stage(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
+                  uint64_t max_n, uint2* packed, unsigned long long* err) {
+  const int blocks = (int)std::min<uint64_t>((max_n + 255) / 256, 148 * 16);
+  if (blocks == 0) return;
+  ++g_launches;
+  k_stage<<<dim3(blocks, P.n_windows), 256, 0, s>>>(ev, ev_off, P, packed, err);
+}
+
+void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out) {
+  const size_t total = (size_t)B * HW;
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  ++g_launches;
+  k_interleave_flows<<<blocks, 256, 0, s>>>(uv, B, HW, out);
+}
+
+void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
+                         const double* pose_tab, const WinParams& P, const double* K,
+                         double2* flows, uint8_t* valid) {
+  const int bx = std::min((P.HW + 255) / 256, 148);
+  ++g_launches;
+  k_motion_field<<<dim3(bx, P.B, P.n_windows), 256, 0, s>>>(depth, mask, pose_tab, P, K[0], K[1],
+                                                           K[2], K[3], flows, valid);
+}
+
+template <typename S2>
+void launch_fwd_splat(cudaStream_t s, const uint2* packed, const uint64_t* ev_off,
+                      const WinParams& P, uint64_t max_n, const double2* flows, S2* stack) {
+  if (max_n == 0) return;
+  ensure_smem_attrs();
+  const unsigned blocks = (unsigned)((max_n + kEvBlock - 1) / kEvBlock);
+  ++g_launches;
+  k_fwd_splat<S2><<<dim3(blocks, P.n_windows), kEvBlock, ev_smem_bytes(P), s>>>(packed, ev_off, P,
+                                                                             flows, stack);
+}
+
+int loss_parts(const WinParams& P) { return std::max(1, std::min((P.HW + kPxBlock - 1) / kPxBlock, 64)); }
+
+template <typename S2>
+void launch_loss(cudaStream_t s, const S2* stack, const WinParams& P, S2* coef,
+                 double* part_acc, unsigned long long* part_act, double* loss, int* no_surv,
+                 long long* n_active, double* scale) {
+  const int parts = loss_parts(P);
+  ++g_launches;
+  k_loss_reduce<S2><<<dim3(parts, P.B + 1, P.n_windows), kPxBlock, 0, s>>>(stack, P, coef,
+                                                                          part_acc, part_act);
+  ++g_launches;
+  k_loss_finalize<<<(P.n_windows + 63) / 64, 64, 0, s>>>(part_acc, part_act, parts, P, loss,
+                                                        no_surv, n_active, scale);
+}
+
+template <typename C2, typename G2>
+void launch_bwd(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
+                uint64_t max_n, const double2* flows, const C2* coef, const double* scale,
+                const int* no_surv, G2* grad) {
+  if (max_n == 0) return;
+  ensure_smem_attrs();
+  const unsigned blocks = (unsigned)((max_n + kEvBlock - 1) / kEvBlock);
+  ++g_launches;
+  k_bwd<C2, G2><<<dim3(blocks, P.n_windows), kEvBlock, ev_smem_bytes(P), s>>>(
+      packed, ev_off, P, flows, coef, scale, no_surv, grad);
+}
+
+int flows_bwd_parts(const WinParams& P) { return (P.HW + kPxBlock - 1) / kPxBlock; }
+
+template <typename G2>
+void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,
+                      const double* pose_tab, const WinParams& P, const double* K, const G2* grad,
+                      double* d_depth, double* pose_part, double* d_poses) {
+  const int parts = flows_bwd_parts(P);
+  ++g_launches;
+  k_flows_bwd<G2><<<dim3(parts, P.n_windows), kPxBlock, 0, s>>>(
+      depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
+  const int total = P.n_windows * P.B * 6;
+  ++g_launches;
+  k_pose_finalize<<<(total + 127) / 128, 128, 0, s>>>(pose_part, parts, P.B, P.n_windows, d_poses);
+}
+
+template <typename S2>
+void launch_unpack_stack(cudaStream_t s, const S2* stack, size_t planes, int HW, double* count,
+                         double* tsum) {
+  const size_t total = planes * HW;
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  if (blocks) k_unpack_stack<S2><<<blocks, 256, 0, s>>>(stack, planes, HW, count, tsum);
+}
+
+template <typename G2>
+void launch_unpack_grad(cudaStream_t s, const G2* g, int B, int HW, double* out) {
+  const size_t total = (size_t)B * HW;
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  if (blocks) k_unpack_grad<G2><<<blocks, 256, 0, s>>>(g, B, HW, out);
+}
+
+void launch_traj_products(cudaStream_t s, const uint2* packed, uint64_t n, const WinParams& P,
+                          const double2* flows, uint8_t* alive, int32_t* bin, double* pos) {
+  if (n == 0) return;
+  ensure_smem_attrs();
+  const unsigned blocks = (unsigned)((n + kEvBlock - 1) / kEvBlock);
+  ++g_launches;
+  k_traj_products<<<blocks, kEvBlock, ev_smem_bytes(P), s>>>(packed, n, P, flows, alive, bin, pos);
+}
+
+#define INST_S(S2)                                                                              \
+  template void launch_fwd_splat<S2>(cudaStream_t, const uint2*, const uint64_t*,                \
+                                     const WinParams&, uint64_t, const double2*, S2*);          \
+  template void launch_loss<S2>(cudaStream_t, const S2*, const WinParams&, S2*, double*,        \
+                                unsigned long long*, double*, int*, long long*, double*);       \
+  template void launch_unpack_stack<S2>(cudaStream_t, const S2*, size_t, int, double*, double*);
+#define INST_B(C2, G2)                                                                          \
+  template void launch_bwd<C2, G2>(cudaStream_t, const uint2*, const uint64_t*, const WinParams&, \
+                                   uint64_t, const double2*, const C2*, const double*,          \
+                                   const int*, G2*);
+INST_B(float2, float2)
+INST_B(float2, double2)
+INST_B(double2, float2)
+INST_B(double2, double2)
+#define INST_G(G2)                                                                              \
+  template void launch_flows_bwd<G2>(cudaStream_t, const double*, const uint8_t*, const double*, \
+                                     const WinParams&, const double*, const G2*, double*,       \
+                                     double*, double*);                                         \
+  template void launch_unpack_grad<G2>(cudaStream_t, const G2*, int, int, double*);
+INST_S(float2)
+INST_S(double2)
+INST_G(float2)
+INST_G(double2)
+
+}  // namespace evcm_b200

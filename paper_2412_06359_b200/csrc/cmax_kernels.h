@@ -1,0 +1,54 @@
+// Host-side declarations of the kernel launchers (internal to libevcm_cuda).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/evcm_cuda.h"
+#include "cmax_device.cuh"
+
+namespace evcm_b200 {
+
+constexpr int kEvBlock = 128;        // threads per block of the per-event kernels
+constexpr int kPxBlock = 256;        // threads per block of the per-pixel kernels
+constexpr int kPoseTab = 40;         // R[9], dR[27], t[3], inv_dt per (window, bin)
+constexpr size_t kEvSmemHeader = 512;  // es + erel tables ahead of the position columns
+
+void reset_launch_count();
+int launch_count();
+
+size_t ev_smem_bytes(const WinParams& P);
+int loss_parts(const WinParams& P);
+int flows_bwd_parts(const WinParams& P);
+
+void launch_stage(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
+                  uint64_t max_n, uint2* packed, unsigned long long* err);
+void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out);
+void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
+                         const double* pose_tab, const WinParams& P, const double* K,
+                         double2* flows, uint8_t* valid);
+template <typename S2>
+void launch_fwd_splat(cudaStream_t s, const uint2* packed, const uint64_t* ev_off,
+                      const WinParams& P, uint64_t max_n, const double2* flows, S2* stack);
+template <typename S2>
+void launch_loss(cudaStream_t s, const S2* stack, const WinParams& P, S2* coef,
+                 double* part_acc, unsigned long long* part_act, double* loss, int* no_surv,
+                 long long* n_active, double* scale);
+template <typename C2, typename G2>
+void launch_bwd(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
+                uint64_t max_n, const double2* flows, const C2* coef, const double* scale,
+                const int* no_surv, G2* grad);
+template <typename G2>
+void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,
+                      const double* pose_tab, const WinParams& P, const double* K, const G2* grad,
+                      double* d_depth, double* pose_part, double* d_poses);
+template <typename S2>
+void launch_unpack_stack(cudaStream_t s, const S2* stack, size_t planes, int HW, double* count,
+                         double* tsum);
+template <typename G2>
+void launch_unpack_grad(cudaStream_t s, const G2* g, int B, int HW, double* out);
+void launch_traj_products(cudaStream_t s, const uint2* packed, uint64_t n, const WinParams& P,
+                          const double2* flows, uint8_t* alive, int32_t* bin, double* pos);
+
+}  // namespace evcm_b200

@@ -1,0 +1,722 @@
+// C-ABI implementation of include/evcm_cuda.h: validation with the reference's
+// error taxonomy, workspace management, host<->device staging, and the stage
+// sequencing of Engine::forward / backward, the motion field and the batched
+// chain. Kernels live in cmax_kernels.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/evcm_cuda.h"
+#include "cmax_kernels.h"
+
+using namespace evcm_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, std::string msg) { throw Failure{code, std::move(msg)}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(EVCM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return EVCM_OK;
+  } catch (const Failure& x) {
+    g_err = x.msg;
+    return x.code;
+  } catch (const std::exception& x) {
+    g_err = x.what();
+    return EVCM_ERR_CUDA;
+  }
+}
+
+// ---- host-side rigid geometry (geometry.hpp:21-135), used to build the
+// per-(window, bin) pose table. Same expression order as the reference so
+// that R is bit-identical (the motion field then matches bit for bit).
+struct M3 {
+  double m[9];
+};
+M3 mul(const M3& a, const M3& b) {
+  M3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r.m[3 * i + j] = a.m[3 * i] * b.m[j] + a.m[3 * i + 1] * b.m[3 + j] + a.m[3 * i + 2] * b.m[6 + j];
+  return r;
+}
+M3 skew(double x, double y, double z) { return {{0, -z, y, z, 0, -x, -y, x, 0}}; }
+
+M3 rodrigues(const double* w) {  // geometry.hpp:94-107
+  const double t2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+  const double t = std::sqrt(t2);
+  double a, b;
+  if (t < 1e-8) {
+    a = 1.0 - t2 / 6.0;
+    b = 0.5 - t2 / 24.0;
+  } else {
+    a = std::sin(t) / t;
+    b = (1.0 - std::cos(t)) / t2;
+  }
+  const M3 S = skew(w[0], w[1], w[2]);
+  const M3 S2 = mul(S, S);
+  static const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  M3 R;
+  for (int i = 0; i < 9; ++i) R.m[i] = (I[i] + a * S.m[i]) + b * S2.m[i];
+  return R;
+}
+
+void rodrigues_jacobian(const double* w, M3 out[3]) {  // geometry.hpp:114-135
+  const double t2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+  const double t = std::sqrt(t2);
+  const M3 S = skew(w[0], w[1], w[2]);
+  static const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  if (t < 1e-4) {
+    for (int k = 0; k < 3; ++k) {
+      const M3 ek = skew(k == 0, k == 1, k == 2);
+      const M3 a = mul(ek, S), b = mul(S, ek);
+      for (int i = 0; i < 9; ++i) out[k].m[i] = ek.m[i] + 0.5 * (a.m[i] + b.m[i]);
+    }
+    return;
+  }
+  const M3 R = rodrigues(w);
+  M3 IR;
+  for (int i = 0; i < 9; ++i) IR.m[i] = I[i] - R.m[i];
+  for (int k = 0; k < 3; ++k) {
+    const double c0 = IR.m[k], c1 = IR.m[3 + k], c2 = IR.m[6 + k];
+    const M3 sc = skew(w[1] * c2 - w[2] * c1, w[2] * c0 - w[0] * c2, w[0] * c1 - w[1] * c0);
+    M3 m;
+    for (int i = 0; i < 9; ++i) m.m[i] = w[k] * S.m[i] + sc.m[i];
+    const M3 p = mul(m, R);
+    for (int i = 0; i < 9; ++i) out[k].m[i] = (1.0 / t2) * p.m[i];
+  }
+}
+
+void validate_pose(const double* p) {  // PoseStep::validate (types.hpp:362-368)
+  const double pi = 3.14159265358979323846;
+  if (!(std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]) < pi))
+    fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi");
+  for (int i = 0; i < 6; ++i)
+    if (!std::isfinite(p[i])) fail(EVCM_ERR_CONFIG, "pose step: non-finite component");
+}
+
+// FlowSequence::zeros edge rule (types.hpp:293-300)
+std::vector<uint64_t> zeros_edges(uint64_t t0, uint64_t t1, int B) {
+  if (B < 1 || t1 <= t0) fail(EVCM_ERR_CONFIG, "flow sequence: need n_bins >= 1 and a nonempty window");
+  std::vector<uint64_t> e(B + 1);
+  const double span = static_cast<double>(t1 - t0);
+  for (int i = 0; i <= B; ++i)
+    e[i] = (i == B) ? t1 : t0 + static_cast<uint64_t>(std::llround(span * i / B));
+  return e;
+}
+
+// ---- workspace ----------------------------------------------------------------
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace
+
+struct evcm_cuda_engine {
+  evcm_cuda_options opt{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::unordered_map<std::string, Buf> bufs;
+  // state of the last forward (Engine::forward -> backward hand-off)
+  bool have_fwd = false;
+  WinParams P{};
+  uint64_t n_events = 0;
+  int last_launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> stage_ms;
+
+  template <typename T>
+  T* get(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    Buf& b = bufs[name];
+    if (b.cap < bytes) {
+      if (b.p) ck(cudaFree(b.p), "cudaFree");
+      b.p = nullptr;
+      ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
+      b.cap = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+
+  void mark(int i) {
+    if (!timing) return;
+    while ((int)ev.size() <= i) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "cudaEventCreate");
+      ev.push_back(e);
+    }
+    ck(cudaEventRecord(ev[i], stream), "cudaEventRecord");
+  }
+  void collect(int n_marks) {
+    stage_ms.clear();
+    if (!timing) return;
+    ck(cudaEventSynchronize(ev[n_marks - 1]), "cudaEventSynchronize");
+    for (int i = 1; i < n_marks; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      stage_ms.push_back(ms);
+    }
+  }
+};
+
+namespace {
+
+void set_device(evcm_cuda_engine* e) { ck(cudaSetDevice(e->opt.device), "cudaSetDevice"); }
+
+// Copy `bytes` from a host or device pointer into a device buffer (or return
+// the device pointer itself).
+template <typename T>
+const T* to_device(evcm_cuda_engine* e, const char* name, const T* src, size_t count, int mem) {
+  if (mem == EVCM_MEM_DEVICE || count == 0) return src;
+  T* d = e->get<T>(name, count);
+  ck(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, e->stream), "H2D");
+  return d;
+}
+
+void from_device(evcm_cuda_engine* e, void* dst, const void* src, size_t bytes, int mem) {
+  if (bytes == 0) return;
+  ck(cudaMemcpyAsync(dst, src, bytes,
+                     mem == EVCM_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     e->stream),
+     "copy out");
+}
+
+// Window parameters from (W, H, edges): Engine::edge_seconds (engine.hpp:244-249)
+WinParams make_params(int W, int H, const uint64_t* edges, int B, int n_windows, uint64_t t0,
+                      uint64_t t_end) {
+  if (B > kMaxBins)
+    fail(EVCM_ERR_CONFIG, "cuda backend: at most " + std::to_string(kMaxBins) + " bins");
+  WinParams P{};
+  P.W = W;
+  P.H = H;
+  P.B = B;
+  P.HW = W * H;
+  P.n_windows = n_windows;
+  for (int i = 0; i <= B; ++i) {
+    P.es[i] = (static_cast<double>(edges[i]) - static_cast<double>(edges[0])) * 1e-6;
+    P.erel[i] = static_cast<uint32_t>(edges[i] - edges[0]);
+  }
+  P.window_s = P.es[B];
+  P.t0 = t0;
+  P.t_end = t_end;
+  return P;
+}
+
+void check_slice_header(const evcm_slice* s) {  // EventSlice::validate (types.hpp:136-139)
+  if (s->width == 0 || s->height == 0)
+    fail(EVCM_ERR_DIMENSION, "event slice: width and height must be positive");
+  if (s->t_end_us < s->t_start_us) fail(EVCM_ERR_TIME_RANGE, "event slice: t_end precedes t_start");
+}
+
+void check_flows(const evcm_slice* s, const evcm_flows* f) {  // FlowSequence::validate + shape/span
+  if (f->n_bins < 1 || !f->edges_us)
+    fail(EVCM_ERR_CONFIG, "flow sequence: need B >= 1 fields and B+1 edges");
+  for (int i = 0; i < f->n_bins; ++i)
+    if (f->edges_us[i] >= f->edges_us[i + 1])
+      fail(EVCM_ERR_CONFIG, "flow sequence: edges must be strictly increasing");
+  if (f->edges_us[0] != s->t_start_us || f->edges_us[f->n_bins] != s->t_end_us)
+    fail(EVCM_ERR_CONFIG, "engine: flow bin edges do not span the slice window");
+  if (s->t_end_us - s->t_start_us >= (1ull << 31))
+    fail(EVCM_ERR_CONFIG, "cuda backend: window longer than 2^31 us");
+}
+
+const char* code_name(int c) {
+  switch (c) {
+    case EVCM_OK: return "OK";
+    case EVCM_ERR_CONFIG: return "ConfigError";
+    case EVCM_ERR_DIMENSION: return "DimensionMismatchError";
+    case EVCM_ERR_COORDINATE: return "CoordinateRangeError";
+    case EVCM_ERR_POLARITY: return "InvalidPolarityError";
+    case EVCM_ERR_UNSORTED: return "UnsortedEventsError";
+    case EVCM_ERR_TIME_RANGE: return "TimeRangeError";
+    case EVCM_ERR_EMPTY: return "EmptySliceError";
+    case EVCM_ERR_STATE: return "ConfigError";
+    default: return "Error";
+  }
+}
+
+// Stage + validate events of n_windows windows (offsets on host). Throws the
+// reference's error for the first invalid event of the first bad window.
+void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off_h, const WinParams& P,
+                  int mem, const evcm_event* ev_host_for_msg) {
+  const int nw = P.n_windows;
+  const uint64_t total = off_h[nw];
+  uint64_t max_n = 0;
+  for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, off_h[w + 1] - off_h[w]);
+  const evcm_event* dev = to_device(e, "events_aos", ev, total, mem);
+  uint64_t* off_d = e->get<uint64_t>("ev_off", nw + 1);
+  ck(cudaMemcpyAsync(off_d, off_h, (nw + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream),
+     "H2D offsets");
+  uint2* packed = e->get<uint2>("packed", total);
+  unsigned long long* err = e->get<unsigned long long>("stage_err", nw);
+  ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
+  launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
+  std::vector<unsigned long long> h(nw);
+  ck(cudaMemcpyAsync(h.data(), err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     e->stream),
+     "D2H err");
+  ck(cudaStreamSynchronize(e->stream), "stage");
+  for (int w = 0; w < nw; ++w) {
+    if (h[w] == ~0ull) continue;
+    const int code = static_cast<int>(h[w] & 0xf);
+    const uint64_t k = h[w] >> 4;
+    std::string msg;
+    switch (code) {
+      case 3: msg = "event slice: coordinate outside the sensor"; break;
+      case 4: msg = "event slice: polarity must be +1 or -1"; break;
+      case 5: msg = "event slice: timestamps must be non-decreasing"; break;
+      default: msg = "event slice: timestamp outside the window"; break;
+    }
+    (void)ev_host_for_msg;
+    fail(code, msg + " (window " + std::to_string(w) + ", event " + std::to_string(k) + ")");
+  }
+}
+
+// Pose table per (window, bin): R[9], dR[27], t[3], inv_dt (host-built).
+const double* upload_pose_table(evcm_cuda_engine* e, const double* poses_h, int nw, int B,
+                                const uint64_t* edges) {
+  std::vector<double> tab(static_cast<size_t>(nw) * B * kPoseTab);
+  for (int w = 0; w < nw; ++w)
+    for (int b = 0; b < B; ++b) {
+      const double* p = poses_h + (static_cast<size_t>(w) * B + b) * 6;
+      validate_pose(p);
+      double* t = tab.data() + (static_cast<size_t>(w) * B + b) * kPoseTab;
+      const M3 R = rodrigues(p);
+      M3 dR[3];
+      rodrigues_jacobian(p, dR);
+      std::memcpy(t, R.m, sizeof R.m);
+      for (int k = 0; k < 3; ++k) std::memcpy(t + 9 + 9 * k, dR[k].m, sizeof dR[k].m);
+      t[36] = p[3];
+      t[37] = p[4];
+      t[38] = p[5];
+      const double dur = (static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6;
+      t[39] = 1.0 / dur;
+    }
+  double* d = e->get<double>("pose_tab", tab.size());
+  ck(cudaMemcpyAsync(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream),
+     "H2D pose table");
+  // tab must outlive the async copy
+  ck(cudaStreamSynchronize(e->stream), "pose table");
+  return d;
+}
+
+template <typename S2>
+void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
+  const size_t R = P.B + 1;
+  S2* stack = e->get<S2>("stack", (size_t)P.n_windows * R * 2 * P.HW);
+  ck(cudaMemsetAsync(stack, 0, (size_t)P.n_windows * R * 2 * P.HW * sizeof(S2), e->stream), "memset");
+  e->mark(2);
+  launch_fwd_splat<S2>(e->stream, e->get<uint2>("packed", 1), e->get<uint64_t>("ev_off", 1), P, max_n,
+                       flows, stack);
+  e->mark(3);
+  const int parts = loss_parts(P);
+  const size_t np = (size_t)P.n_windows * R * parts;
+  launch_loss<S2>(e->stream, stack, P, e->get<S2>("coef", (size_t)P.n_windows * R * 2 * P.HW),
+                  e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np),
+                  e->get<double>("loss", P.n_windows), e->get<int>("no_surv", P.n_windows),
+                  e->get<long long>("n_active", (size_t)P.n_windows * R),
+                  e->get<double>("scale", (size_t)P.n_windows * R));
+  e->mark(4);
+}
+
+void run_forward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
+  if (e->opt.stack_f64) run_forward_t<double2>(e, P, max_n, flows);
+  else run_forward_t<float2>(e, P, max_n, flows);
+}
+
+template <typename C2, typename G2>
+void* run_backward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
+  G2* grad = e->get<G2>("grad", (size_t)P.n_windows * P.B * P.HW);
+  ck(cudaMemsetAsync(grad, 0, (size_t)P.n_windows * P.B * P.HW * sizeof(G2), e->stream), "memset");
+  launch_bwd<C2, G2>(e->stream, e->get<uint2>("packed", 1), e->get<uint64_t>("ev_off", 1), P, max_n,
+                     flows, e->get<C2>("coef", 1), e->get<double>("scale", 1),
+                     e->get<int>("no_surv", 1), grad);
+  return grad;
+}
+
+void* run_backward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
+  if (e->opt.stack_f64)
+    return e->opt.grad_f64 ? run_backward_t<double2, double2>(e, P, max_n, flows)
+                           : run_backward_t<double2, float2>(e, P, max_n, flows);
+  return e->opt.grad_f64 ? run_backward_t<float2, double2>(e, P, max_n, flows)
+                         : run_backward_t<float2, float2>(e, P, max_n, flows);
+}
+
+// Shared front half of forward(): validation, staging, flows.
+const double2* prepare_window(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
+                              WinParams* P_out) {
+  if (!s || !f) fail(EVCM_ERR_CONFIG, "null slice or flows");
+  check_slice_header(s);
+  // per-event validation (device) happens before the flow checks, as in
+  // Engine::validate_window (slice.validate() first, engine.hpp:216)
+  WinParams P0{};
+  P0.W = s->width;
+  P0.H = s->height;
+  P0.HW = s->width * s->height;
+  P0.n_windows = 1;
+  P0.t0 = s->t_start_us;
+  P0.t_end = s->t_end_us;
+  const uint64_t off[2] = {0, s->n_events};
+  if (s->n_events >= (1ull << 32)) fail(EVCM_ERR_CONFIG, "cuda backend: more than 2^32 events");
+  stage_events(e, s->events, off, P0, mem, nullptr);
+  check_flows(s, f);
+  WinParams P = make_params(s->width, s->height, f->edges_us, f->n_bins, 1, s->t_start_us, s->t_end_us);
+  const size_t nf = (size_t)f->n_bins * 2 * P.HW;
+  const double* uv = to_device(e, "flows_planar", f->uv, nf, mem);
+  double2* flows = e->get<double2>("flows", (size_t)f->n_bins * P.HW);
+  launch_interleave_flows(e->stream, uv, f->n_bins, P.HW, flows);
+  *P_out = P;
+  return flows;
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+
+extern "C" {
+
+int evcm_cuda_abi_version(void) { return EVCM_CUDA_ABI_VERSION; }
+
+const char* evcm_cuda_last_error(void) { return g_err.c_str(); }
+
+const char* evcm_cuda_error_name(int status) { return code_name(status); }
+
+void evcm_cuda_default_options(evcm_cuda_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->device = 0;
+  o->deterministic = 0;
+  o->stack_f64 = 1;  // parity precision
+  o->grad_f64 = 0;
+  o->stream = nullptr;
+}
+
+int evcm_cuda_create(const evcm_cuda_options* opts, evcm_cuda_engine** out) {
+  return guarded([&] {
+    if (!out) fail(EVCM_ERR_CONFIG, "null output handle");
+    evcm_cuda_options o;
+    evcm_cuda_default_options(&o);
+    if (opts) o = *opts;
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (o.device < 0 || o.device >= n) fail(EVCM_ERR_CONFIG, "engine: no such CUDA device");
+    auto* e = new evcm_cuda_engine();
+    e->opt = o;
+    set_device(e);
+    if (o.stream) {
+      e->stream = static_cast<cudaStream_t>(o.stream);
+    } else {
+      ck(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      e->own_stream = true;
+    }
+    *out = e;
+  });
+}
+
+void evcm_cuda_destroy(evcm_cuda_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->opt.device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  for (auto& kv : e->bufs)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  if (e->own_stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+int evcm_cuda_set_timing(evcm_cuda_engine* e, int enabled) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    e->timing = enabled != 0;
+  });
+}
+
+int evcm_cuda_stage_times(evcm_cuda_engine* e, double* ms, int max_stages) {
+  if (!e) return 0;
+  const int n = std::min<int>(max_stages, (int)e->stage_ms.size());
+  for (int i = 0; i < n; ++i) ms[i] = e->stage_ms[i];
+  return n;
+}
+
+int evcm_cuda_last_launch_count(evcm_cuda_engine* e) { return e ? e->last_launches : 0; }
+
+size_t evcm_cuda_workspace_bytes(evcm_cuda_engine* e) {
+  size_t s = 0;
+  if (e)
+    for (auto& kv : e->bufs) s += kv.second.cap;
+  return s;
+}
+
+int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
+                      evcm_loss* loss) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    set_device(e);
+    reset_launch_count();
+    e->have_fwd = false;
+    e->mark(0);
+    WinParams P;
+    const double2* flows = prepare_window(e, s, f, mem, &P);
+    e->mark(1);
+    run_forward(e, P, s->n_events, flows);
+    double l = 0;
+    int ns = 0;
+    ck(cudaMemcpyAsync(&l, e->get<double>("loss", 1), sizeof l, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaMemcpyAsync(&ns, e->get<int>("no_surv", 1), sizeof ns, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "forward");
+    e->collect(5);
+    ck(cudaGetLastError(), "forward kernels");
+    if (loss) {
+      loss->value = l;
+      loss->no_survivors = ns;
+    }
+    e->P = P;
+    e->n_events = s->n_events;
+    e->have_fwd = true;
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_forward_products(evcm_cuda_engine* e, double* count, double* tsum, int64_t* n_active,
+                               uint8_t* alive, int32_t* bin, double* pos, size_t* n_alive) {
+  return guarded([&] {
+    if (!e || !e->have_fwd) fail(EVCM_ERR_STATE, "engine: no forward result to read");
+    set_device(e);
+    const WinParams& P = e->P;
+    const size_t R = P.B + 1, HW = P.HW, n = e->n_events;
+    if (count || tsum) {
+      double* c = e->get<double>("prod_count", R * 2 * HW);
+      double* t = e->get<double>("prod_tsum", R * 2 * HW);
+      if (e->opt.stack_f64)
+        launch_unpack_stack<double2>(e->stream, e->get<double2>("stack", 1), R * 2, P.HW, c, t);
+      else
+        launch_unpack_stack<float2>(e->stream, e->get<float2>("stack", 1), R * 2, P.HW, c, t);
+      if (count) from_device(e, count, c, R * 2 * HW * sizeof(double), EVCM_MEM_HOST);
+      if (tsum) from_device(e, tsum, t, R * 2 * HW * sizeof(double), EVCM_MEM_HOST);
+    }
+    if (n_active)
+      from_device(e, n_active, e->get<long long>("n_active", R), R * sizeof(int64_t), EVCM_MEM_HOST);
+    if (alive || bin || pos || n_alive) {
+      uint8_t* a = e->get<uint8_t>("prod_alive", n);
+      int32_t* b = e->get<int32_t>("prod_bin", n);
+      double* p = pos ? e->get<double>("prod_pos", n * R * 2) : nullptr;
+      launch_traj_products(e->stream, e->get<uint2>("packed", 1), n, P, e->get<double2>("flows", 1), a, b, p);
+      std::vector<uint8_t> tmp;
+      uint8_t* ah = alive;
+      if (!ah && n_alive) {
+        tmp.resize(n);
+        ah = tmp.data();
+      }
+      if (ah) from_device(e, ah, a, n, EVCM_MEM_HOST);
+      if (bin) from_device(e, bin, b, n * sizeof(int32_t), EVCM_MEM_HOST);
+      if (pos) from_device(e, pos, p, n * R * 2 * sizeof(double), EVCM_MEM_HOST);
+      ck(cudaStreamSynchronize(e->stream), "products");
+      if (n_alive) {
+        size_t c = 0;
+        for (size_t k = 0; k < n; ++k) c += ah[k];
+        *n_alive = c;
+      }
+    }
+    ck(cudaStreamSynchronize(e->stream), "products");
+  });
+}
+
+int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
+                       double* grad) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    if (!s || !f) fail(EVCM_ERR_CONFIG, "null slice or flows");
+    set_device(e);
+    reset_launch_count();
+    check_slice_header(s);
+    check_flows(s, f);
+    if (!e->have_fwd || e->n_events != s->n_events || e->P.W != s->width || e->P.H != s->height ||
+        e->P.B != f->n_bins)
+      fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
+    const WinParams& P = e->P;
+    e->mark(0);
+    void* g = run_backward(e, P, s->n_events, e->get<double2>("flows", 1));
+    e->mark(1);
+    double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
+    if (e->opt.grad_f64)
+      launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
+    else
+      launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
+    from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
+    ck(cudaStreamSynchronize(e->stream), "backward");
+    e->collect(2);
+    ck(cudaGetLastError(), "backward kernels");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_loss_and_grad(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
+                            evcm_loss* loss, double* grad) {
+  int rc = evcm_cuda_forward(e, s, f, mem, loss);
+  if (rc) return rc;
+  const int l1 = e->last_launches;
+  rc = evcm_cuda_backward(e, s, f, mem, grad);
+  if (!rc) e->last_launches += l1;
+  return rc;
+}
+
+int evcm_cuda_depth_pose_to_flows(evcm_cuda_engine* e, int W, int H, const double* depth,
+                                  const uint8_t* mask, int B, const double* poses, const double* K,
+                                  uint64_t t0, uint64_t t1, int mem, double* flows_out,
+                                  uint8_t* valid, uint64_t* edges_out) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    set_device(e);
+    reset_launch_count();
+    if (B < 1) fail(EVCM_ERR_CONFIG, "depth_pose_to_flows: need one pose per bin");
+    if (W <= 0 || H <= 0 || !depth) fail(EVCM_ERR_DIMENSION, "depth_pose_to_flows: empty depth");
+    const std::vector<uint64_t> edges = zeros_edges(t0, t1, B);
+    WinParams P = make_params(W, H, edges.data(), B, 1, t0, t1);
+    std::vector<double> ph(poses, poses + (mem == EVCM_MEM_HOST ? 6 * B : 0));
+    if (mem == EVCM_MEM_DEVICE) {
+      ph.resize(6 * B);
+      ck(cudaMemcpy(ph.data(), poses, 6 * B * sizeof(double), cudaMemcpyDeviceToHost), "D2H poses");
+    }
+    const double* tab = upload_pose_table(e, ph.data(), 1, B, edges.data());
+    const double* dd = to_device(e, "depth", depth, (size_t)P.HW, mem);
+    const uint8_t* md = mask ? to_device(e, "mask", mask, (size_t)P.HW, mem) : nullptr;
+    double2* fl = e->get<double2>("flows", (size_t)B * P.HW);
+    uint8_t* vd = valid ? e->get<uint8_t>("valid", (size_t)B * P.HW) : nullptr;
+    launch_motion_field(e->stream, dd, md, tab, P, K, fl, vd);
+    double* planar = e->get<double>("flows_planar_out", (size_t)B * 2 * P.HW);
+    launch_unpack_grad<double2>(e->stream, fl, B, P.HW, planar);  // same [B][2][HW] unpack
+    from_device(e, flows_out, planar, (size_t)B * 2 * P.HW * sizeof(double), mem);
+    if (valid) from_device(e, valid, vd, (size_t)B * P.HW, mem);
+    if (edges_out) std::memcpy(edges_out, edges.data(), (B + 1) * sizeof(uint64_t));
+    ck(cudaStreamSynchronize(e->stream), "depth_pose_to_flows");
+    ck(cudaGetLastError(), "motion field");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, const double* depth,
+                                           const uint8_t* mask, int B, const double* poses,
+                                           const double* K, const uint64_t* edges,
+                                           const double* grad, int mem, double* d_depth,
+                                           double* d_poses) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    set_device(e);
+    reset_launch_count();
+    if (B < 1 || !edges) fail(EVCM_ERR_CONFIG, "flows backward: bins, poses, and gradients must align");
+    if (W <= 0 || H <= 0) fail(EVCM_ERR_DIMENSION, "flows backward: grids must match the depth map");
+    WinParams P = make_params(W, H, edges, B, 1, edges[0], edges[B]);
+    std::vector<double> ph(6 * B);
+    if (mem == EVCM_MEM_DEVICE)
+      ck(cudaMemcpy(ph.data(), poses, 6 * B * sizeof(double), cudaMemcpyDeviceToHost), "D2H poses");
+    else
+      std::memcpy(ph.data(), poses, 6 * B * sizeof(double));
+    // rodrigues_jacobian for the backward; geometry.hpp:293-296 does not
+    // re-validate poses, so no validation error here either.
+    std::vector<double> tab((size_t)B * kPoseTab);
+    for (int b = 0; b < B; ++b) {
+      double* t = tab.data() + (size_t)b * kPoseTab;
+      const M3 R = rodrigues(&ph[6 * b]);
+      M3 dR[3];
+      rodrigues_jacobian(&ph[6 * b], dR);
+      std::memcpy(t, R.m, sizeof R.m);
+      for (int k = 0; k < 3; ++k) std::memcpy(t + 9 + 9 * k, dR[k].m, sizeof dR[k].m);
+      t[36] = ph[6 * b + 3];
+      t[37] = ph[6 * b + 4];
+      t[38] = ph[6 * b + 5];
+      t[39] = 1.0 / ((static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6);
+    }
+    double* tab_d = e->get<double>("pose_tab", tab.size());
+    ck(cudaMemcpyAsync(tab_d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D");
+    const double* dd = to_device(e, "depth", depth, (size_t)P.HW, mem);
+    const uint8_t* md = mask ? to_device(e, "mask", mask, (size_t)P.HW, mem) : nullptr;
+    const double* gp = to_device(e, "grad_planar_in", grad, (size_t)B * 2 * P.HW, mem);
+    double2* g2 = e->get<double2>("grad_in", (size_t)B * P.HW);
+    launch_interleave_flows(e->stream, gp, B, P.HW, g2);
+    double* ddo = e->get<double>("d_depth", (size_t)P.HW);
+    double* pp = e->get<double>("pose_part", (size_t)flows_bwd_parts(P) * B * 6);
+    double* dpo = e->get<double>("d_poses", (size_t)B * 6);
+    launch_flows_bwd<double2>(e->stream, dd, md, tab_d, P, K, g2, ddo, pp, dpo);
+    from_device(e, d_depth, ddo, (size_t)P.HW * sizeof(double), mem);
+    from_device(e, d_poses, dpo, (size_t)B * 6 * sizeof(double), mem);
+    ck(cudaStreamSynchronize(e->stream), "flows backward");
+    ck(cudaGetLastError(), "flows backward kernels");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
+  return guarded([&] {
+    if (!e || !bt || !out) fail(EVCM_ERR_CONFIG, "null argument");
+    set_device(e);
+    reset_launch_count();
+    const int nw = bt->n_windows, B = bt->n_bins, W = bt->width, H = bt->height;
+    if (nw < 1) fail(EVCM_ERR_CONFIG, "chain: need at least one window");
+    if (W <= 0 || H <= 0 || W > 65535 || H > 65535) fail(EVCM_ERR_DIMENSION, "chain: bad sensor size");
+    if (bt->t_end_us - bt->t_start_us >= (1ull << 31))
+      fail(EVCM_ERR_CONFIG, "cuda backend: window longer than 2^31 us");
+    const std::vector<uint64_t> edges = zeros_edges(bt->t_start_us, bt->t_end_us, B);
+    WinParams P = make_params(W, H, edges.data(), B, nw, bt->t_start_us, bt->t_end_us);
+    e->have_fwd = false;
+    e->mark(0);
+    // poses are needed on the host for the rotation tables
+    std::vector<double> ph((size_t)nw * B * 6);
+    if (mem == EVCM_MEM_DEVICE)
+      ck(cudaMemcpyAsync(ph.data(), bt->poses, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, e->stream), "D2H poses");
+    else
+      std::memcpy(ph.data(), bt->poses, ph.size() * sizeof(double));
+    ck(cudaStreamSynchronize(e->stream), "poses");
+    const double* tab = upload_pose_table(e, ph.data(), nw, B, edges.data());
+    uint64_t max_n = 0;
+    for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, bt->ev_offsets[w + 1] - bt->ev_offsets[w]);
+    stage_events(e, bt->events, bt->ev_offsets, P, mem, nullptr);
+    const double* depth = to_device(e, "depth", bt->depth, (size_t)nw * P.HW, mem);
+    double2* flows = e->get<double2>("flows", (size_t)nw * B * P.HW);
+    e->mark(1);
+    launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr);
+    run_forward(e, P, max_n, flows);  // marks 2,3,4
+    void* g = run_backward(e, P, max_n, flows);
+    e->mark(5);
+    double* ddo = (mem == EVCM_MEM_DEVICE && out->d_depth) ? out->d_depth : e->get<double>("d_depth", (size_t)nw * P.HW);
+    double* dpo = (mem == EVCM_MEM_DEVICE && out->d_poses) ? out->d_poses : e->get<double>("d_poses", (size_t)nw * B * 6);
+    double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * 6);
+    if (e->opt.grad_f64)
+      launch_flows_bwd<double2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<double2*>(g), ddo, pp, dpo);
+    else
+      launch_flows_bwd<float2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<float2*>(g), ddo, pp, dpo);
+    e->mark(6);
+    if (out->loss) from_device(e, out->loss, e->get<double>("loss", nw), nw * sizeof(double), mem);
+    if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), mem);
+    if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), mem);
+    if (out->d_poses && dpo != out->d_poses) from_device(e, out->d_poses, dpo, (size_t)nw * B * 6 * sizeof(double), mem);
+    ck(cudaStreamSynchronize(e->stream), "chain");
+    e->collect(7);
+    ck(cudaGetLastError(), "chain kernels");
+    e->last_launches = launch_count();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+"""GPU parity of the batched chain (motion field -> forward -> backward ->
+flows backward) against the oracle composition, window by window."""
+import numpy as np
+import pytest
+
+import paper_2412_06359_b200 as P
+from oracle import oracle as O
+from tests.helpers import chain_inputs, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_chain(depth, poses, K, ev, offs, t0=0, t1=100000):
+    out = []
+    for w in range(depth.shape[0]):
+        fl, _ = O.depth_pose_to_flows(depth[w], poses[w], K, t0, t1)
+        win = O.Window(depth.shape[2], depth.shape[1], O.make_edges(t0, t1, poses.shape[1]),
+                       ev[int(offs[w]):int(offs[w + 1])], fl)
+        f = O.forward(win)
+        g = O.backward(win, f)
+        dd, dp = O.depth_pose_to_flows_backward(depth[w], poses[w], K, win.edges, g)
+        out.append((f["loss"], dd, dp))
+    return out
+
+
+@pytest.mark.parametrize("W,H,B,nw,n", [(64, 48, 10, 3, 3000), (128, 96, 4, 2, 20000),
+                                        (346, 260, 10, 2, 100000)])
+def test_chain_batch_host(engine, W, H, B, nw, n):
+    depth, poses, K, ev, offs = chain_inputs(W, H, B, nw, n, seed=W)
+    loss, dd, dp = engine.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    ref = _oracle_chain(depth, poses, K, ev, offs)
+    for w in range(nw):
+        assert abs(loss[w] - ref[w][0]) <= 1e-5 * abs(ref[w][0])
+        assert rel_inf(dd[w], ref[w][1]) <= 1e-5, rel_inf(dd[w], ref[w][1])
+        assert rel_inf(dp[w], ref[w][2]) <= 1e-5, rel_inf(dp[w], ref[w][2])
+
+
+def test_chain_batch_device_matches_host(engine):
+    import torch
+    depth, poses, K, ev, offs = chain_inputs(64, 48, 10, 4, 5000, seed=1)
+    lh, ddh, dph = engine.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    dev = torch.device("cuda:0")
+    td = torch.from_numpy(depth).to(dev)
+    tp = torch.from_numpy(poses).to(dev)
+    te = torch.from_numpy(ev.view(np.uint8)).to(dev)
+    ld, ddd, dpd = engine.chain_batch(td, tp, K, 0, 100000, te, offs)
+    torch.cuda.synchronize()
+    assert rel_inf(ld.cpu().numpy(), lh) <= 1e-12
+    assert rel_inf(ddd.cpu().numpy(), ddh) <= 1e-6
+    assert rel_inf(dpd.cpu().numpy(), dph) <= 1e-6

@@ -1,0 +1,168 @@
+"""GPU parity of Engine::forward / Engine::backward (C-ABI) against the CPU
+oracle (oracle/cmax_oracle.c, pinned bit-exact to the reference).
+
+Tolerances (north_star): bit-exact for bin, alive, n_alive,
+n_active and trajectory positions; <= 1e-5 relative for the loss, the IWE
+stack (||d||_inf/||ref||_inf) and the flow gradients (same norm)."""
+import numpy as np
+import pytest
+
+import paper_2412_06359_b200 as P
+from oracle import oracle as O
+from tests.helpers import rel_inf, smooth_window
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+FD_SEEDS = list(range(100, 110)) + [42, 7] + list(range(500, 508)) + list(range(1300, 1306)) + \
+    list(range(1700, 1704)) + [2500]
+
+
+def _slice(w):
+    return P.EventSlice(w.W, w.H, int(w.edges[0]), int(w.edges[-1]), w.events)
+
+
+def _flows(w):
+    return P.FlowSequence(w.edges.copy(), w.flows.copy())
+
+
+def _check(engine, w, grad_tol=TOL):
+    sl, fl = _slice(w), _flows(w)
+    fwd = engine.forward(sl, fl)
+    ref = O.forward(w, want_pos=True)
+    assert fwd.loss.no_survivors == ref["no_survivors"]
+    np.testing.assert_array_equal(fwd.stack.n_active, ref["n_active"])
+    np.testing.assert_array_equal(fwd.traj.alive, ref["alive"])
+    np.testing.assert_array_equal(fwd.traj.bin, ref["bin"])
+    assert fwd.traj.n_alive == ref["n_alive"]
+    np.testing.assert_array_equal(fwd.traj.pos, ref["pos"])
+    if ref["loss"] == 0.0:
+        assert fwd.loss.value == 0.0
+    else:
+        assert abs(fwd.loss.value - ref["loss"]) <= TOL * abs(ref["loss"])
+    assert rel_inf(fwd.stack.count, ref["count"]) <= TOL
+    assert rel_inf(fwd.stack.tsum, ref["tsum"]) <= TOL
+    g = engine.backward(sl, fl, fwd).grad
+    og = O.backward(w, ref)
+    assert rel_inf(g, og) <= grad_tol, rel_inf(g, og)
+    return fwd, g, ref, og
+
+
+@pytest.mark.parametrize("seed", FD_SEEDS)
+def test_fd_instances(engine, seed):
+    """The reference suite's own margin-screened instances (fdcheck.hpp:94-146)."""
+    w = O.ref_fd_instance(seed) if O.ref_available() else None
+    if w is None:
+        pytest.skip("reference fixture generator not built")
+    _check(engine, w)
+
+
+def test_fd_instances_masked(engine):
+    if not O.ref_available():
+        pytest.skip("reference fixture generator not built")
+    for seed in range(900, 904):
+        w = O.ref_fd_instance(seed, max_events=24, want_masked=True)
+        fwd, *_ = _check(engine, w)
+        assert fwd.traj.n_alive < w.n
+
+
+@pytest.mark.parametrize("W,H,B,n", [(64, 48, 10, 5000), (128, 128, 10, 20000),
+                                     (346, 260, 10, 100000), (37, 23, 3, 3000),
+                                     (50, 40, 1, 2000), (64, 48, 32, 4000)])
+def test_smooth_windows(engine, W, H, B, n):
+    w = smooth_window(W, H, B, n, seed=W + n)
+    _check(engine, w)
+
+
+def test_fp64_accumulators(engine_f64):
+    w = smooth_window(346, 260, 10, 100000, seed=3)
+    _check(engine_f64, w, grad_tol=1e-12)
+
+
+def test_fast_mode_forward(engine_fast):
+    """fp32 stack ("fast" mode): loss and IWE within 1e-6; gradients are not
+    parity-grade on sparse windows and are not checked."""
+    w = smooth_window(346, 260, 10, 100000, seed=4)
+    fwd = engine_fast.forward(_slice(w), _flows(w))
+    ref = O.forward(w)
+    np.testing.assert_array_equal(fwd.stack.n_active, ref["n_active"])
+    assert abs(fwd.loss.value - ref["loss"]) <= 1e-6 * ref["loss"]
+    assert rel_inf(fwd.stack.count, ref["count"]) <= 1e-6
+
+
+def test_empty_slice(engine):
+    """IweStack.EmptySliceGivesZeroStackAndWarningLoss (test_warp.cpp:78-94)."""
+    w = O.Window(8, 8, O.make_edges(0, 1000, 2), np.zeros(0, O.EVENT_DTYPE), np.zeros((2, 2, 8, 8)))
+    fwd = engine.forward(_slice(w), _flows(w))
+    assert fwd.loss.no_survivors and fwd.loss.value == 0.0
+    assert not fwd.stack.count.any() and not fwd.stack.n_active.any()
+    g = engine.backward(_slice(w), _flows(w), fwd).grad
+    assert not np.any(g)
+
+
+def test_single_event_loss_quarter(engine):
+    """IweStack.SingleMidWindowEventUnderZeroFlow (test_warp.cpp:96-113)."""
+    ev = O.make_events([500000], [3], [4], [1])
+    w = O.Window(8, 8, O.make_edges(0, 1000000, 1), ev, np.zeros((1, 2, 8, 8)))
+    fwd = engine.forward(_slice(w), _flows(w))
+    assert not fwd.loss.no_survivors
+    for r in range(2):
+        assert fwd.stack.count[r, 0, 4, 3] == 1.0
+        assert abs(fwd.stack.tsum[r, 0, 4, 3] - 0.5) <= 1e-7
+        assert fwd.stack.n_active[r] == 1
+    assert abs(fwd.loss.value - 0.25) <= 1e-6
+
+
+def test_exit_at_last_reference(engine):
+    """IweStack.EventExitingAtLastReferenceIsExcludedEverywhere (test_warp.cpp:115-129)."""
+    ev = O.make_events([0], [6], [2], [1])
+    uv = np.zeros((1, 2, 8, 8))
+    uv[0, 0] = 2.0
+    w = O.Window(8, 8, O.make_edges(0, 1000000, 1), ev, uv)
+    fwd = engine.forward(_slice(w), _flows(w))
+    assert fwd.loss.no_survivors
+    assert fwd.traj.n_alive == 0
+    assert not fwd.stack.n_active.any()
+
+
+def test_mass_conservation(engine):
+    """IweStack.MassConservationPerReference (test_warp.cpp:131-145), at scale."""
+    w = smooth_window(346, 260, 10, 200000, seed=11)
+    fwd = engine.forward(_slice(w), _flows(w))
+    mass = fwd.stack.count.sum(axis=(1, 2, 3))
+    n_alive = fwd.traj.n_alive
+    assert np.all(np.abs(mass - n_alive) <= 1e-5 * n_alive)
+
+
+def test_true_flow_beats_zero_flow(engine):
+    """ContrastLoss.TrueFlowBeatsZeroFlowOnLinearTrajectory (test_warp.cpp:164-186)."""
+    ev = O.make_events([k * 20000 for k in range(5)], [2 + (80 * k) // 100 for k in range(5)],
+                       [4] * 5, [1] * 5)
+    uv = np.zeros((2, 2, 8, 12))
+    uv[:, 0] = 40.0
+    sl = P.EventSlice(12, 8, 0, 100000, ev)
+    truth = P.FlowSequence(O.make_edges(0, 100000, 2), uv)
+    zero = truth.zeros_like()
+    assert engine.forward(sl, truth).loss.value < engine.forward(sl, zero).loss.value
+    assert P.rsat(sl, truth) < 1.0
+    assert P.rsat(sl, zero) == 1.0
+
+
+def test_gradient_support_limited_to_stencils(engine):
+    """Backward.GradientSupportLimitedToTrajectoryStencils (test_warp.cpp:211-247):
+    exact zeros outside the sampled cells."""
+    w = smooth_window(40, 30, 4, 50, seed=5)
+    fwd, g, ref, og = _check(engine, w)
+    np.testing.assert_array_equal(g == 0.0, og == 0.0)
+
+
+def test_repeatability(engine):
+    w = smooth_window(128, 96, 10, 30000, seed=9)
+    a = engine.forward(_slice(w), _flows(w))
+    la = a.loss.value
+    ga = engine.backward(_slice(w), _flows(w), a).grad.copy()
+    b = engine.forward(_slice(w), _flows(w))
+    gb = engine.backward(_slice(w), _flows(w), b).grad
+    assert abs(la - b.loss.value) <= 1e-9 * abs(la)
+    assert rel_inf(ga, gb) <= 1e-6
