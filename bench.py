@@ -1,0 +1,429 @@
+"""Benchmark of the B200 CMax loss path.
+
+One step = one pass of the hot path over one batch of synthetic windows:
+motion field (depth + poses -> flows) -> warp + splat -> focus loss ->
+per-event backward -> flows backward (d_depth, d_poses), i.e. the
+predictor_loss_and_gradients composition (optimize.hpp:205-241) without decode
+and L_geo, followed by the data-parallel reduction of [loss, d_depth, d_poses]
+(NCCL all-reduce across ranks when N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload B|C]
+    python bench.py --impl reference ...   # the reference CPU path on this host
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+EVENT_DTYPE = np.dtype({"names": ["t_us", "x", "y", "p"], "formats": ["<u8", "<u2", "<u2", "i1"],
+                        "offsets": [0, 8, 10, 12], "itemsize": 16})
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: MVSEC-shape windows, ~100k events each, batch 8, 1 B200
+    "B": dict(W=346, H=260, B=10, n_events=100_000, batch=8, window_us=100_000,
+              name="MVSEC-shape 346x260 windows, 100k events/window, batch 8 per GPU, "
+                   "10 bins (11 refs), 0.1 s windows"),
+    # BASELINE.json configs[2]: DSEC-shape windows, ~1M events each, batch 16, 1 B200
+    "C": dict(W=640, H=480, B=10, n_events=1_000_000, batch=16, window_us=100_000,
+              name="DSEC-shape 640x480 windows, 1M events/window, batch 16 per GPU, "
+                   "10 bins (11 refs), 0.1 s windows"),
+}
+
+HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (SURVEY.md §8(d) chain-level input)
+
+
+def make_inputs(wl, rank, n_windows):
+    """Two fronto-parallel planes (depth 1.0 | 3.0), per-bin ego-motion
+    omega=(0.001,-0.002,0.003), t=(0.02,0.01,0.005), K=(0.9W,0.9W,(W-1)/2,(H-1)/2);
+    events uniform in (t, x, y) with alternating polarity (bench_window semantics,
+    bench.hpp:112-141). All values fp32-representable. The depth map and poses
+    are shared by every window (data-parallel batch over one parameter set)."""
+    W, H, B, n = wl["W"], wl["H"], wl["B"], wl["n_events"]
+    rng = np.random.default_rng(1000 + rank)
+    depth = np.empty((H, W))
+    depth[:, : W // 2] = 1.0
+    depth[:, W // 2:] = 3.0
+    depth = np.ascontiguousarray(np.broadcast_to(depth, (n_windows, H, W)))
+    poses = np.tile(np.array([0.001, -0.002, 0.003, 0.02, 0.01, 0.005]), (n_windows, B, 1))
+    poses = poses.astype(np.float32).astype(np.float64)
+    K = np.array([0.9 * W, 0.9 * W, (W - 1) / 2, (H - 1) / 2]).astype(np.float32).astype(np.float64)
+    ev = np.zeros(n * n_windows, EVENT_DTYPE)
+    for w in range(n_windows):
+        s = slice(w * n, (w + 1) * n)
+        ev["t_us"][s] = np.sort(rng.integers(0, wl["window_us"], n))
+        ev["x"][s] = rng.integers(0, W, n)
+        ev["y"][s] = rng.integers(0, H, n)
+        ev["p"][s] = np.where(np.arange(n) % 2 == 0, 1, -1)
+    offs = np.arange(n_windows + 1, dtype=np.uint64) * n
+    return depth, poses, K, ev, offs
+
+
+def algorithmic_bytes(wl, n_windows):
+    """bytes = N*b_ev + HW*b_px per window, at the precision this
+    build computes in (depth f64 s_d=8, flows f64 s_f=8, IWE stack f64 s_s=8,
+    gradients f32 s_g=4): b_px = 3 s_d + 6B s_f + 12(B+1) s_s + 4B s_g, b_ev = 18.
+    Returns total and the per-kernel split used by the roofline object."""
+    B, HW, n = wl["B"], wl["W"] * wl["H"], wl["n_events"]
+    sd, sf, ss, sg = 8, 8, 8, 4
+    per = {
+        "motion_field": HW * (sd + 2 * B * sf),
+        "warp_splat": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),
+        "loss_reduce": HW * 4 * (B + 1) * ss,
+        "backward": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss + 2 * B * sg),
+        "flows_backward": HW * (2 * B * sg + 2 * sd),
+    }
+    per = {k: v * n_windows for k, v in per.items()}
+    return sum(per.values()), per
+
+
+STAGES = ["staging", "motion_field", "stack_memset", "warp_splat", "loss_reduce",
+          "grad_memset", "backward", "flows_backward"]
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline
+
+
+def run_reference_chain(wl, depth, poses, K, ev, offs, windows, n_workers=0):
+    from oracle import oracle as O
+    d = np.ascontiguousarray(depth[windows])
+    p = np.ascontiguousarray(poses[windows])
+    evs = [ev[int(offs[w]):int(offs[w + 1])] for w in windows]
+    o = np.zeros(len(windows) + 1, np.uint64)
+    o[1:] = np.cumsum([len(x) for x in evs])
+    r = O.ref_chain_batch(d, p, K, 0, wl["window_us"], np.concatenate(evs).astype(EVENT_DTYPE), o,
+                          n_workers=n_workers)
+    return r["seconds"], int(o[-1])
+
+
+def cpu_baseline(wl, depth, poses, K, ev, offs, budget_s=12.0):
+    """The reference itself (oracle/_ref/libevcm_ref.so, built from /root/reference
+    with its Release flags) on this host's cores: one warm-up window, then
+    windows until ~budget_s of CPU work (>= 2 windows)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": "Mevents/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libevcm_ref.so not built"}
+    cores = int(O.ref().ref_hardware_concurrency())
+    run_reference_chain(wl, depth, poses, K, ev, offs, [0])
+    secs, evs, nwin = 0.0, 0, 0
+    while (secs < budget_s or nwin < 2) and nwin < 64:
+        s, n = run_reference_chain(wl, depth, poses, K, ev, offs, [nwin % depth.shape[0]])
+        secs += s
+        evs += n
+        nwin += 1
+    return {"value": evs / secs / 1e6, "unit": "Mevents/s", "cores": cores, "kind": "reference",
+            "sample": f"{nwin} windows of the workload (window by window, as optimize.hpp:327-371), "
+                      f"{secs:.1f} s, depth_pose_to_flows + Engine::loss_and_grad (parallel, "
+                      f"deterministic, n_workers=0) + depth_pose_to_flows_backward",
+            "windows_per_s": nwin / secs}
+
+
+def reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    depth, poses, K, ev, offs = make_inputs(wl, 0, wl["batch"])
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libevcm_ref.so not built"}))
+        return
+    cores = int(O.ref().ref_hardware_concurrency())
+    for i in range(args.warmup):
+        run_reference_chain(wl, depth, poses, K, ev, offs, [i % wl["batch"]])
+    times, n_ev = [], 0
+    for i in range(args.steps):
+        s, n = run_reference_chain(wl, depth, poses, K, ev, offs, [i % wl["batch"]])
+        times.append(s)
+        n_ev += n
+    total = sum(times)
+    value = n_ev / total / 1e6
+    line = {
+        "impl": "reference", "metric": "CMax loss fwd+bwd throughput", "value": value,
+        "unit": "Mevents/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "step": "one window per step (bounded sample)",
+                   "events_per_window": wl["n_events"]},
+        "windows_per_s": args.steps / total,
+        "cpu_baseline": {"value": value, "unit": "Mevents/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} windows, one per step"},
+        "e2e": {"value": value, "unit": "Mevents/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CUDA arm
+
+
+def cuda_arm(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2412_06359_b200 as P
+
+    nwin = wl["batch"]
+    depth, poses, K, ev, offs = make_inputs(wl, rank, nwin)
+    stream = torch.cuda.Stream(dev)
+    eng = P.Engine(P.EngineOptions(device=local, stream=stream.cuda_stream))
+
+    # device-resident inputs / outputs
+    with torch.cuda.stream(stream):
+        d_depth = torch.from_numpy(depth).to(dev)
+        d_poses = torch.from_numpy(poses).to(dev)
+        d_ev = torch.from_numpy(ev.view(np.uint8)).to(dev)
+        out = (torch.empty(nwin, dtype=torch.float64, device=dev),
+               torch.empty((nwin, wl["H"], wl["W"]), dtype=torch.float64, device=dev),
+               torch.empty((nwin, wl["B"], 6), dtype=torch.float64, device=dev))
+        HW, B = wl["W"] * wl["H"], wl["B"]
+        red = torch.empty(1 + HW + B * 6, dtype=torch.float64, device=dev)
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream.synchronize()
+
+    def reduce_and_allreduce():
+        # data-parallel reduction of [sum loss, sum_w d_depth, sum_w d_poses]
+        red[0:1].copy_(out[0].sum().reshape(1))
+        red[1:1 + HW].copy_(out[1].sum(0).reshape(-1))
+        red[1 + HW:].copy_(out[2].sum(0).reshape(-1))
+        if world > 1:
+            dist.all_reduce(red)
+
+    def step():
+        eng.chain_batch(d_depth, d_poses, K, 0, wl["window_us"], d_ev, offs, out=out)
+        reduce_and_allreduce()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        launches_per_step = eng.last_launch_count()
+
+        eng.set_timing(True)
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        stage_ms = np.zeros(len(STAGES))
+        clocks = ClockSampler(local)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clocks.start()
+        time.sleep(0.3)
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (256 MB > 126 MB L2), untimed
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            stage_ms += np.array(eng.stage_times_ms()[: len(STAGES)])
+        torch.cuda.synchronize(dev)
+        clk = clocks.stop()
+        if world > 1:
+            dist.barrier()
+        eng.set_timing(False)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    events_per_step = wl["n_events"] * nwin * world
+    value = events_per_step * args.steps / (total_ms * 1e-3) / 1e6
+    windows_per_s = nwin * world * args.steps / (total_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / its
+    # average CUDA-event duration on the launching stream)
+    stage_ms /= args.steps
+    peak, peak_kind = peaks()
+    total_bytes, per_kernel = algorithmic_bytes(wl, nwin)
+    kern = {k: stage_ms[STAGES.index(k)] for k in per_kernel}
+    dom = max(kern, key=kern.get)
+    achieved = per_kernel[dom] / (kern[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "algorithmic_bytes_per_launch": per_kernel[dom],
+                "launch_ms": kern[dom]}
+    step_roofline = {"algorithmic_bytes_per_step": total_bytes,
+                     "achieved_GBps": total_bytes / (ms_per_step * 1e-3) / 1e9,
+                     "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
+                     "stage_ms": {s: round(float(m), 4) for s, m in zip(STAGES, stage_ms)}}
+
+    # ---- e2e: public API with pinned host buffers, H2D and D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_depth = torch.from_numpy(depth).pin_memory()
+        h_poses = torch.from_numpy(poses).pin_memory()
+        h_ev = torch.from_numpy(ev.view(np.uint8)).pin_memory()
+        h_red = torch.empty_like(red, device="cpu").pin_memory()
+
+        def e2e_step():
+            eng.chain_batch(h_depth, h_poses, K, 0, wl["window_us"], h_ev, offs, out=out,
+                            out_device=True)
+            reduce_and_allreduce()
+            h_red.copy_(red, non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, args.warmup)):
+                e2e_step()
+            stream.synchronize()
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            for i in range(args.steps):
+                flush.zero_()
+                es[i].record(stream)
+                e2e_step()
+                ee[i].record(stream)
+                stream.synchronize()  # the host reads the result every step
+            torch.cuda.synchronize(dev)
+        e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": events_per_step * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mevents/s",
+               "h2d_bytes_per_step": int(h_depth.numel() * 8 + h_poses.numel() * 8 + h_ev.numel()),
+               "d2h_bytes_per_step": int(h_red.numel() * 8),
+               "ms_per_step": e2e_ms / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, depth, poses, K, ev, offs, budget_s=args.cpu_budget_s)
+
+    if rank == 0:
+        line = {
+            "metric": "CMax loss fwd+bwd throughput", "value": value, "unit": "Mevents/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["name"], "windows_per_gpu_per_step": nwin,
+                       "events_per_window": wl["n_events"], "sensor": [wl["W"], wl["H"]],
+                       "bins": wl["B"], "numerics": "parity (fp64 per-event math, fp64 IWE "
+                       "stack, fp32 flow-gradient accumulators)",
+                       "l2": "flushed between timed steps (256 MB write, untimed)",
+                       "inputs": "two-plane depth + per-bin ego-motion, uniform events",
+                       "parallelism": f"dp{world} (windows sharded, NCCL all-reduce of "
+                                      "loss/d_depth/d_poses)"},
+            "windows_per_s": windows_per_s,
+            "roofline": roofline,
+            "step_roofline": step_roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        reference_arm(args, wl)
+    else:
+        cuda_arm(args, wl)
+
+
+if __name__ == "__main__":
+    main()

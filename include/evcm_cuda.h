@@ -207,12 +207,18 @@ typedef struct {
 
 EVCM_API int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* batch, int mem,
                           evcm_chain_out* out);
+/* Same, with separate memory spaces for the inputs and the outputs (e.g. host
+ * inputs staged in, device outputs kept for a following NCCL all-reduce). */
+EVCM_API int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* batch, int in_mem,
+                                    int out_mem, evcm_chain_out* out);
 
 /* ---- instrumentation (PhaseStats analog, engine.hpp:63-66,226-242) --------------- */
 
-/* Per-stage device times (ms, CUDA events) of the last chain/forward/backward
- * call when timing is enabled: stage order = stage, motion, sort, splat, loss,
- * backward, flows_backward. Returns the number of stages written. */
+/* Per-stage device times (ms, CUDA events on the engine stream) of the last
+ * chain / forward / backward call when timing is enabled. Stage order:
+ * 0 staging (H2D + validation), 1 motion field, 2 stack memset, 3 warp+splat,
+ * 4 loss reduce, 5 grad memset, 6 backward, 7 flows backward (0 if the call
+ * did not run the stage). Returns the number of stages written (8). */
 EVCM_API int evcm_cuda_set_timing(evcm_cuda_engine* e, int enabled);
 EVCM_API int evcm_cuda_stage_times(evcm_cuda_engine* e, double* ms, int max_stages);
 /* Number of kernels launched by the last API call (for bench gpu_launches). */

@@ -138,6 +138,8 @@ struct evcm_cuda_engine {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::unordered_map<std::string, Buf> bufs;
+  std::unordered_map<std::string, Buf> pins;  // pinned host staging
+  int stage_nw = 0;
   // state of the last forward (Engine::forward -> backward hand-off)
   bool have_fwd = false;
   WinParams P{};
@@ -160,6 +162,19 @@ struct evcm_cuda_engine {
     return static_cast<T*>(b.p);
   }
 
+  template <typename T>
+  T* pinned(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    Buf& b = pins[name];
+    if (b.cap < bytes) {
+      if (b.p) ck(cudaFreeHost(b.p), "cudaFreeHost");
+      b.p = nullptr;
+      ck(cudaMallocHost(&b.p, bytes), "cudaMallocHost");
+      b.cap = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+
   void mark(int i) {
     if (!timing) return;
     while ((int)ev.size() <= i) {
@@ -169,19 +184,25 @@ struct evcm_cuda_engine {
     }
     ck(cudaEventRecord(ev[i], stream), "cudaEventRecord");
   }
-  void collect(int n_marks) {
-    stage_ms.clear();
+  // stage_ms[i] = time between marks i and i+1, for lo <= i < hi (others 0)
+  void collect_range(int lo, int hi) {
+    stage_ms.assign(8, 0.0);
     if (!timing) return;
-    ck(cudaEventSynchronize(ev[n_marks - 1]), "cudaEventSynchronize");
-    for (int i = 1; i < n_marks; ++i) {
+    ck(cudaEventSynchronize(ev[hi]), "cudaEventSynchronize");
+    for (int i = lo; i < hi; ++i) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-      stage_ms.push_back(ms);
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      stage_ms[i] = ms;
     }
   }
 };
 
 namespace {
+
+// Stage marks (CUDA events on the engine stream), see evcm_cuda_stage_times:
+// 0 start | staging | 1 | motion field | 2 | stack memset | 3 | warp+splat | 4 |
+// loss reduce | 5 | grad memset | 6 | backward | 7 | flows backward | 8
+constexpr int M_FWD0 = 2;
 
 void set_device(evcm_cuda_engine* e) { ck(cudaSetDevice(e->opt.device), "cudaSetDevice"); }
 
@@ -257,28 +278,36 @@ const char* code_name(int c) {
   }
 }
 
-// Stage + validate events of n_windows windows (offsets on host). Throws the
-// reference's error for the first invalid event of the first bad window.
+// Stage + validate events of n_windows windows (offsets on host). Asynchronous:
+// the per-window first-violation keys land in pinned host memory and are
+// checked by check_stage_errors() after the call's final stream sync.
 void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off_h, const WinParams& P,
-                  int mem, const evcm_event* ev_host_for_msg) {
+                  int mem) {
   const int nw = P.n_windows;
   const uint64_t total = off_h[nw];
   uint64_t max_n = 0;
   for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, off_h[w + 1] - off_h[w]);
   const evcm_event* dev = to_device(e, "events_aos", ev, total, mem);
+  uint64_t* off_pin = e->pinned<uint64_t>("ev_off_h", nw + 1);
+  std::memcpy(off_pin, off_h, (nw + 1) * sizeof(uint64_t));
   uint64_t* off_d = e->get<uint64_t>("ev_off", nw + 1);
-  ck(cudaMemcpyAsync(off_d, off_h, (nw + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream),
+  ck(cudaMemcpyAsync(off_d, off_pin, (nw + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream),
      "H2D offsets");
   uint2* packed = e->get<uint2>("packed", total);
   unsigned long long* err = e->get<unsigned long long>("stage_err", nw);
   ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
   launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
-  std::vector<unsigned long long> h(nw);
-  ck(cudaMemcpyAsync(h.data(), err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     e->stream),
+  unsigned long long* err_h = e->pinned<unsigned long long>("stage_err_h", nw);
+  ck(cudaMemcpyAsync(err_h, err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream),
      "D2H err");
-  ck(cudaStreamSynchronize(e->stream), "stage");
-  for (int w = 0; w < nw; ++w) {
+  e->stage_nw = nw;
+}
+
+// After the stream sync: raise the reference's error for the first invalid
+// event of the first bad window (EventSlice::validate order, types.hpp:143-155).
+void check_stage_errors(evcm_cuda_engine* e) {
+  const unsigned long long* h = e->pinned<unsigned long long>("stage_err_h", e->stage_nw);
+  for (int w = 0; w < e->stage_nw; ++w) {
     if (h[w] == ~0ull) continue;
     const int code = static_cast<int>(h[w] & 0xf);
     const uint64_t k = h[w] >> 4;
@@ -289,20 +318,29 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
       case 5: msg = "event slice: timestamps must be non-decreasing"; break;
       default: msg = "event slice: timestamp outside the window"; break;
     }
-    (void)ev_host_for_msg;
     fail(code, msg + " (window " + std::to_string(w) + ", event " + std::to_string(k) + ")");
   }
 }
 
-// Pose table per (window, bin): R[9], dR[27], t[3], inv_dt (host-built).
+void sync_and_check(evcm_cuda_engine* e, const char* what) {
+  ck(cudaStreamSynchronize(e->stream), what);
+  check_stage_errors(e);
+  ck(cudaGetLastError(), what);
+}
+
+// Pose table per (window, bin): R[9], dR[27], t[3], inv_dt, built on the host
+// with the reference's rodrigues / rodrigues_jacobian (bit-identical R) and
+// copied from a pinned staging buffer (no sync needed: every API call ends
+// with a stream sync before the buffer is rewritten).
 const double* upload_pose_table(evcm_cuda_engine* e, const double* poses_h, int nw, int B,
-                                const uint64_t* edges) {
-  std::vector<double> tab(static_cast<size_t>(nw) * B * kPoseTab);
+                                const uint64_t* edges, bool validate) {
+  const size_t n = static_cast<size_t>(nw) * B * kPoseTab;
+  double* tab = e->pinned<double>("pose_tab_h", n);
   for (int w = 0; w < nw; ++w)
     for (int b = 0; b < B; ++b) {
       const double* p = poses_h + (static_cast<size_t>(w) * B + b) * 6;
-      validate_pose(p);
-      double* t = tab.data() + (static_cast<size_t>(w) * B + b) * kPoseTab;
+      if (validate) validate_pose(p);
+      double* t = tab + (static_cast<size_t>(w) * B + b) * kPoseTab;
       const M3 R = rodrigues(p);
       M3 dR[3];
       rodrigues_jacobian(p, dR);
@@ -314,11 +352,8 @@ const double* upload_pose_table(evcm_cuda_engine* e, const double* poses_h, int 
       const double dur = (static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6;
       t[39] = 1.0 / dur;
     }
-  double* d = e->get<double>("pose_tab", tab.size());
-  ck(cudaMemcpyAsync(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream),
-     "H2D pose table");
-  // tab must outlive the async copy
-  ck(cudaStreamSynchronize(e->stream), "pose table");
+  double* d = e->get<double>("pose_tab", n);
+  ck(cudaMemcpyAsync(d, tab, n * sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D pose table");
   return d;
 }
 
@@ -326,11 +361,12 @@ template <typename S2>
 void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
   const size_t R = P.B + 1;
   S2* stack = e->get<S2>("stack", (size_t)P.n_windows * R * 2 * P.HW);
+  e->mark(M_FWD0);
   ck(cudaMemsetAsync(stack, 0, (size_t)P.n_windows * R * 2 * P.HW * sizeof(S2), e->stream), "memset");
-  e->mark(2);
+  e->mark(M_FWD0 + 1);
   launch_fwd_splat<S2>(e->stream, e->get<uint2>("packed", 1), e->get<uint64_t>("ev_off", 1), P, max_n,
                        flows, stack);
-  e->mark(3);
+  e->mark(M_FWD0 + 2);
   const int parts = loss_parts(P);
   const size_t np = (size_t)P.n_windows * R * parts;
   launch_loss<S2>(e->stream, stack, P, e->get<S2>("coef", (size_t)P.n_windows * R * 2 * P.HW),
@@ -338,7 +374,7 @@ void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, cons
                   e->get<double>("loss", P.n_windows), e->get<int>("no_surv", P.n_windows),
                   e->get<long long>("n_active", (size_t)P.n_windows * R),
                   e->get<double>("scale", (size_t)P.n_windows * R));
-  e->mark(4);
+  e->mark(M_FWD0 + 3);
 }
 
 void run_forward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
@@ -350,9 +386,11 @@ template <typename C2, typename G2>
 void* run_backward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
   G2* grad = e->get<G2>("grad", (size_t)P.n_windows * P.B * P.HW);
   ck(cudaMemsetAsync(grad, 0, (size_t)P.n_windows * P.B * P.HW * sizeof(G2), e->stream), "memset");
+  e->mark(M_FWD0 + 4);
   launch_bwd<C2, G2>(e->stream, e->get<uint2>("packed", 1), e->get<uint64_t>("ev_off", 1), P, max_n,
                      flows, e->get<C2>("coef", 1), e->get<double>("scale", 1),
                      e->get<int>("no_surv", 1), grad);
+  e->mark(M_FWD0 + 5);
   return grad;
 }
 
@@ -380,8 +418,13 @@ const double2* prepare_window(evcm_cuda_engine* e, const evcm_slice* s, const ev
   P0.t_end = s->t_end_us;
   const uint64_t off[2] = {0, s->n_events};
   if (s->n_events >= (1ull << 32)) fail(EVCM_ERR_CONFIG, "cuda backend: more than 2^32 events");
-  stage_events(e, s->events, off, P0, mem, nullptr);
-  check_flows(s, f);
+  stage_events(e, s->events, off, P0, mem);
+  try {
+    check_flows(s, f);
+  } catch (const Failure&) {
+    sync_and_check(e, "stage");  // event errors take precedence (engine.hpp:216-217)
+    throw;
+  }
   WinParams P = make_params(s->width, s->height, f->edges_us, f->n_bins, 1, s->t_start_us, s->t_end_us);
   const size_t nf = (size_t)f->n_bins * 2 * P.HW;
   const double* uv = to_device(e, "flows_planar", f->uv, nf, mem);
@@ -442,6 +485,8 @@ void evcm_cuda_destroy(evcm_cuda_engine* e) {
   if (e->stream) cudaStreamSynchronize(e->stream);
   for (auto& kv : e->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& kv : e->pins)
+    if (kv.second.p) cudaFreeHost(kv.second.p);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   if (e->own_stream) cudaStreamDestroy(e->stream);
   delete e;
@@ -486,9 +531,8 @@ int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows
     int ns = 0;
     ck(cudaMemcpyAsync(&l, e->get<double>("loss", 1), sizeof l, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaMemcpyAsync(&ns, e->get<int>("no_surv", 1), sizeof ns, cudaMemcpyDeviceToHost, e->stream), "D2H");
-    ck(cudaStreamSynchronize(e->stream), "forward");
-    e->collect(5);
-    ck(cudaGetLastError(), "forward kernels");
+    sync_and_check(e, "forward");
+    e->collect_range(0, M_FWD0 + 3);
     if (loss) {
       loss->value = l;
       loss->no_survivors = ns;
@@ -557,9 +601,8 @@ int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flow
         e->P.B != f->n_bins)
       fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
     const WinParams& P = e->P;
-    e->mark(0);
+    e->mark(M_FWD0 + 3);
     void* g = run_backward(e, P, s->n_events, e->get<double2>("flows", 1));
-    e->mark(1);
     double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
     if (e->opt.grad_f64)
       launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
@@ -567,7 +610,7 @@ int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flow
       launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
     from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
     ck(cudaStreamSynchronize(e->stream), "backward");
-    e->collect(2);
+    e->collect_range(M_FWD0 + 3, M_FWD0 + 5);
     ck(cudaGetLastError(), "backward kernels");
     e->last_launches = launch_count();
   });
@@ -600,7 +643,7 @@ int evcm_cuda_depth_pose_to_flows(evcm_cuda_engine* e, int W, int H, const doubl
       ph.resize(6 * B);
       ck(cudaMemcpy(ph.data(), poses, 6 * B * sizeof(double), cudaMemcpyDeviceToHost), "D2H poses");
     }
-    const double* tab = upload_pose_table(e, ph.data(), 1, B, edges.data());
+    const double* tab = upload_pose_table(e, ph.data(), 1, B, edges.data(), true);
     const double* dd = to_device(e, "depth", depth, (size_t)P.HW, mem);
     const uint8_t* md = mask ? to_device(e, "mask", mask, (size_t)P.HW, mem) : nullptr;
     double2* fl = e->get<double2>("flows", (size_t)B * P.HW);
@@ -611,8 +654,8 @@ int evcm_cuda_depth_pose_to_flows(evcm_cuda_engine* e, int W, int H, const doubl
     from_device(e, flows_out, planar, (size_t)B * 2 * P.HW * sizeof(double), mem);
     if (valid) from_device(e, valid, vd, (size_t)B * P.HW, mem);
     if (edges_out) std::memcpy(edges_out, edges.data(), (B + 1) * sizeof(uint64_t));
-    ck(cudaStreamSynchronize(e->stream), "depth_pose_to_flows");
-    ck(cudaGetLastError(), "motion field");
+    e->stage_nw = 0;
+    sync_and_check(e, "depth_pose_to_flows");
     e->last_launches = launch_count();
   });
 }
@@ -634,23 +677,8 @@ int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, co
       ck(cudaMemcpy(ph.data(), poses, 6 * B * sizeof(double), cudaMemcpyDeviceToHost), "D2H poses");
     else
       std::memcpy(ph.data(), poses, 6 * B * sizeof(double));
-    // rodrigues_jacobian for the backward; geometry.hpp:293-296 does not
-    // re-validate poses, so no validation error here either.
-    std::vector<double> tab((size_t)B * kPoseTab);
-    for (int b = 0; b < B; ++b) {
-      double* t = tab.data() + (size_t)b * kPoseTab;
-      const M3 R = rodrigues(&ph[6 * b]);
-      M3 dR[3];
-      rodrigues_jacobian(&ph[6 * b], dR);
-      std::memcpy(t, R.m, sizeof R.m);
-      for (int k = 0; k < 3; ++k) std::memcpy(t + 9 + 9 * k, dR[k].m, sizeof dR[k].m);
-      t[36] = ph[6 * b + 3];
-      t[37] = ph[6 * b + 4];
-      t[38] = ph[6 * b + 5];
-      t[39] = 1.0 / ((static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6);
-    }
-    double* tab_d = e->get<double>("pose_tab", tab.size());
-    ck(cudaMemcpyAsync(tab_d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D");
+    // geometry.hpp:293-296 does not re-validate poses, so neither do we.
+    const double* tab_d = upload_pose_table(e, ph.data(), 1, B, edges, false);
     const double* dd = to_device(e, "depth", depth, (size_t)P.HW, mem);
     const uint8_t* md = mask ? to_device(e, "mask", mask, (size_t)P.HW, mem) : nullptr;
     const double* gp = to_device(e, "grad_planar_in", grad, (size_t)B * 2 * P.HW, mem);
@@ -662,13 +690,14 @@ int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, co
     launch_flows_bwd<double2>(e->stream, dd, md, tab_d, P, K, g2, ddo, pp, dpo);
     from_device(e, d_depth, ddo, (size_t)P.HW * sizeof(double), mem);
     from_device(e, d_poses, dpo, (size_t)B * 6 * sizeof(double), mem);
-    ck(cudaStreamSynchronize(e->stream), "flows backward");
-    ck(cudaGetLastError(), "flows backward kernels");
+    e->stage_nw = 0;
+    sync_and_check(e, "flows backward");
     e->last_launches = launch_count();
   });
 }
 
-int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
+int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
+                           evcm_chain_out* out) {
   return guarded([&] {
     if (!e || !bt || !out) fail(EVCM_ERR_CONFIG, "null argument");
     set_device(e);
@@ -676,47 +705,53 @@ int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int m
     const int nw = bt->n_windows, B = bt->n_bins, W = bt->width, H = bt->height;
     if (nw < 1) fail(EVCM_ERR_CONFIG, "chain: need at least one window");
     if (W <= 0 || H <= 0 || W > 65535 || H > 65535) fail(EVCM_ERR_DIMENSION, "chain: bad sensor size");
-    if (bt->t_end_us - bt->t_start_us >= (1ull << 31))
-      fail(EVCM_ERR_CONFIG, "cuda backend: window longer than 2^31 us");
+    if (bt->t_end_us <= bt->t_start_us || bt->t_end_us - bt->t_start_us >= (1ull << 31))
+      fail(EVCM_ERR_CONFIG, "chain: window must be nonempty and shorter than 2^31 us");
     const std::vector<uint64_t> edges = zeros_edges(bt->t_start_us, bt->t_end_us, B);
     WinParams P = make_params(W, H, edges.data(), B, nw, bt->t_start_us, bt->t_end_us);
     e->have_fwd = false;
     e->mark(0);
-    // poses are needed on the host for the rotation tables
-    std::vector<double> ph((size_t)nw * B * 6);
-    if (mem == EVCM_MEM_DEVICE)
-      ck(cudaMemcpyAsync(ph.data(), bt->poses, ph.size() * sizeof(double), cudaMemcpyDeviceToHost, e->stream), "D2H poses");
-    else
-      std::memcpy(ph.data(), bt->poses, ph.size() * sizeof(double));
-    ck(cudaStreamSynchronize(e->stream), "poses");
-    const double* tab = upload_pose_table(e, ph.data(), nw, B, edges.data());
+    // Rotation tables are built on the host (bit-identical to the reference's
+    // rodrigues); device-resident poses are read back first (nw*B*48 bytes).
+    const size_t np = (size_t)nw * B * 6;
+    double* ph = e->pinned<double>("poses_h", np);
+    if (in_mem == EVCM_MEM_DEVICE) {
+      ck(cudaMemcpyAsync(ph, bt->poses, np * sizeof(double), cudaMemcpyDeviceToHost, e->stream), "D2H poses");
+      ck(cudaStreamSynchronize(e->stream), "poses");
+    } else {
+      std::memcpy(ph, bt->poses, np * sizeof(double));
+    }
+    const double* tab = upload_pose_table(e, ph, nw, B, edges.data(), true);
     uint64_t max_n = 0;
     for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, bt->ev_offsets[w + 1] - bt->ev_offsets[w]);
-    stage_events(e, bt->events, bt->ev_offsets, P, mem, nullptr);
-    const double* depth = to_device(e, "depth", bt->depth, (size_t)nw * P.HW, mem);
+    stage_events(e, bt->events, bt->ev_offsets, P, in_mem);
+    const double* depth = to_device(e, "depth", bt->depth, (size_t)nw * P.HW, in_mem);
     double2* flows = e->get<double2>("flows", (size_t)nw * B * P.HW);
     e->mark(1);
     launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr);
-    run_forward(e, P, max_n, flows);  // marks 2,3,4
+    run_forward(e, P, max_n, flows);
     void* g = run_backward(e, P, max_n, flows);
-    e->mark(5);
-    double* ddo = (mem == EVCM_MEM_DEVICE && out->d_depth) ? out->d_depth : e->get<double>("d_depth", (size_t)nw * P.HW);
-    double* dpo = (mem == EVCM_MEM_DEVICE && out->d_poses) ? out->d_poses : e->get<double>("d_poses", (size_t)nw * B * 6);
+    const bool direct = out_mem == EVCM_MEM_DEVICE;
+    double* ddo = (direct && out->d_depth) ? out->d_depth : e->get<double>("d_depth", (size_t)nw * P.HW);
+    double* dpo = (direct && out->d_poses) ? out->d_poses : e->get<double>("d_poses", (size_t)nw * B * 6);
     double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * 6);
     if (e->opt.grad_f64)
       launch_flows_bwd<double2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<double2*>(g), ddo, pp, dpo);
     else
       launch_flows_bwd<float2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<float2*>(g), ddo, pp, dpo);
-    e->mark(6);
-    if (out->loss) from_device(e, out->loss, e->get<double>("loss", nw), nw * sizeof(double), mem);
-    if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), mem);
-    if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), mem);
-    if (out->d_poses && dpo != out->d_poses) from_device(e, out->d_poses, dpo, (size_t)nw * B * 6 * sizeof(double), mem);
-    ck(cudaStreamSynchronize(e->stream), "chain");
-    e->collect(7);
-    ck(cudaGetLastError(), "chain kernels");
+    e->mark(M_FWD0 + 6);
+    if (out->loss) from_device(e, out->loss, e->get<double>("loss", nw), nw * sizeof(double), out_mem);
+    if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), out_mem);
+    if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), out_mem);
+    if (out->d_poses && dpo != out->d_poses) from_device(e, out->d_poses, dpo, (size_t)nw * B * 6 * sizeof(double), out_mem);
+    sync_and_check(e, "chain");
+    e->collect_range(0, M_FWD0 + 6);
     e->last_launches = launch_count();
   });
+}
+
+int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
+  return evcm_cuda_chain_batch2(e, bt, mem, mem, out);
 }
 
 }  // extern "C"

@@ -148,6 +148,7 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_depth_pose_to_flows_backward.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, vp,
                                                          vp, i32, vp, vp]
     L.evcm_cuda_chain_batch.argtypes = [vp, vp, i32, vp]
+    L.evcm_cuda_chain_batch2.argtypes = [vp, vp, i32, i32, vp]
     L.evcm_cuda_set_timing.argtypes = [vp, i32]
     L.evcm_cuda_stage_times.argtypes = [vp, vp, i32]
     L.evcm_cuda_last_launch_count.argtypes = [vp]
@@ -521,32 +522,46 @@ class Engine:
         return depth_pose_to_flows_backward(depth, poses, k, flows, grad, mask=mask, engine=self)
 
     # -- batched chain (optimize.hpp:205-241 composition over many windows)
-    def chain_batch(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out=None):
+    def chain_batch(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out=None,
+                    out_device=None):
         """Per window w: depth_pose_to_flows(depth[w], poses[w]) -> forward ->
-        backward -> depth_pose_to_flows_backward. Returns (loss [n], d_depth
-        [n, H, W], d_poses [n, B, 6]); device (torch) in -> device out."""
+        backward -> depth_pose_to_flows_backward (the predictor_loss_and_gradients
+        composition, optimize.hpp:205-241, without decode / L_geo).
+
+        depth [n, H, W] f64, poses [n, B, 6] f64, events concatenated (evcm::Event
+        records), ev_offsets [n+1] (host). Returns (loss [n], d_depth [n, H, W],
+        d_poses [n, B, 6]). Inputs may be host (numpy / pinned torch) or device
+        (torch cuda); outputs live on the device when ``out_device`` (default:
+        same side as the inputs)."""
         nw, H, W = depth.shape
         B = poses.shape[1]
-        mem = _mem_of(depth, poses, events)
+        in_mem = _mem_of(depth, poses, events)
+        if out_device is None:
+            out_device = in_mem == MEM_DEVICE
+        out_mem = MEM_DEVICE if out_device else MEM_HOST
         K = k.as_array() if isinstance(k, CameraIntrinsics) else np.asarray(k, np.float64)
         offs = np.ascontiguousarray(ev_offsets, np.uint64)
         if out is None:
-            if mem == MEM_DEVICE:
+            if out_mem == MEM_DEVICE:
                 import torch
-                dev = depth.device
+                dev = depth.device if in_mem == MEM_DEVICE else torch.device("cuda", self.opts.device)
                 out = (torch.empty(nw, dtype=torch.float64, device=dev),
                        torch.empty((nw, H, W), dtype=torch.float64, device=dev),
                        torch.empty((nw, B, 6), dtype=torch.float64, device=dev))
             else:
                 out = (np.zeros(nw), np.zeros((nw, H, W)), np.zeros((nw, B, 6)))
-        if mem == MEM_HOST:
-            depth = np.ascontiguousarray(depth, np.float64)
-            poses = np.ascontiguousarray(poses, np.float64)
-            events = np.ascontiguousarray(events, EVENT_DTYPE)
+        if in_mem == MEM_HOST:
+            if not _is_torch(depth):
+                depth = np.ascontiguousarray(depth, np.float64)
+            if not _is_torch(poses):
+                poses = np.ascontiguousarray(poses, np.float64)
+            if not _is_torch(events):
+                events = np.ascontiguousarray(events, EVENT_DTYPE)
         bt = _ChainBatch(nw, W, H, B, int(t_start_us), int(t_end_us), (C.c_double * 4)(*K),
                          _ptr(events), offs.ctypes.data_as(C.c_void_p), _ptr(depth), _ptr(poses))
         co = _ChainOut(_ptr(out[0]), None, _ptr(out[1]), _ptr(out[2]))
-        _raise(load_library().evcm_cuda_chain_batch(self._h, C.byref(bt), mem, C.byref(co)))
+        _raise(load_library().evcm_cuda_chain_batch2(self._h, C.byref(bt), in_mem, out_mem,
+                                                     C.byref(co)))
         return out
 
 
