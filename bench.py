@@ -90,19 +90,22 @@ def algorithmic_bytes(wl, n_windows):
     Returns total and the per-kernel split used by the roofline object."""
     B, HW, n = wl["B"], wl["W"] * wl["H"], wl["n_events"]
     sd, sf, ss, sg = 8, 8, 8, 4
+    # each model term is attributed to the kernel that implements that stage of
+    # the reference; fused kernels carry the terms of every stage they absorb
     per = {
-        "motion_field": HW * (sd + 2 * B * sf),
-        "warp_splat": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),
-        "loss_reduce": HW * 4 * (B + 1) * ss,
-        "backward": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss + 2 * B * sg),
-        "flows_backward": HW * (2 * B * sg + 2 * sd),
+        "motion_field": HW * (sd + 2 * B * sf),                       # K1
+        "traj_records": n * 9 + HW * 2 * B * sf,                      # K2 (warp)
+        "fwd_owner": HW * 8 * (B + 1) * ss,                           # K3 write + K3b read
+        "bwd_event": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),    # K4 gathers
+        "bwd_owner": HW * (4 * B * sg + 2 * sd),                      # K4 grad write + K5
     }
     per = {k: v * n_windows for k, v in per.items()}
     return sum(per.values()), per
 
 
-STAGES = ["staging", "motion_field", "stack_memset", "warp_splat", "loss_reduce",
-          "grad_memset", "backward", "flows_backward"]
+# evcm_cuda_stage_times order for the default (owner-computes) pipeline
+STAGES = ["staging_sort", "motion_field", "traj_records", "fwd_owner", "loss_finalize",
+          "bwd_event", "bwd_owner", "pose_finalize"]
 
 
 # ---------------------------------------------------------------------------

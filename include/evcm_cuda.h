@@ -95,6 +95,9 @@ typedef struct {
   int grad_f64;        /* 1: fp64 flow-gradient accumulators (default 0: fp32, which
                           keeps gradients within ~1e-7 of the reference) */
   void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
+  int algo;            /* 0 (default): owner-computes tiles (deterministic, no global
+                          atomics); 1: per-event global atomics (reference-order-free
+                          cross-check path, honours stack_f64 / grad_f64) */
 } evcm_cuda_options;
 
 /* EventSlice (types.hpp:121-126). */

@@ -27,6 +27,7 @@ namespace evcm_b200 {
 
 static thread_local int g_launches = 0;
 void reset_launch_count() { g_launches = 0; }
+void count_launch() { ++g_launches; }
 int launch_count() { return g_launches; }
 
 // --------------------------------------------------------------------------
@@ -578,6 +579,21 @@ void launch_fwd_splat(cudaStream_t s, const uint2* packed, const uint64_t* ev_of
   ++g_launches;
   k_fwd_splat<S2><<<dim3(blocks, P.n_windows), kEvBlock, ev_smem_bytes(P), s>>>(packed, ev_off, P,
                                                                              flows, stack);
+}
+
+void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned long long* part_act,
+                          int n_parts, const WinParams& P, double* loss, int* no_surv,
+                          long long* n_active, double* scale) {
+  ++g_launches;
+  k_loss_finalize<<<(P.n_windows + 63) / 64, 64, 0, s>>>(part_acc, part_act, n_parts, P, loss,
+                                                        no_surv, n_active, scale);
+}
+
+void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
+                          int n_windows, double* d_poses) {
+  const int total = n_windows * B * 6;
+  ++g_launches;
+  k_pose_finalize<<<(total + 127) / 128, 128, 0, s>>>(pose_part, n_parts, B, n_windows, d_poses);
 }
 
 int loss_parts(const WinParams& P) { return std::max(1, std::min((P.HW + kPxBlock - 1) / kPxBlock, 64)); }

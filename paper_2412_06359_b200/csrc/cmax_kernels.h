@@ -16,6 +16,12 @@ constexpr int kPoseTab = 40;         // R[9], dR[27], t[3], inv_dt per (window, 
 constexpr size_t kEvSmemHeader = 512;  // es + erel tables ahead of the position columns
 
 void reset_launch_count();
+void count_launch();
+void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned long long* part_act,
+                          int n_parts, const WinParams& P, double* loss, int* no_surv,
+                          long long* n_active, double* scale);
+void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
+                          int n_windows, double* d_poses);
 int launch_count();
 
 size_t ev_smem_bytes(const WinParams& P);

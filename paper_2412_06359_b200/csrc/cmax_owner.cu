@@ -1,0 +1,801 @@
+// Owner-computes CMax pipeline (sm_100a): no global atomics on the IWE stack
+// or the flow gradients, no memsets of them, loss/coefficients fused into the
+// splat, flows-backward fused into the gradient gather. See DESIGN.md §Kernels.
+//
+//   k_stage_hist    validate + pack events (8 B) + per-(tile, chunk) histogram
+//   k_sort_scan     exclusive scan of the histogram -> stable slots per tile
+//   k_sort_scatter  stable counting sort of the events by source tile (16x16 px)
+//   k_bin_ptr       per source tile: first event of every time bin
+//   k_traj_records  trajectory (warp.hpp:257-281, exact fp64) -> per (event, ref)
+//                   splat record {cell, pol, dt, compressed bilinear fractions}
+//                   + per (source tile, ref) bounding box of the cells
+//   k_fwd_owner     one warp per (window, owner tile, ref): gathers every record
+//                   landing on its 16x16 tile (sources found through the boxes),
+//                   accumulates count/tsum in fp64 shared memory in a fixed order,
+//                   then writes the per-pixel loss coefficients and the loss /
+//                   n_active partials (IweStack + reference_loss + refresh_active)
+//   k_bwd_event     per event: splat_position_grad at every reference + the
+//                   adjoint sweep (engine.hpp:475-504) -> one (gx, gy) per bin
+//   k_bwd_owner     one warp per (window, owner tile): for every bin gathers the
+//                   (gx, gy) of all events whose sink cell touches the tile
+//                   (BufferGradSink::add, warp.hpp:394-406), then applies
+//                   depth_pose_to_flows_backward (geometry.hpp:300-322) to the
+//                   finished gradient tile: d_depth and pose partials.
+//
+// Determinism: the sort is stable, owners visit sources in index order and
+// events in sorted order, lanes resolve shared-pixel conflicts in lane order,
+// and every partial sum is reduced in a fixed order -> bit-stable run to run.
+#include <cstdint>
+
+#include "cmax_device.cuh"
+#include "cmax_kernels.h"
+#include "cmax_owner.h"
+
+namespace evcm_b200 {
+
+void count_launch();  // cmax_kernels.cu
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kDead = 0xffffffffu;
+constexpr int kListCap = 128;  // sources buffered per owner scan round
+
+__device__ __forceinline__ int tile_of(int x, int y, int ntx) {
+  return (y / kTile) * ntx + (x / kTile);
+}
+
+// Bilinear fractions compressed to one float each with full relative precision
+// on the smaller of (w, 1-w): f = w if w < 0.5 else -(1-w) (sign bit marks the
+// second form, so -0.0 encodes w = 1).
+__device__ __forceinline__ float compress_frac(double w) {
+  return w < 0.5 ? (float)w : -(float)(1.0 - w);
+}
+__device__ __forceinline__ void expand_frac(float f, double& w, double& a) {
+  if (signbit(f)) {
+    a = -(double)f;
+    w = 1.0 - a;
+  } else {
+    w = (double)f;
+    a = 1.0 - w;
+  }
+}
+
+struct CellW {
+  int x0, y0;
+  double wx, wy, ax, ay;  // ax = 1 - wx, ay = 1 - wy
+};
+
+__device__ __forceinline__ CellW decode(const FwdRec& r) {
+  CellW c;
+  c.x0 = (int)(r.cell & 0xffffu);
+  c.y0 = (int)((r.cell >> 16) & 0x7fffu);
+  expand_frac(r.fx, c.wx, c.ax);
+  expand_frac(r.fy, c.wy, c.ay);
+  return c;
+}
+
+// Lane-ordered accumulation of (v0, v1) into a warp-private shared tile:
+// lanes sharing `key` are summed in lane order by the lowest lane, which then
+// does a plain read-modify-write. key < 0: no contribution.
+__device__ __forceinline__ void warp_accumulate2(double* base, int key, double v0, double v1) {
+  const unsigned act = __ballot_sync(kFull, key >= 0);
+  if (key >= 0) {
+    const unsigned peers = __match_any_sync(act, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    double s0 = 0.0, s1 = 0.0;
+    if (lane == leader) {
+      s0 = base[2 * key];
+      s1 = base[2 * key + 1];
+    }
+    unsigned m = peers;
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const double a = __shfl_sync(peers, v0, src);
+      const double b = __shfl_sync(peers, v1, src);
+      s0 += a;
+      s1 += b;
+    }
+    if (lane == leader) {
+      base[2 * key] = s0;
+      base[2 * key + 1] = s1;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Scan the source boxes of reference r for window w and call fn(S) for every
+// source tile whose cells can touch owner tile (tx0, ty0), in increasing S.
+template <typename Fn>
+__device__ __forceinline__ void for_each_source(const uint4* __restrict__ bbox, int nT, int tx0,
+                                                int ty0, uint16_t* list, Fn&& fn) {
+  const int lane = threadIdx.x & 31;
+  const int lx = tx0 - 1, hx = tx0 + kTile - 1, ly = ty0 - 1, hy = ty0 + kTile - 1;
+  int fill = 0;
+  for (int s0 = 0; s0 < nT; s0 += 32) {
+    const int S = s0 + lane;
+    bool hit = false;
+    if (S < nT) {
+      const uint4 b = __ldg(bbox + S);
+      if (b.x != 0xffffffffu) {
+        const int mnx = (int)b.x, mny = (int)b.y;
+        const int mxx = 0xffff - (int)b.z, mxy = 0xffff - (int)b.w;
+        hit = !(mxx < lx || mnx > hx || mxy < ly || mny > hy);
+      }
+    }
+    const unsigned hits = __ballot_sync(kFull, hit);
+    if (hit) list[fill + __popc(hits & ((1u << lane) - 1u))] = (uint16_t)S;
+    fill += __popc(hits);
+    if (fill > kListCap - 32 || s0 + 32 >= nT) {
+      __syncwarp();
+      for (int i = 0; i < fill; ++i) fn((int)list[i]);
+      __syncwarp();
+      fill = 0;
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// sort
+
+__global__ void __launch_bounds__(kSortThreads) k_stage_hist(
+    const evcm_event* __restrict__ ev, const uint64_t* __restrict__ ev_off, WinParams P,
+    TileParams TP, uint2* __restrict__ packed, uint32_t* __restrict__ counts,
+    unsigned long long* __restrict__ err) {
+  extern __shared__ uint32_t hist[];
+  for (int i = threadIdx.x; i < TP.nT; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int w = blockIdx.y;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
+  const uint64_t c1 = c0 + kChunk < n ? c0 + kChunk : n;
+  for (uint64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const evcm_event e = ev[base + k];
+    unsigned code = 0;
+    if (e.x >= P.W || e.y >= P.H) code = 3;
+    else if (e.p != 1 && e.p != -1) code = 4;
+    else if (k > 0 && e.t_us < ev[base + k - 1].t_us) code = 5;
+    else if (e.t_us < P.t0 || e.t_us >= P.t_end) code = 6;
+    if (code) {
+      atomicMin(err + w, ((unsigned long long)k << 4) | code);
+      packed[base + k] = make_uint2(kDead, kDead);
+      continue;
+    }
+    const uint32_t dt = (uint32_t)(e.t_us - P.t0);
+    packed[base + k] = make_uint2(dt | (e.p > 0 ? 0u : 0x80000000u),
+                                  (uint32_t)e.x | ((uint32_t)e.y << 16));
+    atomicAdd(&hist[tile_of(e.x, e.y, TP.ntx)], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x)
+    counts[((size_t)w * TP.nT + t) * TP.nchunks + blockIdx.x] = hist[t];
+}
+
+// Exclusive scan of counts[w][tile][chunk] (tile-major) in place; tile_ptr[w][t]
+// = first sorted slot of tile t, tile_ptr[w][nT] = valid events of the window.
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ counts, TileParams TP,
+                                                    uint32_t* __restrict__ tile_ptr) {
+  __shared__ uint32_t warp_tot[32];
+  const int w = blockIdx.x;
+  const size_t E = (size_t)TP.nT * TP.nchunks;
+  uint32_t* c = counts + (size_t)w * E;
+  const size_t per = (E + blockDim.x - 1) / blockDim.x;
+  const size_t lo = threadIdx.x * per, hi = lo + per < E ? lo + per : E;
+  uint32_t sum = 0;
+  for (size_t i = lo; i < hi; ++i) sum += c[i];
+  // block exclusive scan of `sum`
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;  // inclusive
+  }
+  __syncthreads();
+  uint32_t run = x - sum + (wid > 0 ? warp_tot[wid - 1] : 0u);
+  uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  for (size_t i = lo; i < hi; ++i) {
+    const uint32_t v = c[i];
+    c[i] = run;
+    if (i % TP.nchunks == 0) tp[i / TP.nchunks] = run;
+    run += v;
+  }
+  if (threadIdx.x == blockDim.x - 1) tp[TP.nT] = run;
+}
+
+// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*512, +512).
+__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
+    const uint2* __restrict__ packed, const uint64_t* __restrict__ ev_off, TileParams TP,
+    const uint32_t* __restrict__ offsets, uint2* __restrict__ sorted, uint32_t* __restrict__ perm) {
+  extern __shared__ uint16_t whist[];  // [16 warps][nT]
+  const int nW = kSortThreads / 32;
+  for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
+  __syncthreads();
+  const int w = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t k0 = (uint64_t)blockIdx.x * kChunk + (uint64_t)wid * (kChunk / nW);
+  uint16_t* mine = whist + wid * TP.nT;
+  // pass 1: per-warp tile counts
+  for (int b = 0; b < kChunk / nW; b += 32) {
+    const uint64_t k = k0 + b + lane;
+    int t = -1;
+    if (k < n) {
+      const uint2 e = packed[base + k];
+      if (e.y != kDead) t = tile_of((int)(e.y & 0xffffu), (int)(e.y >> 16), TP.ntx);
+    }
+    const unsigned act = __ballot_sync(kFull, t >= 0);
+    if (t >= 0) {
+      const unsigned peers = __match_any_sync(act, t);
+      if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // pass 2: exclusive prefix over warps, per tile
+  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) {
+    uint16_t run = 0;
+    for (int q = 0; q < nW; ++q) {
+      const uint16_t v = whist[q * TP.nT + t];
+      whist[q * TP.nT + t] = run;
+      run = (uint16_t)(run + v);
+    }
+  }
+  __syncthreads();
+  // pass 3: place in order
+  const uint32_t* off = offsets + (size_t)w * TP.nT * TP.nchunks;
+  for (int b = 0; b < kChunk / nW; b += 32) {
+    const uint64_t k = k0 + b + lane;
+    int t = -1;
+    uint2 e = make_uint2(0, 0);
+    if (k < n) {
+      e = packed[base + k];
+      if (e.y != kDead) t = tile_of((int)(e.y & 0xffffu), (int)(e.y >> 16), TP.ntx);
+    }
+    const unsigned act = __ballot_sync(kFull, t >= 0);
+    if (t >= 0) {
+      const unsigned peers = __match_any_sync(act, t);
+      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+      const uint32_t dst = off[(size_t)t * TP.nchunks + blockIdx.x] + mine[t] + rank;
+      sorted[base + dst] = e;
+      if (perm) perm[base + dst] = (uint32_t)k;
+      __syncwarp(peers);
+      if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+    }
+    __syncwarp();
+  }
+}
+
+// bin_ptr[w][S][b] = first sorted slot of tile S whose event bin is >= b
+// (events are time-ordered inside a tile, so bins are monotone).
+__global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off,
+                          WinParams P, TileParams TP, const uint32_t* __restrict__ tile_ptr,
+                          uint32_t* __restrict__ bin_ptr) {
+  const int w = blockIdx.y;
+  const int S = blockIdx.x * blockDim.x + threadIdx.x;
+  if (S >= TP.nT) return;
+  const uint64_t base = ev_off[w];
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  const uint32_t lo = tp[S], hi = tp[S + 1];
+  uint32_t* out = bin_ptr + ((size_t)w * TP.nT + S) * (P.B + 1);
+  out[0] = lo;
+  out[P.B] = hi;
+  for (int b = 1; b < P.B; ++b) {
+    uint32_t a = lo, z = hi;  // first slot with dt >= erel[b]
+    while (a < z) {
+      const uint32_t m = (a + z) >> 1;
+      if ((sorted[base + m].x & 0x7fffffffu) >= P.erel[b]) z = m; else a = m + 1;
+    }
+    out[b] = a;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// trajectories -> splat records
+
+__global__ void __launch_bounds__(kEvBlock) k_traj_records(
+    const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
+    TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
+    uint64_t n_total, FwdRec* __restrict__ recs, uint4* __restrict__ bbox) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* es = reinterpret_cast<double*>(smem);
+  uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
+  double2* pos = reinterpret_cast<double2*>(smem + kEvSmemHeader) + threadIdx.x;
+  for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
+    es[i] = P.es[i];
+    erel[i] = P.erel[i];
+  }
+  __syncthreads();
+  const int w = blockIdx.y, R = P.B + 1;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = tile_ptr[(size_t)w * (TP.nT + 1) + TP.nT];  // valid (sorted) events
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = k < n;
+  bool alive = false;
+  uint2 e = make_uint2(0, 0);
+  if (valid) {
+    e = sorted[base + k];
+    const uint32_t dt = ev_dt(e);
+    const double t = dm((double)dt, 1e-6);
+    const int j = bin_of(dt, erel, P.B);
+    alive = trajectory((double)ev_x(e), (double)ev_y(e), t, j,
+                       flows + (size_t)w * P.B * P.HW, P, es, pos, blockDim.x);
+  }
+  const int S = valid ? tile_of(ev_x(e), ev_y(e), TP.ntx) : -1;
+  const unsigned amask = __ballot_sync(kFull, alive);
+  const unsigned peers = alive ? __match_any_sync(amask, S) : 0u;
+  const bool leader = alive && (threadIdx.x & 31) == __ffs(peers) - 1;
+  for (int r = 0; r < R; ++r) {
+    FwdRec rec;
+    uint32_t x0 = 0, y0 = 0;
+    if (alive) {
+      const double2 p = pos[r * blockDim.x];
+      const Cell c = bilin_cell(p.x, p.y, P.W, P.H);
+      y0 = (uint32_t)(c.i00 / P.W);
+      x0 = (uint32_t)(c.i00 - (int)y0 * P.W);
+      rec.cell = x0 | (y0 << 16) | ((uint32_t)ev_pol(e) << 31);
+      rec.dt = ev_dt(e);
+      rec.fx = compress_frac(c.wx);
+      rec.fy = compress_frac(c.wy);
+    } else {
+      rec.cell = kDead;
+      rec.dt = 0;
+      rec.fx = rec.fy = 0.f;
+    }
+    if (valid) recs[(size_t)r * n_total + base + k] = rec;
+    if (alive) {
+      const uint32_t mnx = __reduce_min_sync(peers, x0), mny = __reduce_min_sync(peers, y0);
+      const uint32_t cmx = __reduce_min_sync(peers, 0xffffu - x0);
+      const uint32_t cmy = __reduce_min_sync(peers, 0xffffu - y0);
+      if (leader) {
+        uint4* b = bbox + ((size_t)w * R + r) * TP.nT + S;
+        atomicMin(&b->x, mnx);
+        atomicMin(&b->y, mny);
+        atomicMin(&b->z, cmx);
+        atomicMin(&b->w, cmy);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward owner: IWE stack tile + loss partials + coefficient planes
+
+__global__ void __launch_bounds__(32) k_fwd_owner(
+    const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
+    const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
+    const uint4* __restrict__ bbox, double2* __restrict__ coef, double2* __restrict__ stack_out,
+    double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
+  __shared__ __align__(16) double acc[kTile * kTile * 4];  // [px][C0,S0,C1,S1]
+  __shared__ uint16_t list[kListCap];
+  const int T = blockIdx.x, r = blockIdx.y, w = blockIdx.z;
+  const int lane = threadIdx.x;
+  const int R = P.B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
+  for (int i = lane; i < kTile * kTile * 4; i += 32) acc[i] = 0.0;
+  __syncwarp();
+  const uint64_t base = ev_off[w];
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  const FwdRec* rr = recs + (size_t)r * n_total + base;
+  const double esr = P.es[r], win = P.window_s;
+  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
+  for_each_source(bbox + ((size_t)w * R + r) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
+    const uint32_t k0 = tp[S], k1 = tp[S + 1];
+    for (uint32_t kb = k0; kb < k1; kb += 32) {
+      const uint32_t k = kb + lane;
+      FwdRec rec;
+      rec.cell = kDead;
+      if (k < k1) rec = rr[k];
+      const bool live = rec.cell != kDead;
+      CellW c{};
+      double tb = 0.0;
+      int pol = 0;
+      if (live) {
+        c = decode(rec);
+        pol = (int)(rec.cell >> 31);
+        tb = dd(fabs(ds(dm((double)rec.dt, 1e-6), esr)), win);  // engine.hpp:370
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int px = c.x0 + ((q & 1) ? ox : 0), py = c.y0 + ((q & 2) ? oy : 0);
+        const double wq = (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy
+                                                                                   : c.wx * c.wy;
+        const int lx = px - tx0, ly = py - ty0;
+        const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
+        warp_accumulate2(acc, in ? ((ly * kTile + lx) * 2 + pol) : -1, wq, wq * tb);
+      }
+    }
+  });
+  __syncwarp();
+  // finalize: refresh_active + reference_loss terms + splat_position_grad factors
+  double lsum = 0.0;
+  unsigned act = 0;
+  double2* cw = coef + ((size_t)w * R + r) * 2 * HW;
+  for (int q = lane; q < kTile * kTile; q += 32) {
+    const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+    if (px >= W || py >= H) continue;
+    const int g = py * W + px;
+    const double C0 = acc[4 * q], S0 = acc[4 * q + 1], C1 = acc[4 * q + 2], S1 = acc[4 * q + 3];
+    act += (C0 + C1 > 0.0) ? 1u : 0u;
+    const double a0 = S0 / (C0 + kLossEps), a1 = S1 / (C1 + kLossEps);
+    lsum += a0 * a0 + a1 * a1;
+    const double i0 = 1.0 / (C0 + kLossEps), i1 = 1.0 / (C1 + kLossEps);
+    const double b0 = S0 * i0, b1 = S1 * i1;
+    cw[g] = make_double2(b0, b0 * i0);
+    cw[HW + g] = make_double2(b1, b1 * i1);
+    if (stack_out) {
+      double2* so = stack_out + ((size_t)w * R + r) * 2 * HW;
+      so[g] = make_double2(C0, S0);
+      so[HW + g] = make_double2(C1, S1);
+    }
+  }
+  lsum = warp_sum(lsum);
+  for (int o = 16; o > 0; o >>= 1) act += __shfl_xor_sync(kFull, act, o);
+  if (lane == 0) {
+    const size_t slot = ((size_t)w * R + r) * TP.nT + T;
+    part_acc[slot] = lsum;
+    part_act[slot] = act;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, per event: d[r] at every reference + adjoint sweep -> (gx, gy) per bin
+
+__device__ __forceinline__ double2 pos_grad_w(const double2* __restrict__ cp, int W, int ox, int oy,
+                                              const CellW& c, double tb, double scale) {
+  const int i00 = c.y0 * W + c.x0;
+  const double2 k00 = __ldg(cp + i00), k10 = __ldg(cp + i00 + ox);
+  const double2 k01 = __ldg(cp + i00 + oy * W), k11 = __ldg(cp + i00 + oy * W + ox);
+  const double g00 = scale * k00.y * (tb - k00.x);
+  const double g10 = scale * k10.y * (tb - k10.x);
+  const double g01 = scale * k01.y * (tb - k01.x);
+  const double g11 = scale * k11.y * (tb - k11.x);
+  return make_double2(-c.ay * g00 + c.ay * g10 - c.wy * g01 + c.wy * g11,
+                      -c.ax * g00 - c.wx * g10 + c.ax * g01 + c.wx * g11);
+}
+
+__global__ void __launch_bounds__(kEvBlock) k_bwd_event(
+    const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
+    TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
+    const FwdRec* __restrict__ recs, uint64_t n_total, const double2* __restrict__ coef,
+    const double* __restrict__ scale_tab, const int* __restrict__ no_surv,
+    float2* __restrict__ bwd) {
+  __shared__ double es[kMaxRefs];
+  __shared__ uint32_t erel[kMaxRefs];
+  for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
+    es[i] = P.es[i];
+    erel[i] = P.erel[i];
+  }
+  __syncthreads();
+  const int w = blockIdx.y;
+  if (no_surv[w]) return;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = tile_ptr[(size_t)w * (TP.nT + 1) + TP.nT];
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const FwdRec* rk = recs + base + k;  // + r * n_total
+  if (rk[0].cell == kDead) return;     // masked event: contributes nothing (engine.hpp:564)
+  const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
+  const uint2 e = sorted[base + k];
+  const uint32_t dt_us = ev_dt(e);
+  const double t = dm((double)dt_us, 1e-6);
+  const int j = bin_of(dt_us, erel, B);
+  const int pol = ev_pol(e);
+  const double2* cpw = coef + ((size_t)w * R * 2 + pol) * HW;  // + r*2*HW
+  const double* sc = scale_tab + (size_t)w * R;
+  const double2* fl = flows + (size_t)w * B * HW;
+  float2* bo = bwd + base + k;  // + i * n_total
+  const double win = P.window_s;
+  auto tb_of = [&](int r) { return dd(fabs(ds(t, es[r])), win); };
+
+  double2 gb, gf;
+  {
+    const CellW c = decode(rk[0]);
+    gb = pos_grad_w(cpw, W, ox, oy, c, tb_of(0), sc[0]);
+  }
+  {
+    const CellW c = decode(rk[(size_t)B * n_total]);
+    gf = pos_grad_w(cpw + (size_t)B * 2 * HW, W, ox, oy, c, tb_of(B), sc[B]);
+  }
+  for (int s = 0; s < B - 1; ++s) {
+    const bool back = s < j;
+    const int i = back ? s : B - 1 - (s - j);
+    const int r = back ? i + 1 : i;
+    const double dt = back ? es[i] - es[i + 1] : es[i + 1] - es[i];
+    const CellW c = decode(rk[(size_t)r * n_total]);
+    const double2 g = back ? gb : gf;
+    bo[(size_t)i * n_total] = make_float2((float)(dt * g.x), (float)(dt * g.y));
+    // (I + dt J_i)^T g + d[r]   (warp.hpp:91-94, engine.hpp:490-491)
+    const int i00 = c.y0 * W + c.x0;
+    const double2* f = fl + (size_t)i * HW;
+    const double2 a = __ldg(f + i00), b = __ldg(f + i00 + ox);
+    const double2 d0 = __ldg(f + i00 + oy * W), d1 = __ldg(f + i00 + oy * W + ox);
+    const double dux = c.ay * (b.x - a.x) + c.wy * (d1.x - d0.x);
+    const double duy = c.ax * (d0.x - a.x) + c.wx * (d1.x - b.x);
+    const double dvx = c.ay * (b.y - a.y) + c.wy * (d1.y - d0.y);
+    const double dvy = c.ax * (d0.y - a.y) + c.wx * (d1.y - b.y);
+    const double2 d = pos_grad_w(cpw + (size_t)r * 2 * HW, W, ox, oy, c, tb_of(r), sc[r]);
+    const double nx = g.x * (1.0 + dt * dux) + g.y * dt * dvx + d.x;
+    const double ny = g.y * (1.0 + dt * dvy) + g.x * dt * duy + d.y;
+    if (back) gb = make_double2(nx, ny); else gf = make_double2(nx, ny);
+  }
+  const double cb = es[j] - t, cf = es[j + 1] - t;
+  bo[(size_t)j * n_total] = make_float2((float)(cb * gb.x + cf * gf.x), (float)(cb * gb.y + cf * gf.y));
+  (void)H;
+}
+
+// ---------------------------------------------------------------------------
+// backward owner: gradient tile per bin + fused depth_pose_to_flows_backward
+
+__global__ void __launch_bounds__(32) k_bwd_owner(
+    const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
+    TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
+    const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
+    const uint4* __restrict__ bbox, const int* __restrict__ no_surv,
+    const double* __restrict__ depth, const uint8_t* __restrict__ mask,
+    const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
+    double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
+  __shared__ __align__(16) double g[kTile * kTile * 2];  // [px][gu, gv]
+  __shared__ uint16_t list[kListCap];
+  const int T = blockIdx.x, w = blockIdx.y, lane = threadIdx.x;
+  const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
+  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
+  const uint64_t base = ev_off[w];
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
+  const bool skip = no_surv[w] != 0;
+
+  // per-lane pixels of the tile (8 per lane) for the fused flows backward
+  constexpr int kPer = kTile * kTile / 32;
+  double dacc[kPer], dep[kPer], rxs[kPer], rys[kPer];
+  bool ok[kPer];
+#pragma unroll
+  for (int m = 0; m < kPer; ++m) {
+    const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+    const bool in = px < W && py < H;
+    const int gq = py * W + px;
+    dacc[m] = 0.0;
+    dep[m] = (in && depth) ? depth[(size_t)w * HW + gq] : 0.0;
+    ok[m] = in && depth && (!mask || mask[(size_t)w * HW + gq]) && dep[m] > 0.0;
+    rxs[m] = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
+    rys[m] = 1.0 * ((double)py - cy) / fy;
+  }
+
+  auto accumulate = [&](const FwdRec& rec, bool live, float2 v) {
+    CellW c{};
+    if (live) c = decode(rec);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int px = c.x0 + ((q & 1) ? ox : 0), py = c.y0 + ((q & 2) ? oy : 0);
+      const double wq = (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy
+                                                                                 : c.wx * c.wy;
+      const int lx = px - tx0, ly = py - ty0;
+      const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
+      warp_accumulate2(g, in ? (ly * kTile + lx) : -1, wq * (double)v.x, wq * (double)v.y);
+    }
+  };
+
+  for (int i = 0; i < B; ++i) {
+    for (int q = lane; q < kTile * kTile * 2; q += 32) g[q] = 0.0;
+    __syncwarp();
+    if (!skip) {
+      const float2* bi = bwd + (size_t)i * n_total + base;
+      // backward leg: events with bin j > i sink at their reference-(i+1) cell
+      {
+        const FwdRec* rr = recs + (size_t)(i + 1) * n_total + base;
+        for_each_source(bbox + ((size_t)w * R + i + 1) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
+          const uint32_t k0 = bp[(size_t)S * (B + 1) + i + 1], k1 = tp[S + 1];
+          for (uint32_t kb = k0; kb < k1; kb += 32) {
+            const uint32_t k = kb + lane;
+            FwdRec rec;
+            rec.cell = kDead;
+            float2 v = make_float2(0.f, 0.f);
+            if (k < k1) {
+              rec = rr[k];
+              if (rec.cell != kDead) v = bi[k];
+            }
+            accumulate(rec, rec.cell != kDead, v);
+          }
+        });
+      }
+      // forward leg: events with bin j < i sink at their reference-i cell
+      {
+        const FwdRec* rr = recs + (size_t)i * n_total + base;
+        for_each_source(bbox + ((size_t)w * R + i) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
+          const uint32_t k0 = tp[S], k1 = bp[(size_t)S * (B + 1) + i];
+          for (uint32_t kb = k0; kb < k1; kb += 32) {
+            const uint32_t k = kb + lane;
+            FwdRec rec;
+            rec.cell = kDead;
+            float2 v = make_float2(0.f, 0.f);
+            if (k < k1) {
+              rec = rr[k];
+              if (rec.cell != kDead) v = bi[k];
+            }
+            accumulate(rec, rec.cell != kDead, v);
+          }
+        });
+      }
+      // partial steps of events of this tile with bin j == i, at their source pixel
+      {
+        const uint32_t k0 = bp[(size_t)T * (B + 1) + i], k1 = bp[(size_t)T * (B + 1) + i + 1];
+        for (uint32_t kb = k0; kb < k1; kb += 32) {
+          const uint32_t k = kb + lane;
+          int key = -1;
+          float2 v = make_float2(0.f, 0.f);
+          if (k < k1 && recs[base + k].cell != kDead) {
+            const uint2 e = sorted[base + k];
+            key = (ev_y(e) - ty0) * kTile + (ev_x(e) - tx0);
+            v = bi[k];
+          }
+          warp_accumulate2(g, key, (double)v.x, (double)v.y);
+        }
+      }
+    }
+    __syncwarp();
+    // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
+    const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
+    double c6[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) {
+      const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+      const double gu = g[2 * q], gv = g[2 * q + 1];
+      if (grad_out && px < W && py < H) {
+        const int gq = py * W + px;
+        grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
+        grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
+      }
+      if (!pt || !ok[m] || (gu == 0.0 && gv == 0.0)) continue;
+      const double d = dep[m], rx = rxs[m], ry = rys[m];
+      const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
+      const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
+      const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
+      const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
+      if (!(p2 > 0.0)) continue;
+      const double inv_dt = pt[39], iz = 1.0 / p2;
+      const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+      const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+      dacc[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+      c6[3] += gu * ju0 * inv_dt;
+      c6[4] += gv * jv1 * inv_dt;
+      c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double* dR = pt + 9 + 9 * a;
+        const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
+        const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
+        const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
+        c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
+      }
+    }
+    if (pt) {
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        const double v = warp_sum(c6[a]);
+        if (lane == 0) pose_part[(((size_t)w * TP.nT + T) * B + i) * 6 + a] = v;
+      }
+    }
+    __syncwarp();
+  }
+  if (d_depth) {
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) {
+      const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+      if (px < W && py < H) d_depth[(size_t)w * HW + py * W + px] = dacc[m];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+TileParams make_tiles(const WinParams& P, uint64_t max_n) {
+  TileParams TP;
+  TP.ntx = (P.W + kTile - 1) / kTile;
+  TP.nty = (P.H + kTile - 1) / kTile;
+  TP.nT = TP.ntx * TP.nty;
+  TP.nchunks = (int)std::max<uint64_t>(1, (max_n + kChunk - 1) / kChunk);
+  return TP;
+}
+
+size_t sort_scatter_smem(const TileParams& TP) { return (size_t)(kSortThreads / 32) * TP.nT * 2; }
+
+void launch_sort(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
+                 const TileParams& TP, uint2* packed, uint32_t* counts, unsigned long long* err,
+                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_stage_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const dim3 grid(TP.nchunks, P.n_windows);
+  count_launch();
+  k_stage_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(ev, ev_off, P, TP, packed,
+                                                                     counts, err);
+  count_launch();
+  k_sort_scan<<<P.n_windows, 1024, 0, s>>>(counts, TP, tile_ptr);
+  count_launch();
+  k_sort_scatter<<<grid, kSortThreads, sort_scatter_smem(TP), s>>>(packed, ev_off, TP, counts,
+                                                                   sorted, perm);
+}
+
+void launch_bin_ptr(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off, const WinParams& P,
+                    const TileParams& TP, const uint32_t* tile_ptr, uint32_t* bin_ptr) {
+  count_launch();
+  k_bin_ptr<<<dim3((TP.nT + 127) / 128, P.n_windows), 128, 0, s>>>(sorted, ev_off, P, TP,
+                                                                    tile_ptr, bin_ptr);
+}
+
+void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                         const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                         uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
+                         uint4* bbox) {
+  if (max_n == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_traj_records, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kEvSmemHeader + sizeof(double2) * (size_t)kMaxRefs * kEvBlock));
+    attr = true;
+  }
+  const size_t smem = kEvSmemHeader + sizeof(double2) * (size_t)(P.B + 1) * kEvBlock;
+  count_launch();
+  k_traj_records<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, smem,
+                   s>>>(sorted, ev_off, P, TP, tile_ptr, flows, n_total, recs, bbox);
+}
+
+void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
+                      const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
+                      uint64_t n_total, const uint4* bbox, double2* coef, double2* stack_out,
+                      double* part_acc, unsigned long long* part_act) {
+  count_launch();
+  k_fwd_owner<<<dim3(TP.nT, P.B + 1, P.n_windows), 32, 0, s>>>(
+      ev_off, P, TP, tile_ptr, recs, n_total, bbox, coef, stack_out, part_acc, part_act);
+}
+
+void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                      uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
+                      const double2* coef, const double* scale, const int* no_surv, float2* bwd) {
+  if (max_n == 0) return;
+  count_launch();
+  k_bwd_event<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, 0, s>>>(
+      sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, bwd);
+}
+
+void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                      const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
+                      uint64_t n_total, const uint4* bbox, const int* no_surv,
+                      const double* depth, const uint8_t* mask, const double* pose_tab,
+                      const double* K, double* d_depth, double* pose_part, double* grad_out) {
+  const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
+  count_launch();
+  k_bwd_owner<<<dim3(TP.nT, P.n_windows), 32, 0, s>>>(sorted, ev_off, P, TP, tile_ptr, bin_ptr,
+                                                      recs, bwd, n_total, bbox, no_surv, depth,
+                                                      mask, pose_tab, k0, k1, k2, k3, d_depth,
+                                                      pose_part, grad_out);
+}
+
+}  // namespace evcm_b200

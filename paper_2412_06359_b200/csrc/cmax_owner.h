@@ -1,0 +1,57 @@
+// Owner-computes pipeline launchers (cmax_owner.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/evcm_cuda.h"
+#include "cmax_device.cuh"
+
+namespace evcm_b200 {
+
+constexpr int kTile = 16;          // source / owner tile edge (px)
+constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
+constexpr int kSortThreads = 512;  // 16 warps x 512 events
+constexpr int kMaxTiles = 6000;    // sort scatter keeps 16 x nT u16 counters in smem
+
+struct TileParams {
+  int ntx, nty, nT;
+  int nchunks;  // sort chunks per window (max over the batch)
+};
+
+// Per (event, reference) splat record, 16 B. cell = x0 | y0 << 16 | negative
+// polarity << 31 (0xffffffff: masked event); dt = t_us - t0; fx, fy = the
+// compressed bilinear fractions (see compress_frac).
+struct __align__(16) FwdRec {
+  uint32_t cell;
+  uint32_t dt;
+  float fx, fy;
+};
+
+TileParams make_tiles(const WinParams& P, uint64_t max_n);
+void launch_sort(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
+                 const TileParams& TP, uint2* packed, uint32_t* counts, unsigned long long* err,
+                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm);
+void launch_bin_ptr(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off, const WinParams& P,
+                    const TileParams& TP, const uint32_t* tile_ptr, uint32_t* bin_ptr);
+void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                         const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                         uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
+                         uint4* bbox);
+void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
+                      const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
+                      uint64_t n_total, const uint4* bbox, double2* coef, double2* stack_out,
+                      double* part_acc, unsigned long long* part_act);
+void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                      uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
+                      const double2* coef, const double* scale, const int* no_surv, float2* bwd);
+void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
+                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
+                      const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
+                      uint64_t n_total, const uint4* bbox, const int* no_surv,
+                      const double* depth, const uint8_t* mask, const double* pose_tab,
+                      const double* K, double* d_depth, double* pose_part, double* grad_out);
+
+}  // namespace evcm_b200

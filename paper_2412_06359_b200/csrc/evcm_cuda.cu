@@ -13,6 +13,7 @@
 
 #include "../../include/evcm_cuda.h"
 #include "cmax_kernels.h"
+#include "cmax_owner.h"
 
 using namespace evcm_b200;
 
@@ -140,6 +141,10 @@ struct evcm_cuda_engine {
   std::unordered_map<std::string, Buf> bufs;
   std::unordered_map<std::string, Buf> pins;  // pinned host staging
   int stage_nw = 0;
+  // owner pipeline state
+  TileParams TP{};
+  uint64_t n_total = 0, max_n = 0;
+  bool owner() const { return opt.algo == 0; }
   // state of the last forward (Engine::forward -> backward hand-off)
   bool have_fwd = false;
   WinParams P{};
@@ -296,7 +301,22 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   uint2* packed = e->get<uint2>("packed", total);
   unsigned long long* err = e->get<unsigned long long>("stage_err", nw);
   ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
-  launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
+  e->n_total = total;
+  e->max_n = max_n;
+  if (e->owner()) {
+    // validation + packing + stable counting sort by 16x16 source tile
+    const TileParams TP = make_tiles(P, max_n);
+    if (TP.nT > kMaxTiles)
+      fail(EVCM_ERR_CONFIG, "cuda backend: sensor too large (more than " +
+                                std::to_string(kMaxTiles) + " 16x16 tiles)");
+    e->TP = TP;
+    launch_sort(e->stream, dev, off_d, P, TP, packed,
+                e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), err,
+                e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1)),
+                e->get<uint2>("sorted", total), nullptr);
+  } else {
+    launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
+  }
   unsigned long long* err_h = e->pinned<unsigned long long>("stage_err_h", nw);
   ck(cudaMemcpyAsync(err_h, err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream),
      "D2H err");
@@ -377,8 +397,69 @@ void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, cons
   e->mark(M_FWD0 + 3);
 }
 
-void run_forward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
-  if (e->opt.stack_f64) run_forward_t<double2>(e, P, max_n, flows);
+// Owner-computes forward (cmax_owner.cu): bin pointers, trajectory records,
+// per-tile stack + loss partials + coefficient planes, loss finalize.
+void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* flows,
+                       bool want_stack) {
+  const TileParams& TP = e->TP;
+  const int nw = P.n_windows, R = P.B + 1;
+  const uint64_t total = e->n_total;
+  const uint64_t* ev_off = e->get<uint64_t>("ev_off", 1);
+  const uint2* sorted = e->get<uint2>("sorted", 1);
+  const uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", 1);
+  e->mark(M_FWD0);
+  launch_bin_ptr(e->stream, sorted, ev_off, P, TP, tile_ptr,
+                 e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
+  FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
+  uint4* bbox = e->get<uint4>("bbox", (size_t)nw * R * TP.nT);
+  ck(cudaMemsetAsync(bbox, 0xff, (size_t)nw * R * TP.nT * sizeof(uint4), e->stream), "memset");
+  launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, total, recs, bbox);
+  e->mark(M_FWD0 + 1);
+  const size_t np = (size_t)nw * R * TP.nT;
+  double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
+  launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox,
+                   e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
+                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+  e->mark(M_FWD0 + 2);
+  launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
+                       e->get<unsigned long long>("part_act", np), TP.nT, P,
+                       e->get<double>("loss", nw), e->get<int>("no_surv", nw),
+                       e->get<long long>("n_active", (size_t)nw * R),
+                       e->get<double>("scale", (size_t)nw * R));
+  e->mark(M_FWD0 + 3);
+}
+
+// Owner-computes backward: per-event adjoint -> per-bin (gx, gy), then the
+// per-tile gradient gather with the fused flows backward (when depth given)
+// and/or the f64 gradient planes (grad_out, [w][B][2][HW]).
+void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* flows,
+                        const double* depth, const uint8_t* mask, const double* pose_tab,
+                        const double* K, double* d_depth, double* d_poses, double* grad_out) {
+  const TileParams& TP = e->TP;
+  const int nw = P.n_windows, R = P.B + 1;
+  const uint64_t total = e->n_total;
+  const uint64_t* ev_off = e->get<uint64_t>("ev_off", 1);
+  const uint2* sorted = e->get<uint2>("sorted", 1);
+  const uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", 1);
+  const FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
+  float2* bwd = e->get<float2>("bwdrec", (size_t)P.B * total);
+  launch_bwd_event(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, recs, total,
+                   e->get<double2>("coef", 1), e->get<double>("scale", 1), e->get<int>("no_surv", 1),
+                   bwd);
+  e->mark(M_FWD0 + 4);
+  double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.nT * P.B * 6) : nullptr;
+  launch_bwd_owner(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
+                   bwd, total, e->get<uint4>("bbox", 1), e->get<int>("no_surv", 1), depth, mask,
+                   pose_tab, K, d_depth, pose_part, grad_out);
+  e->mark(M_FWD0 + 5);
+  if (depth) launch_pose_finalize(e->stream, pose_part, TP.nT, P.B, nw, d_poses);
+  e->mark(M_FWD0 + 6);
+}
+
+void run_forward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows,
+                 bool want_stack = false) {
+  if (e->owner()) run_forward_owner(e, P, flows, want_stack);
+  else if (e->opt.stack_f64) run_forward_t<double2>(e, P, max_n, flows);
   else run_forward_t<float2>(e, P, max_n, flows);
 }
 
@@ -455,6 +536,7 @@ void evcm_cuda_default_options(evcm_cuda_options* o) {
   o->stack_f64 = 1;  // parity precision
   o->grad_f64 = 0;
   o->stream = nullptr;
+  o->algo = 0;
 }
 
 int evcm_cuda_create(const evcm_cuda_options* opts, evcm_cuda_engine** out) {
@@ -526,7 +608,7 @@ int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows
     WinParams P;
     const double2* flows = prepare_window(e, s, f, mem, &P);
     e->mark(1);
-    run_forward(e, P, s->n_events, flows);
+    run_forward(e, P, s->n_events, flows, /*want_stack=*/true);
     double l = 0;
     int ns = 0;
     ck(cudaMemcpyAsync(&l, e->get<double>("loss", 1), sizeof l, cudaMemcpyDeviceToHost, e->stream), "D2H");
@@ -554,7 +636,7 @@ int evcm_cuda_forward_products(evcm_cuda_engine* e, double* count, double* tsum,
     if (count || tsum) {
       double* c = e->get<double>("prod_count", R * 2 * HW);
       double* t = e->get<double>("prod_tsum", R * 2 * HW);
-      if (e->opt.stack_f64)
+      if (e->owner() || e->opt.stack_f64)
         launch_unpack_stack<double2>(e->stream, e->get<double2>("stack", 1), R * 2, P.HW, c, t);
       else
         launch_unpack_stack<float2>(e->stream, e->get<float2>("stack", 1), R * 2, P.HW, c, t);
@@ -602,15 +684,20 @@ int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flow
       fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
     const WinParams& P = e->P;
     e->mark(M_FWD0 + 3);
-    void* g = run_backward(e, P, s->n_events, e->get<double2>("flows", 1));
     double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
-    if (e->opt.grad_f64)
-      launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
-    else
-      launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
+    if (e->owner()) {
+      run_backward_owner(e, P, e->get<double2>("flows", 1), nullptr, nullptr, nullptr, nullptr,
+                         nullptr, nullptr, out);
+    } else {
+      void* g = run_backward(e, P, s->n_events, e->get<double2>("flows", 1));
+      if (e->opt.grad_f64)
+        launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
+      else
+        launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
+    }
     from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
     ck(cudaStreamSynchronize(e->stream), "backward");
-    e->collect_range(M_FWD0 + 3, M_FWD0 + 5);
+    e->collect_range(M_FWD0 + 3, e->owner() ? M_FWD0 + 5 : M_FWD0 + 5);
     ck(cudaGetLastError(), "backward kernels");
     e->last_launches = launch_count();
   });
@@ -730,16 +817,20 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
     e->mark(1);
     launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr);
     run_forward(e, P, max_n, flows);
-    void* g = run_backward(e, P, max_n, flows);
     const bool direct = out_mem == EVCM_MEM_DEVICE;
     double* ddo = (direct && out->d_depth) ? out->d_depth : e->get<double>("d_depth", (size_t)nw * P.HW);
     double* dpo = (direct && out->d_poses) ? out->d_poses : e->get<double>("d_poses", (size_t)nw * B * 6);
-    double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * 6);
-    if (e->opt.grad_f64)
-      launch_flows_bwd<double2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<double2*>(g), ddo, pp, dpo);
-    else
-      launch_flows_bwd<float2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<float2*>(g), ddo, pp, dpo);
-    e->mark(M_FWD0 + 6);
+    if (e->owner()) {
+      run_backward_owner(e, P, flows, depth, nullptr, tab, bt->K, ddo, dpo, nullptr);
+    } else {
+      void* g = run_backward(e, P, max_n, flows);
+      double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * 6);
+      if (e->opt.grad_f64)
+        launch_flows_bwd<double2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<double2*>(g), ddo, pp, dpo);
+      else
+        launch_flows_bwd<float2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<float2*>(g), ddo, pp, dpo);
+      e->mark(M_FWD0 + 6);
+    }
     if (out->loss) from_device(e, out->loss, e->get<double>("loss", nw), nw * sizeof(double), out_mem);
     if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), out_mem);
     if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), out_mem);

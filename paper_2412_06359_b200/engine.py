@@ -86,7 +86,7 @@ KLOSS_EPS = 1e-9  # warp.hpp:26
 
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int), ("deterministic", C.c_int), ("stack_f64", C.c_int),
-                ("grad_f64", C.c_int), ("stream", C.c_void_p)]
+                ("grad_f64", C.c_int), ("stream", C.c_void_p), ("algo", C.c_int)]
 
 
 class _Slice(C.Structure):
@@ -408,6 +408,7 @@ class EngineOptions:
     stack_f64: bool = True   # parity precision; False = fp32 "fast" stack
     grad_f64: bool = False
     stream: Optional[int] = None  # raw cudaStream_t handle, None = engine-owned
+    algo: str = "owner"  # "owner" (tiles, deterministic) | "atomic" (per-event atomics)
 
 
 class Engine:
@@ -417,8 +418,13 @@ class Engine:
         self.opts = opts or EngineOptions()
         backend_from_name(self.opts.backend)
         L = load_library()
+        if self.opts.algo not in ("owner", "atomic"):
+            raise ConfigError(f"unknown algo '{self.opts.algo}' (owner|atomic)")
+        if self.opts.deterministic and self.opts.algo != "owner":
+            raise ConfigError("deterministic mode needs algo='owner'")
         o = _Options(self.opts.device, int(self.opts.deterministic), int(self.opts.stack_f64),
-                     int(self.opts.grad_f64), self.opts.stream)
+                     int(self.opts.grad_f64), self.opts.stream,
+                     0 if self.opts.algo == "owner" else 1)
         h = C.c_void_p()
         _raise(L.evcm_cuda_create(C.byref(o), C.byref(h)))
         self._h = h

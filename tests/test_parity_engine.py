@@ -80,9 +80,27 @@ def test_fp64_accumulators(engine_f64):
     _check(engine_f64, w, grad_tol=1e-12)
 
 
+@pytest.mark.parametrize("W,H,B,n", [(64, 48, 10, 5000), (346, 260, 10, 100000)])
+def test_atomic_path(engine_atomic, W, H, B, n):
+    """The per-event atomic pipeline (algo='atomic') as an independent cross-check."""
+    _check(engine_atomic, smooth_window(W, H, B, n, seed=W * 3 + n))
+
+
+def test_owner_deterministic(engine):
+    """Owner-computes path: bit-identical loss, stack and gradients run to run."""
+    w = smooth_window(346, 260, 10, 200000, seed=21)
+    a = engine.forward(_slice(w), _flows(w))
+    sa, la = a.stack.count.copy(), a.loss.value
+    ga = engine.backward(_slice(w), _flows(w), a).grad.copy()
+    b = engine.forward(_slice(w), _flows(w))
+    assert b.loss.value == la
+    np.testing.assert_array_equal(b.stack.count, sa)
+    np.testing.assert_array_equal(engine.backward(_slice(w), _flows(w), b).grad, ga)
+
+
 def test_fast_mode_forward(engine_fast):
-    """fp32 stack ("fast" mode): loss and IWE within 1e-6; gradients are not
-    parity-grade on sparse windows and are not checked."""
+    """fp32 stack ("fast" mode of the atomic path): loss and IWE within 1e-6;
+    gradients are not parity-grade on sparse windows."""
     w = smooth_window(346, 260, 10, 100000, seed=4)
     fwd = engine_fast.forward(_slice(w), _flows(w))
     ref = O.forward(w)
