@@ -240,32 +240,50 @@ __global__ void __launch_bounds__(kPxBlock) k_loss_reduce(const S2* __restrict__
 }
 
 // reduce_loss (engine.hpp:442-468): fixed-order sum of the block partials.
+// One CTA per window, one warp per reference: lanes take parts lane, lane+32, ...
+// and reduce with a fixed shuffle tree, so the result is bit-stable.
 // out per window: loss, no_survivors, n_active[R], scale[R] = 2/((n_a+eps) R)
-__global__ void k_loss_finalize(const double* __restrict__ part_acc,
-                                const unsigned long long* __restrict__ part_act, int n_parts,
-                                WinParams P, double* __restrict__ loss,
-                                int* __restrict__ no_surv, long long* __restrict__ n_active,
-                                double* __restrict__ scale) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= P.n_windows) return;
-  const int R = P.B + 1;
-  long long total = 0;
-  double sum = 0.0;
-  for (int r = 0; r < R; ++r) {
+__global__ void __launch_bounds__(1024) k_loss_finalize(const double* __restrict__ part_acc,
+                                                        const unsigned long long* __restrict__ part_act,
+                                                        int n_parts, WinParams P,
+                                                        double* __restrict__ loss,
+                                                        int* __restrict__ no_surv,
+                                                        long long* __restrict__ n_active,
+                                                        double* __restrict__ scale) {
+  __shared__ double s_term[kMaxRefs];
+  __shared__ unsigned long long s_na[kMaxRefs];
+  const int w = blockIdx.x, R = P.B + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int r = wid; r < R; r += nwarps) {
+    const size_t s0 = ((size_t)w * R + r) * n_parts;
     double acc = 0.0;
     unsigned long long na = 0;
-    const size_t s0 = ((size_t)w * R + r) * n_parts;
-    for (int i = 0; i < n_parts; ++i) {
+    for (int i = lane; i < n_parts; i += 32) {
       acc += part_acc[s0 + i];
       na += part_act[s0 + i];
     }
-    n_active[(size_t)w * R + r] = (long long)na;
-    scale[(size_t)w * R + r] = 2.0 / (((double)na + kLossEps) * (double)R);
-    total += (long long)na;
-    sum += acc / ((double)na + kLossEps);
+    for (int o = 16; o > 0; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+    }
+    if (lane == 0) {
+      s_term[r] = acc / ((double)na + kLossEps);
+      s_na[r] = na;
+      n_active[(size_t)w * R + r] = (long long)na;
+      scale[(size_t)w * R + r] = 2.0 / (((double)na + kLossEps) * (double)R);
+    }
   }
-  no_surv[w] = total == 0 ? 1 : 0;
-  loss[w] = total == 0 ? 0.0 : sum / (double)R;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long total = 0;
+    double sum = 0.0;
+    for (int r = 0; r < R; ++r) {
+      total += (long long)s_na[r];
+      sum += s_term[r];
+    }
+    no_surv[w] = total == 0 ? 1 : 0;
+    loss[w] = total == 0 ? 0.0 : sum / (double)R;
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -456,14 +474,18 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
   if (in) d_depth[(size_t)w * HW + q] = dd_acc;
 }
 
+// Fixed-order (lane-strided + shuffle tree) sum of the per-block pose partials;
+// one warp per (window, bin, component).
 __global__ void k_pose_finalize(const double* __restrict__ pose_part, int n_parts, int B,
                                 int n_windows, double* __restrict__ d_poses) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over windows * B * 6
-  if (i >= n_windows * B * 6) return;
-  const int w = i / (B * 6), rem = i % (B * 6);
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= n_windows * B * 6) return;
+  const int w = o / (B * 6), rem = o % (B * 6);
   double v = 0.0;
-  for (int p = 0; p < n_parts; ++p) v += pose_part[((size_t)w * n_parts + p) * B * 6 + rem];
-  d_poses[i] = v;
+  for (int p = lane; p < n_parts; p += 32) v += pose_part[((size_t)w * n_parts + p) * B * 6 + rem];
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  if (lane == 0) d_poses[o] = v;
 }
 
 // --------------------------------------------------------------------------
@@ -585,15 +607,16 @@ void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned
                           int n_parts, const WinParams& P, double* loss, int* no_surv,
                           long long* n_active, double* scale) {
   ++g_launches;
-  k_loss_finalize<<<(P.n_windows + 63) / 64, 64, 0, s>>>(part_acc, part_act, n_parts, P, loss,
-                                                        no_surv, n_active, scale);
+  k_loss_finalize<<<P.n_windows, 32 * std::min(P.B + 1, 32), 0, s>>>(part_acc, part_act, n_parts,
+                                                                     P, loss, no_surv, n_active,
+                                                                     scale);
 }
 
 void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
                           int n_windows, double* d_poses) {
   const int total = n_windows * B * 6;
   ++g_launches;
-  k_pose_finalize<<<(total + 127) / 128, 128, 0, s>>>(pose_part, n_parts, B, n_windows, d_poses);
+  k_pose_finalize<<<(total + 3) / 4, 128, 0, s>>>(pose_part, n_parts, B, n_windows, d_poses);
 }
 
 int loss_parts(const WinParams& P) { return std::max(1, std::min((P.HW + kPxBlock - 1) / kPxBlock, 64)); }
@@ -607,8 +630,8 @@ void launch_loss(cudaStream_t s, const S2* stack, const WinParams& P, S2* coef,
   k_loss_reduce<S2><<<dim3(parts, P.B + 1, P.n_windows), kPxBlock, 0, s>>>(stack, P, coef,
                                                                           part_acc, part_act);
   ++g_launches;
-  k_loss_finalize<<<(P.n_windows + 63) / 64, 64, 0, s>>>(part_acc, part_act, parts, P, loss,
-                                                        no_surv, n_active, scale);
+  k_loss_finalize<<<P.n_windows, 32 * std::min(P.B + 1, 32), 0, s>>>(part_acc, part_act, parts, P,
+                                                                     loss, no_surv, n_active, scale);
 }
 
 template <typename C2, typename G2>
@@ -635,7 +658,7 @@ void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,
       depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
   const int total = P.n_windows * P.B * 6;
   ++g_launches;
-  k_pose_finalize<<<(total + 127) / 128, 128, 0, s>>>(pose_part, parts, P.B, P.n_windows, d_poses);
+  k_pose_finalize<<<(total + 3) / 4, 128, 0, s>>>(pose_part, parts, P.B, P.n_windows, d_poses);
 }
 
 template <typename S2>

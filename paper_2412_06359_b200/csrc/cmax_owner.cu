@@ -378,63 +378,182 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
 }
 
 // ---------------------------------------------------------------------------
+// owner source lists
+
+// For every (window, ref, source tile) with alive events: append S to the list
+// of every owner tile its cell box can touch. Lists are unordered here; owners
+// sort them (<= kListCapO entries) so the visit order is deterministic.
+__global__ void k_build_lists(const uint4* __restrict__ bbox, WinParams P, TileParams TP,
+                              uint32_t* __restrict__ lcount, uint16_t* __restrict__ lists) {
+  const int S = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y, w = blockIdx.z;
+  if (S >= TP.nT) return;
+  const size_t wr = (size_t)w * (P.B + 1) + r;
+  const uint4 b = bbox[wr * TP.nT + S];
+  if (b.x == 0xffffffffu) return;
+  const int mnx = (int)b.x, mny = (int)b.y, mxx = 0xffff - (int)b.z, mxy = 0xffff - (int)b.w;
+  const int tx0 = mnx / kTile, tx1 = min((mxx + 1) / kTile, TP.ntx - 1);
+  const int ty0 = mny / kTile, ty1 = min((mxy + 1) / kTile, TP.nty - 1);
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const size_t T = wr * TP.nT + (size_t)ty * TP.ntx + tx;
+      const uint32_t slot = atomicAdd(lcount + T, 1u);
+      if (slot < kListCapO) lists[T * kListCapO + slot] = (uint16_t)S;
+    }
+}
+
+namespace {
+
+// Sorted source list of (wr, T) into `list`; returns its length, or -1 when the
+// precomputed list overflowed (caller then scans the boxes).
+__device__ __forceinline__ int load_sorted_list(const uint32_t* __restrict__ lcount,
+                                                const uint16_t* __restrict__ lists, size_t slotT,
+                                                uint16_t* list) {
+  const uint32_t cnt = lcount[slotT];
+  if (cnt > (uint32_t)kListCapO) return -1;
+  const uint16_t* src = lists + slotT * kListCapO;
+  for (uint32_t i = 0; i < cnt; ++i) {  // insertion sort, cnt is small
+    const uint16_t v = src[i];
+    int j = (int)i - 1;
+    while (j >= 0 && list[j] > v) {
+      list[j + 1] = list[j];
+      --j;
+    }
+    list[j + 1] = v;
+  }
+  return (int)cnt;
+}
+
+// Virtual concatenation of event ranges [a_l, a_l + len_l): pre[l] = sum of
+// earlier lengths. Returns the slot of virtual index v.
+__device__ __forceinline__ uint32_t virt_slot(const uint32_t* pre, const uint32_t* a, int nl,
+                                              uint32_t v, int* which) {
+  int lo = 0, hi = nl - 1;  // largest l with pre[l] <= v
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  *which = lo;
+  return a[lo] + (v - pre[lo]);
+}
+
+__device__ __forceinline__ double corner_w(const CellW& c, int q) {
+  return (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy : c.wx * c.wy;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // forward owner: IWE stack tile + loss partials + coefficient planes
 
-__global__ void __launch_bounds__(32) k_fwd_owner(
+constexpr int kFwdWarps = 4;
+constexpr int kPrefetch = 4;  // records in flight per lane
+
+__global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
     const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
-    const uint4* __restrict__ bbox, double2* __restrict__ coef, double2* __restrict__ stack_out,
+    const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
+    const uint16_t* __restrict__ lists, double2* __restrict__ coef, double2* __restrict__ stack_out,
     double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
-  __shared__ __align__(16) double acc[kTile * kTile * 4];  // [px][C0,S0,C1,S1]
+  __shared__ __align__(16) double acc[kFwdWarps][kTile * kTile * 4];  // [warp][px][C0,S0,C1,S1]
   __shared__ uint16_t list[kListCap];
+  __shared__ uint32_t pre[kListCap + 1], rng[kListCap];
+  __shared__ int s_nl;
+  __shared__ double s_red[kFwdWarps];
+  __shared__ unsigned s_act[kFwdWarps];
   const int T = blockIdx.x, r = blockIdx.y, w = blockIdx.z;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = P.B + 1, W = P.W, H = P.H, HW = P.HW;
   const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
-  for (int i = lane; i < kTile * kTile * 4; i += 32) acc[i] = 0.0;
-  __syncwarp();
+  const size_t wr = (size_t)w * R + r;
+  for (int i = threadIdx.x; i < kFwdWarps * kTile * kTile * 4; i += blockDim.x) (&acc[0][0])[i] = 0.0;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const FwdRec* rr = recs + (size_t)r * n_total + base;
   const double esr = P.es[r], win = P.window_s;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
-  for_each_source(bbox + ((size_t)w * R + r) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
-    const uint32_t k0 = tp[S], k1 = tp[S + 1];
-    for (uint32_t kb = k0; kb < k1; kb += 32) {
-      const uint32_t k = kb + lane;
-      FwdRec rec;
-      rec.cell = kDead;
-      if (k < k1) rec = rr[k];
-      const bool live = rec.cell != kDead;
-      CellW c{};
-      double tb = 0.0;
-      int pol = 0;
-      if (live) {
-        c = decode(rec);
-        pol = (int)(rec.cell >> 31);
-        tb = dd(fabs(ds(dm((double)rec.dt, 1e-6), esr)), win);  // engine.hpp:370
+  double* mine = acc[wid];
+
+  auto contribute = [&](const FwdRec& rec) {
+    const bool live = rec.cell != kDead;
+    CellW c{};
+    double tb = 0.0;
+    int pol = 0;
+    if (live) {
+      c = decode(rec);
+      pol = (int)(rec.cell >> 31);
+      tb = dd(fabs(ds(dm((double)rec.dt, 1e-6), esr)), win);  // engine.hpp:370
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int lx = c.x0 + ((q & 1) ? ox : 0) - tx0, ly = c.y0 + ((q & 2) ? oy : 0) - ty0;
+      const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
+      const double wq = corner_w(c, q);
+      warp_accumulate2(mine, in ? ((ly * kTile + lx) * 2 + pol) : -1, wq, wq * tb);
+    }
+  };
+
+  if (threadIdx.x == 0) s_nl = load_sorted_list(lcount, lists, wr * TP.nT + T, list);
+  __syncthreads();
+  if (s_nl >= 0) {
+    const int nl = s_nl;
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (int l = 0; l < nl; ++l) {
+        pre[l] = run;
+        rng[l] = tp[list[l]];
+        run += tp[list[l] + 1] - tp[list[l]];
+      }
+      pre[nl] = run;
+    }
+    __syncthreads();
+    // even contiguous split of the virtual event sequence over the warps
+    const uint32_t total = pre[nl];
+    const uint32_t v0 = (uint32_t)(((uint64_t)total * wid) / kFwdWarps);
+    const uint32_t v1 = (uint32_t)(((uint64_t)total * (wid + 1)) / kFwdWarps);
+    for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
+      FwdRec rb[kPrefetch];
+#pragma unroll
+      for (int m = 0; m < kPrefetch; ++m) {
+        const uint32_t v = vb + m * 32 + lane;
+        rb[m].cell = kDead;
+        if (v < v1) {
+          int l;
+          rb[m] = rr[virt_slot(pre, rng, nl, v, &l)];
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int px = c.x0 + ((q & 1) ? ox : 0), py = c.y0 + ((q & 2) ? oy : 0);
-        const double wq = (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy
-                                                                                   : c.wx * c.wy;
-        const int lx = px - tx0, ly = py - ty0;
-        const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
-        warp_accumulate2(acc, in ? ((ly * kTile + lx) * 2 + pol) : -1, wq, wq * tb);
-      }
+      for (int m = 0; m < kPrefetch; ++m)
+        if (vb + m * 32 < v1) contribute(rb[m]);
     }
-  });
-  __syncwarp();
-  // finalize: refresh_active + reference_loss terms + splat_position_grad factors
+  } else if (wid == 0) {
+    // overflowed list: scan every source box in order (slow, rare)
+    for_each_source(bbox + wr * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
+      for (uint32_t kb = tp[S]; kb < tp[S + 1]; kb += 32) {
+        FwdRec rec;
+        rec.cell = kDead;
+        if (kb + lane < tp[S + 1]) rec = rr[kb + lane];
+        contribute(rec);
+      }
+    });
+  }
+  __syncthreads();
+  // merge the warp copies in order, then refresh_active + reference_loss terms
+  // + splat_position_grad factors per pixel
   double lsum = 0.0;
   unsigned act = 0;
-  double2* cw = coef + ((size_t)w * R + r) * 2 * HW;
-  for (int q = lane; q < kTile * kTile; q += 32) {
+  double2* cw = coef + wr * 2 * HW;
+  for (int q = threadIdx.x; q < kTile * kTile; q += blockDim.x) {
     const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
     if (px >= W || py >= H) continue;
+    double C0 = acc[0][4 * q], S0 = acc[0][4 * q + 1], C1 = acc[0][4 * q + 2], S1 = acc[0][4 * q + 3];
+#pragma unroll
+    for (int m = 1; m < kFwdWarps; ++m) {
+      C0 += acc[m][4 * q];
+      S0 += acc[m][4 * q + 1];
+      C1 += acc[m][4 * q + 2];
+      S1 += acc[m][4 * q + 3];
+    }
     const int g = py * W + px;
-    const double C0 = acc[4 * q], S0 = acc[4 * q + 1], C1 = acc[4 * q + 2], S1 = acc[4 * q + 3];
     act += (C0 + C1 > 0.0) ? 1u : 0u;
     const double a0 = S0 / (C0 + kLossEps), a1 = S1 / (C1 + kLossEps);
     lsum += a0 * a0 + a1 * a1;
@@ -443,17 +562,27 @@ __global__ void __launch_bounds__(32) k_fwd_owner(
     cw[g] = make_double2(b0, b0 * i0);
     cw[HW + g] = make_double2(b1, b1 * i1);
     if (stack_out) {
-      double2* so = stack_out + ((size_t)w * R + r) * 2 * HW;
+      double2* so = stack_out + wr * 2 * HW;
       so[g] = make_double2(C0, S0);
       so[HW + g] = make_double2(C1, S1);
     }
   }
   lsum = warp_sum(lsum);
-  for (int o = 16; o > 0; o >>= 1) act += __shfl_xor_sync(kFull, act, o);
+  for (int o2 = 16; o2 > 0; o2 >>= 1) act += __shfl_xor_sync(kFull, act, o2);
   if (lane == 0) {
-    const size_t slot = ((size_t)w * R + r) * TP.nT + T;
-    part_acc[slot] = lsum;
-    part_act[slot] = act;
+    s_red[wid] = lsum;
+    s_act[wid] = act;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    unsigned a = 0;
+    for (int m = 0; m < kFwdWarps; ++m) {
+      s += s_red[m];
+      a += s_act[m];
+    }
+    part_acc[wr * TP.nT + T] = s;
+    part_act[wr * TP.nT + T] = a;
   }
 }
 
@@ -546,163 +675,218 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
 
 // ---------------------------------------------------------------------------
 // backward owner: gradient tile per bin + fused depth_pose_to_flows_backward
+//
+// One CTA per (window, owner tile), one warp per bin i. Warp i gathers the
+// (gx, gy) of: events with bin j > i at their reference-(i+1) cell (backward
+// leg), events with j < i at their reference-i cell (forward leg), and the
+// tile's own events with j == i at their source pixel (the two partial steps),
+// then runs the flows backward of bin i on the finished tile. d_depth sums the
+// per-bin contributions in bin order.
 
-__global__ void __launch_bounds__(32) k_bwd_owner(
+constexpr int kBwdList = 2 * kListCapO + 1;
+constexpr int kBwdWarpBytes = ((kBwdList * 10 + 16 + 15) / 16) * 16;  // per-warp list state
+
+__global__ void __launch_bounds__(1024) k_bwd_owner(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
     const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
-    const uint4* __restrict__ bbox, const int* __restrict__ no_surv,
+    const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
+    const uint16_t* __restrict__ lists, const int* __restrict__ no_surv,
     const double* __restrict__ depth, const uint8_t* __restrict__ mask,
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
     double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
-  __shared__ __align__(16) double g[kTile * kTile * 2];  // [px][gu, gv]
-  __shared__ uint16_t list[kListCap];
-  const int T = blockIdx.x, w = blockIdx.y, lane = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = blockIdx.x, w = blockIdx.y, lane = threadIdx.x & 31, i = threadIdx.x >> 5;
   const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
+  // per-warp shared state
+  double* g = reinterpret_cast<double*>(smem_raw) + (size_t)i * (kTile * kTile * 2);
+  double* ddp = reinterpret_cast<double*>(smem_raw) + (size_t)B * (kTile * kTile * 2) +
+                (size_t)i * (kTile * kTile);
+  unsigned char* wst = smem_raw + (size_t)B * kTile * kTile * 3 * sizeof(double) +
+                       (size_t)i * kBwdWarpBytes;
+  uint32_t* pre = reinterpret_cast<uint32_t*>(wst);             // kBwdList + 1
+  uint32_t* rng = pre + (kBwdList + 1);                          // kBwdList
+  uint16_t* lst = reinterpret_cast<uint16_t*>(rng + kBwdList);   // kBwdList (S per entry)
   const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool skip = no_surv[w] != 0;
+  for (int q = lane; q < kTile * kTile * 2; q += 32) g[q] = 0.0;
+  __syncwarp();
 
-  // per-lane pixels of the tile (8 per lane) for the fused flows backward
-  constexpr int kPer = kTile * kTile / 32;
-  double dacc[kPer], dep[kPer], rxs[kPer], rys[kPer];
-  bool ok[kPer];
-#pragma unroll
-  for (int m = 0; m < kPer; ++m) {
-    const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
-    const bool in = px < W && py < H;
-    const int gq = py * W + px;
-    dacc[m] = 0.0;
-    dep[m] = (in && depth) ? depth[(size_t)w * HW + gq] : 0.0;
-    ok[m] = in && depth && (!mask || mask[(size_t)w * HW + gq]) && dep[m] > 0.0;
-    rxs[m] = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
-    rys[m] = 1.0 * ((double)py - cy) / fy;
-  }
-
-  auto accumulate = [&](const FwdRec& rec, bool live, float2 v) {
-    CellW c{};
-    if (live) c = decode(rec);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int px = c.x0 + ((q & 1) ? ox : 0), py = c.y0 + ((q & 2) ? oy : 0);
-      const double wq = (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy
-                                                                                 : c.wx * c.wy;
-      const int lx = px - tx0, ly = py - ty0;
-      const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
-      warp_accumulate2(g, in ? (ly * kTile + lx) : -1, wq * (double)v.x, wq * (double)v.y);
+  if (!skip) {
+    const float2* bi = bwd + (size_t)i * n_total + base;
+    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward leg cells
+    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward leg cells
+    const size_t slotA = ((size_t)w * R + i + 1) * TP.nT + T, slotB = ((size_t)w * R + i) * TP.nT + T;
+    int nA = 0, nB = 0;
+    if (lane == 0) {
+      nA = load_sorted_list(lcount, lists, slotA, lst);
+      nB = nA >= 0 ? load_sorted_list(lcount, lists, slotB, lst + nA) : -1;
     }
-  };
-
-  for (int i = 0; i < B; ++i) {
-    for (int q = lane; q < kTile * kTile * 2; q += 32) g[q] = 0.0;
-    __syncwarp();
-    if (!skip) {
-      const float2* bi = bwd + (size_t)i * n_total + base;
-      // backward leg: events with bin j > i sink at their reference-(i+1) cell
-      {
-        const FwdRec* rr = recs + (size_t)(i + 1) * n_total + base;
-        for_each_source(bbox + ((size_t)w * R + i + 1) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
-          const uint32_t k0 = bp[(size_t)S * (B + 1) + i + 1], k1 = tp[S + 1];
-          for (uint32_t kb = k0; kb < k1; kb += 32) {
-            const uint32_t k = kb + lane;
-            FwdRec rec;
-            rec.cell = kDead;
-            float2 v = make_float2(0.f, 0.f);
-            if (k < k1) {
-              rec = rr[k];
-              if (rec.cell != kDead) v = bi[k];
-            }
-            accumulate(rec, rec.cell != kDead, v);
-          }
-        });
+    nA = __shfl_sync(kFull, nA, 0);
+    nB = __shfl_sync(kFull, nB, 0);
+    auto accumulate = [&](const FwdRec& rec, float2 v) {
+      const bool live = rec.cell != kDead;
+      CellW c{};
+      if (live) c = decode(rec);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lx = c.x0 + ((q & 1) ? ox : 0) - tx0, ly = c.y0 + ((q & 2) ? oy : 0) - ty0;
+        const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
+        const double wq = corner_w(c, q);
+        warp_accumulate2(g, in ? (ly * kTile + lx) : -1, wq * (double)v.x, wq * (double)v.y);
       }
-      // forward leg: events with bin j < i sink at their reference-i cell
-      {
-        const FwdRec* rr = recs + (size_t)i * n_total + base;
-        for_each_source(bbox + ((size_t)w * R + i) * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
-          const uint32_t k0 = tp[S], k1 = bp[(size_t)S * (B + 1) + i];
-          for (uint32_t kb = k0; kb < k1; kb += 32) {
-            const uint32_t k = kb + lane;
-            FwdRec rec;
-            rec.cell = kDead;
-            float2 v = make_float2(0.f, 0.f);
-            if (k < k1) {
-              rec = rr[k];
-              if (rec.cell != kDead) v = bi[k];
-            }
-            accumulate(rec, rec.cell != kDead, v);
-          }
-        });
-      }
-      // partial steps of events of this tile with bin j == i, at their source pixel
-      {
-        const uint32_t k0 = bp[(size_t)T * (B + 1) + i], k1 = bp[(size_t)T * (B + 1) + i + 1];
-        for (uint32_t kb = k0; kb < k1; kb += 32) {
-          const uint32_t k = kb + lane;
-          int key = -1;
-          float2 v = make_float2(0.f, 0.f);
-          if (k < k1 && recs[base + k].cell != kDead) {
-            const uint2 e = sorted[base + k];
-            key = (ev_y(e) - ty0) * kTile + (ev_x(e) - tx0);
-            v = bi[k];
-          }
-          warp_accumulate2(g, key, (double)v.x, (double)v.y);
+    };
+    if (nA >= 0 && nB >= 0) {
+      // virtual sequence: list A ranges (j > i), list B ranges (j < i)
+      if (lane == 0) {
+        uint32_t run = 0;
+        for (int l = 0; l < nA; ++l) {
+          const int S = lst[l];
+          pre[l] = run;
+          rng[l] = bp[(size_t)S * (B + 1) + i + 1];
+          run += tp[S + 1] - rng[l];
         }
+        for (int l = nA; l < nA + nB; ++l) {
+          const int S = lst[l];
+          pre[l] = run;
+          rng[l] = tp[S];
+          run += bp[(size_t)S * (B + 1) + i] - tp[S];
+        }
+        pre[nA + nB] = run;
+      }
+      __syncwarp();
+      const int nl = nA + nB;
+      const uint32_t total = pre[nl];
+      const uint32_t splitAB = pre[nA];
+      for (uint32_t vb = 0; vb < total; vb += 32 * kPrefetch) {
+        FwdRec rb[kPrefetch];
+        float2 vv[kPrefetch];
+#pragma unroll
+        for (int m = 0; m < kPrefetch; ++m) {
+          const uint32_t v = vb + m * 32 + lane;
+          rb[m].cell = kDead;
+          vv[m] = make_float2(0.f, 0.f);
+          if (v < total) {
+            int l;
+            const uint32_t k = virt_slot(pre, rng, nl, v, &l);
+            rb[m] = (v < splitAB) ? rA[k] : rB[k];
+            if (rb[m].cell != kDead) vv[m] = bi[k];
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < kPrefetch; ++m)
+          if (vb + m * 32 < total) accumulate(rb[m], vv[m]);
+      }
+    } else {
+      // overflowed lists: scan the source boxes (slow, rare)
+      for_each_source(bbox + slotA - T, TP.nT, tx0, ty0, lst, [&](int S) {
+        const uint32_t k1 = tp[S + 1];
+        for (uint32_t kb = bp[(size_t)S * (B + 1) + i + 1]; kb < k1; kb += 32) {
+          FwdRec rec;
+          rec.cell = kDead;
+          float2 v = make_float2(0.f, 0.f);
+          if (kb + lane < k1) {
+            rec = rA[kb + lane];
+            if (rec.cell != kDead) v = bi[kb + lane];
+          }
+          accumulate(rec, v);
+        }
+      });
+      for_each_source(bbox + slotB - T, TP.nT, tx0, ty0, lst, [&](int S) {
+        const uint32_t k1 = bp[(size_t)S * (B + 1) + i];
+        for (uint32_t kb = tp[S]; kb < k1; kb += 32) {
+          FwdRec rec;
+          rec.cell = kDead;
+          float2 v = make_float2(0.f, 0.f);
+          if (kb + lane < k1) {
+            rec = rB[kb + lane];
+            if (rec.cell != kDead) v = bi[kb + lane];
+          }
+          accumulate(rec, v);
+        }
+      });
+    }
+    // partial steps of this tile's events with bin j == i, at their source pixel
+    {
+      const uint32_t k0 = bp[(size_t)T * (B + 1) + i], k1 = bp[(size_t)T * (B + 1) + i + 1];
+      for (uint32_t kb = k0; kb < k1; kb += 32) {
+        const uint32_t k = kb + lane;
+        int key = -1;
+        float2 v = make_float2(0.f, 0.f);
+        if (k < k1 && recs[base + k].cell != kDead) {
+          const uint2 e = sorted[base + k];
+          key = (ev_y(e) - ty0) * kTile + (ev_x(e) - tx0);
+          v = bi[k];
+        }
+        warp_accumulate2(g, key, (double)v.x, (double)v.y);
       }
     }
-    __syncwarp();
-    // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
-    const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
-    double c6[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int m = 0; m < kPer; ++m) {
-      const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
-      const double gu = g[2 * q], gv = g[2 * q + 1];
-      if (grad_out && px < W && py < H) {
-        const int gq = py * W + px;
+  }
+  __syncwarp();
+
+  // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
+  const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
+  double c6[6] = {0, 0, 0, 0, 0, 0};
+  for (int q = lane; q < kTile * kTile; q += 32) {
+    const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+    const double gu = g[2 * q], gv = g[2 * q + 1];
+    double contrib = 0.0;
+    if (px < W && py < H) {
+      const int gq = py * W + px;
+      if (grad_out) {
         grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
         grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
       }
-      if (!pt || !ok[m] || (gu == 0.0 && gv == 0.0)) continue;
-      const double d = dep[m], rx = rxs[m], ry = rys[m];
-      const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
-      const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
-      const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
-      const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
-      if (!(p2 > 0.0)) continue;
-      const double inv_dt = pt[39], iz = 1.0 / p2;
-      const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-      const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-      dacc[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-      c6[3] += gu * ju0 * inv_dt;
-      c6[4] += gv * jv1 * inv_dt;
-      c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
+      const double d = pt ? depth[(size_t)w * HW + gq] : 0.0;
+      const bool ok = pt && (!mask || mask[(size_t)w * HW + gq]) && d > 0.0;
+      if (ok && (gu != 0.0 || gv != 0.0)) {
+        const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
+        const double ry = 1.0 * ((double)py - cy) / fy;
+        const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
+        const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
+        const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
+        const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
+        if (p2 > 0.0) {
+          const double inv_dt = pt[39], iz = 1.0 / p2;
+          const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+          const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+          contrib = (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+          c6[3] += gu * ju0 * inv_dt;
+          c6[4] += gv * jv1 * inv_dt;
+          c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double* dR = pt + 9 + 9 * a;
-        const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-        const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-        const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-        c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
+          for (int a = 0; a < 3; ++a) {
+            const double* dR = pt + 9 + 9 * a;
+            const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
+            const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
+            const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
+            c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
+          }
+        }
       }
     }
-    if (pt) {
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double v = warp_sum(c6[a]);
-        if (lane == 0) pose_part[(((size_t)w * TP.nT + T) * B + i) * 6 + a] = v;
-      }
-    }
-    __syncwarp();
+    ddp[q] = contrib;
   }
-  if (d_depth) {
+  if (pt) {
 #pragma unroll
-    for (int m = 0; m < kPer; ++m) {
-      const int q = lane + 32 * m, px = tx0 + (q % kTile), py = ty0 + (q / kTile);
-      if (px < W && py < H) d_depth[(size_t)w * HW + py * W + px] = dacc[m];
+    for (int a = 0; a < 6; ++a) {
+      const double v = warp_sum(c6[a]);
+      if (lane == 0) pose_part[(((size_t)w * TP.nT + T) * B + i) * 6 + a] = v;
+    }
+  }
+  __syncthreads();
+  if (d_depth) {
+    const double* dd0 = reinterpret_cast<double*>(smem_raw) + (size_t)B * (kTile * kTile * 2);
+    for (int q = threadIdx.x; q < kTile * kTile; q += blockDim.x) {
+      const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+      if (px >= W || py >= H) continue;
+      double s = 0.0;
+      for (int b = 0; b < B; ++b) s += dd0[(size_t)b * kTile * kTile + q];  // bin order
+      d_depth[(size_t)w * HW + py * W + px] = s;
     }
   }
 }
@@ -765,13 +949,22 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                    s>>>(sorted, ev_off, P, TP, tile_ptr, flows, n_total, recs, bbox);
 }
 
+void launch_build_lists(cudaStream_t s, const WinParams& P, const TileParams& TP,
+                        const uint4* bbox, uint32_t* lcount, uint16_t* lists) {
+  count_launch();
+  k_build_lists<<<dim3((TP.nT + 127) / 128, P.B + 1, P.n_windows), 128, 0, s>>>(bbox, P, TP,
+                                                                                lcount, lists);
+}
+
 void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
-                      uint64_t n_total, const uint4* bbox, double2* coef, double2* stack_out,
-                      double* part_acc, unsigned long long* part_act) {
+                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
+                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
+                      unsigned long long* part_act) {
   count_launch();
-  k_fwd_owner<<<dim3(TP.nT, P.B + 1, P.n_windows), 32, 0, s>>>(
-      ev_off, P, TP, tile_ptr, recs, n_total, bbox, coef, stack_out, part_acc, part_act);
+  k_fwd_owner<<<dim3(TP.nT, P.B + 1, P.n_windows), 32 * kFwdWarps, 0, s>>>(
+      ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
+      part_act);
 }
 
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
@@ -787,15 +980,22 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
 void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
-                      uint64_t n_total, const uint4* bbox, const int* no_surv,
-                      const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth, double* pose_part, double* grad_out) {
+                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
+                      const uint16_t* lists, const int* no_surv, const double* depth,
+                      const uint8_t* mask, const double* pose_tab, const double* K,
+                      double* d_depth, double* pose_part, double* grad_out) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
+  const size_t smem = (size_t)P.B * (kTile * kTile * 3 * sizeof(double) + kBwdWarpBytes);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bwd_owner, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)kMaxBins * (kTile * kTile * 3 * sizeof(double) + kBwdWarpBytes)));
+    attr = true;
+  }
   count_launch();
-  k_bwd_owner<<<dim3(TP.nT, P.n_windows), 32, 0, s>>>(sorted, ev_off, P, TP, tile_ptr, bin_ptr,
-                                                      recs, bwd, n_total, bbox, no_surv, depth,
-                                                      mask, pose_tab, k0, k1, k2, k3, d_depth,
-                                                      pose_part, grad_out);
+  k_bwd_owner<<<dim3(TP.nT, P.n_windows), 32 * P.B, smem, s>>>(
+      sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
+      depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
 }
 
 }  // namespace evcm_b200

@@ -14,6 +14,7 @@ constexpr int kTile = 16;          // source / owner tile edge (px)
 constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
 constexpr int kSortThreads = 512;  // 16 warps x 512 events
 constexpr int kMaxTiles = 6000;    // sort scatter keeps 16 x nT u16 counters in smem
+constexpr int kListCapO = 64;      // precomputed source list capacity per (window, ref, owner tile)
 
 struct TileParams {
   int ntx, nty, nT;
@@ -39,10 +40,13 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                          uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
                          uint4* bbox);
+void launch_build_lists(cudaStream_t s, const WinParams& P, const TileParams& TP,
+                        const uint4* bbox, uint32_t* lcount, uint16_t* lists);
 void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
-                      uint64_t n_total, const uint4* bbox, double2* coef, double2* stack_out,
-                      double* part_acc, unsigned long long* part_act);
+                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
+                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
+                      unsigned long long* part_act);
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
@@ -50,8 +54,9 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
 void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
-                      uint64_t n_total, const uint4* bbox, const int* no_surv,
-                      const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth, double* pose_part, double* grad_out);
+                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
+                      const uint16_t* lists, const int* no_surv, const double* depth,
+                      const uint8_t* mask, const double* pose_tab, const double* K,
+                      double* d_depth, double* pose_part, double* grad_out);
 
 }  // namespace evcm_b200

@@ -414,12 +414,15 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint4* bbox = e->get<uint4>("bbox", (size_t)nw * R * TP.nT);
   ck(cudaMemsetAsync(bbox, 0xff, (size_t)nw * R * TP.nT * sizeof(uint4), e->stream), "memset");
   launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, total, recs, bbox);
-  e->mark(M_FWD0 + 1);
   const size_t np = (size_t)nw * R * TP.nT;
+  uint32_t* lcount = e->get<uint32_t>("lcount", np);
+  ck(cudaMemsetAsync(lcount, 0, np * sizeof(uint32_t), e->stream), "memset");
+  launch_build_lists(e->stream, P, TP, bbox, lcount, e->get<uint16_t>("lists", np * kListCapO));
+  e->mark(M_FWD0 + 1);
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
-  launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox,
-                   e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
-                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+  launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount,
+                   e->get<uint16_t>("lists", 1), e->get<double2>("coef", (size_t)nw * R * 2 * P.HW),
+                   stack, e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
   e->mark(M_FWD0 + 2);
   launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
                        e->get<unsigned long long>("part_act", np), TP.nT, P,
@@ -449,8 +452,9 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   e->mark(M_FWD0 + 4);
   double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.nT * P.B * 6) : nullptr;
   launch_bwd_owner(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
-                   bwd, total, e->get<uint4>("bbox", 1), e->get<int>("no_surv", 1), depth, mask,
-                   pose_tab, K, d_depth, pose_part, grad_out);
+                   bwd, total, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
+                   e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask, pose_tab,
+                   K, d_depth, pose_part, grad_out);
   e->mark(M_FWD0 + 5);
   if (depth) launch_pose_finalize(e->stream, pose_part, TP.nT, P.B, nw, d_poses);
   e->mark(M_FWD0 + 6);
