@@ -700,9 +700,7 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
   const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
   // per-warp shared state
   double* g = reinterpret_cast<double*>(smem_raw) + (size_t)i * (kTile * kTile * 2);
-  double* ddp = reinterpret_cast<double*>(smem_raw) + (size_t)B * (kTile * kTile * 2) +
-                (size_t)i * (kTile * kTile);
-  unsigned char* wst = smem_raw + (size_t)B * kTile * kTile * 3 * sizeof(double) +
+  unsigned char* wst = smem_raw + (size_t)B * kTile * kTile * 2 * sizeof(double) +
                        (size_t)i * kBwdWarpBytes;
   uint32_t* pre = reinterpret_cast<uint32_t*>(wst);             // kBwdList + 1
   uint32_t* rng = pre + (kBwdList + 1);                          // kBwdList
@@ -869,7 +867,7 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
         }
       }
     }
-    ddp[q] = contrib;
+    g[2 * q] = contrib;  // the tile is finished: reuse its slot for d_depth of bin i
   }
   if (pt) {
 #pragma unroll
@@ -880,12 +878,12 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
   }
   __syncthreads();
   if (d_depth) {
-    const double* dd0 = reinterpret_cast<double*>(smem_raw) + (size_t)B * (kTile * kTile * 2);
+    const double* dd0 = reinterpret_cast<double*>(smem_raw);
     for (int q = threadIdx.x; q < kTile * kTile; q += blockDim.x) {
       const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
       if (px >= W || py >= H) continue;
       double s = 0.0;
-      for (int b = 0; b < B; ++b) s += dd0[(size_t)b * kTile * kTile + q];  // bin order
+      for (int b = 0; b < B; ++b) s += dd0[(size_t)b * kTile * kTile * 2 + 2 * q];  // bin order
       d_depth[(size_t)w * HW + py * W + px] = s;
     }
   }
@@ -985,12 +983,11 @@ void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint8_t* mask, const double* pose_tab, const double* K,
                       double* d_depth, double* pose_part, double* grad_out) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
-  const size_t smem = (size_t)P.B * (kTile * kTile * 3 * sizeof(double) + kBwdWarpBytes);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bwd_owner, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)kMaxBins * (kTile * kTile * 3 * sizeof(double) + kBwdWarpBytes)));
-    attr = true;
+  const size_t smem = (size_t)P.B * (kTile * kTile * 2 * sizeof(double) + kBwdWarpBytes);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(k_bwd_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
   }
   count_launch();
   k_bwd_owner<<<dim3(TP.nT, P.n_windows), 32 * P.B, smem, s>>>(
