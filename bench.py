@@ -104,7 +104,7 @@ def algorithmic_bytes(wl, n_windows):
 
 
 # evcm_cuda_stage_times order for the default (owner-computes) pipeline
-STAGES = ["staging_sort", "motion_field", "traj_records", "fwd_owner", "loss_finalize",
+STAGES = ["staging", "motion_field", "sort", "traj_records", "fwd_owner", "loss_finalize",
           "bwd_event", "bwd_owner", "pose_finalize"]
 
 
@@ -305,7 +305,7 @@ def cuda_arm(args, wl):
             starts[i].record(stream)
             step()
             ends[i].record(stream)
-            stage_ms += np.array(eng.stage_times_ms()[: len(STAGES)])
+            stage_ms += np.array((eng.stage_times_ms() + [0.0] * len(STAGES))[: len(STAGES)])
         torch.cuda.synchronize(dev)
         clk = clocks.stop()
         if world > 1:

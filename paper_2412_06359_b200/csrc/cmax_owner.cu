@@ -1,30 +1,36 @@
-// Owner-computes CMax pipeline (sm_100a): no global atomics on the IWE stack
-// or the flow gradients, no memsets of them, loss/coefficients fused into the
-// splat, flows-backward fused into the gradient gather. See DESIGN.md §Kernels.
+// Owner-computes CMax pipeline (sm_100a): no global atomics on the IWE stack or
+// the flow gradients and no memsets of them; the focus loss and the per-pixel
+// loss coefficients are fused into the stack accumulation, and the flows
+// backward is fused into the gradient gather. See DESIGN.md §Kernels.
 //
-//   k_stage_hist    validate + pack events (8 B) + per-(tile, chunk) histogram
-//   k_sort_scan     exclusive scan of the histogram -> stable slots per tile
-//   k_sort_scatter  stable counting sort of the events by source tile (16x16 px)
-//   k_bin_ptr       per source tile: first event of every time bin
-//   k_traj_records  trajectory (warp.hpp:257-281, exact fp64) -> per (event, ref)
-//                   splat record {cell, pol, dt, compressed bilinear fractions}
-//                   + per (source tile, ref) bounding box of the cells
-//   k_fwd_owner     one warp per (window, owner tile, ref): gathers every record
-//                   landing on its 16x16 tile (sources found through the boxes),
-//                   accumulates count/tsum in fp64 shared memory in a fixed order,
-//                   then writes the per-pixel loss coefficients and the loss /
-//                   n_active partials (IweStack + reference_loss + refresh_active)
-//   k_bwd_event     per event: splat_position_grad at every reference + the
-//                   adjoint sweep (engine.hpp:475-504) -> one (gx, gy) per bin
-//   k_bwd_owner     one warp per (window, owner tile): for every bin gathers the
-//                   (gx, gy) of all events whose sink cell touches the tile
-//                   (BufferGradSink::add, warp.hpp:394-406), then applies
-//                   depth_pose_to_flows_backward (geometry.hpp:300-322) to the
-//                   finished gradient tile: d_depth and pose partials.
+//   k_stage_pack    validate (EventSlice::validate) + pack events to 8 B
+//   k_key_hist      position of every event at the middle reference (the exact
+//                   trajectory arithmetic of warp.hpp:257-281, partial legs)
+//                   -> 8x8 px sort-tile key + per-(tile, chunk) histogram
+//   k_sort_scan     exclusive scan of the histogram
+//   k_sort_scatter  stable counting sort of the events by key
+//   k_bin_ptr       per sort tile: first event of every time bin
+//   k_traj_records  full trajectory -> per (event, ref) splat record {cell, pol,
+//                   dt, compressed bilinear fractions} + per (sort tile, slot)
+//                   boxes of the cells (slots 0..B: references, B+1..2B: source
+//                   pixel of the events of bin j)
+//   k_build_lists   per (slot, owner tile): the sort tiles whose box touches it
+//   k_fwd_owner     per (window, 32x16 owner tile, ref): fp64 count/tsum of
+//                   every record landing on the tile (fixed order) -> n_active,
+//                   reference_loss terms, splat_position_grad coefficients
+//   k_bwd_event     per event: splat_position_grad at every ref + adjoint sweep
+//                   (engine.hpp:475-504) -> one (gx, gy) per bin
+//   k_bwd_owner     per (window, owner tile, bin group): gradient tile per bin
+//                   (BufferGradSink::add) + fused depth_pose_to_flows_backward
 //
-// Determinism: the sort is stable, owners visit sources in index order and
-// events in sorted order, lanes resolve shared-pixel conflicts in lane order,
-// and every partial sum is reduced in a fixed order -> bit-stable run to run.
+// Sorting by the position at the middle reference keeps every sort tile compact
+// at every reference (a tile of source pixels would smear along the motion by
+// |flow| x window), so each record is read by ~2 owner tiles.
+//
+// Determinism: stable sort; owners visit sort tiles in index order and events
+// in sorted order; lanes resolve shared-pixel conflicts in lane order; per-warp
+// shared copies are merged in warp order; every partial sum is reduced in a
+// fixed order -> results are bit-stable run to run.
 #include <cstdint>
 
 #include "cmax_device.cuh"
@@ -39,15 +45,11 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kDead = 0xffffffffu;
-constexpr int kListCap = 128;  // sources buffered per owner scan round
-
-__device__ __forceinline__ int tile_of(int x, int y, int ntx) {
-  return (y / kTile) * ntx + (x / kTile);
-}
+constexpr int kOwnPx = kOwnW * kOwnH;
 
 // Bilinear fractions compressed to one float each with full relative precision
-// on the smaller of (w, 1-w): f = w if w < 0.5 else -(1-w) (sign bit marks the
-// second form, so -0.0 encodes w = 1).
+// on the smaller of (w, 1-w): f = w if w < 0.5 else -(1-w) (the sign bit marks
+// the second form, so -0.0 encodes w = 1).
 __device__ __forceinline__ float compress_frac(double w) {
   return w < 0.5 ? (float)w : -(float)(1.0 - w);
 }
@@ -75,32 +77,41 @@ __device__ __forceinline__ CellW decode(const FwdRec& r) {
   return c;
 }
 
-// Lane-ordered accumulation of (v0, v1) into a warp-private shared tile:
-// lanes sharing `key` are summed in lane order by the lowest lane, which then
-// does a plain read-modify-write. key < 0: no contribution.
+__device__ __forceinline__ double corner_w(const CellW& c, int q) {
+  return (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy : c.wx * c.wy;
+}
+
+// Lane-ordered accumulation of (v0, v1) into a warp-private shared tile: lanes
+// sharing `key` are summed in lane order by the lowest of them, which then does
+// a plain read-modify-write. key < 0: no contribution. Warp-collective.
 __device__ __forceinline__ void warp_accumulate2(double* base, int key, double v0, double v1) {
   const unsigned act = __ballot_sync(kFull, key >= 0);
   if (key >= 0) {
     const unsigned peers = __match_any_sync(act, key);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
-    double s0 = 0.0, s1 = 0.0;
-    if (lane == leader) {
-      s0 = base[2 * key];
-      s1 = base[2 * key + 1];
-    }
-    unsigned m = peers;
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const double a = __shfl_sync(peers, v0, src);
-      const double b = __shfl_sync(peers, v1, src);
-      s0 += a;
-      s1 += b;
-    }
-    if (lane == leader) {
-      base[2 * key] = s0;
-      base[2 * key + 1] = s1;
+    if (peers == (1u << lane)) {  // common case: no other lane on this pixel
+      base[2 * key] += v0;
+      base[2 * key + 1] += v1;
+    } else {
+      double s0 = 0.0, s1 = 0.0;
+      if (lane == leader) {
+        s0 = base[2 * key];
+        s1 = base[2 * key + 1];
+      }
+      unsigned m = peers;
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const double a = __shfl_sync(peers, v0, src);
+        const double b = __shfl_sync(peers, v1, src);
+        s0 += a;
+        s1 += b;
+      }
+      if (lane == leader) {
+        base[2 * key] = s0;
+        base[2 * key + 1] = s1;
+      }
     }
   }
   __syncwarp();
@@ -111,13 +122,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Scan the source boxes of reference r for window w and call fn(S) for every
-// source tile whose cells can touch owner tile (tx0, ty0), in increasing S.
+__device__ __forceinline__ int sort_tile_of(double x, double y, const WinParams& P,
+                                            const TileParams& TP) {
+  const double xm = (double)(P.W - 1), ym = (double)(P.H - 1);
+  const double cx = x < 0.0 ? 0.0 : (xm < x ? xm : x);  // also maps NaN to 0 via the casts below
+  const double cy = y < 0.0 ? 0.0 : (ym < y ? ym : y);
+  int ix = (int)cx, iy = (int)cy;
+  ix = ix < 0 ? 0 : (ix >= P.W ? P.W - 1 : ix);
+  iy = iy < 0 ? 0 : (iy >= P.H ? P.H - 1 : iy);
+  return (iy / kSortTile) * TP.ntx + ix / kSortTile;
+}
+
+// Scan every box of one slot (sort tiles, increasing) and call fn(S) for those
+// whose cells can touch the owner rectangle [ox0, ox0+kOwnW) x [oy0, oy0+kOwnH).
+// The slow path for overflowed owner lists. Warp-collective.
 template <typename Fn>
-__device__ __forceinline__ void for_each_source(const uint4* __restrict__ bbox, int nT, int tx0,
-                                                int ty0, uint16_t* list, Fn&& fn) {
+__device__ __forceinline__ void scan_sources(const uint4* __restrict__ bbox, int nT, int ox0,
+                                             int oy0, uint16_t* list, int cap, Fn&& fn) {
   const int lane = threadIdx.x & 31;
-  const int lx = tx0 - 1, hx = tx0 + kTile - 1, ly = ty0 - 1, hy = ty0 + kTile - 1;
+  const int lx = ox0 - 1, hx = ox0 + kOwnW - 1, ly = oy0 - 1, hy = oy0 + kOwnH - 1;
   int fill = 0;
   for (int s0 = 0; s0 < nT; s0 += 32) {
     const int S = s0 + lane;
@@ -133,7 +156,7 @@ __device__ __forceinline__ void for_each_source(const uint4* __restrict__ bbox, 
     const unsigned hits = __ballot_sync(kFull, hit);
     if (hit) list[fill + __popc(hits & ((1u << lane) - 1u))] = (uint16_t)S;
     fill += __popc(hits);
-    if (fill > kListCap - 32 || s0 + 32 >= nT) {
+    if (fill > cap - 32 || s0 + 32 >= nT) {
       __syncwarp();
       for (int i = 0; i < fill; ++i) fn((int)list[i]);
       __syncwarp();
@@ -142,26 +165,54 @@ __device__ __forceinline__ void for_each_source(const uint4* __restrict__ bbox, 
   }
 }
 
+// Sorted source list of one (window, slot, owner tile) into `list`; returns its
+// length, or -1 when the precomputed list overflowed. Single thread.
+__device__ __forceinline__ int load_sorted_list(const uint32_t* __restrict__ lcount,
+                                                const uint16_t* __restrict__ lists, size_t slotT,
+                                                uint16_t* list) {
+  const uint32_t cnt = lcount[slotT];
+  if (cnt > (uint32_t)kListCapO) return -1;
+  const uint16_t* src = lists + slotT * kListCapO;
+  for (uint32_t i = 0; i < cnt; ++i) {  // insertion sort, lists are short
+    const uint16_t v = src[i];
+    int j = (int)i - 1;
+    while (j >= 0 && list[j] > v) {
+      list[j + 1] = list[j];
+      --j;
+    }
+    list[j + 1] = v;
+  }
+  return (int)cnt;
+}
+
+// Virtual concatenation of event ranges: pre[l] = sum of earlier lengths,
+// rng[l] = first slot of range l. Returns the slot of virtual index v.
+__device__ __forceinline__ uint32_t virt_slot(const uint32_t* pre, const uint32_t* rng, int nl,
+                                              uint32_t v, int* which) {
+  int lo = 0, hi = nl - 1;  // largest l with pre[l] <= v
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  *which = lo;
+  return rng[lo] + (v - pre[lo]);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// sort
+// staging and sort
 
-__global__ void __launch_bounds__(kSortThreads) k_stage_hist(
+__global__ void __launch_bounds__(kSortThreads) k_stage_pack(
     const evcm_event* __restrict__ ev, const uint64_t* __restrict__ ev_off, WinParams P,
-    TileParams TP, uint2* __restrict__ packed, uint32_t* __restrict__ counts,
-    unsigned long long* __restrict__ err) {
-  extern __shared__ uint32_t hist[];
-  for (int i = threadIdx.x; i < TP.nT; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
+    uint2* __restrict__ packed, unsigned long long* __restrict__ err) {
   const int w = blockIdx.y;
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
-  const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
-  const uint64_t c1 = c0 + kChunk < n ? c0 + kChunk : n;
-  for (uint64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
     const evcm_event e = ev[base + k];
-    unsigned code = 0;
+    unsigned code = 0;  // EventSlice::validate order (types.hpp:143-155)
     if (e.x >= P.W || e.y >= P.H) code = 3;
     else if (e.p != 1 && e.p != -1) code = 4;
     else if (k > 0 && e.t_us < ev[base + k - 1].t_us) code = 5;
@@ -174,7 +225,63 @@ __global__ void __launch_bounds__(kSortThreads) k_stage_hist(
     const uint32_t dt = (uint32_t)(e.t_us - P.t0);
     packed[base + k] = make_uint2(dt | (e.p > 0 ? 0u : 0x80000000u),
                                   (uint32_t)e.x | ((uint32_t)e.y << 16));
-    atomicAdd(&hist[tile_of(e.x, e.y, TP.ntx)], 1u);
+  }
+}
+
+// Position at the middle reference rm = (B+1)/2 with the exact arithmetic of
+// build_trajectory (only the leg from the event towards rm) -> sort key.
+__global__ void __launch_bounds__(kSortThreads) k_key_hist(
+    const uint2* __restrict__ packed, const uint64_t* __restrict__ ev_off, WinParams P,
+    TileParams TP, const double2* __restrict__ flows, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double es[kMaxRefs];
+  __shared__ uint32_t erel[kMaxRefs];
+  for (int i = threadIdx.x; i < TP.nT; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
+    es[i] = P.es[i];
+    erel[i] = P.erel[i];
+  }
+  __syncthreads();
+  const int w = blockIdx.y, W = P.W, H = P.H, HW = P.HW, B = P.B;
+  const int rm = (B + 1) / 2;
+  const uint64_t base = ev_off[w];
+  const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
+  const uint64_t c1 = c0 + kChunk < n ? c0 + kChunk : n;
+  const double2* fl = flows + (size_t)w * B * HW;
+  for (uint64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const uint2 e = packed[base + k];
+    if (e.y == kDead) {
+      keys[base + k] = kDead;
+      continue;
+    }
+    const uint32_t dtu = ev_dt(e);
+    const double t = dm((double)dtu, 1e-6);
+    const int j = bin_of(dtu, erel, B);
+    const double x0 = (double)ev_x(e), y0 = (double)ev_y(e);
+    const double2 u0 = sample_flow(fl + (size_t)j * HW, bilin_cell(x0, y0, W, H));
+    double2 p;
+    if (rm <= j) {  // backward leg down to rm
+      const double db = ds(es[j], t);
+      p = make_double2(da(x0, dm(db, u0.x)), da(y0, dm(db, u0.y)));
+      for (int i = j; i > rm; --i) {
+        const double dt = ds(es[i - 1], es[i]);
+        const double2 u = sample_flow(fl + (size_t)(i - 1) * HW, bilin_cell(p.x, p.y, W, H));
+        p = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
+      }
+    } else {  // forward leg up to rm
+      const double df = ds(es[j + 1], t);
+      p = make_double2(da(x0, dm(df, u0.x)), da(y0, dm(df, u0.y)));
+      for (int i = j + 1; i < rm; ++i) {
+        const double dt = ds(es[i + 1], es[i]);
+        const double2 u = sample_flow(fl + (size_t)i * HW, bilin_cell(p.x, p.y, W, H));
+        p = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
+      }
+    }
+    const uint32_t key = (uint32_t)sort_tile_of(p.x, p.y, P, TP);
+    keys[base + k] = key;
+    atomicAdd(&hist[key], 1u);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < TP.nT; t += blockDim.x)
@@ -193,7 +300,6 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ count
   const size_t lo = threadIdx.x * per, hi = lo + per < E ? lo + per : E;
   uint32_t sum = 0;
   for (size_t i = lo; i < hi; ++i) sum += c[i];
-  // block exclusive scan of `sum`
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t x = sum;
   for (int o = 1; o < 32; o <<= 1) {
@@ -222,10 +328,12 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ count
   if (threadIdx.x == blockDim.x - 1) tp[TP.nT] = run;
 }
 
-// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*512, +512).
+// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*512, +512);
+// per-warp tile counts give each warp its base inside the chunk's segment.
 __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
-    const uint2* __restrict__ packed, const uint64_t* __restrict__ ev_off, TileParams TP,
-    const uint32_t* __restrict__ offsets, uint2* __restrict__ sorted, uint32_t* __restrict__ perm) {
+    const uint2* __restrict__ packed, const uint32_t* __restrict__ keys,
+    const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
+    uint2* __restrict__ sorted, uint32_t* __restrict__ perm) {
   extern __shared__ uint16_t whist[];  // [16 warps][nT]
   const int nW = kSortThreads / 32;
   for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
@@ -235,13 +343,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
   const uint64_t n = ev_off[w + 1] - base;
   const uint64_t k0 = (uint64_t)blockIdx.x * kChunk + (uint64_t)wid * (kChunk / nW);
   uint16_t* mine = whist + wid * TP.nT;
-  // pass 1: per-warp tile counts
-  for (int b = 0; b < kChunk / nW; b += 32) {
+  for (int b = 0; b < kChunk / nW; b += 32) {  // pass 1: per-warp counts
     const uint64_t k = k0 + b + lane;
     int t = -1;
     if (k < n) {
-      const uint2 e = packed[base + k];
-      if (e.y != kDead) t = tile_of((int)(e.y & 0xffffu), (int)(e.y >> 16), TP.ntx);
+      const uint32_t key = keys[base + k];
+      if (key != kDead) t = (int)key;
     }
     const unsigned act = __ballot_sync(kFull, t >= 0);
     if (t >= 0) {
@@ -251,8 +358,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
     __syncwarp();
   }
   __syncthreads();
-  // pass 2: exclusive prefix over warps, per tile
-  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) {
+  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) {  // pass 2: prefix over warps
     uint16_t run = 0;
     for (int q = 0; q < nW; ++q) {
       const uint16_t v = whist[q * TP.nT + t];
@@ -261,22 +367,20 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
     }
   }
   __syncthreads();
-  // pass 3: place in order
   const uint32_t* off = offsets + (size_t)w * TP.nT * TP.nchunks;
-  for (int b = 0; b < kChunk / nW; b += 32) {
+  for (int b = 0; b < kChunk / nW; b += 32) {  // pass 3: place in order
     const uint64_t k = k0 + b + lane;
     int t = -1;
-    uint2 e = make_uint2(0, 0);
     if (k < n) {
-      e = packed[base + k];
-      if (e.y != kDead) t = tile_of((int)(e.y & 0xffffu), (int)(e.y >> 16), TP.ntx);
+      const uint32_t key = keys[base + k];
+      if (key != kDead) t = (int)key;
     }
     const unsigned act = __ballot_sync(kFull, t >= 0);
     if (t >= 0) {
       const unsigned peers = __match_any_sync(act, t);
       const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
       const uint32_t dst = off[(size_t)t * TP.nchunks + blockIdx.x] + mine[t] + rank;
-      sorted[base + dst] = e;
+      sorted[base + dst] = packed[base + k];
       if (perm) perm[base + dst] = (uint32_t)k;
       __syncwarp(peers);
       if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
@@ -286,7 +390,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
 }
 
 // bin_ptr[w][S][b] = first sorted slot of tile S whose event bin is >= b
-// (events are time-ordered inside a tile, so bins are monotone).
+// (the stable sort keeps events time-ordered inside a tile).
 __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off,
                           WinParams P, TileParams TP, const uint32_t* __restrict__ tile_ptr,
                           uint32_t* __restrict__ bin_ptr) {
@@ -310,7 +414,7 @@ __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __re
 }
 
 // ---------------------------------------------------------------------------
-// trajectories -> splat records
+// trajectories -> splat records + per-(sort tile, slot) cell boxes
 
 __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
@@ -325,25 +429,47 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     erel[i] = P.erel[i];
   }
   __syncthreads();
-  const int w = blockIdx.y, R = P.B + 1;
+  const int w = blockIdx.y, R = P.B + 1, NS = R + P.B;
   const uint64_t base = ev_off[w];
-  const uint64_t n = tile_ptr[(size_t)w * (TP.nT + 1) + TP.nT];  // valid (sorted) events
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  const uint64_t n = tp[TP.nT];  // valid (sorted) events
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = k < n;
   bool alive = false;
   uint2 e = make_uint2(0, 0);
+  int j = 0;
+  int S = -1;
   if (valid) {
     e = sorted[base + k];
     const uint32_t dt = ev_dt(e);
     const double t = dm((double)dt, 1e-6);
-    const int j = bin_of(dt, erel, P.B);
+    j = bin_of(dt, erel, P.B);
     alive = trajectory((double)ev_x(e), (double)ev_y(e), t, j,
                        flows + (size_t)w * P.B * P.HW, P, es, pos, blockDim.x);
+    // sort tile of this slot: binary search of k in tile_ptr (events are grouped)
+    int lo = 0, hi = TP.nT - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tp[mid] <= (uint32_t)k) lo = mid; else hi = mid - 1;
+    }
+    S = lo;
   }
-  const int S = valid ? tile_of(ev_x(e), ev_y(e), TP.ntx) : -1;
   const unsigned amask = __ballot_sync(kFull, alive);
   const unsigned peers = alive ? __match_any_sync(amask, S) : 0u;
   const bool leader = alive && (threadIdx.x & 31) == __ffs(peers) - 1;
+  uint4* bb = bbox + (size_t)w * NS * TP.nT;
+  auto box_update = [&](unsigned grp, bool lead, int slot, uint32_t x0, uint32_t y0) {
+    const uint32_t mnx = __reduce_min_sync(grp, x0), mny = __reduce_min_sync(grp, y0);
+    const uint32_t cmx = __reduce_min_sync(grp, 0xffffu - x0);
+    const uint32_t cmy = __reduce_min_sync(grp, 0xffffu - y0);
+    if (lead) {
+      uint4* b = bb + (size_t)slot * TP.nT + S;
+      atomicMin(&b->x, mnx);
+      atomicMin(&b->y, mny);
+      atomicMin(&b->z, cmx);
+      atomicMin(&b->w, cmy);
+    }
+  };
   for (int r = 0; r < R; ++r) {
     FwdRec rec;
     uint32_t x0 = 0, y0 = 0;
@@ -362,91 +488,43 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
       rec.fx = rec.fy = 0.f;
     }
     if (valid) recs[(size_t)r * n_total + base + k] = rec;
-    if (alive) {
-      const uint32_t mnx = __reduce_min_sync(peers, x0), mny = __reduce_min_sync(peers, y0);
-      const uint32_t cmx = __reduce_min_sync(peers, 0xffffu - x0);
-      const uint32_t cmy = __reduce_min_sync(peers, 0xffffu - y0);
-      if (leader) {
-        uint4* b = bbox + ((size_t)w * R + r) * TP.nT + S;
-        atomicMin(&b->x, mnx);
-        atomicMin(&b->y, mny);
-        atomicMin(&b->z, cmx);
-        atomicMin(&b->w, cmy);
-      }
-    }
+    if (alive) box_update(peers, leader, r, x0, y0);
+  }
+  // source-pixel boxes per bin (the partial steps of the backward sink at x0)
+  if (alive) {
+    const unsigned g2 = __match_any_sync(amask, S * kMaxRefs + j);
+    const bool l2 = (threadIdx.x & 31) == __ffs(g2) - 1;
+    box_update(g2, l2, R + j, (uint32_t)ev_x(e), (uint32_t)ev_y(e));
   }
 }
 
 // ---------------------------------------------------------------------------
 // owner source lists
 
-// For every (window, ref, source tile) with alive events: append S to the list
-// of every owner tile its cell box can touch. Lists are unordered here; owners
-// sort them (<= kListCapO entries) so the visit order is deterministic.
+// For every (window, slot, sort tile) with alive events: append S to the list of
+// every owner tile its cell box can touch (cells touch [x0, x0+1] x [y0, y0+1]).
+// Lists are unordered here; owners sort them, so the visit order is fixed.
 __global__ void k_build_lists(const uint4* __restrict__ bbox, WinParams P, TileParams TP,
                               uint32_t* __restrict__ lcount, uint16_t* __restrict__ lists) {
-  const int S = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y, w = blockIdx.z;
+  const int S = blockIdx.x * blockDim.x + threadIdx.x, slot = blockIdx.y, w = blockIdx.z;
   if (S >= TP.nT) return;
-  const size_t wr = (size_t)w * (P.B + 1) + r;
-  const uint4 b = bbox[wr * TP.nT + S];
+  const int NS = 2 * P.B + 1;
+  const size_t ws = (size_t)w * NS + slot;
+  const uint4 b = bbox[ws * TP.nT + S];
   if (b.x == 0xffffffffu) return;
   const int mnx = (int)b.x, mny = (int)b.y, mxx = 0xffff - (int)b.z, mxy = 0xffff - (int)b.w;
-  const int tx0 = mnx / kTile, tx1 = min((mxx + 1) / kTile, TP.ntx - 1);
-  const int ty0 = mny / kTile, ty1 = min((mxy + 1) / kTile, TP.nty - 1);
+  const int tx0 = mnx / kOwnW, tx1 = min((mxx + 1) / kOwnW, TP.otx - 1);
+  const int ty0 = mny / kOwnH, ty1 = min((mxy + 1) / kOwnH, TP.oty - 1);
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
-      const size_t T = wr * TP.nT + (size_t)ty * TP.ntx + tx;
-      const uint32_t slot = atomicAdd(lcount + T, 1u);
-      if (slot < kListCapO) lists[T * kListCapO + slot] = (uint16_t)S;
+      const size_t T = ws * TP.oT + (size_t)ty * TP.otx + tx;
+      const uint32_t c = atomicAdd(lcount + T, 1u);
+      if (c < (uint32_t)kListCapO) lists[T * kListCapO + c] = (uint16_t)S;
     }
 }
-
-namespace {
-
-// Sorted source list of (wr, T) into `list`; returns its length, or -1 when the
-// precomputed list overflowed (caller then scans the boxes).
-__device__ __forceinline__ int load_sorted_list(const uint32_t* __restrict__ lcount,
-                                                const uint16_t* __restrict__ lists, size_t slotT,
-                                                uint16_t* list) {
-  const uint32_t cnt = lcount[slotT];
-  if (cnt > (uint32_t)kListCapO) return -1;
-  const uint16_t* src = lists + slotT * kListCapO;
-  for (uint32_t i = 0; i < cnt; ++i) {  // insertion sort, cnt is small
-    const uint16_t v = src[i];
-    int j = (int)i - 1;
-    while (j >= 0 && list[j] > v) {
-      list[j + 1] = list[j];
-      --j;
-    }
-    list[j + 1] = v;
-  }
-  return (int)cnt;
-}
-
-// Virtual concatenation of event ranges [a_l, a_l + len_l): pre[l] = sum of
-// earlier lengths. Returns the slot of virtual index v.
-__device__ __forceinline__ uint32_t virt_slot(const uint32_t* pre, const uint32_t* a, int nl,
-                                              uint32_t v, int* which) {
-  int lo = 0, hi = nl - 1;  // largest l with pre[l] <= v
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= v) lo = mid; else hi = mid - 1;
-  }
-  *which = lo;
-  return a[lo] + (v - pre[lo]);
-}
-
-__device__ __forceinline__ double corner_w(const CellW& c, int q) {
-  return (q == 0) ? c.ax * c.ay : (q == 1) ? c.wx * c.ay : (q == 2) ? c.ax * c.wy : c.wx * c.wy;
-}
-
-}  // namespace
 
 // ---------------------------------------------------------------------------
 // forward owner: IWE stack tile + loss partials + coefficient planes
-
-constexpr int kFwdWarps = 4;
-constexpr int kPrefetch = 4;  // records in flight per lane
 
 __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
@@ -454,24 +532,24 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
     const uint16_t* __restrict__ lists, double2* __restrict__ coef, double2* __restrict__ stack_out,
     double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
-  __shared__ __align__(16) double acc[kFwdWarps][kTile * kTile * 4];  // [warp][px][C0,S0,C1,S1]
-  __shared__ uint16_t list[kListCap];
-  __shared__ uint32_t pre[kListCap + 1], rng[kListCap];
+  extern __shared__ __align__(16) double acc_all[];  // [warp][px][C0, S0, C1, S1]
+  __shared__ uint16_t list[kListCapO > 128 ? kListCapO : 128];
+  __shared__ uint32_t pre[kListCapO + 1], rng[kListCapO];
   __shared__ int s_nl;
   __shared__ double s_red[kFwdWarps];
   __shared__ unsigned s_act[kFwdWarps];
   const int T = blockIdx.x, r = blockIdx.y, w = blockIdx.z;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int R = P.B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
-  const size_t wr = (size_t)w * R + r;
-  for (int i = threadIdx.x; i < kFwdWarps * kTile * kTile * 4; i += blockDim.x) (&acc[0][0])[i] = 0.0;
+  const int R = P.B + 1, NS = 2 * P.B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
+  for (int i = threadIdx.x; i < kFwdWarps * kOwnPx * 4; i += blockDim.x) acc_all[i] = 0.0;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const FwdRec* rr = recs + (size_t)r * n_total + base;
   const double esr = P.es[r], win = P.window_s;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
-  double* mine = acc[wid];
+  double* mine = acc_all + (size_t)wid * kOwnPx * 4;
+  const size_t ws = (size_t)w * NS + r;
 
   auto contribute = [&](const FwdRec& rec) {
     const bool live = rec.cell != kDead;
@@ -483,16 +561,19 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
       pol = (int)(rec.cell >> 31);
       tb = dd(fabs(ds(dm((double)rec.dt, 1e-6), esr)), win);  // engine.hpp:370
     }
+    const bool any = __any_sync(kFull, live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW &&
+                                           c.y0 + oy >= oy0 && c.y0 < oy0 + kOwnH);
+    if (!any) return;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int lx = c.x0 + ((q & 1) ? ox : 0) - tx0, ly = c.y0 + ((q & 2) ? oy : 0) - ty0;
-      const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
+      const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
+      const bool in = live && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
       const double wq = corner_w(c, q);
-      warp_accumulate2(mine, in ? ((ly * kTile + lx) * 2 + pol) : -1, wq, wq * tb);
+      warp_accumulate2(mine, in ? ((ly * kOwnW + lx) * 2 + pol) : -1, wq, wq * tb);
     }
   };
 
-  if (threadIdx.x == 0) s_nl = load_sorted_list(lcount, lists, wr * TP.nT + T, list);
+  if (threadIdx.x == 0) s_nl = load_sorted_list(lcount, lists, ws * TP.oT + T, list);
   __syncthreads();
   if (s_nl >= 0) {
     const int nl = s_nl;
@@ -506,8 +587,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
       pre[nl] = run;
     }
     __syncthreads();
-    // even contiguous split of the virtual event sequence over the warps
-    const uint32_t total = pre[nl];
+    const uint32_t total = nl > 0 ? pre[nl] : 0u;
     const uint32_t v0 = (uint32_t)(((uint64_t)total * wid) / kFwdWarps);
     const uint32_t v1 = (uint32_t)(((uint64_t)total * (wid + 1)) / kFwdWarps);
     for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
@@ -526,8 +606,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
         if (vb + m * 32 < v1) contribute(rb[m]);
     }
   } else if (wid == 0) {
-    // overflowed list: scan every source box in order (slow, rare)
-    for_each_source(bbox + wr * TP.nT, TP.nT, tx0, ty0, list, [&](int S) {
+    scan_sources(bbox + ws * TP.nT, TP.nT, ox0, oy0, list, 128, [&](int S) {
       for (uint32_t kb = tp[S]; kb < tp[S + 1]; kb += 32) {
         FwdRec rec;
         rec.cell = kDead;
@@ -537,21 +616,22 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     });
   }
   __syncthreads();
-  // merge the warp copies in order, then refresh_active + reference_loss terms
-  // + splat_position_grad factors per pixel
+  // merge warp copies in warp order; refresh_active (warp.hpp:186-192),
+  // reference_loss terms (:306-309), splat_position_grad factors (:346-349)
   double lsum = 0.0;
   unsigned act = 0;
-  double2* cw = coef + wr * 2 * HW;
-  for (int q = threadIdx.x; q < kTile * kTile; q += blockDim.x) {
-    const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+  double2* cw = coef + ((size_t)w * R + r) * 2 * HW;
+  for (int q = threadIdx.x; q < kOwnPx; q += blockDim.x) {
+    const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
     if (px >= W || py >= H) continue;
-    double C0 = acc[0][4 * q], S0 = acc[0][4 * q + 1], C1 = acc[0][4 * q + 2], S1 = acc[0][4 * q + 3];
+    double C0 = acc_all[4 * q], S0 = acc_all[4 * q + 1], C1 = acc_all[4 * q + 2], S1 = acc_all[4 * q + 3];
 #pragma unroll
     for (int m = 1; m < kFwdWarps; ++m) {
-      C0 += acc[m][4 * q];
-      S0 += acc[m][4 * q + 1];
-      C1 += acc[m][4 * q + 2];
-      S1 += acc[m][4 * q + 3];
+      const double* a = acc_all + (size_t)m * kOwnPx * 4 + 4 * q;
+      C0 += a[0];
+      S0 += a[1];
+      C1 += a[2];
+      S1 += a[3];
     }
     const int g = py * W + px;
     act += (C0 + C1 > 0.0) ? 1u : 0u;
@@ -562,7 +642,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     cw[g] = make_double2(b0, b0 * i0);
     cw[HW + g] = make_double2(b1, b1 * i1);
     if (stack_out) {
-      double2* so = stack_out + wr * 2 * HW;
+      double2* so = stack_out + ((size_t)w * R + r) * 2 * HW;
       so[g] = make_double2(C0, S0);
       so[HW + g] = make_double2(C1, S1);
     }
@@ -581,8 +661,9 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
       s += s_red[m];
       a += s_act[m];
     }
-    part_acc[wr * TP.nT + T] = s;
-    part_act[wr * TP.nT + T] = a;
+    const size_t slot = ((size_t)w * R + r) * TP.oT + T;
+    part_acc[slot] = s;
+    part_act[slot] = a;
   }
 }
 
@@ -676,17 +757,19 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
 // ---------------------------------------------------------------------------
 // backward owner: gradient tile per bin + fused depth_pose_to_flows_backward
 //
-// One CTA per (window, owner tile), one warp per bin i. Warp i gathers the
-// (gx, gy) of: events with bin j > i at their reference-(i+1) cell (backward
-// leg), events with j < i at their reference-i cell (forward leg), and the
-// tile's own events with j == i at their source pixel (the two partial steps),
-// then runs the flows backward of bin i on the finished tile. d_depth sums the
-// per-bin contributions in bin order.
+// One CTA per (window, owner tile, bin group), one warp per bin i. Warp i
+// gathers the (gx, gy) of: events with bin j > i at their reference-(i+1) cell
+// (backward leg), events with j < i at their reference-i cell (forward leg),
+// and events with j == i at their source pixel (the two partial steps) --
+// BufferGradSink::add (warp.hpp:394-406) -- then runs the flows backward of
+// bin i (geometry.hpp:300-322) on the finished tile. d_depth sums the per-bin
+// contributions in bin order.
 
-constexpr int kBwdList = 2 * kListCapO + 1;
-constexpr int kBwdWarpBytes = ((kBwdList * 10 + 16 + 15) / 16) * 16;  // per-warp list state
+constexpr int kBwdSeg = 3 * kListCapO;
+constexpr int kBwdWarpBytes =
+    ((kOwnPx * 2 * 8 + kBwdSeg * 2 + (kBwdSeg + 1) * 4 + kBwdSeg * 4 + 15) / 16) * 16;
 
-__global__ void __launch_bounds__(1024) k_bwd_owner(
+__global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
     const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
@@ -696,92 +779,119 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
     double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int T = blockIdx.x, w = blockIdx.y, lane = threadIdx.x & 31, i = threadIdx.x >> 5;
-  const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
-  // per-warp shared state
-  double* g = reinterpret_cast<double*>(smem_raw) + (size_t)i * (kTile * kTile * 2);
-  unsigned char* wst = smem_raw + (size_t)B * kTile * kTile * 2 * sizeof(double) +
-                       (size_t)i * kBwdWarpBytes;
-  uint32_t* pre = reinterpret_cast<uint32_t*>(wst);             // kBwdList + 1
-  uint32_t* rng = pre + (kBwdList + 1);                          // kBwdList
-  uint16_t* lst = reinterpret_cast<uint16_t*>(rng + kBwdList);   // kBwdList (S per entry)
-  const int tx0 = (T % TP.ntx) * kTile, ty0 = (T / TP.ntx) * kTile;
+  const int T = blockIdx.x, grp = blockIdx.y, w = blockIdx.z;
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int B = P.B, R = B + 1, NS = 2 * B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int i = grp * kBwdGroup + wq;          // this warp's bin
+  const int nb = min(kBwdGroup, B - grp * kBwdGroup);  // bins in this CTA
+  unsigned char* wst = smem_raw + (size_t)wq * kBwdWarpBytes;
+  double* g = reinterpret_cast<double*>(wst);                            // [px][gu, gv]
+  uint32_t* pre = reinterpret_cast<uint32_t*>(wst + kOwnPx * 2 * 8);     // kBwdSeg + 1
+  uint32_t* rng = pre + (kBwdSeg + 1);                                    // kBwdSeg
+  uint16_t* lst = reinterpret_cast<uint16_t*>(rng + kBwdSeg);             // kBwdSeg
+  const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
-  const bool skip = no_surv[w] != 0;
-  for (int q = lane; q < kTile * kTile * 2; q += 32) g[q] = 0.0;
+  const bool active = wq < nb;
+  for (int q = lane; q < kOwnPx * 2; q += 32) g[q] = 0.0;
   __syncwarp();
 
-  if (!skip) {
+  if (active && !no_surv[w]) {
     const float2* bi = bwd + (size_t)i * n_total + base;
-    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward leg cells
-    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward leg cells
-    const size_t slotA = ((size_t)w * R + i + 1) * TP.nT + T, slotB = ((size_t)w * R + i) * TP.nT + T;
-    int nA = 0, nB = 0;
+    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
+    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
+    const size_t sA = ((size_t)w * NS + i + 1) * TP.oT + T;
+    const size_t sB = ((size_t)w * NS + i) * TP.oT + T;
+    const size_t sC = ((size_t)w * NS + R + i) * TP.oT + T;
+    int nA = 0, nB = 0, nC = 0;
     if (lane == 0) {
-      nA = load_sorted_list(lcount, lists, slotA, lst);
-      nB = nA >= 0 ? load_sorted_list(lcount, lists, slotB, lst + nA) : -1;
+      nA = load_sorted_list(lcount, lists, sA, lst);
+      nB = nA >= 0 ? load_sorted_list(lcount, lists, sB, lst + nA) : -1;
+      nC = nB >= 0 ? load_sorted_list(lcount, lists, sC, lst + nA + nB) : -1;
     }
     nA = __shfl_sync(kFull, nA, 0);
     nB = __shfl_sync(kFull, nB, 0);
-    auto accumulate = [&](const FwdRec& rec, float2 v) {
+    nC = __shfl_sync(kFull, nC, 0);
+    auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
       const bool live = rec.cell != kDead;
       CellW c{};
       if (live) c = decode(rec);
+      const bool any = __any_sync(kFull, live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW &&
+                                             c.y0 + oy >= oy0 && c.y0 < oy0 + kOwnH);
+      if (!any) return;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int lx = c.x0 + ((q & 1) ? ox : 0) - tx0, ly = c.y0 + ((q & 2) ? oy : 0) - ty0;
-        const bool in = live && lx >= 0 && lx < kTile && ly >= 0 && ly < kTile;
-        const double wq = corner_w(c, q);
-        warp_accumulate2(g, in ? (ly * kTile + lx) : -1, wq * (double)v.x, wq * (double)v.y);
+        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
+        const bool in = live && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
+        const double wgt = corner_w(c, q);
+        warp_accumulate2(g, in ? (ly * kOwnW + lx) : -1, wgt * (double)v.x, wgt * (double)v.y);
       }
     };
-    if (nA >= 0 && nB >= 0) {
-      // virtual sequence: list A ranges (j > i), list B ranges (j < i)
+    auto pixel_key = [&](uint32_t k) {  // source pixel of sorted event k if inside the tile
+      const uint2 e = sorted[base + k];
+      const int lx = ev_x(e) - ox0, ly = ev_y(e) - oy0;
+      return (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) ? ly * kOwnW + lx : -1;
+    };
+    if (nA >= 0 && nB >= 0 && nC >= 0) {
+      const int nl = nA + nB + nC;
       if (lane == 0) {
         uint32_t run = 0;
-        for (int l = 0; l < nA; ++l) {
+        for (int l = 0; l < nl; ++l) {
           const int S = lst[l];
           pre[l] = run;
-          rng[l] = bp[(size_t)S * (B + 1) + i + 1];
-          run += tp[S + 1] - rng[l];
+          uint32_t a, z;
+          if (l < nA) {
+            a = bp[(size_t)S * (B + 1) + i + 1];
+            z = tp[S + 1];
+          } else if (l < nA + nB) {
+            a = tp[S];
+            z = bp[(size_t)S * (B + 1) + i];
+          } else {
+            a = bp[(size_t)S * (B + 1) + i];
+            z = bp[(size_t)S * (B + 1) + i + 1];
+          }
+          rng[l] = a;
+          run += z - a;
         }
-        for (int l = nA; l < nA + nB; ++l) {
-          const int S = lst[l];
-          pre[l] = run;
-          rng[l] = tp[S];
-          run += bp[(size_t)S * (B + 1) + i] - tp[S];
-        }
-        pre[nA + nB] = run;
+        pre[nl] = run;
       }
       __syncwarp();
-      const int nl = nA + nB;
-      const uint32_t total = pre[nl];
-      const uint32_t splitAB = pre[nA];
+      const uint32_t total = nl > 0 ? pre[nl] : 0u;
+      const uint32_t sAB = nl > 0 ? pre[nA] : 0u, sBC = nl > 0 ? pre[nA + nB] : 0u;
       for (uint32_t vb = 0; vb < total; vb += 32 * kPrefetch) {
         FwdRec rb[kPrefetch];
         float2 vv[kPrefetch];
+        int pk[kPrefetch];
 #pragma unroll
         for (int m = 0; m < kPrefetch; ++m) {
           const uint32_t v = vb + m * 32 + lane;
           rb[m].cell = kDead;
           vv[m] = make_float2(0.f, 0.f);
+          pk[m] = -1;
           if (v < total) {
             int l;
             const uint32_t k = virt_slot(pre, rng, nl, v, &l);
-            rb[m] = (v < splitAB) ? rA[k] : rB[k];
-            if (rb[m].cell != kDead) vv[m] = bi[k];
+            if (v < sBC) {
+              rb[m] = (v < sAB) ? rA[k] : rB[k];
+              if (rb[m].cell != kDead) vv[m] = bi[k];
+            } else if (recs[base + k].cell != kDead) {
+              pk[m] = pixel_key(k);
+              if (pk[m] >= 0) vv[m] = bi[k];
+            }
           }
         }
 #pragma unroll
-        for (int m = 0; m < kPrefetch; ++m)
-          if (vb + m * 32 < total) accumulate(rb[m], vv[m]);
+        for (int m = 0; m < kPrefetch; ++m) {
+          if (vb + m * 32 >= total) break;
+          if (vb + m * 32 < sBC) accumulate(rb[m], vv[m]);
+          if (vb + m * 32 + 31 >= sBC) warp_accumulate2(g, pk[m], (double)vv[m].x, (double)vv[m].y);
+        }
       }
     } else {
-      // overflowed lists: scan the source boxes (slow, rare)
-      for_each_source(bbox + slotA - T, TP.nT, tx0, ty0, lst, [&](int S) {
+      // an owner list overflowed: scan the sort-tile boxes in order (slow, rare)
+      scan_sources(bbox + ((size_t)w * NS + i + 1) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
         const uint32_t k1 = tp[S + 1];
         for (uint32_t kb = bp[(size_t)S * (B + 1) + i + 1]; kb < k1; kb += 32) {
           FwdRec rec;
@@ -794,7 +904,7 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
           accumulate(rec, v);
         }
       });
-      for_each_source(bbox + slotB - T, TP.nT, tx0, ty0, lst, [&](int S) {
+      scan_sources(bbox + ((size_t)w * NS + i) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
         const uint32_t k1 = bp[(size_t)S * (B + 1) + i];
         for (uint32_t kb = tp[S]; kb < k1; kb += 32) {
           FwdRec rec;
@@ -807,85 +917,101 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
           accumulate(rec, v);
         }
       });
-    }
-    // partial steps of this tile's events with bin j == i, at their source pixel
-    {
-      const uint32_t k0 = bp[(size_t)T * (B + 1) + i], k1 = bp[(size_t)T * (B + 1) + i + 1];
-      for (uint32_t kb = k0; kb < k1; kb += 32) {
-        const uint32_t k = kb + lane;
-        int key = -1;
-        float2 v = make_float2(0.f, 0.f);
-        if (k < k1 && recs[base + k].cell != kDead) {
-          const uint2 e = sorted[base + k];
-          key = (ev_y(e) - ty0) * kTile + (ev_x(e) - tx0);
-          v = bi[k];
+      scan_sources(bbox + ((size_t)w * NS + R + i) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
+        const uint32_t k1 = bp[(size_t)S * (B + 1) + i + 1];
+        for (uint32_t kb = bp[(size_t)S * (B + 1) + i]; kb < k1; kb += 32) {
+          const uint32_t k = kb + lane;
+          int key = -1;
+          float2 v = make_float2(0.f, 0.f);
+          if (k < k1 && recs[base + k].cell != kDead) {
+            key = pixel_key(k);
+            if (key >= 0) v = bi[k];
+          }
+          warp_accumulate2(g, key, (double)v.x, (double)v.y);
         }
-        warp_accumulate2(g, key, (double)v.x, (double)v.y);
-      }
+      });
     }
   }
   __syncwarp();
 
   // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
-  const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
-  double c6[6] = {0, 0, 0, 0, 0, 0};
-  for (int q = lane; q < kTile * kTile; q += 32) {
-    const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
-    const double gu = g[2 * q], gv = g[2 * q + 1];
-    double contrib = 0.0;
-    if (px < W && py < H) {
-      const int gq = py * W + px;
-      if (grad_out) {
-        grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
-        grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
-      }
-      const double d = pt ? depth[(size_t)w * HW + gq] : 0.0;
-      const bool ok = pt && (!mask || mask[(size_t)w * HW + gq]) && d > 0.0;
-      if (ok && (gu != 0.0 || gv != 0.0)) {
-        const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
-        const double ry = 1.0 * ((double)py - cy) / fy;
-        const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
-        const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
-        const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
-        const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
-        if (p2 > 0.0) {
-          const double inv_dt = pt[39], iz = 1.0 / p2;
-          const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-          const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-          contrib = (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-          c6[3] += gu * ju0 * inv_dt;
-          c6[4] += gv * jv1 * inv_dt;
-          c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
+  if (active) {
+    const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
+    double c6[6] = {0, 0, 0, 0, 0, 0};
+    for (int q = lane; q < kOwnPx; q += 32) {
+      const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
+      const double gu = g[2 * q], gv = g[2 * q + 1];
+      double contrib = 0.0;
+      if (px < W && py < H) {
+        const int gq = py * W + px;
+        if (grad_out) {
+          grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
+          grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
+        }
+        const double d = pt ? depth[(size_t)w * HW + gq] : 0.0;
+        const bool ok = pt && (!mask || mask[(size_t)w * HW + gq]) && d > 0.0;
+        if (ok && (gu != 0.0 || gv != 0.0)) {
+          const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
+          const double ry = 1.0 * ((double)py - cy) / fy;
+          const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
+          const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
+          const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
+          const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
+          if (p2 > 0.0) {
+            const double inv_dt = pt[39], iz = 1.0 / p2;
+            const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+            const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+            contrib = (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+            c6[3] += gu * ju0 * inv_dt;
+            c6[4] += gv * jv1 * inv_dt;
+            c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double* dR = pt + 9 + 9 * a;
-            const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-            const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-            const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-            c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
+            for (int a = 0; a < 3; ++a) {
+              const double* dR = pt + 9 + 9 * a;
+              const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
+              const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
+              const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
+              c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) *
+                       inv_dt;
+            }
           }
         }
       }
+      g[2 * q] = contrib;  // tile finished: reuse the slot for this bin's d_depth
     }
-    g[2 * q] = contrib;  // the tile is finished: reuse its slot for d_depth of bin i
-  }
-  if (pt) {
+    if (pt) {
 #pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      const double v = warp_sum(c6[a]);
-      if (lane == 0) pose_part[(((size_t)w * TP.nT + T) * B + i) * 6 + a] = v;
+      for (int a = 0; a < 6; ++a) {
+        const double v = warp_sum(c6[a]);
+        if (lane == 0) pose_part[(((size_t)w * TP.oT + T) * B + i) * 6 + a] = v;
+      }
     }
   }
   __syncthreads();
   if (d_depth) {
-    const double* dd0 = reinterpret_cast<double*>(smem_raw);
-    for (int q = threadIdx.x; q < kTile * kTile; q += blockDim.x) {
-      const int px = tx0 + (q % kTile), py = ty0 + (q / kTile);
+    const int G = (B + kBwdGroup - 1) / kBwdGroup;
+    for (int q = threadIdx.x; q < kOwnPx; q += blockDim.x) {
+      const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
       if (px >= W || py >= H) continue;
       double s = 0.0;
-      for (int b = 0; b < B; ++b) s += dd0[(size_t)b * kTile * kTile * 2 + 2 * q];  // bin order
-      d_depth[(size_t)w * HW + py * W + px] = s;
+      for (int b = 0; b < nb; ++b)  // bin order
+        s += reinterpret_cast<const double*>(smem_raw + (size_t)b * kBwdWarpBytes)[2 * q];
+      // G == 1: d_depth [w][HW]; G > 1: per-group partial planes [w][grp][HW]
+      d_depth[((size_t)w * G + grp) * HW + py * W + px] = s;
     }
+  }
+}
+
+// d_depth = sum over bin groups, in group order (only when B > kBwdGroup)
+__global__ void k_ddepth_sum(const double* __restrict__ parts, int G, int HW, int n_windows,
+                             double* __restrict__ d_depth) {
+  const size_t total = (size_t)n_windows * HW;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t w = i / HW, q = i % HW;
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += parts[(w * G + g) * HW + q];
+    d_depth[i] = s;
   }
 }
 
@@ -894,37 +1020,46 @@ __global__ void __launch_bounds__(1024) k_bwd_owner(
 
 TileParams make_tiles(const WinParams& P, uint64_t max_n) {
   TileParams TP;
-  TP.ntx = (P.W + kTile - 1) / kTile;
-  TP.nty = (P.H + kTile - 1) / kTile;
+  TP.ntx = (P.W + kSortTile - 1) / kSortTile;
+  TP.nty = (P.H + kSortTile - 1) / kSortTile;
   TP.nT = TP.ntx * TP.nty;
+  TP.otx = (P.W + kOwnW - 1) / kOwnW;
+  TP.oty = (P.H + kOwnH - 1) / kOwnH;
+  TP.oT = TP.otx * TP.oty;
   TP.nchunks = (int)std::max<uint64_t>(1, (max_n + kChunk - 1) / kChunk);
   return TP;
 }
 
-size_t sort_scatter_smem(const TileParams& TP) { return (size_t)(kSortThreads / 32) * TP.nT * 2; }
-
-void launch_sort(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
-                 const TileParams& TP, uint2* packed, uint32_t* counts, unsigned long long* err,
-                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_stage_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sort_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+static void set_smem(const void* fn, size_t bytes, size_t* have) {
+  if (bytes > 48 * 1024 && bytes > *have) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    *have = bytes;
   }
+}
+
+void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off,
+                       const WinParams& P, uint64_t max_n, uint2* packed, unsigned long long* err) {
+  const int blocks = (int)std::min<uint64_t>((max_n + kSortThreads - 1) / kSortThreads, 148 * 8);
+  if (blocks == 0) return;
+  count_launch();
+  k_stage_pack<<<dim3(blocks, P.n_windows), kSortThreads, 0, s>>>(ev, ev_off, P, packed, err);
+}
+
+void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
+                 const TileParams& TP, const double2* flows, uint32_t* keys, uint32_t* counts,
+                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm, uint32_t* bin_ptr) {
+  static size_t a1 = 0, a2 = 0;
+  set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
+  set_smem(reinterpret_cast<const void*>(k_sort_scatter), (size_t)(kSortThreads / 32) * TP.nT * 2, &a2);
   const dim3 grid(TP.nchunks, P.n_windows);
   count_launch();
-  k_stage_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(ev, ev_off, P, TP, packed,
-                                                                     counts, err);
+  k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, flows,
+                                                                  keys, counts);
   count_launch();
   k_sort_scan<<<P.n_windows, 1024, 0, s>>>(counts, TP, tile_ptr);
   count_launch();
-  k_sort_scatter<<<grid, kSortThreads, sort_scatter_smem(TP), s>>>(packed, ev_off, TP, counts,
-                                                                   sorted, perm);
-}
-
-void launch_bin_ptr(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off, const WinParams& P,
-                    const TileParams& TP, const uint32_t* tile_ptr, uint32_t* bin_ptr) {
+  k_sort_scatter<<<grid, kSortThreads, (size_t)(kSortThreads / 32) * TP.nT * 2, s>>>(
+      packed, keys, ev_off, TP, counts, sorted, perm);
   count_launch();
   k_bin_ptr<<<dim3((TP.nT + 127) / 128, P.n_windows), 128, 0, s>>>(sorted, ev_off, P, TP,
                                                                     tile_ptr, bin_ptr);
@@ -933,25 +1068,18 @@ void launch_bin_ptr(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                          uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
-                         uint4* bbox) {
-  if (max_n == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_traj_records, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kEvSmemHeader + sizeof(double2) * (size_t)kMaxRefs * kEvBlock));
-    attr = true;
-  }
+                         uint4* bbox, uint32_t* lcount, uint16_t* lists) {
+  static size_t a = 0;
   const size_t smem = kEvSmemHeader + sizeof(double2) * (size_t)(P.B + 1) * kEvBlock;
+  set_smem(reinterpret_cast<const void*>(k_traj_records), smem, &a);
+  if (max_n > 0) {
+    count_launch();
+    k_traj_records<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock,
+                     smem, s>>>(sorted, ev_off, P, TP, tile_ptr, flows, n_total, recs, bbox);
+  }
   count_launch();
-  k_traj_records<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, smem,
-                   s>>>(sorted, ev_off, P, TP, tile_ptr, flows, n_total, recs, bbox);
-}
-
-void launch_build_lists(cudaStream_t s, const WinParams& P, const TileParams& TP,
-                        const uint4* bbox, uint32_t* lcount, uint16_t* lists) {
-  count_launch();
-  k_build_lists<<<dim3((TP.nT + 127) / 128, P.B + 1, P.n_windows), 128, 0, s>>>(bbox, P, TP,
-                                                                                lcount, lists);
+  k_build_lists<<<dim3((TP.nT + 127) / 128, 2 * P.B + 1, P.n_windows), 128, 0, s>>>(bbox, P, TP,
+                                                                                    lcount, lists);
 }
 
 void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
@@ -959,8 +1087,11 @@ void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
                       unsigned long long* part_act) {
+  static size_t a = 0;
+  const size_t smem = (size_t)kFwdWarps * kOwnPx * 4 * sizeof(double);
+  set_smem(reinterpret_cast<const void*>(k_fwd_owner), smem, &a);
   count_launch();
-  k_fwd_owner<<<dim3(TP.nT, P.B + 1, P.n_windows), 32 * kFwdWarps, 0, s>>>(
+  k_fwd_owner<<<dim3(TP.oT, P.B + 1, P.n_windows), 32 * kFwdWarps, smem, s>>>(
       ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
       part_act);
 }
@@ -975,24 +1106,31 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
       sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, bwd);
 }
 
+int bwd_groups(const WinParams& P) { return (P.B + kBwdGroup - 1) / kBwdGroup; }
+
 void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, const int* no_surv, const double* depth,
                       const uint8_t* mask, const double* pose_tab, const double* K,
-                      double* d_depth, double* pose_part, double* grad_out) {
+                      double* d_depth, double* d_depth_parts, double* pose_part,
+                      double* grad_out) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
-  const size_t smem = (size_t)P.B * (kTile * kTile * 2 * sizeof(double) + kBwdWarpBytes);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(k_bwd_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  const int G = bwd_groups(P);
+  const int warps = std::min(P.B, kBwdGroup);
+  const size_t smem = (size_t)warps * kBwdWarpBytes;
+  static size_t a = 0;
+  set_smem(reinterpret_cast<const void*>(k_bwd_owner), smem, &a);
+  double* dd_out = (d_depth && G > 1) ? d_depth_parts : d_depth;
   count_launch();
-  k_bwd_owner<<<dim3(TP.nT, P.n_windows), 32 * P.B, smem, s>>>(
+  k_bwd_owner<<<dim3(TP.oT, G, P.n_windows), 32 * warps, smem, s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
-      depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
+      depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
+  if (d_depth && G > 1) {
+    count_launch();
+    k_ddepth_sum<<<148 * 4, 256, 0, s>>>(d_depth_parts, G, P.HW, P.n_windows, d_depth);
+  }
 }
 
 }  // namespace evcm_b200

@@ -10,20 +10,26 @@
 
 namespace evcm_b200 {
 
-constexpr int kTile = 16;          // source / owner tile edge (px)
+constexpr int kSortTile = 8;       // sort tiles: 8x8 px of the position at the middle reference
+constexpr int kOwnW = 32;          // owner tiles: 32x16 px of the IWE stack / gradient planes
+constexpr int kOwnH = 16;
 constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
 constexpr int kSortThreads = 512;  // 16 warps x 512 events
 constexpr int kMaxTiles = 6000;    // sort scatter keeps 16 x nT u16 counters in smem
-constexpr int kListCapO = 64;      // precomputed source list capacity per (window, ref, owner tile)
+constexpr int kListCapO = 64;      // source-list capacity per (window, slot, owner tile)
+constexpr int kFwdWarps = 4;       // warps (private fp64 copies) per forward owner CTA
+constexpr int kPrefetch = 4;       // records in flight per lane in the owner loops
+constexpr int kBwdGroup = 12;      // bins (warps) per backward owner CTA
 
 struct TileParams {
-  int ntx, nty, nT;
-  int nchunks;  // sort chunks per window (max over the batch)
+  int ntx, nty, nT;  // sort tiles
+  int otx, oty, oT;  // owner tiles
+  int nchunks;       // sort chunks per window (max over the batch)
 };
 
 // Per (event, reference) splat record, 16 B. cell = x0 | y0 << 16 | negative
 // polarity << 31 (0xffffffff: masked event); dt = t_us - t0; fx, fy = the
-// compressed bilinear fractions (see compress_frac).
+// compressed bilinear fractions (cmax_owner.cu: compress_frac).
 struct __align__(16) FwdRec {
   uint32_t cell;
   uint32_t dt;
@@ -31,17 +37,16 @@ struct __align__(16) FwdRec {
 };
 
 TileParams make_tiles(const WinParams& P, uint64_t max_n);
-void launch_sort(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
-                 const TileParams& TP, uint2* packed, uint32_t* counts, unsigned long long* err,
-                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm);
-void launch_bin_ptr(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off, const WinParams& P,
-                    const TileParams& TP, const uint32_t* tile_ptr, uint32_t* bin_ptr);
+int bwd_groups(const WinParams& P);
+void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off,
+                       const WinParams& P, uint64_t max_n, uint2* packed, unsigned long long* err);
+void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
+                 const TileParams& TP, const double2* flows, uint32_t* keys, uint32_t* counts,
+                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm, uint32_t* bin_ptr);
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                          uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
-                         uint4* bbox);
-void launch_build_lists(cudaStream_t s, const WinParams& P, const TileParams& TP,
-                        const uint4* bbox, uint32_t* lcount, uint16_t* lists);
+                         uint4* bbox, uint32_t* lcount, uint16_t* lists);
 void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
@@ -57,6 +62,7 @@ void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, const int* no_surv, const double* depth,
                       const uint8_t* mask, const double* pose_tab, const double* K,
-                      double* d_depth, double* pose_part, double* grad_out);
+                      double* d_depth, double* d_depth_parts, double* pose_part,
+                      double* grad_out);
 
 }  // namespace evcm_b200

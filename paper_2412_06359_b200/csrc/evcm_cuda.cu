@@ -191,7 +191,7 @@ struct evcm_cuda_engine {
   }
   // stage_ms[i] = time between marks i and i+1, for lo <= i < hi (others 0)
   void collect_range(int lo, int hi) {
-    stage_ms.assign(8, 0.0);
+    stage_ms.assign(9, 0.0);
     if (!timing) return;
     ck(cudaEventSynchronize(ev[hi]), "cudaEventSynchronize");
     for (int i = lo; i < hi; ++i) {
@@ -304,16 +304,13 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   e->n_total = total;
   e->max_n = max_n;
   if (e->owner()) {
-    // validation + packing + stable counting sort by 16x16 source tile
+    // validation + packing; the sort needs the flows and runs in the forward
     const TileParams TP = make_tiles(P, max_n);
     if (TP.nT > kMaxTiles)
       fail(EVCM_ERR_CONFIG, "cuda backend: sensor too large (more than " +
-                                std::to_string(kMaxTiles) + " 16x16 tiles)");
+                                std::to_string(kMaxTiles) + " 8x8 sort tiles)");
     e->TP = TP;
-    launch_sort(e->stream, dev, off_d, P, TP, packed,
-                e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), err,
-                e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1)),
-                e->get<uint2>("sorted", total), nullptr);
+    launch_stage_pack(e->stream, dev, off_d, P, max_n, packed, err);
   } else {
     launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
   }
@@ -397,44 +394,50 @@ void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, cons
   e->mark(M_FWD0 + 3);
 }
 
-// Owner-computes forward (cmax_owner.cu): bin pointers, trajectory records,
-// per-tile stack + loss partials + coefficient planes, loss finalize.
+// Owner-computes forward (cmax_owner.cu): sort by the position at the middle
+// reference, trajectory records + source lists, per-tile stack + loss partials +
+// coefficient planes, loss finalize. Marks 2..6.
 void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* flows,
                        bool want_stack) {
   const TileParams& TP = e->TP;
-  const int nw = P.n_windows, R = P.B + 1;
+  const int nw = P.n_windows, R = P.B + 1, NS = 2 * P.B + 1;
   const uint64_t total = e->n_total;
   const uint64_t* ev_off = e->get<uint64_t>("ev_off", 1);
-  const uint2* sorted = e->get<uint2>("sorted", 1);
-  const uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", 1);
-  e->mark(M_FWD0);
-  launch_bin_ptr(e->stream, sorted, ev_off, P, TP, tile_ptr,
-                 e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
+  uint2* sorted = e->get<uint2>("sorted", total);
+  uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1));
+  e->mark(2);
+  launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows,
+              e->get<uint32_t>("sort_keys", total),
+              e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
+              nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
+  e->mark(3);
   FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
-  uint4* bbox = e->get<uint4>("bbox", (size_t)nw * R * TP.nT);
-  ck(cudaMemsetAsync(bbox, 0xff, (size_t)nw * R * TP.nT * sizeof(uint4), e->stream), "memset");
-  launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, total, recs, bbox);
-  const size_t np = (size_t)nw * R * TP.nT;
-  uint32_t* lcount = e->get<uint32_t>("lcount", np);
-  ck(cudaMemsetAsync(lcount, 0, np * sizeof(uint32_t), e->stream), "memset");
-  launch_build_lists(e->stream, P, TP, bbox, lcount, e->get<uint16_t>("lists", np * kListCapO));
-  e->mark(M_FWD0 + 1);
+  uint4* bbox = e->get<uint4>("bbox", (size_t)nw * NS * TP.nT);
+  ck(cudaMemsetAsync(bbox, 0xff, (size_t)nw * NS * TP.nT * sizeof(uint4), e->stream), "memset");
+  const size_t nl = (size_t)nw * NS * TP.oT;
+  uint32_t* lcount = e->get<uint32_t>("lcount", nl);
+  ck(cudaMemsetAsync(lcount, 0, nl * sizeof(uint32_t), e->stream), "memset");
+  uint16_t* lists = e->get<uint16_t>("lists", nl * kListCapO);
+  launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, total, recs,
+                      bbox, lcount, lists);
+  e->mark(4);
+  const size_t np = (size_t)nw * R * TP.oT;
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
-  launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount,
-                   e->get<uint16_t>("lists", 1), e->get<double2>("coef", (size_t)nw * R * 2 * P.HW),
-                   stack, e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
-  e->mark(M_FWD0 + 2);
+  launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
+                   e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
+                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+  e->mark(5);
   launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
-                       e->get<unsigned long long>("part_act", np), TP.nT, P,
+                       e->get<unsigned long long>("part_act", np), TP.oT, P,
                        e->get<double>("loss", nw), e->get<int>("no_surv", nw),
                        e->get<long long>("n_active", (size_t)nw * R),
                        e->get<double>("scale", (size_t)nw * R));
-  e->mark(M_FWD0 + 3);
+  e->mark(6);
 }
 
 // Owner-computes backward: per-event adjoint -> per-bin (gx, gy), then the
-// per-tile gradient gather with the fused flows backward (when depth given)
-// and/or the f64 gradient planes (grad_out, [w][B][2][HW]).
+// per-tile gradient gather with the fused flows backward (when depth is given)
+// and/or the f64 gradient planes (grad_out, [w][B][2][HW]). Marks 7..9.
 void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* flows,
                         const double* depth, const uint8_t* mask, const double* pose_tab,
                         const double* K, double* d_depth, double* d_poses, double* grad_out) {
@@ -449,15 +452,17 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   launch_bwd_event(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, recs, total,
                    e->get<double2>("coef", 1), e->get<double>("scale", 1), e->get<int>("no_surv", 1),
                    bwd);
-  e->mark(M_FWD0 + 4);
-  double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.nT * P.B * 6) : nullptr;
+  e->mark(7);
+  double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * 6) : nullptr;
+  const int G = bwd_groups(P);
+  double* dd_parts = (depth && G > 1) ? e->get<double>("d_depth_parts", (size_t)nw * G * P.HW) : nullptr;
   launch_bwd_owner(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
                    e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask, pose_tab,
-                   K, d_depth, pose_part, grad_out);
-  e->mark(M_FWD0 + 5);
-  if (depth) launch_pose_finalize(e->stream, pose_part, TP.nT, P.B, nw, d_poses);
-  e->mark(M_FWD0 + 6);
+                   K, depth ? d_depth : nullptr, dd_parts, pose_part, grad_out);
+  e->mark(8);
+  if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
+  e->mark(9);
 }
 
 void run_forward(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows,
@@ -618,7 +623,7 @@ int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows
     ck(cudaMemcpyAsync(&l, e->get<double>("loss", 1), sizeof l, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaMemcpyAsync(&ns, e->get<int>("no_surv", 1), sizeof ns, cudaMemcpyDeviceToHost, e->stream), "D2H");
     sync_and_check(e, "forward");
-    e->collect_range(0, M_FWD0 + 3);
+    e->collect_range(0, e->owner() ? 6 : M_FWD0 + 3);
     if (loss) {
       loss->value = l;
       loss->no_survivors = ns;
@@ -687,7 +692,7 @@ int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flow
         e->P.B != f->n_bins)
       fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
     const WinParams& P = e->P;
-    e->mark(M_FWD0 + 3);
+    e->mark(e->owner() ? 6 : M_FWD0 + 3);
     double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
     if (e->owner()) {
       run_backward_owner(e, P, e->get<double2>("flows", 1), nullptr, nullptr, nullptr, nullptr,
@@ -701,7 +706,7 @@ int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flow
     }
     from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
     ck(cudaStreamSynchronize(e->stream), "backward");
-    e->collect_range(M_FWD0 + 3, e->owner() ? M_FWD0 + 5 : M_FWD0 + 5);
+    if (e->owner()) e->collect_range(6, 9); else e->collect_range(M_FWD0 + 3, M_FWD0 + 5);
     ck(cudaGetLastError(), "backward kernels");
     e->last_launches = launch_count();
   });
@@ -840,7 +845,7 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
     if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), out_mem);
     if (out->d_poses && dpo != out->d_poses) from_device(e, out->d_poses, dpo, (size_t)nw * B * 6 * sizeof(double), out_mem);
     sync_and_check(e, "chain");
-    e->collect_range(0, M_FWD0 + 6);
+    e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);
     e->last_launches = launch_count();
   });
 }
