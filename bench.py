@@ -257,7 +257,8 @@ def cuda_arm(args, wl):
     nwin = wl["batch"]
     depth, poses, K, ev, offs = make_inputs(wl, rank, nwin)
     stream = torch.cuda.Stream(dev)
-    eng = P.Engine(P.EngineOptions(device=local, stream=stream.cuda_stream))
+    eng = P.Engine(P.EngineOptions(device=local, stream=stream.cuda_stream,
+                                   deterministic=args.deterministic))
 
     # device-resident inputs / outputs
     with torch.cuda.stream(stream):
@@ -394,6 +395,7 @@ def cuda_arm(args, wl):
                        "bins": wl["B"], "numerics": "parity (fp64 per-event math, fp64 IWE "
                        "stack, fp32 flow-gradient accumulators)",
                        "l2": "flushed between timed steps (256 MB write, untimed)",
+                       "mode": "deterministic" if args.deterministic else "fast (smem fp64 atomics)",
                        "inputs": "two-plane depth + per-bin ego-motion, uniform events",
                        "parallelism": f"dp{world} (windows sharded, NCCL all-reduce of "
                                       "loss/d_depth/d_poses)"},
@@ -418,6 +420,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bit-stable owner accumulation (fixed-order, slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     args = ap.parse_args()

@@ -24,6 +24,8 @@ struct WinParams {
   int HW;            // W*H
   int n_windows;
   double window_s;   // edges_s[B] (engine.hpp:380)
+  double inv_window; // 1 / window_s: owner kernels form tb = |t - e_r| * inv_window in the
+                     // forward AND the backward, so count/tsum cancel exactly as in fp64
   double es[kMaxRefs];      // edge times on the window clock, s (engine.hpp:244-249)
   uint32_t erel[kMaxRefs];  // edges_us[i] - edges_us[0]
   uint64_t t0, t_end;       // slice window [t0, t_end)

@@ -166,23 +166,54 @@ __device__ __forceinline__ void scan_sources(const uint4* __restrict__ bbox, int
 }
 
 // Sorted source list of one (window, slot, owner tile) into `list`; returns its
-// length, or -1 when the precomputed list overflowed. Single thread.
-__device__ __forceinline__ int load_sorted_list(const uint32_t* __restrict__ lcount,
-                                                const uint16_t* __restrict__ lists, size_t slotT,
-                                                uint16_t* list) {
+// length, or -1 when the precomputed list overflowed (the caller then scans).
+// Warp-collective version: rank-sort the (unique) sources in parallel.
+__device__ __forceinline__ int warp_load_sorted_list(const uint32_t* __restrict__ lcount,
+                                                     const uint16_t* __restrict__ lists,
+                                                     size_t slotT, uint16_t* list) {
+  const int lane = threadIdx.x & 31;
   const uint32_t cnt = lcount[slotT];
   if (cnt > (uint32_t)kListCapO) return -1;
   const uint16_t* src = lists + slotT * kListCapO;
-  for (uint32_t i = 0; i < cnt; ++i) {  // insertion sort, lists are short
-    const uint16_t v = src[i];
-    int j = (int)i - 1;
-    while (j >= 0 && list[j] > v) {
-      list[j + 1] = list[j];
-      --j;
-    }
-    list[j + 1] = v;
+  for (uint32_t e = lane; e < cnt; e += 32) {
+    const uint16_t v = src[e];
+    int rank = 0;
+    for (uint32_t q = 0; q < cnt; ++q) rank += src[q] < v ? 1 : 0;
+    list[rank] = v;
   }
+  __syncwarp();
   return (int)cnt;
+}
+
+// Warp-collective exclusive scan of per-entry lengths: pre[l] (l <= n), rng[l] =
+// first slot of entry l, for entries [l0, l0 + n) of a concatenated list whose
+// running total starts at `carry`. lohi(l) -> (first, end) slot of entry l.
+template <typename F>
+__device__ __forceinline__ uint32_t warp_ranges(int l0, int n, uint32_t carry, uint32_t* pre,
+                                                uint32_t* rng, F&& lohi) {
+  const int lane = threadIdx.x & 31;
+  for (int b = 0; b < n; b += 32) {
+    const int l = b + lane;
+    uint32_t lo = 0, len = 0;
+    if (l < n) {
+      const uint2 r = lohi(l0 + l);
+      lo = r.x;
+      len = r.y - r.x;
+    }
+    uint32_t x = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (l < n) {
+      pre[l0 + l] = carry + x - len;
+      rng[l0 + l] = lo;
+    }
+    carry += __shfl_sync(kFull, x, 31);
+  }
+  if (lane == 0) pre[l0 + n] = carry;
+  __syncwarp();
+  return carry;
 }
 
 // Virtual concatenation of event ranges: pre[l] = sum of earlier lengths,
@@ -526,29 +557,35 @@ __global__ void k_build_lists(const uint4* __restrict__ bbox, WinParams P, TileP
 // ---------------------------------------------------------------------------
 // forward owner: IWE stack tile + loss partials + coefficient planes
 
-__global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
+// kDet: kFwdWarps warps, each with a private fp64 tile accumulated in lane order
+// and merged in warp order (bit-stable). !kDet: 8 warps share one tile through
+// shared-memory fp64 atomics (faster, order-dependent rounding only).
+template <bool kDet>
+__global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
     const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
     const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
     const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
     const uint16_t* __restrict__ lists, double2* __restrict__ coef, double2* __restrict__ stack_out,
     double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
-  extern __shared__ __align__(16) double acc_all[];  // [warp][px][C0, S0, C1, S1]
+  constexpr int NW = kDet ? kFwdWarps : 8;
+  constexpr int NC = kDet ? kFwdWarps : 1;  // accumulator copies
+  extern __shared__ __align__(16) double acc_all[];  // [copy][px][C0, S0, C1, S1]
   __shared__ uint16_t list[kListCapO > 128 ? kListCapO : 128];
   __shared__ uint32_t pre[kListCapO + 1], rng[kListCapO];
   __shared__ int s_nl;
-  __shared__ double s_red[kFwdWarps];
-  __shared__ unsigned s_act[kFwdWarps];
+  __shared__ double s_red[NW];
+  __shared__ unsigned s_act[NW];
   const int T = blockIdx.x, r = blockIdx.y, w = blockIdx.z;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = P.B + 1, NS = 2 * P.B + 1, W = P.W, H = P.H, HW = P.HW;
   const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
-  for (int i = threadIdx.x; i < kFwdWarps * kOwnPx * 4; i += blockDim.x) acc_all[i] = 0.0;
+  for (int i = threadIdx.x; i < NC * kOwnPx * 4; i += blockDim.x) acc_all[i] = 0.0;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const FwdRec* rr = recs + (size_t)r * n_total + base;
-  const double esr = P.es[r], win = P.window_s;
+  const double esr = P.es[r], iwin = P.inv_window;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
-  double* mine = acc_all + (size_t)wid * kOwnPx * 4;
+  double* mine = acc_all + (kDet ? (size_t)wid * kOwnPx * 4 : 0);
   const size_t ws = (size_t)w * NS + r;
 
   auto contribute = [&](const FwdRec& rec) {
@@ -559,37 +596,50 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     if (live) {
       c = decode(rec);
       pol = (int)(rec.cell >> 31);
-      tb = dd(fabs(ds(dm((double)rec.dt, 1e-6), esr)), win);  // engine.hpp:370
+      tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
     }
-    const bool any = __any_sync(kFull, live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW &&
-                                           c.y0 + oy >= oy0 && c.y0 < oy0 + kOwnH);
-    if (!any) return;
+    const bool touch = live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW && c.y0 + oy >= oy0 &&
+                       c.y0 < oy0 + kOwnH;
+    if (kDet) {
+      if (!__any_sync(kFull, touch)) return;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-      const bool in = live && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
-      const double wq = corner_w(c, q);
-      warp_accumulate2(mine, in ? ((ly * kOwnW + lx) * 2 + pol) : -1, wq, wq * tb);
+      for (int q = 0; q < 4; ++q) {
+        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
+        const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
+        const double wq = corner_w(c, q);
+        warp_accumulate2(mine, in ? ((ly * kOwnW + lx) * 2 + pol) : -1, wq, wq * tb);
+      }
+    } else if (touch) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
+        if (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) {
+          const double wq = corner_w(c, q);
+          double* a = mine + 4 * (ly * kOwnW + lx) + 2 * pol;
+          atomicAdd(a, wq);
+          atomicAdd(a + 1, wq * tb);
+        }
+      }
     }
   };
 
-  if (threadIdx.x == 0) s_nl = load_sorted_list(lcount, lists, ws * TP.oT + T, list);
+  if (wid == 0) {
+    const int nl = warp_load_sorted_list(lcount, lists, ws * TP.oT + T, list);
+    if (nl >= 0)
+      warp_ranges(0, nl, 0u, pre, rng, [&](int l) {
+        const int S = list[l];
+        return make_uint2(tp[S], tp[S + 1]);
+      });
+    if (lane == 0) s_nl = nl;
+  }
   __syncthreads();
   if (s_nl >= 0) {
     const int nl = s_nl;
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      for (int l = 0; l < nl; ++l) {
-        pre[l] = run;
-        rng[l] = tp[list[l]];
-        run += tp[list[l] + 1] - tp[list[l]];
-      }
-      pre[nl] = run;
-    }
-    __syncthreads();
     const uint32_t total = nl > 0 ? pre[nl] : 0u;
-    const uint32_t v0 = (uint32_t)(((uint64_t)total * wid) / kFwdWarps);
-    const uint32_t v1 = (uint32_t)(((uint64_t)total * (wid + 1)) / kFwdWarps);
+    const uint32_t v0 = (uint32_t)(((uint64_t)total * wid) / NW);
+    const uint32_t v1 = (uint32_t)(((uint64_t)total * (wid + 1)) / NW);
+    int l = 0;
+    if (v0 < v1) virt_slot(pre, rng, nl, v0, &l);  // segment of the warp's first element
     for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
       FwdRec rb[kPrefetch];
 #pragma unroll
@@ -597,8 +647,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
         const uint32_t v = vb + m * 32 + lane;
         rb[m].cell = kDead;
         if (v < v1) {
-          int l;
-          rb[m] = rr[virt_slot(pre, rng, nl, v, &l)];
+          while (pre[l + 1] <= v) ++l;  // v increases monotonically per lane
+          rb[m] = rr[rng[l] + (v - pre[l])];
         }
       }
 #pragma unroll
@@ -616,8 +666,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     });
   }
   __syncthreads();
-  // merge warp copies in warp order; refresh_active (warp.hpp:186-192),
-  // reference_loss terms (:306-309), splat_position_grad factors (:346-349)
+  // merge the copies in order; refresh_active (warp.hpp:186-192), reference_loss
+  // terms (:306-309), splat_position_grad factors (:346-349)
   double lsum = 0.0;
   unsigned act = 0;
   double2* cw = coef + ((size_t)w * R + r) * 2 * HW;
@@ -626,7 +676,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
     if (px >= W || py >= H) continue;
     double C0 = acc_all[4 * q], S0 = acc_all[4 * q + 1], C1 = acc_all[4 * q + 2], S1 = acc_all[4 * q + 3];
 #pragma unroll
-    for (int m = 1; m < kFwdWarps; ++m) {
+    for (int m = 1; m < NC; ++m) {
       const double* a = acc_all + (size_t)m * kOwnPx * 4 + 4 * q;
       C0 += a[0];
       S0 += a[1];
@@ -657,7 +707,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_fwd_owner(
   if (threadIdx.x == 0) {
     double s = 0.0;
     unsigned a = 0;
-    for (int m = 0; m < kFwdWarps; ++m) {
+    for (int m = 0; m < NW; ++m) {
       s += s_red[m];
       a += s_act[m];
     }
@@ -715,8 +765,8 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
   const double* sc = scale_tab + (size_t)w * R;
   const double2* fl = flows + (size_t)w * B * HW;
   float2* bo = bwd + base + k;  // + i * n_total
-  const double win = P.window_s;
-  auto tb_of = [&](int r) { return dd(fabs(ds(t, es[r])), win); };
+  const double iwin = P.inv_window;  // same tb formula as k_fwd_owner
+  auto tb_of = [&](int r) { return fabs(t - es[r]) * iwin; };
 
   double2 gb, gf;
   {
@@ -805,15 +855,9 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
     const size_t sA = ((size_t)w * NS + i + 1) * TP.oT + T;
     const size_t sB = ((size_t)w * NS + i) * TP.oT + T;
     const size_t sC = ((size_t)w * NS + R + i) * TP.oT + T;
-    int nA = 0, nB = 0, nC = 0;
-    if (lane == 0) {
-      nA = load_sorted_list(lcount, lists, sA, lst);
-      nB = nA >= 0 ? load_sorted_list(lcount, lists, sB, lst + nA) : -1;
-      nC = nB >= 0 ? load_sorted_list(lcount, lists, sC, lst + nA + nB) : -1;
-    }
-    nA = __shfl_sync(kFull, nA, 0);
-    nB = __shfl_sync(kFull, nB, 0);
-    nC = __shfl_sync(kFull, nC, 0);
+    const int nA = warp_load_sorted_list(lcount, lists, sA, lst);
+    const int nB = nA >= 0 ? warp_load_sorted_list(lcount, lists, sB, lst + nA) : -1;
+    const int nC = nB >= 0 ? warp_load_sorted_list(lcount, lists, sC, lst + nA + nB) : -1;
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
       const bool live = rec.cell != kDead;
       CellW c{};
@@ -836,30 +880,15 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
     };
     if (nA >= 0 && nB >= 0 && nC >= 0) {
       const int nl = nA + nB + nC;
-      if (lane == 0) {
-        uint32_t run = 0;
-        for (int l = 0; l < nl; ++l) {
-          const int S = lst[l];
-          pre[l] = run;
-          uint32_t a, z;
-          if (l < nA) {
-            a = bp[(size_t)S * (B + 1) + i + 1];
-            z = tp[S + 1];
-          } else if (l < nA + nB) {
-            a = tp[S];
-            z = bp[(size_t)S * (B + 1) + i];
-          } else {
-            a = bp[(size_t)S * (B + 1) + i];
-            z = bp[(size_t)S * (B + 1) + i + 1];
-          }
-          rng[l] = a;
-          run += z - a;
-        }
-        pre[nl] = run;
-      }
-      __syncwarp();
-      const uint32_t total = nl > 0 ? pre[nl] : 0u;
-      const uint32_t sAB = nl > 0 ? pre[nA] : 0u, sBC = nl > 0 ? pre[nA + nB] : 0u;
+      warp_ranges(0, nl, 0u, pre, rng, [&](int l) {
+        const int S = lst[l];
+        if (l < nA) return make_uint2(bp[(size_t)S * (B + 1) + i + 1], tp[S + 1]);
+        if (l < nA + nB) return make_uint2(tp[S], bp[(size_t)S * (B + 1) + i]);
+        return make_uint2(bp[(size_t)S * (B + 1) + i], bp[(size_t)S * (B + 1) + i + 1]);
+      });
+      const uint32_t total = pre[nl];
+      const uint32_t sAB = pre[nA], sBC = pre[nA + nB];
+      int lcur = 0;
       for (uint32_t vb = 0; vb < total; vb += 32 * kPrefetch) {
         FwdRec rb[kPrefetch];
         float2 vv[kPrefetch];
@@ -871,8 +900,8 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
           vv[m] = make_float2(0.f, 0.f);
           pk[m] = -1;
           if (v < total) {
-            int l;
-            const uint32_t k = virt_slot(pre, rng, nl, v, &l);
+            while (pre[lcur + 1] <= v) ++lcur;
+            const uint32_t k = rng[lcur] + (v - pre[lcur]);
             if (v < sBC) {
               rb[m] = (v < sAB) ? rA[k] : rB[k];
               if (rb[m].cell != kDead) vv[m] = bi[k];
@@ -1086,14 +1115,22 @@ void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act) {
-  static size_t a = 0;
-  const size_t smem = (size_t)kFwdWarps * kOwnPx * 4 * sizeof(double);
-  set_smem(reinterpret_cast<const void*>(k_fwd_owner), smem, &a);
+                      unsigned long long* part_act, bool deterministic) {
+  static size_t a = 0, b = 0;
   count_launch();
-  k_fwd_owner<<<dim3(TP.oT, P.B + 1, P.n_windows), 32 * kFwdWarps, smem, s>>>(
-      ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
-      part_act);
+  if (deterministic) {
+    const size_t smem = (size_t)kFwdWarps * kOwnPx * 4 * sizeof(double);
+    set_smem(reinterpret_cast<const void*>(k_fwd_owner<true>), smem, &a);
+    k_fwd_owner<true><<<dim3(TP.oT, P.B + 1, P.n_windows), 32 * kFwdWarps, smem, s>>>(
+        ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
+        part_act);
+  } else {
+    const size_t smem = (size_t)kOwnPx * 4 * sizeof(double);
+    set_smem(reinterpret_cast<const void*>(k_fwd_owner<false>), smem, &b);
+    k_fwd_owner<false><<<dim3(TP.oT, P.B + 1, P.n_windows), 256, smem, s>>>(
+        ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
+        part_act);
+  }
 }
 
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,

@@ -51,7 +51,7 @@ void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act);
+                      unsigned long long* part_act, bool deterministic);
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,

@@ -245,6 +245,7 @@ WinParams make_params(int W, int H, const uint64_t* edges, int B, int n_windows,
     P.erel[i] = static_cast<uint32_t>(edges[i] - edges[0]);
   }
   P.window_s = P.es[B];
+  P.inv_window = 1.0 / P.window_s;
   P.t0 = t0;
   P.t_end = t_end;
   return P;
@@ -425,7 +426,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
   launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
                    e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
-                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np),
+                   e->opt.deterministic != 0);
   e->mark(5);
   launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
                        e->get<unsigned long long>("part_act", np), TP.oT, P,

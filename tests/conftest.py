@@ -35,3 +35,9 @@ def engine_fast():
 def engine_atomic():
     import paper_2412_06359_b200 as P
     return P.Engine(P.EngineOptions(algo="atomic"))
+
+
+@pytest.fixture(scope="session")
+def engine_det():
+    import paper_2412_06359_b200 as P
+    return P.Engine(P.EngineOptions(deterministic=True))

@@ -69,10 +69,15 @@ def test_fd_instances_masked(engine):
 
 @pytest.mark.parametrize("W,H,B,n", [(64, 48, 10, 5000), (128, 128, 10, 20000),
                                      (346, 260, 10, 100000), (37, 23, 3, 3000),
-                                     (50, 40, 1, 2000), (64, 48, 32, 4000)])
+                                     (50, 40, 1, 2000), (64, 48, 32, 4000), (33, 17, 16, 3000)])
 def test_smooth_windows(engine, W, H, B, n):
     w = smooth_window(W, H, B, n, seed=W + n)
     _check(engine, w)
+
+
+@pytest.mark.parametrize("W,H,B,n", [(64, 48, 10, 5000), (346, 260, 10, 100000), (64, 48, 32, 4000)])
+def test_smooth_windows_deterministic(engine_det, W, H, B, n):
+    _check(engine_det, smooth_window(W, H, B, n, seed=W + 2 * n))
 
 
 def test_fp64_accumulators(engine_f64):
@@ -86,8 +91,10 @@ def test_atomic_path(engine_atomic, W, H, B, n):
     _check(engine_atomic, smooth_window(W, H, B, n, seed=W * 3 + n))
 
 
-def test_owner_deterministic(engine):
-    """Owner-computes path: bit-identical loss, stack and gradients run to run."""
+def test_owner_deterministic(engine_det):
+    """Owner-computes path, deterministic mode: bit-identical loss, stack and
+    gradients run to run."""
+    engine = engine_det
     w = smooth_window(346, 260, 10, 200000, seed=21)
     a = engine.forward(_slice(w), _flows(w))
     sa, la = a.stack.count.copy(), a.loss.value
