@@ -55,6 +55,7 @@ __device__ __forceinline__ int bin_of(uint32_t dt, const uint32_t* erel, int B) 
 // `oy` are the flat offsets to x1 and y1 (0 when the sensor is 1 px wide/high).
 struct Cell {
   int i00, ox, oy;
+  int x0, y0;
   double wx, wy;
 };
 
@@ -67,6 +68,8 @@ __device__ __forceinline__ Cell bilin_cell(double x, double y, int W, int H) {
   if (W >= 2) { x0 = (int)floor(cx); x0 = x0 < W - 2 ? x0 : W - 2; }
   if (H >= 2) { y0 = (int)floor(cy); y0 = y0 < H - 2 ? y0 : H - 2; }
   Cell c;
+  c.x0 = x0;
+  c.y0 = y0;
   c.i00 = y0 * W + x0;
   c.ox = (x0 + 1 < W - 1 ? x0 + 1 : W - 1) - x0;
   c.oy = ((y0 + 1 < H - 1 ? y0 + 1 : H - 1) - y0) * W;

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ count
 __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
     const uint2* __restrict__ packed, const uint32_t* __restrict__ keys,
     const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
-    uint2* __restrict__ sorted, uint32_t* __restrict__ perm) {
+    uint2* __restrict__ sorted, uint32_t* __restrict__ perm, uint32_t* __restrict__ sorted_keys) {
   extern __shared__ uint16_t whist[];  // [16 warps][nT]
   const int nW = kSortThreads / 32;
   for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
       const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
       const uint32_t dst = off[(size_t)t * TP.nchunks + blockIdx.x] + mine[t] + rank;
       sorted[base + dst] = packed[base + k];
+      sorted_keys[base + dst] = (uint32_t)t;
       if (perm) perm[base + dst] = (uint32_t)k;
       __syncwarp(peers);
       if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
@@ -449,8 +450,9 @@ __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __re
 
 __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
-    TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
-    uint64_t n_total, FwdRec* __restrict__ recs, uint4* __restrict__ bbox) {
+    TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ sorted_keys,
+    const double2* __restrict__ flows, uint64_t n_total, FwdRec* __restrict__ recs,
+    uint4* __restrict__ bbox) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* es = reinterpret_cast<double*>(smem);
   uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
@@ -477,13 +479,7 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     j = bin_of(dt, erel, P.B);
     alive = trajectory((double)ev_x(e), (double)ev_y(e), t, j,
                        flows + (size_t)w * P.B * P.HW, P, es, pos, blockDim.x);
-    // sort tile of this slot: binary search of k in tile_ptr (events are grouped)
-    int lo = 0, hi = TP.nT - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tp[mid] <= (uint32_t)k) lo = mid; else hi = mid - 1;
-    }
-    S = lo;
+    S = (int)sorted_keys[base + k];  // sort tile of this slot
   }
   const unsigned amask = __ballot_sync(kFull, alive);
   const unsigned peers = alive ? __match_any_sync(amask, S) : 0u;
@@ -507,8 +503,8 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     if (alive) {
       const double2 p = pos[r * blockDim.x];
       const Cell c = bilin_cell(p.x, p.y, P.W, P.H);
-      y0 = (uint32_t)(c.i00 / P.W);
-      x0 = (uint32_t)(c.i00 - (int)y0 * P.W);
+      x0 = (uint32_t)c.x0;
+      y0 = (uint32_t)c.y0;
       rec.cell = x0 | (y0 << 16) | ((uint32_t)ev_pol(e) << 31);
       rec.dt = ev_dt(e);
       rec.fx = compress_frac(c.wx);
@@ -819,7 +815,11 @@ constexpr int kBwdSeg = 3 * kListCapO;
 constexpr int kBwdWarpBytes =
     ((kOwnPx * 2 * 8 + kBwdSeg * 2 + (kBwdSeg + 1) * 4 + kBwdSeg * 4 + 15) / 16) * 16;
 
-__global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
+// kDet: one warp per bin, lane-ordered accumulation (bit-stable). !kDet: two
+// warps per bin split the bin's events and add into the shared tile with
+// shared-memory fp64 atomics.
+template <bool kDet>
+__global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
     const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
@@ -828,12 +828,14 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
     const double* __restrict__ depth, const uint8_t* __restrict__ mask,
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
     double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
+  constexpr int kSplit = kDet ? 1 : 2;  // warps per bin
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_n[kBwdGroup][4];
   const int T = blockIdx.x, grp = blockIdx.y, w = blockIdx.z;
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) / kSplit, sub = (threadIdx.x >> 5) % kSplit;
   const int B = P.B, R = B + 1, NS = 2 * B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int i = grp * kBwdGroup + wq;          // this warp's bin
-  const int nb = min(kBwdGroup, B - grp * kBwdGroup);  // bins in this CTA
+  const int i = grp * kBwdGroup + wq;                     // this warp's bin
+  const int nb = min(kBwdGroup, B - grp * kBwdGroup);     // bins in this CTA
   unsigned char* wst = smem_raw + (size_t)wq * kBwdWarpBytes;
   double* g = reinterpret_cast<double*>(wst);                            // [px][gu, gv]
   uint32_t* pre = reinterpret_cast<uint32_t*>(wst + kOwnPx * 2 * 8);     // kBwdSeg + 1
@@ -845,32 +847,56 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool active = wq < nb;
-  for (int q = lane; q < kOwnPx * 2; q += 32) g[q] = 0.0;
-  __syncwarp();
-
-  if (active && !no_surv[w]) {
-    const float2* bi = bwd + (size_t)i * n_total + base;
-    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
-    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
-    const size_t sA = ((size_t)w * NS + i + 1) * TP.oT + T;
-    const size_t sB = ((size_t)w * NS + i) * TP.oT + T;
-    const size_t sC = ((size_t)w * NS + R + i) * TP.oT + T;
+  const bool run = active && !no_surv[w];
+  for (int q = lane + 32 * sub; q < kOwnPx * 2; q += 32 * kSplit) g[q] = 0.0;
+  const size_t sA = ((size_t)w * NS + i + 1) * TP.oT + T;
+  const size_t sB = ((size_t)w * NS + i) * TP.oT + T;
+  const size_t sC = ((size_t)w * NS + R + i) * TP.oT + T;
+  if (run && sub == 0) {
     const int nA = warp_load_sorted_list(lcount, lists, sA, lst);
     const int nB = nA >= 0 ? warp_load_sorted_list(lcount, lists, sB, lst + nA) : -1;
     const int nC = nB >= 0 ? warp_load_sorted_list(lcount, lists, sC, lst + nA + nB) : -1;
+    if (nA >= 0 && nB >= 0 && nC >= 0)
+      warp_ranges(0, nA + nB + nC, 0u, pre, rng, [&](int l) {
+        const int S = lst[l];
+        if (l < nA) return make_uint2(bp[(size_t)S * (B + 1) + i + 1], tp[S + 1]);
+        if (l < nA + nB) return make_uint2(tp[S], bp[(size_t)S * (B + 1) + i]);
+        return make_uint2(bp[(size_t)S * (B + 1) + i], bp[(size_t)S * (B + 1) + i + 1]);
+      });
+    if (lane == 0) {
+      s_n[wq][0] = nA;
+      s_n[wq][1] = nB;
+      s_n[wq][2] = nC;
+    }
+  }
+  __syncthreads();
+
+  if (run) {
+    const float2* bi = bwd + (size_t)i * n_total + base;
+    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
+    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
+    const int nA = s_n[wq][0], nB = s_n[wq][1], nC = s_n[wq][2];
+    auto add = [&](int key, double v0, double v1) {  // one corner into the bin tile
+      if (kDet) {
+        warp_accumulate2(g, key, v0, v1);
+      } else if (key >= 0) {
+        atomicAdd(g + 2 * key, v0);
+        atomicAdd(g + 2 * key + 1, v1);
+      }
+    };
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
       const bool live = rec.cell != kDead;
       CellW c{};
       if (live) c = decode(rec);
-      const bool any = __any_sync(kFull, live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW &&
-                                             c.y0 + oy >= oy0 && c.y0 < oy0 + kOwnH);
-      if (!any) return;
+      const bool touch = live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW && c.y0 + oy >= oy0 &&
+                         c.y0 < oy0 + kOwnH;
+      if (kDet ? !__any_sync(kFull, touch) : !touch) return;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-        const bool in = live && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
+        const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
         const double wgt = corner_w(c, q);
-        warp_accumulate2(g, in ? (ly * kOwnW + lx) : -1, wgt * (double)v.x, wgt * (double)v.y);
+        add(in ? (ly * kOwnW + lx) : -1, wgt * (double)v.x, wgt * (double)v.y);
       }
     };
     auto pixel_key = [&](uint32_t k) {  // source pixel of sorted event k if inside the tile
@@ -880,16 +906,13 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
     };
     if (nA >= 0 && nB >= 0 && nC >= 0) {
       const int nl = nA + nB + nC;
-      warp_ranges(0, nl, 0u, pre, rng, [&](int l) {
-        const int S = lst[l];
-        if (l < nA) return make_uint2(bp[(size_t)S * (B + 1) + i + 1], tp[S + 1]);
-        if (l < nA + nB) return make_uint2(tp[S], bp[(size_t)S * (B + 1) + i]);
-        return make_uint2(bp[(size_t)S * (B + 1) + i], bp[(size_t)S * (B + 1) + i + 1]);
-      });
       const uint32_t total = pre[nl];
       const uint32_t sAB = pre[nA], sBC = pre[nA + nB];
+      const uint32_t v0 = (uint32_t)(((uint64_t)total * sub) / kSplit);
+      const uint32_t v1 = (uint32_t)(((uint64_t)total * (sub + 1)) / kSplit);
       int lcur = 0;
-      for (uint32_t vb = 0; vb < total; vb += 32 * kPrefetch) {
+      if (v0 < v1) virt_slot(pre, rng, nl, v0, &lcur);
+      for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
         FwdRec rb[kPrefetch];
         float2 vv[kPrefetch];
         int pk[kPrefetch];
@@ -899,7 +922,7 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
           rb[m].cell = kDead;
           vv[m] = make_float2(0.f, 0.f);
           pk[m] = -1;
-          if (v < total) {
+          if (v < v1) {
             while (pre[lcur + 1] <= v) ++lcur;
             const uint32_t k = rng[lcur] + (v - pre[lcur]);
             if (v < sBC) {
@@ -913,12 +936,12 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
         }
 #pragma unroll
         for (int m = 0; m < kPrefetch; ++m) {
-          if (vb + m * 32 >= total) break;
+          if (vb + m * 32 >= v1) break;
           if (vb + m * 32 < sBC) accumulate(rb[m], vv[m]);
-          if (vb + m * 32 + 31 >= sBC) warp_accumulate2(g, pk[m], (double)vv[m].x, (double)vv[m].y);
+          if (vb + m * 32 + 31 >= sBC) add(pk[m], (double)vv[m].x, (double)vv[m].y);
         }
       }
-    } else {
+    } else if (sub == 0) {
       // an owner list overflowed: scan the sort-tile boxes in order (slow, rare)
       scan_sources(bbox + ((size_t)w * NS + i + 1) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
         const uint32_t k1 = tp[S + 1];
@@ -956,12 +979,13 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
             key = pixel_key(k);
             if (key >= 0) v = bi[k];
           }
-          warp_accumulate2(g, key, (double)v.x, (double)v.y);
+          add(key, (double)v.x, (double)v.y);
         }
       });
     }
   }
-  __syncwarp();
+  __syncthreads();
+  if (sub != 0) return;  // one warp per bin runs the flows backward
 
   // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
   if (active) {
@@ -1016,10 +1040,17 @@ __global__ void __launch_bounds__(32 * kBwdGroup) k_bwd_owner(
       }
     }
   }
-  __syncthreads();
+  if (kSplit > 1) {
+    // named barrier over the sub == 0 warps only (the others have exited)
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * ((blockDim.x >> 5) / kSplit)));
+  } else {
+    __syncthreads();
+  }
   if (d_depth) {
     const int G = (B + kBwdGroup - 1) / kBwdGroup;
-    for (int q = threadIdx.x; q < kOwnPx; q += blockDim.x) {
+    const int nthr = 32 * ((blockDim.x >> 5) / kSplit);
+    const int tid = 32 * wq + lane;
+    for (int q = tid; q < kOwnPx; q += nthr) {
       const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
       if (px >= W || py >= H) continue;
       double s = 0.0;
@@ -1075,8 +1106,9 @@ void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_
 }
 
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
-                 const TileParams& TP, const double2* flows, uint32_t* keys, uint32_t* counts,
-                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm, uint32_t* bin_ptr) {
+                 const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
+                 uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
+                 uint32_t* bin_ptr) {
   static size_t a1 = 0, a2 = 0;
   set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
   set_smem(reinterpret_cast<const void*>(k_sort_scatter), (size_t)(kSortThreads / 32) * TP.nT * 2, &a2);
@@ -1088,7 +1120,7 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   k_sort_scan<<<P.n_windows, 1024, 0, s>>>(counts, TP, tile_ptr);
   count_launch();
   k_sort_scatter<<<grid, kSortThreads, (size_t)(kSortThreads / 32) * TP.nT * 2, s>>>(
-      packed, keys, ev_off, TP, counts, sorted, perm);
+      packed, keys, ev_off, TP, counts, sorted, perm, keys + n_total);
   count_launch();
   k_bin_ptr<<<dim3((TP.nT + 127) / 128, P.n_windows), 128, 0, s>>>(sorted, ev_off, P, TP,
                                                                     tile_ptr, bin_ptr);
@@ -1096,15 +1128,17 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
 
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                         uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
-                         uint4* bbox, uint32_t* lcount, uint16_t* lists) {
+                         const uint32_t* sorted_keys, uint64_t max_n, const double2* flows,
+                         uint64_t n_total, FwdRec* recs, uint4* bbox, uint32_t* lcount,
+                         uint16_t* lists) {
   static size_t a = 0;
   const size_t smem = kEvSmemHeader + sizeof(double2) * (size_t)(P.B + 1) * kEvBlock;
   set_smem(reinterpret_cast<const void*>(k_traj_records), smem, &a);
   if (max_n > 0) {
     count_launch();
     k_traj_records<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock,
-                     smem, s>>>(sorted, ev_off, P, TP, tile_ptr, flows, n_total, recs, bbox);
+                     smem, s>>>(sorted, ev_off, P, TP, tile_ptr, sorted_keys, flows, n_total, recs,
+                                bbox);
   }
   count_launch();
   k_build_lists<<<dim3((TP.nT + 127) / 128, 2 * P.B + 1, P.n_windows), 128, 0, s>>>(bbox, P, TP,
@@ -1152,18 +1186,25 @@ void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint16_t* lists, const int* no_surv, const double* depth,
                       const uint8_t* mask, const double* pose_tab, const double* K,
                       double* d_depth, double* d_depth_parts, double* pose_part,
-                      double* grad_out) {
+                      double* grad_out, bool deterministic) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   const int G = bwd_groups(P);
   const int warps = std::min(P.B, kBwdGroup);
   const size_t smem = (size_t)warps * kBwdWarpBytes;
-  static size_t a = 0;
-  set_smem(reinterpret_cast<const void*>(k_bwd_owner), smem, &a);
+  static size_t a = 0, b = 0;
   double* dd_out = (d_depth && G > 1) ? d_depth_parts : d_depth;
   count_launch();
-  k_bwd_owner<<<dim3(TP.oT, G, P.n_windows), 32 * warps, smem, s>>>(
-      sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
-      depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
+  if (deterministic) {
+    set_smem(reinterpret_cast<const void*>(k_bwd_owner<true>), smem, &a);
+    k_bwd_owner<true><<<dim3(TP.oT, G, P.n_windows), 32 * warps, smem, s>>>(
+        sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
+        depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
+  } else {
+    set_smem(reinterpret_cast<const void*>(k_bwd_owner<false>), smem, &b);
+    k_bwd_owner<false><<<dim3(TP.oT, G, P.n_windows), 64 * warps, smem, s>>>(
+        sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
+        depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
+  }
   if (d_depth && G > 1) {
     count_launch();
     k_ddepth_sum<<<148 * 4, 256, 0, s>>>(d_depth_parts, G, P.HW, P.n_windows, d_depth);

@@ -40,13 +40,16 @@ TileParams make_tiles(const WinParams& P, uint64_t max_n);
 int bwd_groups(const WinParams& P);
 void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off,
                        const WinParams& P, uint64_t max_n, uint2* packed, unsigned long long* err);
+// keys: 2 * n_total entries (unsorted keys, then keys in sorted order)
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
-                 const TileParams& TP, const double2* flows, uint32_t* keys, uint32_t* counts,
-                 uint32_t* tile_ptr, uint2* sorted, uint32_t* perm, uint32_t* bin_ptr);
+                 const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
+                 uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
+                 uint32_t* bin_ptr);
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                         uint64_t max_n, const double2* flows, uint64_t n_total, FwdRec* recs,
-                         uint4* bbox, uint32_t* lcount, uint16_t* lists);
+                         const uint32_t* sorted_keys, uint64_t max_n, const double2* flows,
+                         uint64_t n_total, FwdRec* recs, uint4* bbox, uint32_t* lcount,
+                         uint16_t* lists);
 void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
@@ -63,6 +66,6 @@ void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint16_t* lists, const int* no_surv, const double* depth,
                       const uint8_t* mask, const double* pose_tab, const double* K,
                       double* d_depth, double* d_depth_parts, double* pose_part,
-                      double* grad_out);
+                      double* grad_out, bool deterministic);
 
 }  // namespace evcm_b200

@@ -407,8 +407,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint2* sorted = e->get<uint2>("sorted", total);
   uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1));
   e->mark(2);
-  launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows,
-              e->get<uint32_t>("sort_keys", total),
+  uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total);
+  launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
               e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
               nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
   e->mark(3);
@@ -419,8 +419,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint32_t* lcount = e->get<uint32_t>("lcount", nl);
   ck(cudaMemsetAsync(lcount, 0, nl * sizeof(uint32_t), e->stream), "memset");
   uint16_t* lists = e->get<uint16_t>("lists", nl * kListCapO);
-  launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, total, recs,
-                      bbox, lcount, lists);
+  launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, keys + total, e->max_n, flows,
+                      total, recs, bbox, lcount, lists);
   e->mark(4);
   const size_t np = (size_t)nw * R * TP.oT;
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
@@ -461,7 +461,8 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   launch_bwd_owner(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
                    e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask, pose_tab,
-                   K, depth ? d_depth : nullptr, dd_parts, pose_part, grad_out);
+                   K, depth ? d_depth : nullptr, dd_parts, pose_part, grad_out,
+                   e->opt.deterministic != 0);
   e->mark(8);
   if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
   e->mark(9);
