@@ -4,10 +4,9 @@
 // backward is fused into the gradient gather. See DESIGN.md §Kernels.
 //
 //   k_stage_pack    validate (EventSlice::validate) + pack events to 8 B
-//   k_key_hist      position of every event at the middle reference (the exact
-//                   trajectory arithmetic of warp.hpp:257-281, partial legs)
-//                   -> 8x8 px sort-tile key + per-(tile, chunk) histogram
-//   k_sort_scan     exclusive scan of the histogram
+//   k_key_hist      approximate position of every event at the middle reference
+//                   -> 8x8 px sort-tile key + per-(chunk, tile) histogram
+//   k_sort_colscan  per tile: prefix over chunks; k_sort_tilescan: tile offsets
 //   k_sort_scatter  stable counting sort of the events by key
 //   k_bin_ptr       per sort tile: first event of every time bin
 //   k_traj_records  full trajectory -> per (event, ref) splat record {cell, pol,
@@ -115,6 +114,32 @@ __device__ __forceinline__ void warp_accumulate2(double* base, int key, double v
     }
   }
   __syncwarp();
+}
+
+// (a, b) += into a 16 B-aligned pair of shared doubles with one 128-bit CAS per
+// attempt (ATOMS.CAS.128, sm_90+): the fast-mode owner accumulation.
+__device__ __forceinline__ void smem_add2(double* addr, double a, double b) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(addr);
+  double o0, o1;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o0), "=d"(o1) : "r"(sa));
+  while (true) {
+    const double n0 = o0 + a, n1 = o1 + b;
+    unsigned long long r0, r1;
+    asm volatile(
+        "{\n .reg .b128 cmp, val, res;\n"
+        " mov.b128 cmp, {%2, %3};\n mov.b128 val, {%4, %5};\n"
+        " atom.shared.cas.b128 res, [%6], cmp, val;\n"
+        " mov.b128 {%0, %1}, res;\n}"
+        : "=l"(r0), "=l"(r1)
+        : "l"(__double_as_longlong(o0)), "l"(__double_as_longlong(o1)),
+          "l"(__double_as_longlong(n0)), "l"(__double_as_longlong(n1)), "r"(sa)
+        : "memory");
+    if (r0 == (unsigned long long)__double_as_longlong(o0) &&
+        r1 == (unsigned long long)__double_as_longlong(o1))
+      break;
+    o0 = __longlong_as_double(r0);
+    o1 = __longlong_as_double(r1);
+  }
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -259,8 +284,11 @@ __global__ void __launch_bounds__(kSortThreads) k_stage_pack(
   }
 }
 
-// Position at the middle reference rm = (B+1)/2 with the exact arithmetic of
-// build_trajectory (only the leg from the event towards rm) -> sort key.
+// Sort key: 8x8 tile of the event's approximate position at the middle
+// reference rm = (B+1)/2, extrapolated with the flow of its own bin at its own
+// (integer) pixel: x0 + u_j(x0) * (e_rm - t). One 16 B load per event; any
+// deterministic key is valid, this one keeps every tile compact at every ref.
+// counts layout: [w][chunk][tile] (coalesced writes and column scans).
 __global__ void __launch_bounds__(kSortThreads) k_key_hist(
     const uint2* __restrict__ packed, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const double2* __restrict__ flows, uint32_t* __restrict__ keys,
@@ -274,8 +302,8 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
     erel[i] = P.erel[i];
   }
   __syncthreads();
-  const int w = blockIdx.y, W = P.W, H = P.H, HW = P.HW, B = P.B;
-  const int rm = (B + 1) / 2;
+  const int w = blockIdx.y, HW = P.HW, B = P.B;
+  const double em = es[(B + 1) / 2];
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
   const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
@@ -288,93 +316,95 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
       continue;
     }
     const uint32_t dtu = ev_dt(e);
-    const double t = dm((double)dtu, 1e-6);
     const int j = bin_of(dtu, erel, B);
-    const double x0 = (double)ev_x(e), y0 = (double)ev_y(e);
-    const double2 u0 = sample_flow(fl + (size_t)j * HW, bilin_cell(x0, y0, W, H));
-    double2 p;
-    if (rm <= j) {  // backward leg down to rm
-      const double db = ds(es[j], t);
-      p = make_double2(da(x0, dm(db, u0.x)), da(y0, dm(db, u0.y)));
-      for (int i = j; i > rm; --i) {
-        const double dt = ds(es[i - 1], es[i]);
-        const double2 u = sample_flow(fl + (size_t)(i - 1) * HW, bilin_cell(p.x, p.y, W, H));
-        p = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
-      }
-    } else {  // forward leg up to rm
-      const double df = ds(es[j + 1], t);
-      p = make_double2(da(x0, dm(df, u0.x)), da(y0, dm(df, u0.y)));
-      for (int i = j + 1; i < rm; ++i) {
-        const double dt = ds(es[i + 1], es[i]);
-        const double2 u = sample_flow(fl + (size_t)i * HW, bilin_cell(p.x, p.y, W, H));
-        p = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
-      }
-    }
-    const uint32_t key = (uint32_t)sort_tile_of(p.x, p.y, P, TP);
+    const int x0 = ev_x(e), y0 = ev_y(e);
+    const double2 u = __ldg(fl + (size_t)j * HW + y0 * P.W + x0);
+    const double dt = em - (double)dtu * 1e-6;
+    const uint32_t key = (uint32_t)sort_tile_of(x0 + u.x * dt, y0 + u.y * dt, P, TP);
     keys[base + k] = key;
     atomicAdd(&hist[key], 1u);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x)
-    counts[((size_t)w * TP.nT + t) * TP.nchunks + blockIdx.x] = hist[t];
+  uint32_t* cw = counts + ((size_t)w * TP.nchunks + blockIdx.x) * TP.nT;
+  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) cw[t] = hist[t];
 }
 
-// Exclusive scan of counts[w][tile][chunk] (tile-major) in place; tile_ptr[w][t]
-// = first sorted slot of tile t, tile_ptr[w][nT] = valid events of the window.
-__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ counts, TileParams TP,
-                                                    uint32_t* __restrict__ tile_ptr) {
-  __shared__ uint32_t warp_tot[32];
-  const int w = blockIdx.x;
-  const size_t E = (size_t)TP.nT * TP.nchunks;
-  uint32_t* c = counts + (size_t)w * E;
-  const size_t per = (E + blockDim.x - 1) / blockDim.x;
-  const size_t lo = threadIdx.x * per, hi = lo + per < E ? lo + per : E;
-  uint32_t sum = 0;
-  for (size_t i = lo; i < hi; ++i) sum += c[i];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t x = sum;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t t = warp_tot[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, t, o);
-      if (lane >= o) t += y;
-    }
-    warp_tot[lane] = t;  // inclusive
-  }
-  __syncthreads();
-  uint32_t run = x - sum + (wid > 0 ? warp_tot[wid - 1] : 0u);
-  uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
-  for (size_t i = lo; i < hi; ++i) {
-    const uint32_t v = c[i];
-    c[i] = run;
-    if (i % TP.nchunks == 0) tp[i / TP.nchunks] = run;
+// Per tile: exclusive prefix over chunks (in place, counts -> offsets inside the
+// tile) and the tile total. One thread per (window, tile); reads are coalesced
+// across tiles.
+__global__ void k_sort_colscan(uint32_t* __restrict__ counts, TileParams TP,
+                               uint32_t* __restrict__ totals) {
+  const int w = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= TP.nT) return;
+  uint32_t* c = counts + (size_t)w * TP.nchunks * TP.nT + t;
+  uint32_t run = 0;
+  for (int ch = 0; ch < TP.nchunks; ++ch) {
+    const uint32_t v = c[(size_t)ch * TP.nT];
+    c[(size_t)ch * TP.nT] = run;
     run += v;
   }
-  if (threadIdx.x == blockDim.x - 1) tp[TP.nT] = run;
+  totals[(size_t)w * TP.nT + t] = run;
 }
 
-// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*512, +512);
-// per-warp tile counts give each warp its base inside the chunk's segment.
-__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
+// Exclusive scan of the tile totals: tile_ptr[w][t] = first sorted slot of tile
+// t, tile_ptr[w][nT] = valid events of the window. One CTA per window.
+__global__ void __launch_bounds__(1024) k_sort_tilescan(const uint32_t* __restrict__ totals,
+                                                        TileParams TP,
+                                                        uint32_t* __restrict__ tile_ptr) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t s_carry;
+  const int w = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t* tot = totals + (size_t)w * TP.nT;
+  uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int b = 0; b < TP.nT; b += blockDim.x) {
+    const int t = b + threadIdx.x;
+    const uint32_t v = t < TP.nT ? tot[t] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t q = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, q, o);
+        if (lane >= o) q += y;
+      }
+      warp_tot[lane] = q;
+    }
+    __syncthreads();
+    const uint32_t excl = s_carry + x - v + (wid > 0 ? warp_tot[wid - 1] : 0u);
+    if (t < TP.nT) tp[t] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tp[TP.nT] = s_carry;
+}
+
+// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*kChunk/nW, ...);
+// per-warp tile counts (u16) give each warp its base inside the chunk's run of
+// the tile, so the output keeps the input (time) order inside every tile.
+__global__ void __launch_bounds__(kScatterThreads) k_sort_scatter(
     const uint2* __restrict__ packed, const uint32_t* __restrict__ keys,
     const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
-    uint2* __restrict__ sorted, uint32_t* __restrict__ perm, uint32_t* __restrict__ sorted_keys) {
-  extern __shared__ uint16_t whist[];  // [16 warps][nT]
-  const int nW = kSortThreads / 32;
+    const uint32_t* __restrict__ tile_ptr, uint2* __restrict__ sorted, uint32_t* __restrict__ perm,
+    uint32_t* __restrict__ sorted_keys) {
+  extern __shared__ uint16_t whist[];  // [nW warps][nT]
+  constexpr int nW = kScatterThreads / 32;
+  constexpr int per = kChunk / nW;
   for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
   __syncthreads();
   const int w = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
-  const uint64_t k0 = (uint64_t)blockIdx.x * kChunk + (uint64_t)wid * (kChunk / nW);
+  const uint64_t k0 = (uint64_t)blockIdx.x * kChunk + (uint64_t)wid * per;
   uint16_t* mine = whist + wid * TP.nT;
-  for (int b = 0; b < kChunk / nW; b += 32) {  // pass 1: per-warp counts
+  for (int b = 0; b < per; b += 32) {  // pass 1: per-warp counts
     const uint64_t k = k0 + b + lane;
     int t = -1;
     if (k < n) {
@@ -389,17 +419,18 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
     __syncwarp();
   }
   __syncthreads();
+  const uint32_t* off = offsets + ((size_t)w * TP.nchunks + blockIdx.x) * TP.nT;
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) {  // pass 2: prefix over warps
-    uint16_t run = 0;
+    uint32_t run = 0;
     for (int q = 0; q < nW; ++q) {
-      const uint16_t v = whist[q * TP.nT + t];
-      whist[q * TP.nT + t] = run;
-      run = (uint16_t)(run + v);
+      const uint32_t v = whist[q * TP.nT + t];
+      whist[q * TP.nT + t] = (uint16_t)run;
+      run += v;
     }
   }
   __syncthreads();
-  const uint32_t* off = offsets + (size_t)w * TP.nT * TP.nchunks;
-  for (int b = 0; b < kChunk / nW; b += 32) {  // pass 3: place in order
+  for (int b = 0; b < per; b += 32) {  // pass 3: place in order
     const uint64_t k = k0 + b + lane;
     int t = -1;
     if (k < n) {
@@ -410,7 +441,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(
     if (t >= 0) {
       const unsigned peers = __match_any_sync(act, t);
       const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-      const uint32_t dst = off[(size_t)t * TP.nchunks + blockIdx.x] + mine[t] + rank;
+      const uint32_t dst = tp[t] + off[t] + mine[t] + rank;
       sorted[base + dst] = packed[base + k];
       sorted_keys[base + dst] = (uint32_t)t;
       if (perm) perm[base + dst] = (uint32_t)k;
@@ -611,9 +642,7 @@ __global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
         const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
         if (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) {
           const double wq = corner_w(c, q);
-          double* a = mine + 4 * (ly * kOwnW + lx) + 2 * pol;
-          atomicAdd(a, wq);
-          atomicAdd(a + 1, wq * tb);
+          smem_add2(mine + 4 * (ly * kOwnW + lx) + 2 * pol, wq, wq * tb);
         }
       }
     }
@@ -880,8 +909,7 @@ __global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
       if (kDet) {
         warp_accumulate2(g, key, v0, v1);
       } else if (key >= 0) {
-        atomicAdd(g + 2 * key, v0);
-        atomicAdd(g + 2 * key + 1, v1);
+        smem_add2(g + 2 * key, v0, v1);
       }
     };
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
@@ -1110,17 +1138,21 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
                  uint32_t* bin_ptr) {
   static size_t a1 = 0, a2 = 0;
+  const size_t sc_smem = (size_t)(kScatterThreads / 32) * TP.nT * 2;
   set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
-  set_smem(reinterpret_cast<const void*>(k_sort_scatter), (size_t)(kSortThreads / 32) * TP.nT * 2, &a2);
+  set_smem(reinterpret_cast<const void*>(k_sort_scatter), sc_smem, &a2);
   const dim3 grid(TP.nchunks, P.n_windows);
+  uint32_t* totals = keys + 2 * n_total;  // nw * nT scratch after the two key arrays
   count_launch();
   k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, flows,
                                                                   keys, counts);
   count_launch();
-  k_sort_scan<<<P.n_windows, 1024, 0, s>>>(counts, TP, tile_ptr);
+  k_sort_colscan<<<dim3((TP.nT + 255) / 256, P.n_windows), 256, 0, s>>>(counts, TP, totals);
   count_launch();
-  k_sort_scatter<<<grid, kSortThreads, (size_t)(kSortThreads / 32) * TP.nT * 2, s>>>(
-      packed, keys, ev_off, TP, counts, sorted, perm, keys + n_total);
+  k_sort_tilescan<<<P.n_windows, 1024, 0, s>>>(totals, TP, tile_ptr);
+  count_launch();
+  k_sort_scatter<<<grid, kScatterThreads, sc_smem, s>>>(packed, keys, ev_off, TP, counts, tile_ptr,
+                                                        sorted, perm, keys + n_total);
   count_launch();
   k_bin_ptr<<<dim3((TP.nT + 127) / 128, P.n_windows), 128, 0, s>>>(sorted, ev_off, P, TP,
                                                                     tile_ptr, bin_ptr);

@@ -14,12 +14,13 @@ constexpr int kSortTile = 8;       // sort tiles: 8x8 px of the position at the 
 constexpr int kOwnW = 32;          // owner tiles: 32x16 px of the IWE stack / gradient planes
 constexpr int kOwnH = 16;
 constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
-constexpr int kSortThreads = 512;  // 16 warps x 512 events
-constexpr int kMaxTiles = 6000;    // sort scatter keeps 16 x nT u16 counters in smem
+constexpr int kSortThreads = 512;  // key/histogram CTA size
+constexpr int kScatterThreads = 256;  // 8 warps x 1024 events per scatter chunk
+constexpr int kMaxTiles = 12000;   // sort scatter keeps 8 x nT u16 counters in smem
 constexpr int kListCapO = 64;      // source-list capacity per (window, slot, owner tile)
 constexpr int kFwdWarps = 4;       // warps (private fp64 copies) per forward owner CTA
 constexpr int kPrefetch = 4;       // records in flight per lane in the owner loops
-constexpr int kBwdGroup = 12;      // bins (warps) per backward owner CTA
+constexpr int kBwdGroup = 5;       // bins per backward owner CTA (more CTAs, less tail)
 
 struct TileParams {
   int ntx, nty, nT;  // sort tiles
@@ -40,7 +41,8 @@ TileParams make_tiles(const WinParams& P, uint64_t max_n);
 int bwd_groups(const WinParams& P);
 void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off,
                        const WinParams& P, uint64_t max_n, uint2* packed, unsigned long long* err);
-// keys: 2 * n_total entries (unsorted keys, then keys in sorted order)
+// keys: 2 * n_total + n_windows * nT entries (unsorted keys, keys in sorted
+// order, per-tile totals)
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
                  const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,

@@ -310,6 +310,8 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
     if (TP.nT > kMaxTiles)
       fail(EVCM_ERR_CONFIG, "cuda backend: sensor too large (more than " +
                                 std::to_string(kMaxTiles) + " 8x8 sort tiles)");
+    if (max_n > 0xffff * (uint64_t)kChunk)
+      fail(EVCM_ERR_CONFIG, "cuda backend: too many events in one window");
     e->TP = TP;
     launch_stage_pack(e->stream, dev, off_d, P, max_n, packed, err);
   } else {
@@ -407,7 +409,7 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint2* sorted = e->get<uint2>("sorted", total);
   uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1));
   e->mark(2);
-  uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total);
+  uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total + (size_t)nw * TP.nT);
   launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
               e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
               nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
