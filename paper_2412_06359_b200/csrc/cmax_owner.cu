@@ -616,17 +616,17 @@ __global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
   const size_t ws = (size_t)w * NS + r;
 
   auto contribute = [&](const FwdRec& rec) {
-    const bool live = rec.cell != kDead;
+    const int cx0 = (int)(rec.cell & 0xffffu), cy0 = (int)((rec.cell >> 16) & 0x7fffu);
+    const bool touch = rec.cell != kDead && cx0 + ox >= ox0 && cx0 < ox0 + kOwnW &&
+                       cy0 + oy >= oy0 && cy0 < oy0 + kOwnH;
     CellW c{};
     double tb = 0.0;
     int pol = 0;
-    if (live) {
+    if (touch) {
       c = decode(rec);
       pol = (int)(rec.cell >> 31);
       tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
     }
-    const bool touch = live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW && c.y0 + oy >= oy0 &&
-                       c.y0 < oy0 + kOwnH;
     if (kDet) {
       if (!__any_sync(kFull, touch)) return;
 #pragma unroll
@@ -642,7 +642,9 @@ __global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
         const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
         if (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) {
           const double wq = corner_w(c, q);
-          smem_add2(mine + 4 * (ly * kOwnW + lx) + 2 * pol, wq, wq * tb);
+          double* a = mine + 4 * (ly * kOwnW + lx) + 2 * pol;
+          atomicAdd(a, wq);
+          atomicAdd(a + 1, wq * tb);
         }
       }
     }
@@ -909,7 +911,8 @@ __global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
       if (kDet) {
         warp_accumulate2(g, key, v0, v1);
       } else if (key >= 0) {
-        smem_add2(g + 2 * key, v0, v1);
+        atomicAdd(g + 2 * key, v0);
+        atomicAdd(g + 2 * key + 1, v1);
       }
     };
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
