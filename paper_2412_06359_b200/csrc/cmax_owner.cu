@@ -142,6 +142,35 @@ __device__ __forceinline__ void smem_add2(double* addr, double a, double b) {
   }
 }
 
+// Warp-aggregated shared-memory accumulation (fast mode): lanes sharing `key`
+// are summed by the lowest of them, which issues the only atomic for that
+// address (the warp's records are spatially clustered, so without this the
+// CAS loops would serialise on duplicate addresses). Other warps of the CTA
+// add into the same tile concurrently. Warp-collective.
+__device__ __forceinline__ void warp_atomic_add2(double* base, int key, double v0, double v1) {
+  const unsigned act = __ballot_sync(kFull, key >= 0);
+  if (key >= 0) {
+    const unsigned peers = __match_any_sync(act, key);
+    const int lane = threadIdx.x & 31;
+    double s0 = v0, s1 = v1;
+    if (peers != (1u << lane)) {
+      s0 = 0.0;
+      s1 = 0.0;
+      unsigned m = peers;
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        s0 += __shfl_sync(peers, v0, src);
+        s1 += __shfl_sync(peers, v1, src);
+      }
+    }
+    if (lane == __ffs(peers) - 1) {
+      atomicAdd(base + 2 * key, s0);
+      atomicAdd(base + 2 * key + 1, s1);
+    }
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
@@ -627,26 +656,15 @@ __global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
       pol = (int)(rec.cell >> 31);
       tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
     }
-    if (kDet) {
-      if (!__any_sync(kFull, touch)) return;
+    if (!__any_sync(kFull, touch)) return;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-        const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
-        const double wq = corner_w(c, q);
-        warp_accumulate2(mine, in ? ((ly * kOwnW + lx) * 2 + pol) : -1, wq, wq * tb);
-      }
-    } else if (touch) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-        if (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) {
-          const double wq = corner_w(c, q);
-          double* a = mine + 4 * (ly * kOwnW + lx) + 2 * pol;
-          atomicAdd(a, wq);
-          atomicAdd(a + 1, wq * tb);
-        }
-      }
+    for (int q = 0; q < 4; ++q) {
+      const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
+      const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
+      const double wq = corner_w(c, q);
+      const int key = in ? ((ly * kOwnW + lx) * 2 + pol) : -1;
+      if (kDet) warp_accumulate2(mine, key, wq, wq * tb);
+      else warp_atomic_add2(mine, key, wq, wq * tb);
     }
   };
 
@@ -907,13 +925,9 @@ __global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
     const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
     const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
     const int nA = s_n[wq][0], nB = s_n[wq][1], nC = s_n[wq][2];
-    auto add = [&](int key, double v0, double v1) {  // one corner into the bin tile
-      if (kDet) {
-        warp_accumulate2(g, key, v0, v1);
-      } else if (key >= 0) {
-        atomicAdd(g + 2 * key, v0);
-        atomicAdd(g + 2 * key + 1, v1);
-      }
+    auto add = [&](int key, double v0, double v1) {  // one corner into the bin tile (collective)
+      if (kDet) warp_accumulate2(g, key, v0, v1);
+      else warp_atomic_add2(g, key, v0, v1);
     };
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
       const bool live = rec.cell != kDead;
@@ -921,7 +935,7 @@ __global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
       if (live) c = decode(rec);
       const bool touch = live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW && c.y0 + oy >= oy0 &&
                          c.y0 < oy0 + kOwnH;
-      if (kDet ? !__any_sync(kFull, touch) : !touch) return;
+      if (!__any_sync(kFull, touch)) return;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;

@@ -11,16 +11,16 @@
 namespace evcm_b200 {
 
 constexpr int kSortTile = 8;       // sort tiles: 8x8 px of the position at the middle reference
-constexpr int kOwnW = 64;          // owner tiles: 64x32 px of the IWE stack / gradient planes
-constexpr int kOwnH = 32;
+constexpr int kOwnW = 32;          // owner tiles: 32x16 px of the IWE stack / gradient planes
+constexpr int kOwnH = 16;
 constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
 constexpr int kSortThreads = 512;  // key/histogram CTA size
 constexpr int kScatterThreads = 256;  // 8 warps x 1024 events per scatter chunk
 constexpr int kMaxTiles = 12000;   // sort scatter keeps 8 x nT u16 counters in smem
 constexpr int kListCapO = 128;     // source-list capacity per (window, slot, owner tile)
-constexpr int kFwdWarps = 2;       // warps (private fp64 copies) per deterministic forward owner
+constexpr int kFwdWarps = 4;       // warps (private fp64 copies) per deterministic forward owner
 constexpr int kPrefetch = 4;       // records in flight per lane in the owner loops
-constexpr int kBwdGroup = 2;       // bins per backward owner CTA
+constexpr int kBwdGroup = 5;       // bins per backward owner CTA
 
 struct TileParams {
   int ntx, nty, nT;  // sort tiles
