@@ -83,7 +83,7 @@ def make_inputs(wl, rank, n_windows):
     return depth, poses, K, ev, offs
 
 
-def algorithmic_bytes(wl, n_windows):
+def algorithmic_bytes(wl, n_windows, algo="owner"):
     """bytes = N*b_ev + HW*b_px per window, at the precision this
     build computes in (depth f64 s_d=8, flows f64 s_f=8, IWE stack f64 s_s=8,
     gradients f32 s_g=4): b_px = 3 s_d + 6B s_f + 12(B+1) s_s + 4B s_g, b_ev = 18.
@@ -92,20 +92,33 @@ def algorithmic_bytes(wl, n_windows):
     sd, sf, ss, sg = 8, 8, 8, 4
     # each model term is attributed to the kernel that implements that stage of
     # the reference; fused kernels carry the terms of every stage they absorb
-    per = {
-        "motion_field": HW * (sd + 2 * B * sf),                       # K1
-        "traj_records": n * 9 + HW * 2 * B * sf,                      # K2 (warp)
-        "fwd_owner": HW * 8 * (B + 1) * ss,                           # K3 write + K3b read
-        "bwd_event": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),    # K4 gathers
-        "bwd_owner": HW * (4 * B * sg + 2 * sd),                      # K4 grad write + K5
-    }
+    if algo == "owner":
+        per = {
+            "motion_field": HW * (sd + 2 * B * sf),                       # K1
+            "traj_records": n * 9 + HW * 2 * B * sf,                      # K2 (warp)
+            "fwd_owner": HW * 8 * (B + 1) * ss,                           # K3 write + K3b read
+            "bwd_event": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),    # K4 gathers
+            "bwd_owner": HW * (4 * B * sg + 2 * sd),                      # K4 grad write + K5
+        }
+    else:
+        per = {
+            "motion_field": HW * (sd + 2 * B * sf),                       # K1
+            "warp_splat": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss),   # K2 + K3 write
+            "loss_reduce": HW * 4 * (B + 1) * ss,                         # K3b
+            "backward": n * 9 + HW * (2 * B * sf + 4 * (B + 1) * ss + 2 * B * sg),  # K4
+            "flows_backward": HW * (2 * B * sg + 2 * sd),                 # K5
+        }
     per = {k: v * n_windows for k, v in per.items()}
     return sum(per.values()), per
 
 
-# evcm_cuda_stage_times order for the default (owner-computes) pipeline
-STAGES = ["staging", "motion_field", "sort", "traj_records", "fwd_owner", "loss_finalize",
-          "bwd_event", "bwd_owner", "pose_finalize"]
+# evcm_cuda_stage_times order per pipeline (include/evcm_cuda.h)
+STAGES_BY_ALGO = {
+    "owner": ["staging", "motion_field", "sort", "traj_records", "fwd_owner", "loss_finalize",
+              "bwd_event", "bwd_owner", "pose_finalize"],
+    "atomic": ["staging", "motion_field", "stack_memset", "warp_splat", "loss_reduce",
+               "grad_memset", "backward", "flows_backward", "unused"],
+}
 
 
 # ---------------------------------------------------------------------------
@@ -258,7 +271,7 @@ def cuda_arm(args, wl):
     depth, poses, K, ev, offs = make_inputs(wl, rank, nwin)
     stream = torch.cuda.Stream(dev)
     eng = P.Engine(P.EngineOptions(device=local, stream=stream.cuda_stream,
-                                   deterministic=args.deterministic))
+                                   deterministic=args.deterministic, algo=args.algo))
 
     # device-resident inputs / outputs
     with torch.cuda.stream(stream):
@@ -273,13 +286,12 @@ def cuda_arm(args, wl):
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream.synchronize()
 
+    from paper_2412_06359_b200.dist import allreduce_window_sums, pack_window_sums
+
     def reduce_and_allreduce():
         # data-parallel reduction of [sum loss, sum_w d_depth, sum_w d_poses]
-        red[0:1].copy_(out[0].sum().reshape(1))
-        red[1:1 + HW].copy_(out[1].sum(0).reshape(-1))
-        red[1 + HW:].copy_(out[2].sum(0).reshape(-1))
-        if world > 1:
-            dist.all_reduce(red)
+        pack_window_sums(out[0], out[1], out[2], out=red)
+        allreduce_window_sums(red)
 
     def step():
         eng.chain_batch(d_depth, d_poses, K, 0, wl["window_us"], d_ev, offs, out=out)
@@ -290,6 +302,8 @@ def cuda_arm(args, wl):
             step()
         stream.synchronize()
         launches_per_step = eng.last_launch_count()
+        algo_ran = eng.last_algo()
+        STAGES = STAGES_BY_ALGO[algo_ran]
 
         eng.set_timing(True)
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -327,7 +341,7 @@ def cuda_arm(args, wl):
     # average CUDA-event duration on the launching stream)
     stage_ms /= args.steps
     peak, peak_kind = peaks()
-    total_bytes, per_kernel = algorithmic_bytes(wl, nwin)
+    total_bytes, per_kernel = algorithmic_bytes(wl, nwin, algo_ran)
     kern = {k: stage_ms[STAGES.index(k)] for k in per_kernel}
     dom = max(kern, key=kern.get)
     achieved = per_kernel[dom] / (kern[dom] * 1e-3) / 1e9
@@ -395,7 +409,8 @@ def cuda_arm(args, wl):
                        "bins": wl["B"], "numerics": "parity (fp64 per-event math, fp64 IWE "
                        "stack, fp32 flow-gradient accumulators)",
                        "l2": "flushed between timed steps (256 MB write, untimed)",
-                       "mode": "deterministic" if args.deterministic else "fast (smem fp64 atomics)",
+                       "mode": ("deterministic" if args.deterministic else "fast") +
+                               f" (algo {args.algo} -> {algo_ran})",
                        "inputs": "two-plane depth + per-bin ego-motion, uniform events",
                        "parallelism": f"dp{world} (windows sharded, NCCL all-reduce of "
                                       "loss/d_depth/d_poses)"},
@@ -420,6 +435,7 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--algo", default="auto", choices=["auto", "owner", "atomic"])
     ap.add_argument("--deterministic", action="store_true",
                     help="bit-stable owner accumulation (fixed-order, slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

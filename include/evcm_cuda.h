@@ -95,9 +95,10 @@ typedef struct {
   int grad_f64;        /* 1: fp64 flow-gradient accumulators (default 0: fp32, which
                           keeps gradients within ~1e-7 of the reference) */
   void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
-  int algo;            /* 0 (default): owner-computes tiles (deterministic, no global
-                          atomics); 1: per-event global atomics (reference-order-free
-                          cross-check path, honours stack_f64 / grad_f64) */
+  int algo;            /* 0: owner-computes tiles (no global atomics; the only path with
+                          deterministic = 1); 1: per-event global atomics (honours
+                          stack_f64 / grad_f64); 2 (default): auto — owner when the
+                          batch has >= 2 events per pixel per window or deterministic */
 } evcm_cuda_options;
 
 /* EventSlice (types.hpp:121-126). */
@@ -224,6 +225,13 @@ EVCM_API int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch*
  * did not run the stage). Returns the number of stages written (8). */
 EVCM_API int evcm_cuda_set_timing(evcm_cuda_engine* e, int enabled);
 EVCM_API int evcm_cuda_stage_times(evcm_cuda_engine* e, double* ms, int max_stages);
+/* Pipeline the last call ran: 0 owner-computes, 1 per-event atomics. Stage
+ * order of evcm_cuda_stage_times for the atomic pipeline: staging, motion field,
+ * stack memset, warp+splat, loss reduce, grad memset, backward, flows backward;
+ * for the owner pipeline: staging, motion field, sort, trajectory records +
+ * source lists, forward owner, loss finalize, per-event backward, backward
+ * owner (+ fused flows backward), pose finalize. */
+EVCM_API int evcm_cuda_last_algo(evcm_cuda_engine* e);
 /* Number of kernels launched by the last API call (for bench gpu_launches). */
 EVCM_API int evcm_cuda_last_launch_count(evcm_cuda_engine* e);
 /* Device memory currently held by the engine's workspaces, in bytes (the

@@ -663,8 +663,12 @@ __global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
       const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
       const double wq = corner_w(c, q);
       const int key = in ? ((ly * kOwnW + lx) * 2 + pol) : -1;
-      if (kDet) warp_accumulate2(mine, key, wq, wq * tb);
-      else warp_atomic_add2(mine, key, wq, wq * tb);
+      if (kDet) {
+        warp_accumulate2(mine, key, wq, wq * tb);
+      } else if (key >= 0) {
+        atomicAdd(mine + 2 * key, wq);
+        atomicAdd(mine + 2 * key + 1, wq * tb);
+      }
     }
   };
 
@@ -926,8 +930,12 @@ __global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
     const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
     const int nA = s_n[wq][0], nB = s_n[wq][1], nC = s_n[wq][2];
     auto add = [&](int key, double v0, double v1) {  // one corner into the bin tile (collective)
-      if (kDet) warp_accumulate2(g, key, v0, v1);
-      else warp_atomic_add2(g, key, v0, v1);
+      if (kDet) {
+        warp_accumulate2(g, key, v0, v1);
+      } else if (key >= 0) {
+        atomicAdd(g + 2 * key, v0);
+        atomicAdd(g + 2 * key + 1, v1);
+      }
     };
     auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
       const bool live = rec.cell != kDead;

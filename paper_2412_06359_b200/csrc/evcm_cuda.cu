@@ -144,7 +144,9 @@ struct evcm_cuda_engine {
   // owner pipeline state
   TileParams TP{};
   uint64_t n_total = 0, max_n = 0;
-  bool owner() const { return opt.algo == 0; }
+  // resolved per call in stage_events: opt.algo 0 owner, 1 atomic, 2 auto
+  bool use_owner = true;
+  bool owner() const { return use_owner; }
   // state of the last forward (Engine::forward -> backward hand-off)
   bool have_fwd = false;
   WinParams P{};
@@ -304,6 +306,12 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
   e->n_total = total;
   e->max_n = max_n;
+  // algo auto: the owner pipeline wins once there are >= ~2 events per pixel and
+  // per window (measured crossover); deterministic mode needs it.
+  if (e->opt.algo == 2)
+    e->use_owner = e->opt.deterministic || (double)total >= 2.0 * (double)P.HW * nw;
+  else
+    e->use_owner = e->opt.algo == 0 || e->opt.deterministic;
   if (e->owner()) {
     // validation + packing; the sort needs the flows and runs in the forward
     const TileParams TP = make_tiles(P, max_n);
@@ -550,7 +558,7 @@ void evcm_cuda_default_options(evcm_cuda_options* o) {
   o->stack_f64 = 1;  // parity precision
   o->grad_f64 = 0;
   o->stream = nullptr;
-  o->algo = 0;
+  o->algo = 2;  // auto
 }
 
 int evcm_cuda_create(const evcm_cuda_options* opts, evcm_cuda_engine** out) {
@@ -603,6 +611,8 @@ int evcm_cuda_stage_times(evcm_cuda_engine* e, double* ms, int max_stages) {
 }
 
 int evcm_cuda_last_launch_count(evcm_cuda_engine* e) { return e ? e->last_launches : 0; }
+
+int evcm_cuda_last_algo(evcm_cuda_engine* e) { return e ? (e->owner() ? 0 : 1) : -1; }
 
 size_t evcm_cuda_workspace_bytes(evcm_cuda_engine* e) {
   size_t s = 0;

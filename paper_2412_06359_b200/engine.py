@@ -152,6 +152,7 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_set_timing.argtypes = [vp, i32]
     L.evcm_cuda_stage_times.argtypes = [vp, vp, i32]
     L.evcm_cuda_last_launch_count.argtypes = [vp]
+    L.evcm_cuda_last_algo.argtypes = [vp]
     L.evcm_cuda_workspace_bytes.argtypes = [vp]
     L.evcm_cuda_workspace_bytes.restype = sz
     _lib = L
@@ -408,7 +409,7 @@ class EngineOptions:
     stack_f64: bool = True   # parity precision; False = fp32 "fast" stack
     grad_f64: bool = False
     stream: Optional[int] = None  # raw cudaStream_t handle, None = engine-owned
-    algo: str = "owner"  # "owner" (tiles, deterministic) | "atomic" (per-event atomics)
+    algo: str = "auto"  # "owner" (tiles) | "atomic" (per-event atomics) | "auto"
 
 
 class Engine:
@@ -418,13 +419,13 @@ class Engine:
         self.opts = opts or EngineOptions()
         backend_from_name(self.opts.backend)
         L = load_library()
-        if self.opts.algo not in ("owner", "atomic"):
-            raise ConfigError(f"unknown algo '{self.opts.algo}' (owner|atomic)")
-        if self.opts.deterministic and self.opts.algo != "owner":
-            raise ConfigError("deterministic mode needs algo='owner'")
+        algos = {"owner": 0, "atomic": 1, "auto": 2}
+        if self.opts.algo not in algos:
+            raise ConfigError(f"unknown algo '{self.opts.algo}' (owner|atomic|auto)")
+        if self.opts.deterministic and self.opts.algo == "atomic":
+            raise ConfigError("deterministic mode needs algo='owner' or 'auto'")
         o = _Options(self.opts.device, int(self.opts.deterministic), int(self.opts.stack_f64),
-                     int(self.opts.grad_f64), self.opts.stream,
-                     0 if self.opts.algo == "owner" else 1)
+                     int(self.opts.grad_f64), self.opts.stream, algos[self.opts.algo])
         h = C.c_void_p()
         _raise(L.evcm_cuda_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -516,6 +517,9 @@ class Engine:
 
     def last_launch_count(self) -> int:
         return int(load_library().evcm_cuda_last_launch_count(self._h))
+
+    def last_algo(self) -> str:
+        return {0: "owner", 1: "atomic"}.get(load_library().evcm_cuda_last_algo(self._h), "?")
 
     def workspace_bytes(self) -> int:
         return int(load_library().evcm_cuda_workspace_bytes(self._h))

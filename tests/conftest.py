@@ -15,8 +15,9 @@ def pytest_configure(config):
 
 @pytest.fixture(scope="session")
 def engine():
+    """The owner-computes pipeline (fast mode)."""
     import paper_2412_06359_b200 as P
-    return P.Engine()
+    return P.Engine(P.EngineOptions(algo="owner"))
 
 
 @pytest.fixture(scope="session")

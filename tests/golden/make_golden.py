@@ -1,0 +1,66 @@
+"""Generates the golden fixtures in tests/golden/ by running the UNMODIFIED
+reference (oracle/_ref/libevcm_ref.so, compiled from /root/reference by
+oracle/Makefile). Run in the dev container (the reference tree is not on the GPU
+box):  python tests/golden/make_golden.py
+
+Each fixture is an .npz with the inputs and the reference outputs:
+  fd_<seed>.npz      random_fd_instance (fdcheck.hpp:94-146) -> Engine (naive backend)
+  smooth_32x24.npz   smooth-flow window (bench_window semantics + spatial variation)
+  geom_13x9.npz      depth_pose_to_flows / _backward on a masked depth map
+  chain_<seed>.npz   make_chain_instance (tests/chain_support.hpp:119-184) decoded
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle import oracle as O  # noqa: E402
+from tests.helpers import smooth_window  # noqa: E402
+
+
+def save(name, **arrs):
+    np.savez_compressed(os.path.join(HERE, name), **arrs)
+
+
+def window_fixture(name, w):
+    r = O.ref_loss_and_grad(w, backend="naive", want_pos=True)
+    save(name, W=w.W, H=w.H, edges=w.edges, events=w.events.view(np.uint8).reshape(-1, 16),
+         flows=w.flows, loss=r["loss"], no_survivors=r["no_survivors"], count=r["count"],
+         tsum=r["tsum"], n_active=r["n_active"], alive=r["alive"], bin=r["bin"], pos=r["pos"],
+         grad=r["grad"])
+
+
+def main():
+    if not O.ref_available():
+        O.build(ref=True)
+    for seed in (100, 7, 503, 1300):
+        window_fixture(f"fd_{seed}.npz", O.ref_fd_instance(seed))
+    window_fixture("fd_masked_900.npz", O.ref_fd_instance(900, max_events=24, want_masked=True))
+    window_fixture("smooth_32x24.npz", smooth_window(32, 24, 4, 600, seed=5))
+    rng = np.random.default_rng(11)
+    H, W, B = 9, 13, 3
+    depth = rng.uniform(0.8, 3.0, (H, W)).astype(np.float32).astype(np.float64)
+    mask = (rng.uniform(size=(H, W)) > 0.15).astype(np.uint8)
+    poses = np.concatenate([rng.uniform(-0.02, 0.02, (B, 3)), rng.uniform(-0.1, 0.1, (B, 3))], 1)
+    poses[1, 5] = -2.5  # some pixels behind the camera
+    K = np.array([0.9 * W, 0.95 * W, (W - 1) / 2 + 0.3, (H - 1) / 2 - 0.2])
+    flows, valid, edges = O.ref_depth_pose_to_flows(depth, poses, K, 0, 100000, mask)
+    g = rng.uniform(-1, 1, (B, 2, H, W))
+    dd, dp = O.ref_depth_pose_to_flows_backward(depth, poses, K, edges, g, mask)
+    save("geom_13x9.npz", depth=depth, mask=mask, poses=poses, K=K, flows=flows, valid=valid,
+         edges=edges, grad=g, d_depth=dd, d_poses=dp)
+    for seed in (1, 20):
+        ev, depth, poses, K = O.ref_chain_instance(seed)
+        fl, _, edges = O.ref_depth_pose_to_flows(depth, poses, K, 0, 100000)
+        w = O.Window(depth.shape[1], depth.shape[0], edges, ev, fl)
+        r = O.ref_loss_and_grad(w, backend="naive")
+        dd, dp = O.ref_depth_pose_to_flows_backward(depth, poses, K, edges, r["grad"])
+        save(f"chain_{seed}.npz", depth=depth, poses=poses, K=K, edges=edges,
+             events=ev.view(np.uint8).reshape(-1, 16), loss=r["loss"], d_depth=dd, d_poses=dp)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
