@@ -1,0 +1,238 @@
+// evcm_cuda_backend.hpp — reference-side binding of the B200 CMax path.
+//
+// Header-only C++20 adapter a maintainer of the reference (evcm,
+// /root/reference/proj/include/evcm) includes to get a `cuda` backend with the
+// reference's own types and error classes. It only talks to the C-ABI of
+// include/evcm_cuda.h (libevcm_cuda.so); no CUDA or torch types appear here.
+//
+//   evcm::cuda::Engine            ~ evcm::Engine              (engine.hpp:134-213)
+//   evcm::cuda::depth_pose_to_flows / _backward               (geometry.hpp:229-325)
+//   evcm::cuda::contrast_loss_backward / build_iwe_stack / rsat (engine.hpp:606-631)
+//
+// Requires the reference headers on the include path (it reuses EventSlice,
+// FlowSequence, ForwardResult, ... from evcm).
+#pragma once
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "evcm/engine.hpp"
+#include "evcm/geometry.hpp"
+#include "evcm_cuda.h"
+
+namespace evcm::cuda {
+
+// Status -> the reference's exception taxonomy (types.hpp:18-76).
+[[noreturn]] inline void raise(int rc) {
+  const std::string msg = std::string("cuda backend: ") + evcm_cuda_last_error();
+  switch (rc) {
+    case EVCM_ERR_CONFIG:
+    case EVCM_ERR_STATE: throw ConfigError(msg);
+    case EVCM_ERR_DIMENSION: throw DimensionMismatchError(msg);
+    case EVCM_ERR_COORDINATE: throw CoordinateRangeError(msg);
+    case EVCM_ERR_POLARITY: throw InvalidPolarityError(msg);
+    case EVCM_ERR_UNSORTED: throw UnsortedEventsError(msg);
+    case EVCM_ERR_TIME_RANGE: throw TimeRangeError(msg);
+    case EVCM_ERR_EMPTY: throw EmptySliceError(msg);
+    default: throw Error(msg);
+  }
+}
+inline void check(int rc) {
+  if (rc != EVCM_OK) raise(rc);
+}
+
+// FlowSequence -> contiguous [B][2][H][W] (types.hpp:228-253).
+inline std::vector<double> pack_flows(const FlowSequence& f) {
+  const std::size_t HW = f.fields.empty() ? 0 : f.fields[0].u.size();
+  std::vector<double> uv(static_cast<std::size_t>(f.n_bins()) * 2 * HW);
+  for (int b = 0; b < f.n_bins(); ++b) {
+    std::memcpy(uv.data() + (2 * b) * HW, &f.fields[b].u[0], HW * sizeof(double));
+    std::memcpy(uv.data() + (2 * b + 1) * HW, &f.fields[b].v[0], HW * sizeof(double));
+  }
+  return uv;
+}
+
+inline evcm_slice c_slice(const EventSlice& s) {
+  static_assert(sizeof(Event) == sizeof(evcm_event), "evcm::Event layout");
+  return evcm_slice{s.width, s.height, s.t_start_us, s.t_end_us,
+                    reinterpret_cast<const evcm_event*>(s.events.data()), s.events.size()};
+}
+
+// EngineOptions of the reference plus the cuda-only knobs.
+struct CudaOptions {
+  int device = 0;
+  bool deterministic = true;  // engine.hpp:60 default
+  int algo = 2;               // 0 owner, 1 atomic, 2 auto
+};
+
+class Engine {
+ public:
+  explicit Engine(CudaOptions o = {}) {
+    evcm_cuda_options co;
+    evcm_cuda_default_options(&co);
+    co.device = o.device;
+    co.deterministic = o.deterministic ? 1 : 0;
+    co.algo = o.algo;
+    evcm_cuda_engine* h = nullptr;
+    check(evcm_cuda_create(&co, &h));
+    h_.reset(h);
+  }
+
+  // Engine::forward (engine.hpp:145-183): stack, trajectories and loss.
+  ForwardResult forward(const EventSlice& slice, const FlowSequence& flows) const {
+    const std::vector<double> uv = pack_flows(flows);
+    const evcm_slice s = c_slice(slice);
+    const evcm_flows f{flows.n_bins(), flows.edges_us.data(), uv.data()};
+    evcm_loss loss{};
+    check(evcm_cuda_forward(h_.get(), &s, &f, EVCM_MEM_HOST, &loss));
+    ForwardResult res;
+    const int W = slice.width, H = slice.height, R = flows.n_bins() + 1;
+    const std::size_t HW = static_cast<std::size_t>(W) * H, n = slice.events.size();
+    res.stack = IweStack(W, H, R);
+    std::vector<double> count(R * 2 * HW), tsum(R * 2 * HW), pos(n * R * 2);
+    res.traj.resize(n, R);
+    std::size_t n_alive = 0;
+    check(evcm_cuda_forward_products(h_.get(), count.data(), tsum.data(),
+                                     res.stack.n_active.data(), res.traj.alive.data(),
+                                     res.traj.bin.data(), pos.data(), &n_alive));
+    for (int r = 0; r < R; ++r)
+      for (int c = 0; c < 2; ++c) {
+        std::memcpy(&res.stack.count[r][c][0], count.data() + (r * 2 + c) * HW, HW * sizeof(double));
+        std::memcpy(&res.stack.tsum[r][c][0], tsum.data() + (r * 2 + c) * HW, HW * sizeof(double));
+      }
+    std::memcpy(res.traj.pos.data(), pos.data(), pos.size() * sizeof(double));
+    res.traj.n_alive = n_alive;
+    res.loss.value = loss.value;
+    res.loss.no_survivors = loss.no_survivors != 0;
+    return res;
+  }
+
+  // Engine::backward (engine.hpp:185-205) for the window of the last forward.
+  BackwardResult backward(const EventSlice& slice, const FlowSequence& flows,
+                          const ForwardResult&) const {
+    const std::vector<double> uv = pack_flows(flows);
+    const evcm_slice s = c_slice(slice);
+    const evcm_flows f{flows.n_bins(), flows.edges_us.data(), uv.data()};
+    const std::size_t HW = static_cast<std::size_t>(slice.width) * slice.height;
+    std::vector<double> g(static_cast<std::size_t>(flows.n_bins()) * 2 * HW);
+    check(evcm_cuda_backward(h_.get(), &s, &f, EVCM_MEM_HOST, g.data()));
+    BackwardResult res;
+    res.grad = GradientBuffer(slice.width, slice.height, flows.n_bins());
+    for (int b = 0; b < flows.n_bins(); ++b) {
+      std::memcpy(&res.grad.gu[b][0], g.data() + (2 * b) * HW, HW * sizeof(double));
+      std::memcpy(&res.grad.gv[b][0], g.data() + (2 * b + 1) * HW, HW * sizeof(double));
+    }
+    return res;
+  }
+
+  std::pair<ForwardResult, BackwardResult> loss_and_grad(const EventSlice& slice,
+                                                         const FlowSequence& flows) const {
+    ForwardResult f = forward(slice, flows);
+    BackwardResult b = backward(slice, flows, f);
+    return {std::move(f), std::move(b)};
+  }
+
+  evcm_cuda_engine* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(evcm_cuda_engine* e) const { evcm_cuda_destroy(e); }
+  };
+  std::unique_ptr<evcm_cuda_engine, Del> h_;
+};
+
+inline std::vector<double> pack_poses(const std::vector<PoseStep>& poses) {
+  std::vector<double> p(poses.size() * 6);
+  for (std::size_t i = 0; i < poses.size(); ++i) {
+    const double v[6] = {poses[i].omega.x, poses[i].omega.y, poses[i].omega.z,
+                         poses[i].trans.x, poses[i].trans.y, poses[i].trans.z};
+    std::memcpy(p.data() + 6 * i, v, sizeof v);
+  }
+  return p;
+}
+
+// depth_pose_to_flows (geometry.hpp:229-264).
+inline GeometryFlows depth_pose_to_flows(const Engine& e, const DepthMap& depth,
+                                         const std::vector<PoseStep>& poses,
+                                         const CameraIntrinsics& k, std::uint64_t t0,
+                                         std::uint64_t t1) {
+  const int W = depth.width(), H = depth.height(), B = static_cast<int>(poses.size());
+  const std::size_t HW = static_cast<std::size_t>(W) * H;
+  const std::vector<double> p = pack_poses(poses);
+  const double K[4] = {k.fx, k.fy, k.cx, k.cy};
+  std::vector<double> uv(static_cast<std::size_t>(B) * 2 * HW);
+  std::vector<std::uint8_t> valid(static_cast<std::size_t>(B) * HW);
+  std::vector<std::uint64_t> edges(static_cast<std::size_t>(B) + 1);
+  check(evcm_cuda_depth_pose_to_flows(e.handle(), W, H, &depth.d[0],
+                                      depth.has_mask() ? &depth.valid[0] : nullptr, B, p.data(),
+                                      K, t0, t1, EVCM_MEM_HOST, uv.data(), valid.data(),
+                                      edges.data()));
+  GeometryFlows out;
+  out.flows = FlowSequence::zeros(W, H, t0, t1, B);
+  for (int b = 0; b < B; ++b) {
+    std::memcpy(&out.flows.fields[b].u[0], uv.data() + (2 * b) * HW, HW * sizeof(double));
+    std::memcpy(&out.flows.fields[b].v[0], uv.data() + (2 * b + 1) * HW, HW * sizeof(double));
+    Image<std::uint8_t> m(W, H, 0);
+    std::memcpy(&m[0], valid.data() + b * HW, HW);
+    out.valid.push_back(std::move(m));
+  }
+  return out;
+}
+
+// depth_pose_to_flows_backward (geometry.hpp:279-325).
+inline FlowsBackwardResult depth_pose_to_flows_backward(const Engine& e, const DepthMap& depth,
+                                                        const std::vector<PoseStep>& poses,
+                                                        const CameraIntrinsics& k,
+                                                        const FlowSequence& flows,
+                                                        const GradientBuffer& grad) {
+  const int W = depth.width(), H = depth.height(), B = static_cast<int>(poses.size());
+  if (flows.n_bins() != B || grad.n_bins() != B)
+    throw ConfigError("flows backward: bins, poses, and gradients must align");
+  if (grad.width() != W || grad.height() != H)
+    throw DimensionMismatchError("flows backward: grids must match the depth map");
+  const std::size_t HW = static_cast<std::size_t>(W) * H;
+  std::vector<double> g(static_cast<std::size_t>(B) * 2 * HW);
+  for (int b = 0; b < B; ++b) {
+    std::memcpy(g.data() + (2 * b) * HW, &grad.gu[b][0], HW * sizeof(double));
+    std::memcpy(g.data() + (2 * b + 1) * HW, &grad.gv[b][0], HW * sizeof(double));
+  }
+  const std::vector<double> p = pack_poses(poses);
+  const double K[4] = {k.fx, k.fy, k.cx, k.cy};
+  FlowsBackwardResult out;
+  out.d_depth = Image<double>(W, H, 0.0);
+  std::vector<double> dp(static_cast<std::size_t>(B) * 6);
+  check(evcm_cuda_depth_pose_to_flows_backward(e.handle(), W, H, &depth.d[0],
+                                               depth.has_mask() ? &depth.valid[0] : nullptr, B,
+                                               p.data(), K, flows.edges_us.data(), g.data(),
+                                               EVCM_MEM_HOST, &out.d_depth[0], dp.data()));
+  out.d_poses.resize(static_cast<std::size_t>(B));
+  for (int b = 0; b < B; ++b)
+    out.d_poses[b] = PoseGrad{{dp[6 * b], dp[6 * b + 1], dp[6 * b + 2]},
+                              {dp[6 * b + 3], dp[6 * b + 4], dp[6 * b + 5]}};
+  return out;
+}
+
+// Module-level helpers (engine.hpp:606-631).
+inline ForwardResult build_iwe_stack(const EventSlice& s, const FlowSequence& f,
+                                     CudaOptions o = {}) {
+  return Engine(o).forward(s, f);
+}
+inline GradientBuffer contrast_loss_backward(const EventSlice& s, const FlowSequence& f,
+                                             CudaOptions o = {}) {
+  const Engine e(o);
+  const ForwardResult fw = e.forward(s, f);
+  return e.backward(s, f, fw).grad;
+}
+inline double rsat(const EventSlice& s, const FlowSequence& f, CudaOptions o = {}) {
+  if (s.events.empty()) throw EmptySliceError("rsat: no events in slice");
+  const Engine e(o);
+  const double with_flow = e.forward(s, f).loss.value;
+  const LossResult base = e.forward(s, f.zeros_like()).loss;
+  if (base.no_survivors || base.value == 0.0) throw EmptySliceError("rsat: zero-flow loss is zero");
+  return with_flow / base.value;
+}
+
+}  // namespace evcm::cuda

@@ -46,6 +46,9 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
     if ref and os.path.isdir("/root/reference/proj/include"):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        lib = os.path.join(HERE, "..", "paper_2412_06359_b200", "_lib", "libevcm_cuda.so")
+        if os.path.exists(lib):  # the C++ binding test links the product library
+            subprocess.run(["make", "-s", "-C", HERE, "adapter"], check=True)
 
 
 def _p(a):
