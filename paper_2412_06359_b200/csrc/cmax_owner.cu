@@ -116,61 +116,6 @@ __device__ __forceinline__ void warp_accumulate2(double* base, int key, double v
   __syncwarp();
 }
 
-// (a, b) += into a 16 B-aligned pair of shared doubles with one 128-bit CAS per
-// attempt (ATOMS.CAS.128, sm_90+): the fast-mode owner accumulation.
-__device__ __forceinline__ void smem_add2(double* addr, double a, double b) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(addr);
-  double o0, o1;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(o0), "=d"(o1) : "r"(sa));
-  while (true) {
-    const double n0 = o0 + a, n1 = o1 + b;
-    unsigned long long r0, r1;
-    asm volatile(
-        "{\n .reg .b128 cmp, val, res;\n"
-        " mov.b128 cmp, {%2, %3};\n mov.b128 val, {%4, %5};\n"
-        " atom.shared.cas.b128 res, [%6], cmp, val;\n"
-        " mov.b128 {%0, %1}, res;\n}"
-        : "=l"(r0), "=l"(r1)
-        : "l"(__double_as_longlong(o0)), "l"(__double_as_longlong(o1)),
-          "l"(__double_as_longlong(n0)), "l"(__double_as_longlong(n1)), "r"(sa)
-        : "memory");
-    if (r0 == (unsigned long long)__double_as_longlong(o0) &&
-        r1 == (unsigned long long)__double_as_longlong(o1))
-      break;
-    o0 = __longlong_as_double(r0);
-    o1 = __longlong_as_double(r1);
-  }
-}
-
-// Warp-aggregated shared-memory accumulation (fast mode): lanes sharing `key`
-// are summed by the lowest of them, which issues the only atomic for that
-// address (the warp's records are spatially clustered, so without this the
-// CAS loops would serialise on duplicate addresses). Other warps of the CTA
-// add into the same tile concurrently. Warp-collective.
-__device__ __forceinline__ void warp_atomic_add2(double* base, int key, double v0, double v1) {
-  const unsigned act = __ballot_sync(kFull, key >= 0);
-  if (key >= 0) {
-    const unsigned peers = __match_any_sync(act, key);
-    const int lane = threadIdx.x & 31;
-    double s0 = v0, s1 = v1;
-    if (peers != (1u << lane)) {
-      s0 = 0.0;
-      s1 = 0.0;
-      unsigned m = peers;
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        s0 += __shfl_sync(peers, v0, src);
-        s1 += __shfl_sync(peers, v1, src);
-      }
-    }
-    if (lane == __ffs(peers) - 1) {
-      atomicAdd(base + 2 * key, s0);
-      atomicAdd(base + 2 * key + 1, s1);
-    }
-  }
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
