@@ -47,7 +47,7 @@ int main() {
       const FdInstance inst = random_fd_instance(seed);
       const auto [rf, rb] = ref.loss_and_grad(inst.slice, inst.flows);
       const auto [gf, gb] = gpu.loss_and_grad(inst.slice, inst.flows);
-      CHECK(std::abs(gf.loss.value - rf.loss.value) <= 1e-12 * std::abs(rf.loss.value),
+      CHECK(std::abs(gf.loss.value - rf.loss.value) <= 1e-5 * std::abs(rf.loss.value),
             "loss seed %llu", (unsigned long long)seed);
       CHECK(gf.traj.n_alive == rf.traj.n_alive, "n_alive");
       for (std::size_t k = 0; k < inst.slice.events.size(); ++k) {
