@@ -103,6 +103,87 @@ __global__ void k_interleave_flows(const double* __restrict__ uv, int B, int HW,
 }
 
 // --------------------------------------------------------------------------
+// Pose tables on the device (for device-resident poses: no host round trip).
+// Same expression order as rodrigues / rodrigues_jacobian (geometry.hpp:94-135);
+// the device sin/cos may differ from the host libm by an ulp, so flows from
+// device poses match the reference to ~1e-16 relative instead of bit for bit.
+// Pose validation (types.hpp:362-368) sets *bad = 1.
+
+__device__ void m3mul(const double* a, const double* b, double* r) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+__device__ void m3skew(double x, double y, double z, double* s) {
+  s[0] = 0; s[1] = -z; s[2] = y; s[3] = z; s[4] = 0; s[5] = -x; s[6] = -y; s[7] = x; s[8] = 0;
+}
+__device__ void rodrigues_dev(const double* w, double* R) {
+  const double t2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+  const double t = sqrt(t2);
+  double a, b;
+  if (t < 1e-8) {
+    a = 1.0 - t2 / 6.0;
+    b = 0.5 - t2 / 24.0;
+  } else {
+    a = sin(t) / t;
+    b = (1.0 - cos(t)) / t2;
+  }
+  double S[9], S2[9];
+  m3skew(w[0], w[1], w[2], S);
+  m3mul(S, S, S2);
+  for (int i = 0; i < 9; ++i) R[i] = ((i % 4 == 0 ? 1.0 : 0.0) + a * S[i]) + b * S2[i];
+}
+
+__global__ void k_pose_table(const double* __restrict__ poses, int n, int B,
+                             const double* __restrict__ inv_dt, double* __restrict__ tab,
+                             int* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (window, bin)
+  if (i >= n) return;
+  const double* p = poses + 6 * (size_t)i;
+  const double pi = 3.14159265358979323846;
+  if (!(sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]) < pi) || !isfinite(p[0]) || !isfinite(p[1]) ||
+      !isfinite(p[2]) || !isfinite(p[3]) || !isfinite(p[4]) || !isfinite(p[5]))
+    atomicExch(bad, 1);
+  double* t = tab + (size_t)i * kPoseTab;
+  double R[9], S[9];
+  rodrigues_dev(p, R);
+  for (int q = 0; q < 9; ++q) t[q] = R[q];
+  const double t2 = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+  m3skew(p[0], p[1], p[2], S);
+  if (sqrt(t2) < 1e-4) {
+    for (int kk = 0; kk < 3; ++kk) {
+      double ek[9], a[9], b[9];
+      m3skew(kk == 0, kk == 1, kk == 2, ek);
+      m3mul(ek, S, a);
+      m3mul(S, ek, b);
+      for (int q = 0; q < 9; ++q) t[9 + 9 * kk + q] = ek[q] + 0.5 * (a[q] + b[q]);
+    }
+  } else {
+    double IR[9];
+    for (int q = 0; q < 9; ++q) IR[q] = (q % 4 == 0 ? 1.0 : 0.0) - R[q];
+    for (int kk = 0; kk < 3; ++kk) {
+      const double c0 = IR[kk], c1 = IR[3 + kk], c2 = IR[6 + kk];
+      double sc[9], m[9], pr[9];
+      m3skew(p[1] * c2 - p[2] * c1, p[2] * c0 - p[0] * c2, p[0] * c1 - p[1] * c0, sc);
+      for (int q = 0; q < 9; ++q) m[q] = p[kk] * S[q] + sc[q];
+      m3mul(m, R, pr);
+      for (int q = 0; q < 9; ++q) t[9 + 9 * kk + q] = (1.0 / t2) * pr[q];
+    }
+  }
+  t[36] = p[3];
+  t[37] = p[4];
+  t[38] = p[5];
+  t[39] = inv_dt[i % B];
+}
+
+void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B,
+                       const double* inv_dt, double* tab, int* bad) {
+  const int n = n_windows * B;
+  ++g_launches;
+  k_pose_table<<<(n + 63) / 64, 64, 0, s>>>(poses, n, B, inv_dt, tab, bad);
+}
+
+// --------------------------------------------------------------------------
 // K1: motion field (depth_pose_to_flows, geometry.hpp:229-264)
 
 // pose table per (window, bin): R[9], dR[27], t[3], inv_dt  -> 40 doubles
@@ -392,6 +473,12 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd(const uint2* __restrict__ pack
 // --------------------------------------------------------------------------
 // K5: flows backward (depth_pose_to_flows_backward, geometry.hpp:279-325)
 
+// Each thread owns kK5Px pixels (stride blockDim.x); bins are the outer loop so
+// the 6 pose partials of a bin stay in registers and are reduced once per warp
+// per bin; d_depth accumulates over bins in registers (bin order, as the
+// reference's outer loop, geometry.hpp:293-323).
+constexpr int kK5Px = 8;
+
 template <typename G2>
 __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict__ depth,
                                                         const uint8_t* __restrict__ mask,
@@ -402,76 +489,83 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
                                                         double* __restrict__ d_depth,
                                                         double* __restrict__ pose_part) {
   __shared__ double s_pose[kMaxBins * kPoseTab];
-  __shared__ double s_red[kPxBlock / 32][6];
+  __shared__ double s_red[kPxBlock / 32][kMaxBins][6];
   const int w = blockIdx.y;
   const int B = P.B, HW = P.HW;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < B * kPoseTab; i += blockDim.x)
     s_pose[i] = pose_tab[(size_t)w * B * kPoseTab + i];
   __syncthreads();
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = q < HW;
-  double d = 0.0;
-  bool px_ok = false;
-  double rx = 0.0, ry = 0.0;
-  if (in) {
-    d = depth[(size_t)w * HW + q];
-    px_ok = (!mask || mask[(size_t)w * HW + q]) && d > 0.0;
-    const int y = q / P.W, x = q - y * P.W;
-    rx = 1.0 * ((double)x - cx) / fx;  // backproject(x, 1.0, k)
-    ry = 1.0 * ((double)y - cy) / fy;
+  const int q0 = blockIdx.x * blockDim.x * kK5Px + threadIdx.x;
+  double dd[kK5Px], dep[kK5Px], rx[kK5Px], ry[kK5Px];
+  bool ok[kK5Px];
+#pragma unroll
+  for (int m = 0; m < kK5Px; ++m) {
+    const int q = q0 + m * blockDim.x;
+    dd[m] = 0.0;
+    ok[m] = false;
+    dep[m] = rx[m] = ry[m] = 0.0;
+    if (q < HW) {
+      dep[m] = depth[(size_t)w * HW + q];
+      ok[m] = (!mask || mask[(size_t)w * HW + q]) && dep[m] > 0.0;
+      const int y = q / P.W, x = q - y * P.W;
+      rx[m] = 1.0 * ((double)x - cx) / fx;  // backproject(x, 1.0, k)
+      ry[m] = 1.0 * ((double)y - cy) / fy;
+    }
   }
-  double dd_acc = 0.0;
   const G2* gw = grad + (size_t)w * B * HW;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int b = 0; b < B; ++b) {
     const double* pt = s_pose + b * kPoseTab;
     double c6[6] = {0, 0, 0, 0, 0, 0};
-    if (px_ok) {
+#pragma unroll
+    for (int m = 0; m < kK5Px; ++m) {
+      const int q = q0 + m * blockDim.x;
+      if (!ok[m]) continue;
       const auto gg = gw[(size_t)b * HW + q];
       const double gu = gg.x, gv = gg.y;
-      if (gu != 0.0 || gv != 0.0) {
-        const double* Rm = pt;
-        const double rr0 = Rm[0] * rx + Rm[1] * ry + Rm[2];
-        const double rr1 = Rm[3] * rx + Rm[4] * ry + Rm[5];
-        const double rr2 = Rm[6] * rx + Rm[7] * ry + Rm[8];
-        const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
-        if (p2 > 0.0) {
-          const double inv_dt = pt[39];
-          const double iz = 1.0 / p2;
-          const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-          const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-          dd_acc += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-          c6[3] = gu * ju0 * inv_dt;
-          c6[4] = gv * jv1 * inv_dt;
-          c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
+      if (gu == 0.0 && gv == 0.0) continue;
+      const double d = dep[m];
+      const double rr0 = pt[0] * rx[m] + pt[1] * ry[m] + pt[2];
+      const double rr1 = pt[3] * rx[m] + pt[4] * ry[m] + pt[5];
+      const double rr2 = pt[6] * rx[m] + pt[7] * ry[m] + pt[8];
+      const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
+      if (!(p2 > 0.0)) continue;
+      const double inv_dt = pt[39];
+      const double iz = 1.0 / p2;
+      const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+      const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+      dd[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+      c6[3] += gu * ju0 * inv_dt;
+      c6[4] += gv * jv1 * inv_dt;
+      c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double* dR = pt + 9 + 9 * a;
-            const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-            const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-            const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-            const double qx = d * m0, qy = d * m1, qz = d * m2;
-            c6[a] = (gu * (ju0 * qx + ju2 * qz) + gv * (jv1 * qy + jv2 * qz)) * inv_dt;
-          }
-        }
+      for (int a = 0; a < 3; ++a) {
+        const double* dR = pt + 9 + 9 * a;
+        const double m0 = dR[0] * rx[m] + dR[1] * ry[m] + dR[2];
+        const double m1 = dR[3] * rx[m] + dR[4] * ry[m] + dR[5];
+        const double m2 = dR[6] * rx[m] + dR[7] * ry[m] + dR[8];
+        c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
       }
     }
-    // warp + block reduction of the 6 pose partials for bin b
 #pragma unroll
     for (int a = 0; a < 6; ++a) {
       double v = c6[a];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s_red[wid][a] = v;
+      if (lane == 0) s_red[wid][b][a] = v;
     }
-    __syncthreads();
-    if (threadIdx.x < 6) {
-      double v = 0.0;
-      for (int i = 0; i < kPxBlock / 32; ++i) v += s_red[i][threadIdx.x];
-      pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * 6 + threadIdx.x] = v;
-    }
-    __syncthreads();
   }
-  if (in) d_depth[(size_t)w * HW + q] = dd_acc;
+#pragma unroll
+  for (int m = 0; m < kK5Px; ++m) {
+    const int q = q0 + m * blockDim.x;
+    if (q < HW) d_depth[(size_t)w * HW + q] = dd[m];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < B * 6; i += blockDim.x) {
+    const int b = i / 6, a = i % 6;
+    double v = 0.0;
+    for (int q = 0; q < kPxBlock / 32; ++q) v += s_red[q][b][a];  // warp order
+    pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * 6 + a] = v;
+  }
 }
 
 // Fixed-order (lane-strided + shuffle tree) sum of the per-block pose partials;
@@ -646,7 +740,7 @@ void launch_bwd(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, con
       packed, ev_off, P, flows, coef, scale, no_surv, grad);
 }
 
-int flows_bwd_parts(const WinParams& P) { return (P.HW + kPxBlock - 1) / kPxBlock; }
+int flows_bwd_parts(const WinParams& P) { return (P.HW + kPxBlock * kK5Px - 1) / (kPxBlock * kK5Px); }
 
 template <typename G2>
 void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,

@@ -30,6 +30,8 @@ int flows_bwd_parts(const WinParams& P);
 
 void launch_stage(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, const WinParams& P,
                   uint64_t max_n, uint2* packed, unsigned long long* err);
+void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B,
+                       const double* inv_dt, double* tab, int* bad);
 void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out);
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,

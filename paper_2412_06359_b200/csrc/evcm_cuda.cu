@@ -141,6 +141,7 @@ struct evcm_cuda_engine {
   std::unordered_map<std::string, Buf> bufs;
   std::unordered_map<std::string, Buf> pins;  // pinned host staging
   int stage_nw = 0;
+  bool check_pose_flag = false;  // device pose tables: validation result pending
   // owner pipeline state
   TileParams TP{};
   uint64_t n_total = 0, max_n = 0;
@@ -352,6 +353,13 @@ void check_stage_errors(evcm_cuda_engine* e) {
 
 void sync_and_check(evcm_cuda_engine* e, const char* what) {
   ck(cudaStreamSynchronize(e->stream), what);
+  // depth_pose_to_flows validates poses before Engine::forward validates events
+  // (optimize.hpp:211-213), so a bad pose wins over a bad event.
+  if (e->check_pose_flag) {
+    e->check_pose_flag = false;
+    if (*e->pinned<int>("pose_bad_h", 1))
+      fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi and components finite");
+  }
   check_stage_errors(e);
   ck(cudaGetLastError(), what);
 }
@@ -822,17 +830,30 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
     WinParams P = make_params(W, H, edges.data(), B, nw, bt->t_start_us, bt->t_end_us);
     e->have_fwd = false;
     e->mark(0);
-    // Rotation tables are built on the host (bit-identical to the reference's
-    // rodrigues); device-resident poses are read back first (nw*B*48 bytes).
-    const size_t np = (size_t)nw * B * 6;
-    double* ph = e->pinned<double>("poses_h", np);
+    // Rotation tables: host poses -> built on the host with the reference's own
+    // expression order (bit-identical flows); device poses -> k_pose_table (no
+    // host round trip; validation reported through a device flag).
+    const double* tab;
     if (in_mem == EVCM_MEM_DEVICE) {
-      ck(cudaMemcpyAsync(ph, bt->poses, np * sizeof(double), cudaMemcpyDeviceToHost, e->stream), "D2H poses");
-      ck(cudaStreamSynchronize(e->stream), "poses");
+      double* inv = e->pinned<double>("inv_dt_h", B);
+      for (int b = 0; b < B; ++b)
+        inv[b] = 1.0 / ((static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6);
+      double* inv_d = e->get<double>("inv_dt", B);
+      ck(cudaMemcpyAsync(inv_d, inv, B * sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D");
+      int* bad = e->get<int>("pose_bad", 1);
+      ck(cudaMemsetAsync(bad, 0, sizeof(int), e->stream), "memset");
+      double* tab_d = e->get<double>("pose_tab", (size_t)nw * B * kPoseTab);
+      launch_pose_table(e->stream, bt->poses, nw, B, inv_d, tab_d, bad);
+      ck(cudaMemcpyAsync(e->pinned<int>("pose_bad_h", 1), bad, sizeof(int), cudaMemcpyDeviceToHost,
+                         e->stream), "D2H");
+      e->check_pose_flag = true;
+      tab = tab_d;
     } else {
+      const size_t np = (size_t)nw * B * 6;
+      double* ph = e->pinned<double>("poses_h", np);
       std::memcpy(ph, bt->poses, np * sizeof(double));
+      tab = upload_pose_table(e, ph, nw, B, edges.data(), true);
     }
-    const double* tab = upload_pose_table(e, ph, nw, B, edges.data(), true);
     uint64_t max_n = 0;
     for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, bt->ev_offsets[w + 1] - bt->ev_offsets[w]);
     stage_events(e, bt->events, bt->ev_offsets, P, in_mem);
