@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd(const uint2* __restrict__ pack
 // the 6 pose partials of a bin stay in registers and are reduced once per warp
 // per bin; d_depth accumulates over bins in registers (bin order, as the
 // reference's outer loop, geometry.hpp:293-323).
-constexpr int kK5Px = 8;
+constexpr int kK5Px = 2;
 
 template <typename G2>
 __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict__ depth,
