@@ -452,44 +452,56 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
 }
 
 // ---------------------------------------------------------------------------
-// backward: one CTA per (owner tile, bin, window). For bin i the candidates
-// are: events with j > i at their reference-(i+1) cell (backward leg), events
-// with j < i at their reference-i cell (forward leg), events with j == i at
-// their source pixel (the two partial steps), each with its per-bin adjoint
-// value (k_bwd_event) -- BufferGradSink::add (warp.hpp:394-406). The finished
-// gradient tile of bin i feeds the flows backward of bin i
-// (geometry.hpp:300-322): per-bin d_depth planes (summed over bins in order by
-// k_ddepth_sum) and per-(tile, bin) pose partials.
+// backward: one CTA per (owner tile, window), warp specialised like the
+// forward. For a reference r in 1..B-1 every alive event's record is the sink
+// (BufferGradSink::add, warp.hpp:394-406) of exactly one bin: r - 1 when
+// r <= j (backward leg: bin i sinks at pos[i+1]) and r otherwise (forward leg:
+// bin i sinks at pos[i]); references 0 and B are never sinks
+// (engine.hpp:475-504). Each bin also receives its events' source-pixel sink
+// (the two partial steps, weight 1 at (x, y)). So the CTA streams the
+// forward's per-reference candidate lists, references 1..B-1 in order, into
+// two rolling fixed-point gradient tiles (bins r - 1 and r); after reference r
+// (and the source sinks of bin r - 1) bin r - 1 is complete and feeds the fused
+// depth_pose_to_flows_backward (geometry.hpp:300-322); d_depth sums the bins
+// in order in registers.
 //
-// Staging: records (16 B, legs A/B) go to stage16 at their candidate index;
-// the 8 B adjoint values (and, for the source-pixel leg, the 8 B packed events)
-// are copied as 16 B-aligned supersets into per-range slots of stage8v/stage8e.
+// Staging layout: every range gets an even-aligned slot region of
+// roundup2(len + 2) slots; its 8 B values (sink values, packed events) are
+// bulk-copied as the 16 B-aligned superset starting at the region, and its
+// records at the same slot offset, so slot s holds the record, value and event
+// of one candidate; the slack slots of every region are flagged in a bitmask.
 
-__global__ void __launch_bounds__(kThreads, 2) k_bwd_cells(
+constexpr int kStageQ = 1536;  // slots per buffer
+
+struct BRound {
+  uint32_t n;  // slots
+  int r;       // reference (kind 0) or bin (kind 1)
+  int kind;    // 0: record sinks of reference r, 1: source-pixel sinks of bin r
+  int last;    // last round of this (kind, r)
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
-    const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
+    const FwdRec* __restrict__ recs, const float2* __restrict__ vals, uint64_t n_total,
     const uint32_t* __restrict__ gmax, const uint4* __restrict__ bbox,
     const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
     const int* __restrict__ no_surv, const double* __restrict__ depth,
     const uint8_t* __restrict__ mask, const double* __restrict__ pose_tab, double fx, double fy,
     double cx, double cy, double* __restrict__ d_depth, double* __restrict__ pose_part,
     double* __restrict__ grad_out) {
-  constexpr int k8 = kStageB + 3 * kBatchCap;  // 8 B slots incl. per-range alignment slack
   extern __shared__ __align__(16) unsigned char smem[];
-  uint4* stage16 = reinterpret_cast<uint4*>(smem);                 // kStageB
-  float2* stage8v = reinterpret_cast<float2*>(stage16 + kStageB);  // k8 adjoint values
-  uint2* stage8e = reinterpret_cast<uint2*>(stage8v + k8);         // k8 packed events
-  uint32_t* acc = reinterpret_cast<uint32_t*>(stage8e + k8);       // [gu, gv][lo, hi][kPlane]
-  uint32_t* tl = acc + 4 * kPlane;                                 // touching candidates
-  const uint32_t acc_s = smem_u32(acc);
+  uint4* stage16 = reinterpret_cast<uint4*>(smem);                     // [2][kStageQ] records
+  float2* stage8 = reinterpret_cast<float2*>(stage16 + 2 * kStageQ);   // [2][kStageQ] values
+  uint32_t* acc = reinterpret_cast<uint32_t*>(stage8 + 2 * kStageQ);   // [tile][gu, gv][lo, hi][kPlane]
   __shared__ Batch bt;
-  __shared__ int s_nt;
-  __shared__ uint32_t off8[kBatchCap];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_pose[kWarps][6];
+  __shared__ BRound desc[2];
+  __shared__ uint32_t roff[kBatchCap];
+  __shared__ uint32_t fake[2][kStageQ / 32];  // slack slots of the staged round
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ double s_pose[2][kWarps][6];
 
-  const int T = blockIdx.x, i = blockIdx.y, w = blockIdx.z;
+  const int T = blockIdx.x, w = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int B = P.B, R = B + 1, NS = 2 * B + 1, W = P.W, H = P.H, HW = P.HW;
   const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
@@ -498,7 +510,138 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_cells(
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool run = !no_surv[w];
-  const int lxp = tid % kOwnW, lyp = tid / kOwnW;
+
+  for (int i = tid; i < 8 * kPlane; i += kFwdThreads) acc[i] = 0u;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kWarps);
+    mbar_init(&empty[1], kWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (wid == 0) {
+    // ---------------- producer ----------------
+    uint32_t it = 0;
+    // stage the rounds of one (kind, r) group: kind 0 = reference r (list slot r,
+    // full sort-tile ranges), kind 1 = source sinks of bin r (list slot R + r,
+    // the bin's sub-range of every sort tile)
+    auto group = [&](int kind, int r) {
+      const size_t ws = (size_t)w * NS + (kind == 0 ? r : R + r);
+      const FwdRec* rr = recs + (size_t)r * n_total + base;
+      const float2* vv = vals + (size_t)(kind == 0 ? r - 1 : B - 1) * n_total;
+      if (lane == 0) bt.seg = -1;
+      __syncwarp();
+      int more = run ? 1 : 0;
+      bool emitted = false;
+      while (more || !emitted) {
+        int nl = 0;
+        uint32_t total = 0;
+        if (more) {
+          next_batch<1>(
+              bt, lcount, lists, bbox, TP.nT, ox0, oy0, [&](int) { return ws * TP.oT + T; },
+              [&](int) { return ws * TP.nT; },
+              [&](int, int S) {
+                if (kind == 0) return make_uint2(tp[S], tp[S + 1]);
+                const uint32_t* b = bp + (size_t)S * (B + 1);
+                return make_uint2(b[r], b[r + 1]);
+              });
+          nl = bt.nl;
+          total = nl > 0 ? bt.pre[nl] : 0u;
+          more = bt.more;
+        } else {
+          more = 0;
+        }
+        // virtual candidates per round, leaving room for <= 3 slack slots per range
+        const uint32_t capv = kStageQ - 3u * (uint32_t)min(nl, kBatchCap);
+        for (uint32_t rb = 0; rb < total || (rb == 0 && !more && !emitted); rb += capv) {
+          const int b = it & 1;
+          if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+          uint4* s16 = stage16 + b * kStageQ;
+          float2* s8 = stage8 + b * kStageQ;
+          uint2* s8e = reinterpret_cast<uint2*>(s16);  // kind 1: packed events
+          uint32_t* fk = fake[b];
+          for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
+          // region offsets: exclusive scan of roundup2(len + 2) over the ranges
+          uint32_t carry = 0;
+          for (int l0 = 0; l0 < nl; l0 += 32) {
+            const int l = l0 + lane;
+            uint32_t sz = 0;
+            if (l < nl) {
+              uint32_t lo, hi;
+              clip(bt, l, rb, capv, lo, hi);
+              sz = lo < hi ? ((hi - lo + 3) & ~1u) : 0u;
+            }
+            uint32_t x = sz;
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(kFull, x, o);
+              if (lane >= o) x += y;
+            }
+            if (l < nl) roff[l] = carry + x - sz;
+            carry += __shfl_sync(kFull, x, 31);
+          }
+          __syncwarp();
+          const uint32_t nslots = carry;
+          uint32_t bytes = 0;
+          for (int l = lane; l < nl; l += 32) {
+            uint32_t lo, hi;
+            clip(bt, l, rb, capv, lo, hi);
+            if (lo >= hi) continue;
+            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), len = hi - lo;
+            const uint32_t par = (uint32_t)((base + k0) & 1ull);  // n_total is even
+            const uint32_t s0 = roff[l], sz = (uint32_t)((len + 3) & ~1ull);
+            const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
+            // slack slots (no candidate of this range): s0 if par, [s0+par+len, s0+sz)
+            if (par) atomicOr(fk + (s0 >> 5), 1u << (s0 & 31));
+            for (uint32_t q = s0 + par + (uint32_t)len; q < s0 + sz; ++q)
+              atomicOr(fk + (q >> 5), 1u << (q & 31));
+            bytes += (uint32_t)(kind == 0 ? len * sizeof(FwdRec) : (a1 - a0) * 8);
+            bytes += (uint32_t)((a1 - a0) * 8);
+          }
+          bytes = warp_sum_u32(bytes);
+          if (lane == 0) {
+            desc[b].n = nslots;
+            desc[b].r = r;
+            desc[b].kind = kind;
+            desc[b].last = (!more && rb + capv >= total) ? 1 : 0;
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(&full[b], bytes);
+          __syncwarp();
+          for (int l = lane; l < nl; l += 32) {
+            uint32_t lo, hi;
+            clip(bt, l, rb, capv, lo, hi);
+            if (lo >= hi) continue;
+            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), len = hi - lo;
+            const uint32_t par = (uint32_t)((base + k0) & 1ull);
+            const uint32_t s0 = roff[l];
+            const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
+            bulk_g2s(s8 + s0, vv + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+            if (kind == 0)
+              bulk_g2s(s16 + s0 + par, rr + k0, (uint32_t)(len * sizeof(FwdRec)), &full[b]);
+            else
+              bulk_g2s(s8e + s0, sorted + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+          }
+          ++it;
+          emitted = true;
+          if (total == 0) break;
+        }
+      }
+    };
+    for (int r = 1; r < B; ++r) {
+      group(0, r);
+      group(1, r - 1);
+    }
+    group(1, B - 1);
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int ct = tid - 32, cw = wid - 1;
+  const uint32_t acc_s = smem_u32(acc);
+  const int lxp = ct % kOwnW, lyp = ct / kOwnW;
   const int px = ox0 + lxp, py = oy0 + lyp;
   const bool own_px = px < W && py < H;
   const int gq = py * W + px, op = lyp * kRowW + lxp;
@@ -508,226 +651,106 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_cells(
   int e2 = 0;
   frexp((double)__uint_as_float(gmax[w]), &e2);
   const double gsc = ldexp(1.0, 49 - e2), igsc = ldexp(1.0, e2 - 49);
-  double dd = 0.0;  // this bin's d_depth of the pixel
-  uint32_t phase = 0;
-
-  for (int k = tid; k < 4 * kPlane; k += kThreads) acc[k] = 0u;
-  if (tid == 0) {
-    s_nt = 0;
-    bt.seg = -1;
-    mbar_init(&bar, 1);
-  }
-  __syncthreads();
-  {
-    const uint64_t vbase = (uint64_t)i * n_total + base;  // bwd[i] of this window
-    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
-    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
-    int more = run ? 1 : 0;
-    while (more) {
-      if (wid == 0)
-        next_batch<3>(
-            bt, lcount, lists, bbox, TP.nT, ox0, oy0,
-            [&](int s) {
-              const int slot = s == 0 ? i + 1 : (s == 1 ? i : R + i);
-              return ((size_t)w * NS + slot) * TP.oT + T;
-            },
-            [&](int s) {
-              const int slot = s == 0 ? i + 1 : (s == 1 ? i : R + i);
-              return ((size_t)w * NS + slot) * TP.nT;
-            },
-            [&](int s, int S) {
-              const uint32_t* b = bp + (size_t)S * (B + 1);
-              if (s == 0) return make_uint2(b[i + 1], tp[S + 1]);
-              if (s == 1) return make_uint2(tp[S], b[i]);
-              return make_uint2(b[i], b[i + 1]);
-            });
-      __syncthreads();
-      const int nl = bt.nl;
-      const uint32_t total = nl > 0 ? bt.pre[nl] : 0u;
-      more = bt.more;
-      auto seg_of = [&](int l) {
-        const uint32_t v = bt.pre[l];
-        return (v >= bt.seg_end[0] ? 1 : 0) + (v >= bt.seg_end[1] ? 1 : 0);
-      };
-      for (uint32_t rb = 0; rb < total; rb += kStageB) {
-        if (wid == 0) {
-          // per-range 8 B slot offsets (exclusive scan of the even slot sizes)
-          uint32_t carry = 0;
-          for (int l0 = 0; l0 < nl; l0 += 32) {
-            const int l = l0 + lane;
-            uint32_t n8 = 0;
-            if (l < nl) {
-              uint32_t lo, hi;
-              clip(bt, l, rb, kStageB, lo, hi);
-              n8 = lo < hi ? ((hi - lo + 3) & ~1u) : 0;
-            }
-            uint32_t x = n8;
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(kFull, x, o);
-              if (lane >= o) x += y;
-            }
-            if (l < nl) off8[l] = carry + x - n8;
-            carry += __shfl_sync(kFull, x, 31);
-          }
-          __syncwarp();
-          uint32_t bytes = 0;
-          for (int l = lane; l < nl; l += 32) {
-            uint32_t lo, hi;
-            clip(bt, l, rb, kStageB, lo, hi);
-            if (lo >= hi) continue;
-            const int sg = seg_of(l);
-            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), nn = hi - lo;
-            if (sg < 2) bytes += (uint32_t)(nn * sizeof(FwdRec));
-            const uint64_t a0 = (vbase + k0) & ~1ull, a1 = (vbase + k0 + nn + 1) & ~1ull;
-            bytes += (uint32_t)((a1 - a0) * 8);
-            if (sg == 2) {
-              const uint64_t e0 = (base + k0) & ~1ull, e1 = (base + k0 + nn + 1) & ~1ull;
-              bytes += (uint32_t)((e1 - e0) * 8);
-            }
-          }
-          bytes = warp_sum_u32(bytes);
-          fence_proxy_async();
-          if (lane == 0) mbar_arrive_expect_tx(&bar, bytes);
-          __syncwarp();
-          for (int l = lane; l < nl; l += 32) {
-            uint32_t lo, hi;
-            clip(bt, l, rb, kStageB, lo, hi);
-            if (lo >= hi) continue;
-            const int sg = seg_of(l);
-            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), nn = hi - lo;
-            if (sg < 2)
-              bulk_g2s(stage16 + (lo - rb), (sg == 0 ? rA : rB) + k0, (uint32_t)(nn * sizeof(FwdRec)),
-                       &bar);
-            const uint64_t a0 = (vbase + k0) & ~1ull, a1 = (vbase + k0 + nn + 1) & ~1ull;
-            bulk_g2s(stage8v + off8[l], bwd + a0, (uint32_t)((a1 - a0) * 8), &bar);
-            if (sg == 2) {
-              const uint64_t e0 = (base + k0) & ~1ull, e1 = (base + k0 + nn + 1) & ~1ull;
-              bulk_g2s(stage8e + off8[l], sorted + e0, (uint32_t)((e1 - e0) * 8), &bar);
-            }
-          }
-        }
-        __syncthreads();  // off8 visible
-        mbar_wait(&bar, phase);
-        phase ^= 1;
-        // pass 1, one warp per range: compact the candidates whose cell touches
-        // the tile as (candidate index, range)
-        for (int l = wid; l < nl; l += kWarps) {
-          uint32_t lo, hi;
-          clip(bt, l, rb, kStageB, lo, hi);
-          if (lo >= hi) continue;
-          const int sg = seg_of(l);
-          const uint32_t pe = (uint32_t)((base + bt.rng[l] + (lo - bt.pre[l])) & 1ull) + off8[l];
-          for (uint32_t v0 = lo; v0 < hi; v0 += 32) {
-            const uint32_t v = v0 + lane;
-            bool hit = false;
-            if (v < hi) {
-              int x0, y0;
-              if (sg < 2) {
-                const uint32_t cell = stage16[v - rb].x;
-                x0 = (int)(cell & 0xffffu);
-                y0 = (int)((cell >> 16) & 0x7fffu);
-                hit = cell != kDead;  // masked event (engine.hpp:564)
-              } else {
-                const uint2 e = stage8e[pe + (v - lo)];
-                x0 = W >= 2 ? min(ev_x(e), W - 2) : 0;
-                y0 = H >= 2 ? min(ev_y(e), H - 2) : 0;
-                hit = true;
-              }
-              const int lx = x0 - ox0, ly = y0 - oy0;
-              hit = hit && lx + ox >= 0 && lx < kOwnW && ly + oy >= 0 && ly < kOwnH;
-            }
-            const unsigned bal = __ballot_sync(kFull, hit);
-            int b0 = 0;
-            if (lane == 0 && bal) b0 = atomicAdd(&s_nt, __popc(bal));
-            b0 = __shfl_sync(kFull, b0, 0);
-            if (hit) tl[b0 + __popc(bal & ((1u << lane) - 1u))] = (v - rb) | ((uint32_t)l << 16);
-          }
-        }
-        __syncthreads();
-        // pass 2 (full warps): BufferGradSink::add corners as exact fixed-point sums
-        const int nt = s_nt;
-        for (int t = tid; t < nt; t += kThreads) {
-          const uint32_t ent = tl[t];
-          const uint32_t idx = ent & 0xffffu;
-          const int l = (int)(ent >> 16);
-          const int sg = seg_of(l);
-          const uint32_t lo = max(bt.pre[l], rb);
-          const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]);
-          const uint32_t p = idx + rb - lo;
-          int x0, y0;
-          double wx, ax, wy, ay;
-          if (sg < 2) {
-            const uint4 rec = stage16[idx];
-            x0 = (int)(rec.x & 0xffffu);
-            y0 = (int)((rec.x >> 16) & 0x7fffu);
-            expand_frac(__uint_as_float(rec.z), wx, ax);
-            expand_frac(__uint_as_float(rec.w), wy, ay);
-          } else {
-            // bilin_cell at the integer source pixel: weight 0 or 1 (border
-            // cell); masked events carry a zero adjoint value (k_bwd_event)
-            const uint2 e = stage8e[(uint32_t)((base + k0) & 1ull) + off8[l] + p];
-            const int ex = ev_x(e), ey = ev_y(e);
-            x0 = W >= 2 ? min(ex, W - 2) : 0;
-            y0 = H >= 2 ? min(ey, H - 2) : 0;
-            wx = ex > x0 ? 1.0 : 0.0;
-            wy = ey > y0 ? 1.0 : 0.0;
-            ax = 1.0 - wx;
-            ay = 1.0 - wy;
-          }
-          const float2 g = stage8v[(uint32_t)((vbase + k0) & 1ull) + off8[l] + p];
-          const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
-          const int lx = x0 - ox0, ly = y0 - oy0;
-          const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
-          const int o00 = ly * kRowW + lx;
+  double dd = 0.0;  // d_depth of this pixel, bins summed in order
+  uint32_t it = 0;
+  for (int done = 0; done < B;) {
+    const int b = it & 1;
+    mbar_wait(&full[b], (it >> 1) & 1);
+    const BRound d = desc[b];
+    const uint4* s16 = stage16 + b * kStageQ;
+    const float2* s8 = stage8 + b * kStageQ;
+    const uint2* s8e = reinterpret_cast<const uint2*>(s16);
+    const uint32_t* fk = fake[b];
+    if (d.kind == 0) {
+      for (uint32_t v = ct; v < d.n; v += kCons) {
+        if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
+        const uint4 rec = s16[v];
+        const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
+        if (rec.x == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) continue;
+        const float2 g = s8[v];
+        if (g.x == 0.f && g.y == 0.f) continue;
+        // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
+        const int j = bin_of(rec.y, P.erel, B);
+        const int bin = (d.r <= j) ? d.r - 1 : d.r;
+        const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
+        double wx, ax, wy, ay;
+        expand_frac(__uint_as_float(rec.z), wx, ax);
+        expand_frac(__uint_as_float(rec.w), wy, ay);
+        const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
+        const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
+        const int o00 = ly * kRowW + lx;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
-            const double wq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
-            if (in && wq != 0.0) {
-              const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
-              const uint32_t a = acc_s + 4u * (uint32_t)o;
-              fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wq * gx));
-              fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wq * gy));
-            }
+        for (int q = 0; q < 4; ++q) {
+          const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
+          const double wq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
+          if (in && wq != 0.0) {
+            const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
+            const uint32_t a = pt + 4u * (uint32_t)o;
+            fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wq * gx));
+            fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wq * gy));
           }
         }
-        if (tid == 0) s_nt = 0;
-        __syncthreads();  // stage buffers are free for the next round
+      }
+    } else {
+      // source-pixel sinks of bin d.r: weight 1 at the event's own pixel
+      const uint32_t pt = acc_s + (uint32_t)(d.r & 1) * (4 * kPlane * 4);
+      for (uint32_t v = ct; v < d.n; v += kCons) {
+        if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
+        const uint2 e = s8e[v];
+        const int lx = ev_x(e) - ox0, ly = ev_y(e) - oy0;
+        if (lx < 0 || lx >= kOwnW || ly < 0 || ly >= kOwnH) continue;
+        const float2 g = s8[v];
+        if (g.x == 0.f && g.y == 0.f) continue;
+        const uint32_t a = pt + 4u * (uint32_t)(ly * kRowW + lx);
+        fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn((double)g.x * gsc));
+        fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn((double)g.y * gsc));
       }
     }
-    // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+    ++it;
+    if (!(d.kind == 1 && d.last)) continue;
+
+    // bin i = d.r complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
+    const int i = d.r;
+    consumer_sync(kCons);
     double c6[6] = {0, 0, 0, 0, 0, 0};
-    if (own_px) {
-      const double gu = (double)(long long)fx_read(acc + op, acc + kPlane + op) * igsc;
-      const double gv = (double)(long long)fx_read(acc + 2 * kPlane + op, acc + 3 * kPlane + op) * igsc;
-      if (grad_out) {
-        grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
-        grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
-      }
-      if (dok && (gu != 0.0 || gv != 0.0)) {
-        const double* pt = pose_tab + ((size_t)w * B + i) * kPoseTab;
-        const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
-        const double ry = 1.0 * ((double)py - cy) / fy;
-        const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
-        const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
-        const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
-        const double p0 = dpx * rr0 + pt[36], p1 = dpx * rr1 + pt[37], p2 = dpx * rr2 + pt[38];
-        if (p2 > 0.0) {
-          const double inv_dt = pt[39], iz = 1.0 / p2;
-          const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-          const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-          dd += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-          c6[3] = gu * ju0 * inv_dt;
-          c6[4] = gv * jv1 * inv_dt;
-          c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
+    {
+      const uint32_t* at = acc + (i & 1) * 4 * kPlane;
+      const double gu = (double)(long long)fx_read(at + op, at + kPlane + op) * igsc;
+      const double gv = (double)(long long)fx_read(at + 2 * kPlane + op, at + 3 * kPlane + op) * igsc;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double* dR = pt + 9 + 9 * a;
-            const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-            const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-            const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-            c6[a] = (gu * (ju0 * dpx * m0 + ju2 * dpx * m2) + gv * (jv1 * dpx * m1 + jv2 * dpx * m2)) *
-                    inv_dt;
+      for (int k = 0; k < 4; ++k) acc[((i & 1) * 4 + k) * kPlane + op] = 0u;  // tile of bin i + 2
+      if (own_px) {
+        if (grad_out) {
+          grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
+          grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
+        }
+        if (dok && (gu != 0.0 || gv != 0.0)) {
+          const double* ptab = pose_tab + ((size_t)w * B + i) * kPoseTab;
+          const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
+          const double ry = 1.0 * ((double)py - cy) / fy;
+          const double rr0 = ptab[0] * rx + ptab[1] * ry + ptab[2];
+          const double rr1 = ptab[3] * rx + ptab[4] * ry + ptab[5];
+          const double rr2 = ptab[6] * rx + ptab[7] * ry + ptab[8];
+          const double p0 = dpx * rr0 + ptab[36], p1 = dpx * rr1 + ptab[37], p2 = dpx * rr2 + ptab[38];
+          if (p2 > 0.0) {
+            const double inv_dt = ptab[39], iz = 1.0 / p2;
+            const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
+            const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
+            dd += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+            c6[3] = gu * ju0 * inv_dt;
+            c6[4] = gv * jv1 * inv_dt;
+            c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const double* dR = ptab + 9 + 9 * a;
+              const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
+              const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
+              const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
+              c6[a] = (gu * (ju0 * dpx * m0 + ju2 * dpx * m2) + gv * (jv1 * dpx * m1 + jv2 * dpx * m2)) *
+                      inv_dt;
+            }
           }
         }
       }
@@ -736,17 +759,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_cells(
 #pragma unroll
       for (int a = 0; a < 6; ++a) {
         const double v = warp_sum(c6[a]);
-        if (lane == 0) s_pose[wid][a] = v;
-      }
-      __syncthreads();
-      if (tid < 6) {
-        double sum = 0.0;
-        for (int m = 0; m < kWarps; ++m) sum += s_pose[m][tid];
-        pose_part[(((size_t)w * TP.oT + T) * B + i) * 6 + tid] = sum;
+        if (lane == 0) s_pose[i & 1][cw][a] = v;
       }
     }
+    consumer_sync(kCons);  // also: the zeroed tile is ready for bin i + 2
+    if (pose_part && ct < 6) {
+      double sum = 0.0;
+      for (int m = 0; m < kWarps; ++m) sum += s_pose[i & 1][m][ct];
+      pose_part[(((size_t)w * TP.oT + T) * B + i) * 6 + ct] = sum;
+    }
+    ++done;
   }
-  if (d_depth && own_px) d_depth[((size_t)w * B + i) * HW + gq] = dd;
+  if (d_depth && own_px) d_depth[(size_t)w * HW + gq] = dd;
   (void)H;
 }
 
@@ -757,9 +781,7 @@ static size_t fwd_cells_smem() {
   return 2 * (size_t)kStageP * sizeof(FwdRec) + 9 * kPlane * sizeof(uint32_t);
 }
 static size_t bwd_cells_smem() {
-  const size_t k8 = kStageB + 3 * kBatchCap;
-  return (size_t)kStageB * 16 + 2 * k8 * 8 + 4 * kPlane * sizeof(uint32_t) +
-         kStageB * sizeof(uint32_t);
+  return 2 * (size_t)kStageQ * (16 + 8) + 8 * kPlane * sizeof(uint32_t);
 }
 static void smem_attr(const void* fn, size_t bytes) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -785,15 +807,15 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
                       const uint32_t* lcount, const uint16_t* lists, const int* no_surv,
                       const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth_bins, double* pose_part, double* grad_out) {
+                      const double* K, double* d_depth, double* pose_part, double* grad_out) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   static bool attr = false;
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_bwd_cells), bwd_cells_smem());
   attr = true;
   count_launch();
-  k_bwd_cells<<<dim3(TP.oT, P.B, P.n_windows), kThreads, bwd_cells_smem(), s>>>(
+  k_bwd_cells<<<dim3(TP.oT, P.n_windows), kFwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, no_surv,
-      depth, mask, pose_tab, k0, k1, k2, k3, d_depth_bins, pose_part, grad_out);
+      depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
 }
 
 }  // namespace evcm_b200

@@ -560,9 +560,11 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const FwdRec* rk = recs + base + k;  // + r * n_total
-  if (rk[0].cell == kDead) {           // masked event: contributes nothing (engine.hpp:564);
-    const uint32_t dtu = ev_dt(sorted[base + k]);  // its source-pixel sink value is 0
-    bwd[(size_t)bin_of(dtu, erel, P.B) * n_total + base + k] = make_float2(0.f, 0.f);
+  // sink values: bwd[(r - 1) * n_total + slot] for the sink at reference r in
+  // 1..B-1 (each is the sink of exactly one bin: r - 1 if r <= j, else r), and
+  // bwd[(B - 1) * n_total + slot] for the source-pixel sink of bin j
+  if (rk[0].cell == kDead) {  // masked event: contributes nothing (engine.hpp:564)
+    bwd[(size_t)(P.B - 1) * n_total + base + k] = make_float2(0.f, 0.f);
     return;
   }
   const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
     const CellW c = decode(rk[(size_t)r * n_total]);
     const double2 g = back ? gb : gf;
     const float2 o = make_float2((float)(dt * g.x), (float)(dt * g.y));
-    bo[(size_t)i * n_total] = o;
+    bo[(size_t)(r - 1) * n_total] = o;
     gm = fmaxf(gm, fmaxf(fabsf(o.x), fabsf(o.y)));
     // (I + dt J_i)^T g + d[r]   (warp.hpp:91-94, engine.hpp:490-491)
     const int i00 = c.y0 * W + c.x0;
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
   }
   const double cb = es[j] - t, cf = es[j + 1] - t;
   const float2 o = make_float2((float)(cb * gb.x + cf * gf.x), (float)(cb * gb.y + cf * gf.y));
-  bo[(size_t)j * n_total] = o;
+  bo[(size_t)(B - 1) * n_total] = o;
   gm = fmaxf(gm, fmaxf(fabsf(o.x), fabsf(o.y)));
   // window max |value|: the fixed-point scale of the backward owner (cmax_cells.cu)
   const unsigned am = __activemask();

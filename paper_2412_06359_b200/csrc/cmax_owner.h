@@ -86,6 +86,6 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
                       const uint32_t* lcount, const uint16_t* lists, const int* no_surv,
                       const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth_bins, double* pose_part, double* grad_out);
+                      const double* K, double* d_depth, double* pose_part, double* grad_out);
 
 }  // namespace evcm_b200

@@ -305,7 +305,7 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   uint2* packed = e->get<uint2>("packed", total);
   unsigned long long* err = e->get<unsigned long long>("stage_err", nw);
   ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
-  e->n_total = total;
+  e->n_total = (total + 1) & ~1ull;  // even plane stride (16 B-aligned 8 B sub-arrays)
   e->max_n = max_n;
   // algo auto: the owner pipeline wins once there are >= ~2 events per pixel and
   // per window (measured crossover); deterministic mode needs it.
@@ -442,15 +442,10 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   e->mark(4);
   const size_t np = (size_t)nw * R * TP.oT;
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
-  if (e->opt.deterministic)
-    launch_fwd_owner(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
-                     e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
-                     e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np),
-                     true);
-  else
-    launch_fwd_cells(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
-                     e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
-                     e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+  // fixed-point accumulation: bit-deterministic in both modes
+  launch_fwd_cells(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
+                   e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
+                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
   e->mark(5);
   launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
                        e->get<unsigned long long>("part_act", np), TP.oT, P,
@@ -480,22 +475,10 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
                    bwd, gmax);
   e->mark(7);
   double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * 6) : nullptr;
-  if (e->opt.deterministic) {
-    const int G = bwd_groups(P);
-    double* dd_parts =
-        (depth && G > 1) ? e->get<double>("d_depth_parts", (size_t)nw * G * P.HW) : nullptr;
-    launch_bwd_owner(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1),
-                     recs, bwd, total, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
-                     e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask,
-                     pose_tab, K, depth ? d_depth : nullptr, dd_parts, pose_part, grad_out, true);
-  } else {
-    double* dd_bins = depth ? e->get<double>("d_depth_bins", (size_t)nw * P.B * P.HW) : nullptr;
-    launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1),
-                     recs, bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
-                     e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask,
-                     pose_tab, K, dd_bins, pose_part, grad_out);
-    if (depth) launch_ddepth_sum(e->stream, dd_bins, P.B, P.HW, nw, d_depth);
-  }
+  launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
+                   bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
+                   e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask, pose_tab,
+                   K, depth ? d_depth : nullptr, pose_part, grad_out);
   e->mark(8);
   if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
   e->mark(9);
