@@ -49,12 +49,9 @@ namespace {
 
 constexpr int kThreads = 512;                      // 16 warps
 constexpr int kWarps = kThreads / 32;
-constexpr int kStageF = 3072;                      // staged candidates per forward round
-constexpr int kStageB = 2048;                      // staged candidates per backward round
 constexpr int kBatchCap = 3 * kListCapO;           // sort-tile ranges per batch
 constexpr int kRowW = kOwnW + 1;                   // padded accumulator row (bank spread)
 constexpr int kPlane = kOwnH * kRowW;              // words per accumulator plane
-constexpr int kFxFwd = 50;                         // fractional bits of the IWE sums
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk) --------------------------------
 

@@ -14,13 +14,10 @@
 //                   boxes of the cells (slots 0..B: references, B+1..2B: source
 //                   pixel of the events of bin j)
 //   k_build_lists   per (slot, owner tile): the sort tiles whose box touches it
-//   k_fwd_owner     per (window, 32x16 owner tile, ref): fp64 count/tsum of
-//                   every record landing on the tile (fixed order) -> n_active,
-//                   reference_loss terms, splat_position_grad coefficients
 //   k_bwd_event     per event: splat_position_grad at every ref + adjoint sweep
-//                   (engine.hpp:475-504) -> one (gx, gy) per bin
-//   k_bwd_owner     per (window, owner tile, bin group): gradient tile per bin
-//                   (BufferGradSink::add) + fused depth_pose_to_flows_backward
+//                   (engine.hpp:475-504) -> one (gx, gy) per sink
+// The owner-tile accumulation kernels (IWE stack + loss coefficients; flow
+// gradient tiles + fused flows backward) are in cmax_cells.cu.
 //
 // Sorting by the position at the middle reference keeps every sort tile compact
 // at every reference (a tile of source pixels would smear along the motion by
@@ -369,162 +366,6 @@ __global__ void k_build_lists(const uint4* __restrict__ bbox, WinParams P, TileP
 }
 
 // ---------------------------------------------------------------------------
-// forward owner: IWE stack tile + loss partials + coefficient planes
-
-// kDet: kFwdWarps warps, each with a private fp64 tile accumulated in lane order
-// and merged in warp order (bit-stable). !kDet: 8 warps share one tile through
-// shared-memory fp64 atomics (faster, order-dependent rounding only).
-template <bool kDet>
-__global__ void __launch_bounds__(kDet ? 32 * kFwdWarps : 256) k_fwd_owner(
-    const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
-    const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
-    const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
-    const uint16_t* __restrict__ lists, double2* __restrict__ coef, double2* __restrict__ stack_out,
-    double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
-  constexpr int NW = kDet ? kFwdWarps : 8;
-  constexpr int NC = kDet ? kFwdWarps : 1;  // accumulator copies
-  extern __shared__ __align__(16) double acc_all[];  // [copy][px][C0, S0, C1, S1]
-  __shared__ uint16_t list[kListCapO > 128 ? kListCapO : 128];
-  __shared__ uint32_t pre[kListCapO + 1], rng[kListCapO];
-  __shared__ int s_nl;
-  __shared__ double s_red[NW];
-  __shared__ unsigned s_act[NW];
-  const int T = blockIdx.x, r = blockIdx.y, w = blockIdx.z;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int R = P.B + 1, NS = 2 * P.B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
-  for (int i = threadIdx.x; i < NC * kOwnPx * 4; i += blockDim.x) acc_all[i] = 0.0;
-  const uint64_t base = ev_off[w];
-  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
-  const FwdRec* rr = recs + (size_t)r * n_total + base;
-  const double esr = P.es[r], iwin = P.inv_window;
-  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
-  double* mine = acc_all + (kDet ? (size_t)wid * kOwnPx * 4 : 0);
-  const size_t ws = (size_t)w * NS + r;
-
-  auto contribute = [&](const FwdRec& rec) {
-    const int cx0 = (int)(rec.cell & 0xffffu), cy0 = (int)((rec.cell >> 16) & 0x7fffu);
-    const bool touch = rec.cell != kDead && cx0 + ox >= ox0 && cx0 < ox0 + kOwnW &&
-                       cy0 + oy >= oy0 && cy0 < oy0 + kOwnH;
-    CellW c{};
-    double tb = 0.0;
-    int pol = 0;
-    if (touch) {
-      c = decode(rec);
-      pol = (int)(rec.cell >> 31);
-      tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
-    }
-    if (!__any_sync(kFull, touch)) return;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-      const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
-      const double wq = corner_w(c, q);
-      const int key = in ? ((ly * kOwnW + lx) * 2 + pol) : -1;
-      if (kDet) {
-        warp_accumulate2(mine, key, wq, wq * tb);
-      } else if (key >= 0) {
-        atomicAdd(mine + 2 * key, wq);
-        atomicAdd(mine + 2 * key + 1, wq * tb);
-      }
-    }
-  };
-
-  if (wid == 0) {
-    const int nl = warp_load_sorted_list(lcount, lists, ws * TP.oT + T, list);
-    if (nl >= 0)
-      warp_ranges(0, nl, 0u, pre, rng, [&](int l) {
-        const int S = list[l];
-        return make_uint2(tp[S], tp[S + 1]);
-      });
-    if (lane == 0) s_nl = nl;
-  }
-  __syncthreads();
-  if (s_nl >= 0) {
-    const int nl = s_nl;
-    const uint32_t total = nl > 0 ? pre[nl] : 0u;
-    const uint32_t v0 = (uint32_t)(((uint64_t)total * wid) / NW);
-    const uint32_t v1 = (uint32_t)(((uint64_t)total * (wid + 1)) / NW);
-    int l = 0;
-    if (v0 < v1) virt_slot(pre, rng, nl, v0, &l);  // segment of the warp's first element
-    for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
-      FwdRec rb[kPrefetch];
-#pragma unroll
-      for (int m = 0; m < kPrefetch; ++m) {
-        const uint32_t v = vb + m * 32 + lane;
-        rb[m].cell = kDead;
-        if (v < v1) {
-          while (pre[l + 1] <= v) ++l;  // v increases monotonically per lane
-          rb[m] = rr[rng[l] + (v - pre[l])];
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < kPrefetch; ++m)
-        if (vb + m * 32 < v1) contribute(rb[m]);
-    }
-  } else if (wid == 0) {
-    scan_sources(bbox + ws * TP.nT, TP.nT, ox0, oy0, list, 128, [&](int S) {
-      for (uint32_t kb = tp[S]; kb < tp[S + 1]; kb += 32) {
-        FwdRec rec;
-        rec.cell = kDead;
-        if (kb + lane < tp[S + 1]) rec = rr[kb + lane];
-        contribute(rec);
-      }
-    });
-  }
-  __syncthreads();
-  // merge the copies in order; refresh_active (warp.hpp:186-192), reference_loss
-  // terms (:306-309), splat_position_grad factors (:346-349)
-  double lsum = 0.0;
-  unsigned act = 0;
-  double2* cw = coef + ((size_t)w * R + r) * 2 * HW;
-  for (int q = threadIdx.x; q < kOwnPx; q += blockDim.x) {
-    const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
-    if (px >= W || py >= H) continue;
-    double C0 = acc_all[4 * q], S0 = acc_all[4 * q + 1], C1 = acc_all[4 * q + 2], S1 = acc_all[4 * q + 3];
-#pragma unroll
-    for (int m = 1; m < NC; ++m) {
-      const double* a = acc_all + (size_t)m * kOwnPx * 4 + 4 * q;
-      C0 += a[0];
-      S0 += a[1];
-      C1 += a[2];
-      S1 += a[3];
-    }
-    const int g = py * W + px;
-    act += (C0 + C1 > 0.0) ? 1u : 0u;
-    const double a0 = S0 / (C0 + kLossEps), a1 = S1 / (C1 + kLossEps);
-    lsum += a0 * a0 + a1 * a1;
-    const double i0 = 1.0 / (C0 + kLossEps), i1 = 1.0 / (C1 + kLossEps);
-    const double b0 = S0 * i0, b1 = S1 * i1;
-    cw[g] = make_double2(b0, b0 * i0);
-    cw[HW + g] = make_double2(b1, b1 * i1);
-    if (stack_out) {
-      double2* so = stack_out + ((size_t)w * R + r) * 2 * HW;
-      so[g] = make_double2(C0, S0);
-      so[HW + g] = make_double2(C1, S1);
-    }
-  }
-  lsum = warp_sum(lsum);
-  for (int o2 = 16; o2 > 0; o2 >>= 1) act += __shfl_xor_sync(kFull, act, o2);
-  if (lane == 0) {
-    s_red[wid] = lsum;
-    s_act[wid] = act;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    unsigned a = 0;
-    for (int m = 0; m < NW; ++m) {
-      s += s_red[m];
-      a += s_act[m];
-    }
-    const size_t slot = ((size_t)w * R + r) * TP.oT + T;
-    part_acc[slot] = s;
-    part_act[slot] = a;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // backward, per event: d[r] at every reference + adjoint sweep -> (gx, gy) per bin
 
 __device__ __forceinline__ double2 pos_grad_w(const double2* __restrict__ cp, int W, int ox, int oy,
@@ -627,281 +468,6 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
 }
 
 // ---------------------------------------------------------------------------
-// backward owner: gradient tile per bin + fused depth_pose_to_flows_backward
-//
-// One CTA per (window, owner tile, bin group), one warp per bin i. Warp i
-// gathers the (gx, gy) of: events with bin j > i at their reference-(i+1) cell
-// (backward leg), events with j < i at their reference-i cell (forward leg),
-// and events with j == i at their source pixel (the two partial steps) --
-// BufferGradSink::add (warp.hpp:394-406) -- then runs the flows backward of
-// bin i (geometry.hpp:300-322) on the finished tile. d_depth sums the per-bin
-// contributions in bin order.
-
-constexpr int kBwdSeg = 3 * kListCapO;
-constexpr int kBwdWarpBytes =
-    ((kOwnPx * 2 * 8 + kBwdSeg * 2 + (kBwdSeg + 1) * 4 + kBwdSeg * 4 + 15) / 16) * 16;
-
-// kDet: one warp per bin, lane-ordered accumulation (bit-stable). !kDet: two
-// warps per bin split the bin's events and add into the shared tile with
-// shared-memory fp64 atomics.
-template <bool kDet>
-__global__ void __launch_bounds__(32 * kBwdGroup * (kDet ? 1 : 2)) k_bwd_owner(
-    const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
-    TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
-    const FwdRec* __restrict__ recs, const float2* __restrict__ bwd, uint64_t n_total,
-    const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
-    const uint16_t* __restrict__ lists, const int* __restrict__ no_surv,
-    const double* __restrict__ depth, const uint8_t* __restrict__ mask,
-    const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
-    double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
-  constexpr int kSplit = kDet ? 1 : 2;  // warps per bin
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_n[kBwdGroup][4];
-  const int T = blockIdx.x, grp = blockIdx.y, w = blockIdx.z;
-  const int lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) / kSplit, sub = (threadIdx.x >> 5) % kSplit;
-  const int B = P.B, R = B + 1, NS = 2 * B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int i = grp * kBwdGroup + wq;                     // this warp's bin
-  const int nb = min(kBwdGroup, B - grp * kBwdGroup);     // bins in this CTA
-  unsigned char* wst = smem_raw + (size_t)wq * kBwdWarpBytes;
-  double* g = reinterpret_cast<double*>(wst);                            // [px][gu, gv]
-  uint32_t* pre = reinterpret_cast<uint32_t*>(wst + kOwnPx * 2 * 8);     // kBwdSeg + 1
-  uint32_t* rng = pre + (kBwdSeg + 1);                                    // kBwdSeg
-  uint16_t* lst = reinterpret_cast<uint16_t*>(rng + kBwdSeg);             // kBwdSeg
-  const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
-  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
-  const uint64_t base = ev_off[w];
-  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
-  const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
-  const bool active = wq < nb;
-  const bool run = active && !no_surv[w];
-  for (int q = lane + 32 * sub; q < kOwnPx * 2; q += 32 * kSplit) g[q] = 0.0;
-  const size_t sA = ((size_t)w * NS + i + 1) * TP.oT + T;
-  const size_t sB = ((size_t)w * NS + i) * TP.oT + T;
-  const size_t sC = ((size_t)w * NS + R + i) * TP.oT + T;
-  if (run && sub == 0) {
-    const int nA = warp_load_sorted_list(lcount, lists, sA, lst);
-    const int nB = nA >= 0 ? warp_load_sorted_list(lcount, lists, sB, lst + nA) : -1;
-    const int nC = nB >= 0 ? warp_load_sorted_list(lcount, lists, sC, lst + nA + nB) : -1;
-    if (nA >= 0 && nB >= 0 && nC >= 0)
-      warp_ranges(0, nA + nB + nC, 0u, pre, rng, [&](int l) {
-        const int S = lst[l];
-        if (l < nA) return make_uint2(bp[(size_t)S * (B + 1) + i + 1], tp[S + 1]);
-        if (l < nA + nB) return make_uint2(tp[S], bp[(size_t)S * (B + 1) + i]);
-        return make_uint2(bp[(size_t)S * (B + 1) + i], bp[(size_t)S * (B + 1) + i + 1]);
-      });
-    if (lane == 0) {
-      s_n[wq][0] = nA;
-      s_n[wq][1] = nB;
-      s_n[wq][2] = nC;
-    }
-  }
-  __syncthreads();
-
-  if (run) {
-    const float2* bi = bwd + (size_t)i * n_total + base;
-    const FwdRec* rA = recs + (size_t)(i + 1) * n_total + base;  // backward-leg cells (j > i)
-    const FwdRec* rB = recs + (size_t)i * n_total + base;        // forward-leg cells (j < i)
-    const int nA = s_n[wq][0], nB = s_n[wq][1], nC = s_n[wq][2];
-    auto add = [&](int key, double v0, double v1) {  // one corner into the bin tile (collective)
-      if (kDet) {
-        warp_accumulate2(g, key, v0, v1);
-      } else if (key >= 0) {
-        atomicAdd(g + 2 * key, v0);
-        atomicAdd(g + 2 * key + 1, v1);
-      }
-    };
-    auto accumulate = [&](const FwdRec& rec, float2 v) {  // 4-corner sink
-      const bool live = rec.cell != kDead;
-      CellW c{};
-      if (live) c = decode(rec);
-      const bool touch = live && c.x0 + ox >= ox0 && c.x0 < ox0 + kOwnW && c.y0 + oy >= oy0 &&
-                         c.y0 < oy0 + kOwnH;
-      if (!__any_sync(kFull, touch)) return;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int lx = c.x0 + ((q & 1) ? ox : 0) - ox0, ly = c.y0 + ((q & 2) ? oy : 0) - oy0;
-        const bool in = touch && lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH;
-        const double wgt = corner_w(c, q);
-        add(in ? (ly * kOwnW + lx) : -1, wgt * (double)v.x, wgt * (double)v.y);
-      }
-    };
-    auto pixel_key = [&](uint32_t k) {  // source pixel of sorted event k if inside the tile
-      const uint2 e = sorted[base + k];
-      const int lx = ev_x(e) - ox0, ly = ev_y(e) - oy0;
-      return (lx >= 0 && lx < kOwnW && ly >= 0 && ly < kOwnH) ? ly * kOwnW + lx : -1;
-    };
-    if (nA >= 0 && nB >= 0 && nC >= 0) {
-      const int nl = nA + nB + nC;
-      const uint32_t total = pre[nl];
-      const uint32_t sAB = pre[nA], sBC = pre[nA + nB];
-      const uint32_t v0 = (uint32_t)(((uint64_t)total * sub) / kSplit);
-      const uint32_t v1 = (uint32_t)(((uint64_t)total * (sub + 1)) / kSplit);
-      int lcur = 0;
-      if (v0 < v1) virt_slot(pre, rng, nl, v0, &lcur);
-      for (uint32_t vb = v0; vb < v1; vb += 32 * kPrefetch) {
-        FwdRec rb[kPrefetch];
-        float2 vv[kPrefetch];
-        int pk[kPrefetch];
-#pragma unroll
-        for (int m = 0; m < kPrefetch; ++m) {
-          const uint32_t v = vb + m * 32 + lane;
-          rb[m].cell = kDead;
-          vv[m] = make_float2(0.f, 0.f);
-          pk[m] = -1;
-          if (v < v1) {
-            while (pre[lcur + 1] <= v) ++lcur;
-            const uint32_t k = rng[lcur] + (v - pre[lcur]);
-            if (v < sBC) {
-              rb[m] = (v < sAB) ? rA[k] : rB[k];
-              if (rb[m].cell != kDead) vv[m] = bi[k];
-            } else if (recs[base + k].cell != kDead) {
-              pk[m] = pixel_key(k);
-              if (pk[m] >= 0) vv[m] = bi[k];
-            }
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < kPrefetch; ++m) {
-          if (vb + m * 32 >= v1) break;
-          if (vb + m * 32 < sBC) accumulate(rb[m], vv[m]);
-          if (vb + m * 32 + 31 >= sBC) add(pk[m], (double)vv[m].x, (double)vv[m].y);
-        }
-      }
-    } else if (sub == 0) {
-      // an owner list overflowed: scan the sort-tile boxes in order (slow, rare)
-      scan_sources(bbox + ((size_t)w * NS + i + 1) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
-        const uint32_t k1 = tp[S + 1];
-        for (uint32_t kb = bp[(size_t)S * (B + 1) + i + 1]; kb < k1; kb += 32) {
-          FwdRec rec;
-          rec.cell = kDead;
-          float2 v = make_float2(0.f, 0.f);
-          if (kb + lane < k1) {
-            rec = rA[kb + lane];
-            if (rec.cell != kDead) v = bi[kb + lane];
-          }
-          accumulate(rec, v);
-        }
-      });
-      scan_sources(bbox + ((size_t)w * NS + i) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
-        const uint32_t k1 = bp[(size_t)S * (B + 1) + i];
-        for (uint32_t kb = tp[S]; kb < k1; kb += 32) {
-          FwdRec rec;
-          rec.cell = kDead;
-          float2 v = make_float2(0.f, 0.f);
-          if (kb + lane < k1) {
-            rec = rB[kb + lane];
-            if (rec.cell != kDead) v = bi[kb + lane];
-          }
-          accumulate(rec, v);
-        }
-      });
-      scan_sources(bbox + ((size_t)w * NS + R + i) * TP.nT, TP.nT, ox0, oy0, lst, kBwdSeg, [&](int S) {
-        const uint32_t k1 = bp[(size_t)S * (B + 1) + i + 1];
-        for (uint32_t kb = bp[(size_t)S * (B + 1) + i]; kb < k1; kb += 32) {
-          const uint32_t k = kb + lane;
-          int key = -1;
-          float2 v = make_float2(0.f, 0.f);
-          if (k < k1 && recs[base + k].cell != kDead) {
-            key = pixel_key(k);
-            if (key >= 0) v = bi[k];
-          }
-          add(key, (double)v.x, (double)v.y);
-        }
-      });
-    }
-  }
-  __syncthreads();
-  if (sub != 0) return;  // one warp per bin runs the flows backward
-
-  // fused depth_pose_to_flows_backward for bin i (geometry.hpp:300-322)
-  if (active) {
-    const double* pt = pose_tab ? pose_tab + ((size_t)w * B + i) * kPoseTab : nullptr;
-    double c6[6] = {0, 0, 0, 0, 0, 0};
-    for (int q = lane; q < kOwnPx; q += 32) {
-      const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
-      const double gu = g[2 * q], gv = g[2 * q + 1];
-      double contrib = 0.0;
-      if (px < W && py < H) {
-        const int gq = py * W + px;
-        if (grad_out) {
-          grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
-          grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
-        }
-        const double d = pt ? depth[(size_t)w * HW + gq] : 0.0;
-        const bool ok = pt && (!mask || mask[(size_t)w * HW + gq]) && d > 0.0;
-        if (ok && (gu != 0.0 || gv != 0.0)) {
-          const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
-          const double ry = 1.0 * ((double)py - cy) / fy;
-          const double rr0 = pt[0] * rx + pt[1] * ry + pt[2];
-          const double rr1 = pt[3] * rx + pt[4] * ry + pt[5];
-          const double rr2 = pt[6] * rx + pt[7] * ry + pt[8];
-          const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
-          if (p2 > 0.0) {
-            const double inv_dt = pt[39], iz = 1.0 / p2;
-            const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-            const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-            contrib = (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-            c6[3] += gu * ju0 * inv_dt;
-            c6[4] += gv * jv1 * inv_dt;
-            c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const double* dR = pt + 9 + 9 * a;
-              const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-              const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-              const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-              c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) *
-                       inv_dt;
-            }
-          }
-        }
-      }
-      g[2 * q] = contrib;  // tile finished: reuse the slot for this bin's d_depth
-    }
-    if (pt) {
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double v = warp_sum(c6[a]);
-        if (lane == 0) pose_part[(((size_t)w * TP.oT + T) * B + i) * 6 + a] = v;
-      }
-    }
-  }
-  if (kSplit > 1) {
-    // named barrier over the sub == 0 warps only (the others have exited)
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * ((blockDim.x >> 5) / kSplit)));
-  } else {
-    __syncthreads();
-  }
-  if (d_depth) {
-    const int G = (B + kBwdGroup - 1) / kBwdGroup;
-    const int nthr = 32 * ((blockDim.x >> 5) / kSplit);
-    const int tid = 32 * wq + lane;
-    for (int q = tid; q < kOwnPx; q += nthr) {
-      const int px = ox0 + (q % kOwnW), py = oy0 + (q / kOwnW);
-      if (px >= W || py >= H) continue;
-      double s = 0.0;
-      for (int b = 0; b < nb; ++b)  // bin order
-        s += reinterpret_cast<const double*>(smem_raw + (size_t)b * kBwdWarpBytes)[2 * q];
-      // G == 1: d_depth [w][HW]; G > 1: per-group partial planes [w][grp][HW]
-      d_depth[((size_t)w * G + grp) * HW + py * W + px] = s;
-    }
-  }
-}
-
-// d_depth = sum over bin groups (or bins), in order
-__global__ void k_ddepth_sum(const double* __restrict__ parts, int G, int HW, int n_windows,
-                             double* __restrict__ d_depth) {
-  const size_t total = (size_t)n_windows * HW;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t w = i / HW, q = i % HW;
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += parts[(w * G + g) * HW + q];
-    d_depth[i] = s;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // launchers
 
 TileParams make_tiles(const WinParams& P, uint64_t max_n) {
@@ -975,28 +541,6 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                                                                                     lcount, lists);
 }
 
-void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
-                      const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
-                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act, bool deterministic) {
-  static size_t a = 0, b = 0;
-  count_launch();
-  if (deterministic) {
-    const size_t smem = (size_t)kFwdWarps * kOwnPx * 4 * sizeof(double);
-    set_smem(reinterpret_cast<const void*>(k_fwd_owner<true>), smem, &a);
-    k_fwd_owner<true><<<dim3(TP.oT, P.B + 1, P.n_windows), 32 * kFwdWarps, smem, s>>>(
-        ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
-        part_act);
-  } else {
-    const size_t smem = (size_t)kOwnPx * 4 * sizeof(double);
-    set_smem(reinterpret_cast<const void*>(k_fwd_owner<false>), smem, &b);
-    k_fwd_owner<false><<<dim3(TP.oT, P.B + 1, P.n_windows), 256, smem, s>>>(
-        ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
-        part_act);
-  }
-}
-
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
@@ -1007,46 +551,6 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
   count_launch();
   k_bwd_event<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, 0, s>>>(
       sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, bwd, gmax);
-}
-
-int bwd_groups(const WinParams& P) { return (P.B + kBwdGroup - 1) / kBwdGroup; }
-
-void launch_ddepth_sum(cudaStream_t s, const double* parts, int G, int HW, int n_windows,
-                       double* d_depth) {
-  count_launch();
-  k_ddepth_sum<<<148 * 4, 256, 0, s>>>(parts, G, HW, n_windows, d_depth);
-}
-
-void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
-                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                      const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
-                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, const int* no_surv, const double* depth,
-                      const uint8_t* mask, const double* pose_tab, const double* K,
-                      double* d_depth, double* d_depth_parts, double* pose_part,
-                      double* grad_out, bool deterministic) {
-  const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
-  const int G = bwd_groups(P);
-  const int warps = std::min(P.B, kBwdGroup);
-  const size_t smem = (size_t)warps * kBwdWarpBytes;
-  static size_t a = 0, b = 0;
-  double* dd_out = (d_depth && G > 1) ? d_depth_parts : d_depth;
-  count_launch();
-  if (deterministic) {
-    set_smem(reinterpret_cast<const void*>(k_bwd_owner<true>), smem, &a);
-    k_bwd_owner<true><<<dim3(TP.oT, G, P.n_windows), 32 * warps, smem, s>>>(
-        sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
-        depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
-  } else {
-    set_smem(reinterpret_cast<const void*>(k_bwd_owner<false>), smem, &b);
-    k_bwd_owner<false><<<dim3(TP.oT, G, P.n_windows), 64 * warps, smem, s>>>(
-        sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, bbox, lcount, lists, no_surv,
-        depth, mask, pose_tab, k0, k1, k2, k3, dd_out, pose_part, grad_out);
-  }
-  if (d_depth && G > 1) {
-    count_launch();
-    k_ddepth_sum<<<148 * 4, 256, 0, s>>>(d_depth_parts, G, P.HW, P.n_windows, d_depth);
-  }
 }
 
 }  // namespace evcm_b200

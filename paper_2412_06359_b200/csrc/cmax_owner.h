@@ -18,9 +18,6 @@ constexpr int kSortThreads = 512;  // key/histogram CTA size
 constexpr int kScatterThreads = 256;  // 8 warps x 1024 events per scatter chunk
 constexpr int kMaxTiles = 12000;   // sort scatter keeps 8 x nT u16 counters in smem
 constexpr int kListCapO = 128;     // source-list capacity per (window, slot, owner tile)
-constexpr int kFwdWarps = 4;       // warps (private fp64 copies) per deterministic forward owner
-constexpr int kPrefetch = 4;       // records in flight per lane in the owner loops
-constexpr int kBwdGroup = 5;       // bins per backward owner CTA
 
 struct TileParams {
   int ntx, nty, nT;  // sort tiles
@@ -38,10 +35,6 @@ struct __align__(16) FwdRec {
 };
 
 TileParams make_tiles(const WinParams& P, uint64_t max_n);
-int bwd_groups(const WinParams& P);
-// d_depth[w] = sum over g < G of parts[w][g] (in order)
-void launch_ddepth_sum(cudaStream_t s, const double* parts, int G, int HW, int n_windows,
-                       double* d_depth);
 void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off,
                        const WinParams& P, uint64_t max_n, uint2* packed, unsigned long long* err);
 // keys: 2 * n_total + n_windows * nT entries (unsorted keys, keys in sorted
@@ -55,25 +48,11 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                          const uint32_t* sorted_keys, uint64_t max_n, const double2* flows,
                          uint64_t n_total, FwdRec* recs, uint4* bbox, uint32_t* lcount,
                          uint16_t* lists);
-void launch_fwd_owner(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
-                      const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
-                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act, bool deterministic);
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
                       const double2* coef, const double* scale, const int* no_surv, float2* bwd,
                       uint32_t* gmax);
-void launch_bwd_owner(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
-                      const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                      const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
-                      uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, const int* no_surv, const double* depth,
-                      const uint8_t* mask, const double* pose_tab, const double* K,
-                      double* d_depth, double* d_depth_parts, double* pose_part,
-                      double* grad_out, bool deterministic);
-
 // Owner kernels with exact fixed-point shared-memory accumulation (cmax_cells.cu).
 void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
