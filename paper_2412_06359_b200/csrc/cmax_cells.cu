@@ -255,6 +255,92 @@ __device__ __forceinline__ void clip(const Batch& bt, int l, uint32_t rb, uint32
 }
 
 // ---------------------------------------------------------------------------
+// Precomputed candidate ranges (k_ranges): per (window, slot, owner tile) list,
+// kRgCap uint2 entries: e[0] = {count (kOverflow: the list overflowed), total},
+// e[1 + l] = {first record slot, exclusive prefix of the lengths}. The
+// producers fetch a whole list with one cp.async.bulk.
+
+constexpr int kRgCap = kListCapO + 2;  // 130 entries = 1040 B (a multiple of 16)
+constexpr uint32_t kOverflow = 0xffffffffu;
+
+// Ranges of up to two lists concatenated in virtual candidate space: ranges
+// [0, n0) from a (kind 0), then [n0, n0 + n1) from b (kind 1).
+struct Cat {
+  const uint2* a;
+  const uint2* b;
+  int n0, n1;
+  uint32_t t0, t1;
+  __device__ __forceinline__ int nl() const { return n0 + n1; }
+  __device__ __forceinline__ uint32_t total() const { return t0 + t1; }
+  __device__ __forceinline__ uint32_t pre(int l) const {
+    return l < n0 ? a[1 + l].y : (l < n0 + n1 ? t0 + b[1 + l - n0].y : t0 + t1);
+  }
+  __device__ __forceinline__ uint32_t rng(int l) const { return l < n0 ? a[1 + l].x : b[1 + l - n0].x; }
+};
+__device__ __forceinline__ Cat make_cat(const uint2* a, const uint2* b) {
+  Cat c;
+  c.a = a;
+  c.b = b;
+  c.n0 = a ? (int)a[0].x : 0;
+  c.t0 = a ? a[0].y : 0u;
+  c.n1 = b ? (int)b[0].x : 0;
+  c.t1 = b ? b[0].y : 0u;
+  return c;
+}
+// the next batch of an overflowed list, via next_batch, as a Cat view in fb
+__device__ __forceinline__ void batch_to_view(const Batch& bt, uint2* fb) {
+  const int lane = threadIdx.x & 31;
+  for (int l = lane; l < bt.nl; l += 32) fb[1 + l] = make_uint2(bt.rng[l], bt.pre[l]);
+  if (lane == 0) fb[0] = make_uint2((uint32_t)bt.nl, bt.nl > 0 ? bt.pre[bt.nl] : 0u);
+  __syncwarp();
+}
+
+__global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
+                         const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
+                         WinParams P, TileParams TP, uint2* __restrict__ ranges) {
+  const int lane = threadIdx.x & 31;
+  const size_t gid = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int NS = 2 * P.B + 1, R = P.B + 1;
+  if (gid >= (size_t)P.n_windows * NS * TP.oT) return;
+  const size_t ws = gid / TP.oT;
+  const int slot = (int)(ws % NS), w = (int)(ws / NS);
+  const uint32_t cnt = lcount[gid];
+  uint2* out = ranges + gid * kRgCap;
+  if (cnt > (uint32_t)kListCapO) {
+    if (lane == 0) out[0] = make_uint2(kOverflow, 0u);
+    return;
+  }
+  const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
+  const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (P.B + 1);
+  uint32_t carry = 0;
+  for (uint32_t l0 = 0; l0 < cnt; l0 += 32) {
+    const uint32_t l = l0 + lane;
+    uint32_t lo = 0, len = 0;
+    if (l < cnt) {
+      const int S = lists[gid * kListCapO + l];
+      uint32_t hi;
+      if (slot < R) {  // reference slot: every event of the sort tile
+        lo = tp[S];
+        hi = tp[S + 1];
+      } else {  // source slot of bin i: the tile's events of bin i (time-sorted)
+        const uint32_t* b = bp + (size_t)S * (P.B + 1);
+        lo = b[slot - R];
+        hi = b[slot - R + 1];
+      }
+      len = hi - lo;
+    }
+    uint32_t x = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (l < cnt) out[1 + l] = make_uint2(lo, carry + x - len);
+    carry += __shfl_sync(kFull, x, 31);
+  }
+  if (lane == 0) out[0] = make_uint2(cnt, carry);
+}
+
+// ---------------------------------------------------------------------------
 // forward: one CTA per (owner tile, window), references in order, warp
 // specialised. Warp 0 (producer) builds each round's candidate ranges and
 // stages them with cp.async.bulk into one of two buffers (full/empty mbarrier
@@ -277,15 +363,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
     const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
     const uint4* __restrict__ bbox, const uint32_t* __restrict__ lcount,
-    const uint16_t* __restrict__ lists, double2* __restrict__ coef, double2* __restrict__ stack_out,
-    double* __restrict__ part_acc, unsigned long long* __restrict__ part_act) {
+    const uint16_t* __restrict__ lists, const uint2* __restrict__ ranges,
+    double2* __restrict__ coef, double2* __restrict__ stack_out, double* __restrict__ part_acc,
+    unsigned long long* __restrict__ part_act) {
   extern __shared__ __align__(16) unsigned char smem[];
   FwdRec* stage = reinterpret_cast<FwdRec*>(smem);                    // [2][kStageP]
   uint32_t* acc = reinterpret_cast<uint32_t*>(stage + 2 * kStageP);   // [pol][C, S][lo, hi][kPlane]
   uint32_t* flag = acc + 8 * kPlane;                                  // [kPlane] some w > 0
   __shared__ Batch bt;
   __shared__ RoundDesc desc[2];
-  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ __align__(16) uint2 rv[2][kRgCap];    // prefetched ranges
+  __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
+  __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
   __shared__ double s_red[2][kWarps];
   __shared__ unsigned s_act[2][kWarps];
 
@@ -303,50 +392,73 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     mbar_init(&full[1], 1);
     mbar_init(&empty[0], kWarps);
     mbar_init(&empty[1], kWarps);
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (wid == 0) {
     // ---------------- producer ----------------
-    uint32_t it = 0;
-    for (int r = 0; r < R; ++r) {
-      const FwdRec* rr = recs + (size_t)r * n_total + base;
-      const size_t ws = (size_t)w * NS + r;
-      if (lane == 0) bt.seg = -1;
+    // ranges of reference r: precomputed list (prefetched one reference ahead)
+    auto prefetch = [&](int r) {
+      const size_t gid = ((size_t)w * NS + r) * TP.oT + T;
+      fence_proxy_async();
       __syncwarp();
-      int more = 1;
-      while (more) {
-        next_batch<1>(bt, lcount, lists, bbox, TP.nT, ox0, oy0,
-                      [&](int) { return ws * TP.oT + T; }, [&](int) { return ws * TP.nT; },
-                      [&](int, int S) { return make_uint2(tp[S], tp[S + 1]); });
-        const int nl = bt.nl;
-        const uint32_t total = nl > 0 ? bt.pre[nl] : 0u;
-        more = bt.more;
-        // rounds of this batch (an empty final batch still emits one round)
-        for (uint32_t rb = 0; rb < total || (rb == 0 && !more); rb += kStageP) {
-          const uint32_t n = total > rb ? min(total - rb, (uint32_t)kStageP) : 0u;
-          const int b = it & 1;
-          if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
-          FwdRec* sb = stage + b * kStageP;
-          if (lane == 0) {
-            desc[b].n = n;
-            desc[b].r = r;
-            desc[b].last = (!more && rb + kStageP >= total) ? 1 : 0;
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_expect_tx(&full[b], n * (uint32_t)sizeof(FwdRec));
-          __syncwarp();
-          for (int l = lane; l < nl; l += 32) {
-            uint32_t lo, hi;
-            clip(bt, l, rb, kStageP, lo, hi);
-            if (lo < hi)
-              bulk_g2s(sb + (lo - rb), rr + bt.rng[l] + (lo - bt.pre[l]),
-                       (hi - lo) * (uint32_t)sizeof(FwdRec), &full[b]);
-          }
-          ++it;
-          if (total == 0) break;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&rbar[r & 1], kRgCap * (uint32_t)sizeof(uint2));
+        bulk_g2s(rv[r & 1], ranges + gid * kRgCap, kRgCap * (uint32_t)sizeof(uint2), &rbar[r & 1]);
+      }
+    };
+    uint32_t it = 0;
+    // stage the rounds of one view; `final`: its last round ends reference r
+    auto rounds = [&](const Cat& cv, int r, bool final) {
+      const FwdRec* rr = recs + (size_t)r * n_total + base;
+      const int nl = cv.nl();
+      const uint32_t total = cv.total();
+      for (uint32_t rb = 0; rb < total || (rb == 0 && final); rb += kStageP) {
+        const uint32_t n = total > rb ? min(total - rb, (uint32_t)kStageP) : 0u;
+        const int b = it & 1;
+        if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+        FwdRec* sb = stage + b * kStageP;
+        if (lane == 0) {
+          desc[b].n = n;
+          desc[b].r = r;
+          desc[b].last = (final && rb + kStageP >= total) ? 1 : 0;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[b], n * (uint32_t)sizeof(FwdRec));
+        __syncwarp();
+        for (int l = lane; l < nl; l += 32) {
+          const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + kStageP);
+          if (lo < hi)
+            bulk_g2s(sb + (lo - rb), rr + cv.rng(l) + (lo - cv.pre(l)),
+                     (hi - lo) * (uint32_t)sizeof(FwdRec), &full[b]);
+        }
+        ++it;
+        if (total == 0) break;
+      }
+    };
+    prefetch(0);
+    for (int r = 0; r < R; ++r) {
+      if (r + 1 < R) prefetch(r + 1);
+      mbar_wait(&rbar[r & 1], (r >> 1) & 1);
+      const uint2* v = rv[r & 1];
+      if (v[0].x != kOverflow) {
+        rounds(make_cat(v, nullptr), r, true);
+      } else {  // overflowed list: scan the sort-tile boxes batch by batch
+        const size_t ws = (size_t)w * NS + r;
+        if (lane == 0) bt.seg = -1;
+        __syncwarp();
+        int more = 1;
+        while (more) {
+          next_batch<1>(bt, lcount, lists, bbox, TP.nT, ox0, oy0,
+                        [&](int) { return ws * TP.oT + T; }, [&](int) { return ws * TP.nT; },
+                        [&](int, int S) { return make_uint2(tp[S], tp[S + 1]); });
+          more = bt.more;
+          batch_to_view(bt, fb);
+          rounds(make_cat(fb, nullptr), r, !more);
         }
       }
     }
@@ -471,10 +583,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
 constexpr int kStageQ = 1536;  // slots per buffer
 
 struct BRound {
-  uint32_t n;  // slots
-  int r;       // reference (kind 0) or bin (kind 1)
-  int kind;    // 0: record sinks of reference r, 1: source-pixel sinks of bin r
-  int last;    // last round of this (kind, r)
+  uint32_t n;      // slots
+  uint32_t split;  // slots [0, split): record sinks of reference r; [split, n): source sinks of bin r - 1
+  int r;           // group
+  int last;        // last round of the group: bin r - 1 is complete
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
@@ -483,19 +595,21 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     const FwdRec* __restrict__ recs, const float2* __restrict__ vals, uint64_t n_total,
     const uint32_t* __restrict__ gmax, const uint4* __restrict__ bbox,
     const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
-    const int* __restrict__ no_surv, const double* __restrict__ depth,
-    const uint8_t* __restrict__ mask, const double* __restrict__ pose_tab, double fx, double fy,
-    double cx, double cy, double* __restrict__ d_depth, double* __restrict__ pose_part,
-    double* __restrict__ grad_out) {
+    const uint2* __restrict__ ranges, const int* __restrict__ no_surv,
+    const double* __restrict__ depth, const uint8_t* __restrict__ mask,
+    const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
+    double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* stage16 = reinterpret_cast<uint4*>(smem);                     // [2][kStageQ] records
   float2* stage8 = reinterpret_cast<float2*>(stage16 + 2 * kStageQ);   // [2][kStageQ] values
   uint32_t* acc = reinterpret_cast<uint32_t*>(stage8 + 2 * kStageQ);   // [tile][gu, gv][lo, hi][kPlane]
   __shared__ Batch bt;
   __shared__ BRound desc[2];
-  __shared__ uint32_t roff[kBatchCap];
+  __shared__ uint32_t roff[2 * kListCapO + 1 > kBatchCap ? 2 * kListCapO + 1 : kBatchCap];
   __shared__ uint32_t fake[2][kStageQ / 32];  // slack slots of the staged round
-  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ __align__(16) uint2 rv[2][2][kRgCap];   // prefetched ranges (reference, source)
+  __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
+  __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
   __shared__ double s_pose[2][kWarps][6];
 
   const int T = blockIdx.x, w = blockIdx.y;
@@ -514,124 +628,154 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     mbar_init(&full[1], 1);
     mbar_init(&empty[0], kWarps);
     mbar_init(&empty[1], kWarps);
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (wid == 0) {
     // ---------------- producer ----------------
-    uint32_t it = 0;
-    // stage the rounds of one (kind, r) group: kind 0 = reference r (list slot r,
-    // full sort-tile ranges), kind 1 = source sinks of bin r (list slot R + r,
-    // the bin's sub-range of every sort tile)
-    auto group = [&](int kind, int r) {
-      const size_t ws = (size_t)w * NS + (kind == 0 ? r : R + r);
-      const FwdRec* rr = recs + (size_t)r * n_total + base;
-      const float2* vv = vals + (size_t)(kind == 0 ? r - 1 : B - 1) * n_total;
-      if (lane == 0) bt.seg = -1;
+    // group g = 1..B: the record sinks of reference g (g < B, list slot g) then
+    // the source-pixel sinks of bin g - 1 (list slot R + g - 1); after group g
+    // bin g - 1 is complete. Ranges are prefetched one group ahead.
+    auto prefetch = [&](int g) {
+      const size_t gref = ((size_t)w * NS + g) * TP.oT + T;
+      const size_t gsrc = ((size_t)w * NS + R + g - 1) * TP.oT + T;
+      fence_proxy_async();
       __syncwarp();
-      int more = run ? 1 : 0;
-      bool emitted = false;
-      while (more || !emitted) {
-        int nl = 0;
-        uint32_t total = 0;
-        if (more) {
-          next_batch<1>(
-              bt, lcount, lists, bbox, TP.nT, ox0, oy0, [&](int) { return ws * TP.oT + T; },
-              [&](int) { return ws * TP.nT; },
-              [&](int, int S) {
-                if (kind == 0) return make_uint2(tp[S], tp[S + 1]);
-                const uint32_t* b = bp + (size_t)S * (B + 1);
-                return make_uint2(b[r], b[r + 1]);
-              });
-          nl = bt.nl;
-          total = nl > 0 ? bt.pre[nl] : 0u;
-          more = bt.more;
-        } else {
-          more = 0;
-        }
-        // virtual candidates per round, leaving room for <= 3 slack slots per range
-        const uint32_t capv = kStageQ - 3u * (uint32_t)min(nl, kBatchCap);
-        for (uint32_t rb = 0; rb < total || (rb == 0 && !more && !emitted); rb += capv) {
-          const int b = it & 1;
-          if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
-          uint4* s16 = stage16 + b * kStageQ;
-          float2* s8 = stage8 + b * kStageQ;
-          uint2* s8e = reinterpret_cast<uint2*>(s16);  // kind 1: packed events
-          uint32_t* fk = fake[b];
-          for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
-          // region offsets: exclusive scan of roundup2(len + 2) over the ranges
-          uint32_t carry = 0;
-          for (int l0 = 0; l0 < nl; l0 += 32) {
-            const int l = l0 + lane;
-            uint32_t sz = 0;
-            if (l < nl) {
-              uint32_t lo, hi;
-              clip(bt, l, rb, capv, lo, hi);
-              sz = lo < hi ? ((hi - lo + 3) & ~1u) : 0u;
-            }
-            uint32_t x = sz;
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(kFull, x, o);
-              if (lane >= o) x += y;
-            }
-            if (l < nl) roff[l] = carry + x - sz;
-            carry += __shfl_sync(kFull, x, 31);
-          }
-          __syncwarp();
-          const uint32_t nslots = carry;
-          uint32_t bytes = 0;
-          for (int l = lane; l < nl; l += 32) {
-            uint32_t lo, hi;
-            clip(bt, l, rb, capv, lo, hi);
-            if (lo >= hi) continue;
-            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), len = hi - lo;
-            const uint32_t par = (uint32_t)((base + k0) & 1ull);  // n_total is even
-            const uint32_t s0 = roff[l], sz = (uint32_t)((len + 3) & ~1ull);
-            const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
-            // slack slots (no candidate of this range): s0 if par, [s0+par+len, s0+sz)
-            if (par) atomicOr(fk + (s0 >> 5), 1u << (s0 & 31));
-            for (uint32_t q = s0 + par + (uint32_t)len; q < s0 + sz; ++q)
-              atomicOr(fk + (q >> 5), 1u << (q & 31));
-            bytes += (uint32_t)(kind == 0 ? len * sizeof(FwdRec) : (a1 - a0) * 8);
-            bytes += (uint32_t)((a1 - a0) * 8);
-          }
-          bytes = warp_sum_u32(bytes);
-          if (lane == 0) {
-            desc[b].n = nslots;
-            desc[b].r = r;
-            desc[b].kind = kind;
-            desc[b].last = (!more && rb + capv >= total) ? 1 : 0;
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_expect_tx(&full[b], bytes);
-          __syncwarp();
-          for (int l = lane; l < nl; l += 32) {
-            uint32_t lo, hi;
-            clip(bt, l, rb, capv, lo, hi);
-            if (lo >= hi) continue;
-            const uint64_t k0 = bt.rng[l] + (lo - bt.pre[l]), len = hi - lo;
-            const uint32_t par = (uint32_t)((base + k0) & 1ull);
-            const uint32_t s0 = roff[l];
-            const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
-            bulk_g2s(s8 + s0, vv + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
-            if (kind == 0)
-              bulk_g2s(s16 + s0 + par, rr + k0, (uint32_t)(len * sizeof(FwdRec)), &full[b]);
-            else
-              bulk_g2s(s8e + s0, sorted + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
-          }
-          ++it;
-          emitted = true;
-          if (total == 0) break;
-        }
+      if (lane == 0) {
+        const uint32_t one = kRgCap * (uint32_t)sizeof(uint2);
+        mbar_arrive_expect_tx(&rbar[g & 1], g < B ? 2 * one : one);
+        if (g < B) bulk_g2s(rv[g & 1][0], ranges + gref * kRgCap, one, &rbar[g & 1]);
+        bulk_g2s(rv[g & 1][1], ranges + gsrc * kRgCap, one, &rbar[g & 1]);
       }
     };
-    for (int r = 1; r < B; ++r) {
-      group(0, r);
-      group(1, r - 1);
+    uint32_t it = 0;
+    auto rounds = [&](const Cat& cv, int g, bool final) {
+      const FwdRec* rr = recs + (size_t)min(g, B) * n_total + base;
+      const float2* v0 = vals + (size_t)(g - 1) * n_total;  // sinks at reference g
+      const float2* v1 = vals + (size_t)(B - 1) * n_total;  // source-pixel sinks
+      const int nl = cv.nl(), n0 = cv.n0;
+      const uint32_t total = cv.total();
+      // virtual candidates per round, leaving room for <= 3 slack slots per range
+      const uint32_t capv = kStageQ - 3u * (uint32_t)nl;
+      for (uint32_t rb = 0; rb < total || (rb == 0 && final); rb += capv) {
+        const int b = it & 1;
+        if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+        uint4* s16 = stage16 + b * kStageQ;
+        float2* s8 = stage8 + b * kStageQ;
+        // kind 1 packed events: upper half of the record buffer (slot v at byte
+        // 8 * (kStageQ + v) > 16 * v for every record slot v < split)
+        uint2* s8e = reinterpret_cast<uint2*>(s16) + kStageQ;
+        uint32_t* fk = fake[b];
+        for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
+        // region offsets: exclusive scan of roundup2(len + 2) over the ranges
+        uint32_t carry = 0;
+        for (int l0 = 0; l0 < nl; l0 += 32) {
+          const int l = l0 + lane;
+          uint32_t sz = 0;
+          if (l < nl) {
+            const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
+            sz = lo < hi ? ((hi - lo + 3) & ~1u) : 0u;
+          }
+          uint32_t x = sz;
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+          }
+          if (l < nl) roff[l] = carry + x - sz;
+          carry += __shfl_sync(kFull, x, 31);
+        }
+        __syncwarp();
+        const uint32_t nslots = carry;
+        uint32_t bytes = 0;
+        for (int l = lane; l < nl; l += 32) {
+          const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
+          if (lo >= hi) continue;
+          const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
+          const uint32_t par = (uint32_t)((base + k0) & 1ull);  // n_total is even
+          const uint32_t s0 = roff[l], sz = (uint32_t)((len + 3) & ~1ull);
+          const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
+          // slack slots (no candidate of this range): s0 if par, [s0+par+len, s0+sz)
+          if (par) atomicOr(fk + (s0 >> 5), 1u << (s0 & 31));
+          for (uint32_t q = s0 + par + (uint32_t)len; q < s0 + sz; ++q)
+            atomicOr(fk + (q >> 5), 1u << (q & 31));
+          bytes += (uint32_t)(l < n0 ? len * sizeof(FwdRec) : (a1 - a0) * 8);
+          bytes += (uint32_t)((a1 - a0) * 8);
+        }
+        bytes = warp_sum_u32(bytes);
+        if (lane == 0) {
+          desc[b].n = nslots;
+          desc[b].split = n0 < nl ? roff[n0] : nslots;
+          desc[b].r = g;
+          desc[b].last = (final && rb + capv >= total) ? 1 : 0;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[b], bytes);
+        __syncwarp();
+        for (int l = lane; l < nl; l += 32) {
+          const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
+          if (lo >= hi) continue;
+          const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
+          const uint32_t par = (uint32_t)((base + k0) & 1ull);
+          const uint32_t s0 = roff[l];
+          const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
+          if (l < n0) {
+            bulk_g2s(s8 + s0, v0 + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+            bulk_g2s(s16 + s0 + par, rr + k0, (uint32_t)(len * sizeof(FwdRec)), &full[b]);
+          } else {
+            bulk_g2s(s8 + s0, v1 + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+            bulk_g2s(s8e + s0, sorted + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+          }
+        }
+        ++it;
+        if (total == 0) break;
+      }
+    };
+    // overflowed list (more than kListCapO sort tiles): scan the boxes batch by batch
+    auto scan_rounds = [&](int kind, int g, bool final) {
+      const int slot = kind == 0 ? g : R + g - 1;
+      const size_t ws = (size_t)w * NS + slot;
+      if (lane == 0) bt.seg = -1;
+      __syncwarp();
+      int more = 1;
+      while (more) {
+        next_batch<1>(bt, lcount, lists, bbox, TP.nT, ox0, oy0,
+                      [&](int) { return ws * TP.oT + T; }, [&](int) { return ws * TP.nT; },
+                      [&](int, int S) {
+                        if (kind == 0) return make_uint2(tp[S], tp[S + 1]);
+                        const uint32_t* b = bp + (size_t)S * (B + 1);
+                        return make_uint2(b[g - 1], b[g]);
+                      });
+        more = bt.more;
+        batch_to_view(bt, fb);
+        rounds(kind == 0 ? make_cat(fb, nullptr) : make_cat(nullptr, fb), g, final && !more);
+      }
+    };
+    if (run) {
+      prefetch(1);
+      for (int g = 1; g <= B; ++g) {
+        if (g + 1 <= B) prefetch(g + 1);
+        mbar_wait(&rbar[g & 1], ((g - 1) >> 1) & 1);
+        const uint2* va = g < B ? rv[g & 1][0] : nullptr;
+        const uint2* vb = rv[g & 1][1];
+        const bool oa = va && va[0].x == kOverflow, ob = vb[0].x == kOverflow;
+        if (!oa && !ob) {
+          rounds(make_cat(va, vb), g, true);
+        } else {
+          if (va) {
+            if (oa) scan_rounds(0, g, false);
+            else rounds(make_cat(va, nullptr), g, false);
+          }
+          if (ob) scan_rounds(1, g, true);
+          else rounds(make_cat(nullptr, vb), g, true);
+        }
+      }
+    } else {  // no survivors: every bin is zero, still finish each one
+      for (int g = 1; g <= B; ++g) rounds(make_cat(nullptr, nullptr), g, true);
     }
-    group(1, B - 1);
     return;
   }
 
@@ -656,42 +800,42 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     const BRound d = desc[b];
     const uint4* s16 = stage16 + b * kStageQ;
     const float2* s8 = stage8 + b * kStageQ;
-    const uint2* s8e = reinterpret_cast<const uint2*>(s16);
+    const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
-    if (d.kind == 0) {
-      for (uint32_t v = ct; v < d.n; v += kCons) {
-        if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
-        const uint4 rec = s16[v];
-        const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
-        if (rec.x == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) continue;
-        const float2 g = s8[v];
-        if (g.x == 0.f && g.y == 0.f) continue;
-        // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
-        const int j = bin_of(rec.y, P.erel, B);
-        const int bin = (d.r <= j) ? d.r - 1 : d.r;
-        const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
-        double wx, ax, wy, ay;
-        expand_frac(__uint_as_float(rec.z), wx, ax);
-        expand_frac(__uint_as_float(rec.w), wy, ay);
-        const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
-        const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
-        const int o00 = ly * kRowW + lx;
+    // record sinks of reference d.r (slots < split)
+    for (uint32_t v = ct; v < d.split; v += kCons) {
+      if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
+      const uint4 rec = s16[v];
+      const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
+      if (rec.x == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) continue;
+      const float2 g = s8[v];
+      if (g.x == 0.f && g.y == 0.f) continue;
+      // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
+      const int j = bin_of(rec.y, P.erel, B);
+      const int bin = (d.r <= j) ? d.r - 1 : d.r;
+      const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
+      double wx, ax, wy, ay;
+      expand_frac(__uint_as_float(rec.z), wx, ax);
+      expand_frac(__uint_as_float(rec.w), wy, ay);
+      const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
+      const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
+      const int o00 = ly * kRowW + lx;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
-          const double wq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
-          if (in && wq != 0.0) {
-            const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
-            const uint32_t a = pt + 4u * (uint32_t)o;
-            fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wq * gx));
-            fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wq * gy));
-          }
+      for (int q = 0; q < 4; ++q) {
+        const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
+        const double wq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
+        if (in && wq != 0.0) {
+          const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
+          const uint32_t a = pt + 4u * (uint32_t)o;
+          fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wq * gx));
+          fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wq * gy));
         }
       }
-    } else {
-      // source-pixel sinks of bin d.r: weight 1 at the event's own pixel
-      const uint32_t pt = acc_s + (uint32_t)(d.r & 1) * (4 * kPlane * 4);
-      for (uint32_t v = ct; v < d.n; v += kCons) {
+    }
+    // source-pixel sinks of bin d.r - 1 (slots >= split): weight 1 at the event's pixel
+    {
+      const uint32_t pt = acc_s + (uint32_t)((d.r - 1) & 1) * (4 * kPlane * 4);
+      for (uint32_t v = d.split + ct; v < d.n; v += kCons) {
         if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
         const uint2 e = s8e[v];
         const int lx = ev_x(e) - ox0, ly = ev_y(e) - oy0;
@@ -706,10 +850,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);
     ++it;
-    if (!(d.kind == 1 && d.last)) continue;
+    if (!d.last) continue;
 
-    // bin i = d.r complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
-    const int i = d.r;
+    // bin i = d.r - 1 complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
+    const int i = d.r - 1;
     consumer_sync(kCons);
     double c6[6] = {0, 0, 0, 0, 0, 0};
     {
@@ -787,32 +931,43 @@ static void smem_attr(const void* fn, size_t bytes) {
 void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act) {
+                      const uint16_t* lists, const uint2* ranges, double2* coef, double2* stack_out,
+                      double* part_acc, unsigned long long* part_act) {
   static bool attr = false;
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_fwd_cells), fwd_cells_smem());
   attr = true;
   count_launch();
   k_fwd_cells<<<dim3(TP.oT, P.n_windows), kFwdThreads, fwd_cells_smem(), s>>>(
-      ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, coef, stack_out, part_acc,
-      part_act);
+      ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, ranges, coef, stack_out,
+      part_acc, part_act);
 }
 
 void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
-                      const uint32_t* lcount, const uint16_t* lists, const int* no_surv,
-                      const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth, double* pose_part, double* grad_out) {
+                      const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
+                      const int* no_surv, const double* depth, const uint8_t* mask,
+                      const double* pose_tab, const double* K, double* d_depth, double* pose_part,
+                      double* grad_out) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   static bool attr = false;
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_bwd_cells), bwd_cells_smem());
   attr = true;
   count_launch();
   k_bwd_cells<<<dim3(TP.oT, P.n_windows), kFwdThreads, bwd_cells_smem(), s>>>(
-      sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, no_surv,
+      sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
+      no_surv,
       depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
+}
+
+void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,
+                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const WinParams& P,
+                   const TileParams& TP, uint2* ranges) {
+  const size_t lists_n = (size_t)P.n_windows * (2 * P.B + 1) * TP.oT;
+  count_launch();
+  k_ranges<<<(unsigned)((lists_n * 32 + 255) / 256), 256, 0, s>>>(lcount, lists, tile_ptr, bin_ptr, P,
+                                                                  TP, ranges);
 }
 
 }  // namespace evcm_b200

@@ -57,14 +57,20 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
 void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
-                      const uint16_t* lists, double2* coef, double2* stack_out, double* part_acc,
-                      unsigned long long* part_act);
+                      const uint16_t* lists, const uint2* ranges, double2* coef, double2* stack_out,
+                      double* part_acc, unsigned long long* part_act);
 void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
-                      const uint32_t* lcount, const uint16_t* lists, const int* no_surv,
-                      const double* depth, const uint8_t* mask, const double* pose_tab,
-                      const double* K, double* d_depth, double* pose_part, double* grad_out);
+                      const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
+                      const int* no_surv, const double* depth, const uint8_t* mask,
+                      const double* pose_tab, const double* K, double* d_depth, double* pose_part,
+                      double* grad_out);
+// Per (window, slot, owner tile) list: precomputed candidate ranges (kListCapO + 2
+// uint2 entries; see cmax_cells.cu)
+void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,
+                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const WinParams& P,
+                   const TileParams& TP, uint2* ranges);
 
 }  // namespace evcm_b200

@@ -439,11 +439,13 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint16_t* lists = e->get<uint16_t>("lists", nl * kListCapO);
   launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, keys + total, e->max_n, flows,
                       total, recs, bbox, lcount, lists);
+  uint2* ranges = e->get<uint2>("ranges", nl * (kListCapO + 2));
+  launch_ranges(e->stream, lcount, lists, tile_ptr, e->get<uint32_t>("bin_ptr", 1), P, TP, ranges);
   e->mark(4);
   const size_t np = (size_t)nw * R * TP.oT;
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
   // fixed-point accumulation: bit-deterministic in both modes
-  launch_fwd_cells(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists,
+  launch_fwd_cells(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists, ranges,
                    e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
                    e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
   e->mark(5);
@@ -477,7 +479,8 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * 6) : nullptr;
   launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
-                   e->get<uint16_t>("lists", 1), e->get<int>("no_surv", 1), depth, mask, pose_tab,
+                   e->get<uint16_t>("lists", 1), e->get<uint2>("ranges", 1), e->get<int>("no_surv", 1),
+                   depth, mask, pose_tab,
                    K, depth ? d_depth : nullptr, pose_part, grad_out);
   e->mark(8);
   if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
