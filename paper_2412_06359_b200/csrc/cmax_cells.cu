@@ -50,7 +50,9 @@ namespace {
 constexpr int kThreads = 512;                      // 16 warps
 constexpr int kWarps = kThreads / 32;
 constexpr int kBatchCap = 3 * kListCapO;           // sort-tile ranges per batch
-constexpr int kRowW = kOwnW + 1;                   // padded accumulator row (bank spread)
+// accumulator row stride = 8 (mod 32): an 8 x 8 pixel block (the cells of one
+// sort tile's events, which share a warp) covers all 32 shared-memory banks
+constexpr int kRowW = kOwnW + 8;
 constexpr int kPlane = kOwnH * kRowW;              // words per accumulator plane
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk) --------------------------------
@@ -225,6 +227,35 @@ __device__ void next_batch(Batch& bt, const uint32_t* __restrict__ lcount,
   __syncwarp();
 }
 
+// Warp-level stream compaction: the warp scans slots [v0, n) 32 at a time with
+// stride kStride, `hit(v)` classifies slot v, and `work(v)` runs only on full
+// warps of hits (queued in the warp's 64-entry shared queue), so the heavy
+// corner path does not run at the density of the (about 50 %) hits.
+template <int kStride, typename Hit, typename Work>
+__device__ __forceinline__ void compacted(uint32_t v0, uint32_t n, uint16_t* q, Hit&& hit,
+                                          Work&& work) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int qn = 0;
+  for (uint32_t vb = v0; vb < n; vb += kStride) {
+    const uint32_t v = vb + lane;
+    const bool h = v < n && hit(v);
+    const unsigned bal = __ballot_sync(0xffffffffu, h);
+    if (h) q[qn + __popc(bal & lt)] = (uint16_t)v;
+    qn += __popc(bal);
+    __syncwarp();
+    if (qn >= 32) {
+      work((uint32_t)q[lane]);
+      __syncwarp();
+      if (lane < qn - 32) q[lane] = q[lane + 32];
+      qn -= 32;
+      __syncwarp();
+    }
+  }
+  if (lane < qn) work((uint32_t)q[lane]);
+  __syncwarp();
+}
+
 // Exact fixed-point accumulation into a (lo, hi) pair of 32-bit shared words at
 // shared-window addresses a_lo / a_hi: two native ATOMS.ADD, the first one's
 // return value giving the carry (add.cc / addc) into the second.
@@ -369,12 +400,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
   extern __shared__ __align__(16) unsigned char smem[];
   FwdRec* stage = reinterpret_cast<FwdRec*>(smem);                    // [2][kStageP]
   uint32_t* acc = reinterpret_cast<uint32_t*>(stage + 2 * kStageP);   // [pol][C, S][lo, hi][kPlane]
-  uint32_t* flag = acc + 8 * kPlane;                                  // [kPlane] some w > 0
+  uint32_t* flag = acc + 8 * kPlane;  // [kPlane] a w > 0 rounded to 0 in fixed point
   __shared__ Batch bt;
   __shared__ RoundDesc desc[2];
   __shared__ __align__(16) uint2 rv[2][kRgCap];    // prefetched ranges
   __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
   __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
+  __shared__ uint16_t wq[kWarps][64];  // per-warp compaction queues
   __shared__ double s_red[2][kWarps];
   __shared__ unsigned s_act[2][kWarps];
 
@@ -476,32 +508,39 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     const FwdRec* sb = stage + b * kStageP;
     const double esr = P.es[d.r], iwin = P.inv_window;
     // splat_bilinear corners (warp.hpp:147-160) as exact fixed-point sums
-    for (uint32_t v = ct; v < d.n; v += kCons) {
-      const FwdRec rec = sb[v];
-      const int lx = (int)(rec.cell & 0xffffu) - ox0, ly = (int)((rec.cell >> 16) & 0x7fffu) - oy0;
-      if (rec.cell == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) continue;
-      double wx, ax, wy, ay;
-      expand_frac(rec.fx, wx, ax);
-      expand_frac(rec.fy, wy, ay);
-      const double tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
-      // polarity_index plane set; corner weights pre-scaled by 2^50 (exact)
-      const uint32_t pa = acc_s + (rec.cell >> 31) * (4 * kPlane * 4);
-      const double sx0 = ax * 0x1p50, sx1 = wx * 0x1p50;
-      const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
-      const int o00 = ly * kRowW + lx;
+    compacted<kCons>(
+        (uint32_t)cw * 32, d.n, wq[cw],
+        [&](uint32_t v) {
+          const uint32_t cell = sb[v].cell;
+          const int lx = (int)(cell & 0xffffu) - ox0, ly = (int)((cell >> 16) & 0x7fffu) - oy0;
+          return cell != kDead && lx + ox >= 0 && lx < kOwnW && ly + oy >= 0 && ly < kOwnH;
+        },
+        [&](uint32_t v) {
+          const FwdRec rec = sb[v];
+          const int lx = (int)(rec.cell & 0xffffu) - ox0, ly = (int)((rec.cell >> 16) & 0x7fffu) - oy0;
+          double wx, ax, wy, ay;
+          expand_frac(rec.fx, wx, ax);
+          expand_frac(rec.fy, wy, ay);
+          const double tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
+          // polarity_index plane set; corner weights pre-scaled by 2^50 (exact)
+          const uint32_t pa = acc_s + (rec.cell >> 31) * (4 * kPlane * 4);
+          const double sx0 = ax * 0x1p50, sx1 = wx * 0x1p50;
+          const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
+          const int o00 = ly * kRowW + lx;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
-        const double wq = ((q & 1) ? sx1 : sx0) * ((q & 2) ? wy : ay);
-        if (in && wq > 0.0) {
-          const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
-          flag[o] = 1u;
-          const uint32_t a = pa + 4u * (uint32_t)o;
-          fx_add(a, a + 4 * kPlane, __double2ull_rn(wq));
-          fx_add(a + 8 * kPlane, a + 12 * kPlane, __double2ull_rn(wq * tb));
-        }
-      }
-    }
+          for (int q = 0; q < 4; ++q) {
+            const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
+            const double wqq = ((q & 1) ? sx1 : sx0) * ((q & 2) ? wy : ay);
+            if (in && wqq > 0.0) {
+              const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
+              const uint32_t a = pa + 4u * (uint32_t)o;
+              const unsigned long long qc = __double2ull_rn(wqq);
+              if (qc == 0ull) flag[o] = 1u;  // w > 0 below the fixed-point resolution
+              fx_add(a, a + 4 * kPlane, qc);
+              fx_add(a + 8 * kPlane, a + 12 * kPlane, __double2ull_rn(wqq * tb));
+            }
+          }
+        });
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);
     ++it;
@@ -522,7 +561,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         const double C1 = (double)fx_read(acc + 4 * kPlane + o, acc + 5 * kPlane + o) * 0x1p-50;
         const double S1 = (double)fx_read(acc + 6 * kPlane + o, acc + 7 * kPlane + o) * 0x1p-50;
         const int g = py * W + px;
-        actv = flag[o];
+        actv = (flag[o] || C0 > 0.0 || C1 > 0.0) ? 1u : 0u;  // refresh_active: some w > 0
         const double i0 = 1.0 / (C0 + kLossEps), i1 = 1.0 / (C1 + kLossEps);
         const double c0 = S0 * i0, c1 = S1 * i1;
         lsum = c0 * c0 + c1 * c1;
@@ -610,6 +649,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   __shared__ __align__(16) uint2 rv[2][2][kRgCap];   // prefetched ranges (reference, source)
   __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
   __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
+  __shared__ uint16_t wq[kWarps][64];  // per-warp compaction queues
   __shared__ double s_pose[2][kWarps][6];
 
   const int T = blockIdx.x, w = blockIdx.y;
@@ -788,6 +828,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   const int gq = py * W + px, op = lyp * kRowW + lxp;
   const double dpx = own_px && depth ? depth[(size_t)w * HW + gq] : 0.0;
   const bool dok = own_px && depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
+  // backproject(x, 1.0, k) (geometry.hpp:147-149), bin-independent
+  const double rx = 1.0 * ((double)px - cx) / fx, ry = 1.0 * ((double)py - cy) / fy;
   // fixed-point scale of this window's gradient terms: |w g| <= max|g| < 2^e
   int e2 = 0;
   frexp((double)__uint_as_float(gmax[w]), &e2);
@@ -803,35 +845,42 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
     // record sinks of reference d.r (slots < split)
-    for (uint32_t v = ct; v < d.split; v += kCons) {
-      if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
-      const uint4 rec = s16[v];
-      const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
-      if (rec.x == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) continue;
-      const float2 g = s8[v];
-      if (g.x == 0.f && g.y == 0.f) continue;
-      // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
-      const int j = bin_of(rec.y, P.erel, B);
-      const int bin = (d.r <= j) ? d.r - 1 : d.r;
-      const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
-      double wx, ax, wy, ay;
-      expand_frac(__uint_as_float(rec.z), wx, ax);
-      expand_frac(__uint_as_float(rec.w), wy, ay);
-      const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
-      const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
-      const int o00 = ly * kRowW + lx;
+    compacted<kCons>(
+        (uint32_t)cw * 32, d.split, wq[cw],
+        [&](uint32_t v) {
+          if ((fk[v >> 5] >> (v & 31)) & 1u) return false;
+          const uint32_t cell = s16[v].x;
+          const int lx = (int)(cell & 0xffffu) - ox0, ly = (int)((cell >> 16) & 0x7fffu) - oy0;
+          if (cell == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) return false;
+          const float2 g = s8[v];
+          return g.x != 0.f || g.y != 0.f;
+        },
+        [&](uint32_t v) {
+          const uint4 rec = s16[v];
+          const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
+          const float2 g = s8[v];
+          // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
+          const int j = bin_of(rec.y, P.erel, B);
+          const int bin = (d.r <= j) ? d.r - 1 : d.r;
+          const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
+          double wx, ax, wy, ay;
+          expand_frac(__uint_as_float(rec.z), wx, ax);
+          expand_frac(__uint_as_float(rec.w), wy, ay);
+          const double gx = (double)g.x * gsc, gy = (double)g.y * gsc;
+          const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
+          const int o00 = ly * kRowW + lx;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
-        const double wq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
-        if (in && wq != 0.0) {
-          const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
-          const uint32_t a = pt + 4u * (uint32_t)o;
-          fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wq * gx));
-          fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wq * gy));
-        }
-      }
-    }
+          for (int q = 0; q < 4; ++q) {
+            const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
+            const double wqq = ((q & 1) ? wx : ax) * ((q & 2) ? wy : ay);
+            if (in && wqq != 0.0) {
+              const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
+              const uint32_t a = pt + 4u * (uint32_t)o;
+              fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wqq * gx));
+              fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wqq * gy));
+            }
+          }
+        });
     // source-pixel sinks of bin d.r - 1 (slots >= split): weight 1 at the event's pixel
     {
       const uint32_t pt = acc_s + (uint32_t)((d.r - 1) & 1) * (4 * kPlane * 4);
@@ -869,8 +918,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
         }
         if (dok && (gu != 0.0 || gv != 0.0)) {
           const double* ptab = pose_tab + ((size_t)w * B + i) * kPoseTab;
-          const double rx = 1.0 * ((double)px - cx) / fx;  // backproject(x, 1.0, k)
-          const double ry = 1.0 * ((double)py - cy) / fy;
           const double rr0 = ptab[0] * rx + ptab[1] * ry + ptab[2];
           const double rr1 = ptab[3] * rx + ptab[4] * ry + ptab[5];
           const double rr2 = ptab[6] * rx + ptab[7] * ry + ptab[8];

@@ -122,10 +122,16 @@ __global__ void k_sort_colscan(uint32_t* __restrict__ counts, TileParams TP,
   if (t >= TP.nT) return;
   uint32_t* c = counts + (size_t)w * TP.nchunks * TP.nT + t;
   uint32_t run = 0;
-  for (int ch = 0; ch < TP.nchunks; ++ch) {
-    const uint32_t v = c[(size_t)ch * TP.nT];
-    c[(size_t)ch * TP.nT] = run;
-    run += v;
+  constexpr int U = 8;  // independent loads in flight per thread
+  for (int ch0 = 0; ch0 < TP.nchunks; ch0 += U) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ch0 + u < TP.nchunks ? c[(size_t)(ch0 + u) * TP.nT] : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ch0 + u < TP.nchunks) c[(size_t)(ch0 + u) * TP.nT] = run;
+      run += v[u];
+    }
   }
   totals[(size_t)w * TP.nT + t] = run;
 }
