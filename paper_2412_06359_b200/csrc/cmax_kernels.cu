@@ -187,42 +187,48 @@ void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B
 // K1: motion field (depth_pose_to_flows, geometry.hpp:229-264)
 
 // pose table per (window, bin): R[9], dR[27], t[3], inv_dt  -> 40 doubles
+// One thread per pixel, bins in a loop: the back-projection (two IEEE fp64
+// divisions) is bin-independent and computed once; same expressions as the
+// reference, so the flows stay bit-identical.
 __global__ void k_motion_field(const double* __restrict__ depth, const uint8_t* __restrict__ mask,
                                const double* __restrict__ pose_tab, WinParams P, double fx,
                                double fy, double cx, double cy, double2* __restrict__ flows,
                                uint8_t* __restrict__ valid) {
-  const int w = blockIdx.z, b = blockIdx.y;
-  const int HW = P.HW;
-  const double* pt = pose_tab + ((size_t)w * P.B + b) * kPoseTab;
-  const double* Rm = pt;
-  const double* tr = pt + 36;
-  const double inv_dt = pt[39];
+  const int w = blockIdx.y;
+  const int HW = P.HW, B = P.B;
   const double* dep = depth + (size_t)w * HW;
-  double2* out = flows + ((size_t)w * P.B + b) * HW;
-  uint8_t* vout = valid ? valid + ((size_t)w * P.B + b) * HW : nullptr;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < HW; q += gridDim.x * blockDim.x) {
-    double2 f = make_double2(0.0, 0.0);
-    uint8_t ok = 0;
     const double d = dep[q];
-    if ((!mask || mask[(size_t)w * HW + q]) && d > 0.0) {
-      const int y = q / P.W, x = q - y * P.W;
-      // backproject (geometry.hpp:147-149)
-      const double bx = dd(dm(d, ds((double)x, cx)), fx);
-      const double by = dd(dm(d, ds((double)y, cy)), fy);
-      const double bz = d;
-      // rot * v + trans (geometry.hpp:77-81, 159)
-      const double px = da(da(da(dm(Rm[0], bx), dm(Rm[1], by)), dm(Rm[2], bz)), tr[0]);
-      const double py = da(da(da(dm(Rm[3], bx), dm(Rm[4], by)), dm(Rm[5], bz)), tr[1]);
-      const double pz = da(da(da(dm(Rm[6], bx), dm(Rm[7], by)), dm(Rm[8], bz)), tr[2]);
-      if (pz > 0.0) {
-        const double ux = da(dd(dm(fx, px), pz), cx);
-        const double uy = da(dd(dm(fy, py), pz), cy);
-        f = make_double2(dm(ds(ux, (double)x), inv_dt), dm(ds(uy, (double)y), inv_dt));
-        ok = 1;
-      }
+    const bool dv = (!mask || mask[(size_t)w * HW + q]) && d > 0.0;
+    const int y = q / P.W, x = q - y * P.W;
+    double bx = 0.0, by = 0.0;
+    if (dv) {  // backproject (geometry.hpp:147-149)
+      bx = dd(dm(d, ds((double)x, cx)), fx);
+      by = dd(dm(d, ds((double)y, cy)), fy);
     }
-    out[q] = f;
-    if (vout) vout[q] = ok;
+    const double bz = d;
+    for (int b = 0; b < B; ++b) {
+      const double* pt = pose_tab + ((size_t)w * B + b) * kPoseTab;
+      double2 f = make_double2(0.0, 0.0);
+      uint8_t ok = 0;
+      if (dv) {
+        const double* Rm = pt;
+        const double* tr = pt + 36;
+        // rot * v + trans (geometry.hpp:77-81, 159)
+        const double px = da(da(da(dm(Rm[0], bx), dm(Rm[1], by)), dm(Rm[2], bz)), tr[0]);
+        const double py = da(da(da(dm(Rm[3], bx), dm(Rm[4], by)), dm(Rm[5], bz)), tr[1]);
+        const double pz = da(da(da(dm(Rm[6], bx), dm(Rm[7], by)), dm(Rm[8], bz)), tr[2]);
+        if (pz > 0.0) {
+          const double inv_dt = pt[39];
+          const double ux = da(dd(dm(fx, px), pz), cx);
+          const double uy = da(dd(dm(fy, py), pz), cy);
+          f = make_double2(dm(ds(ux, (double)x), inv_dt), dm(ds(uy, (double)y), inv_dt));
+          ok = 1;
+        }
+      }
+      flows[((size_t)w * B + b) * HW + q] = f;
+      if (valid) valid[((size_t)w * B + b) * HW + q] = ok;
+    }
   }
 }
 
@@ -680,10 +686,10 @@ void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, do
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,
                          double2* flows, uint8_t* valid) {
-  const int bx = std::min((P.HW + 255) / 256, 148);
+  const int bx = (P.HW + 255) / 256;
   ++g_launches;
-  k_motion_field<<<dim3(bx, P.B, P.n_windows), 256, 0, s>>>(depth, mask, pose_tab, P, K[0], K[1],
-                                                           K[2], K[3], flows, valid);
+  k_motion_field<<<dim3(bx, P.n_windows), 256, 0, s>>>(depth, mask, pose_tab, P, K[0], K[1], K[2],
+                                                      K[3], flows, valid);
 }
 
 template <typename S2>

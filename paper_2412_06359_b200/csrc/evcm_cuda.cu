@@ -307,10 +307,10 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
   e->n_total = (total + 1) & ~1ull;  // even plane stride (16 B-aligned 8 B sub-arrays)
   e->max_n = max_n;
-  // algo auto: the owner pipeline wins once there are >= ~2 events per pixel and
-  // per window (measured crossover); deterministic mode needs it.
+  // algo auto: the owner pipeline (deterministic, fixed-point) ties the atomic one
+  // at ~1 event per pixel and window and wins above (measured)
   if (e->opt.algo == 2)
-    e->use_owner = e->opt.deterministic || (double)total >= 2.0 * (double)P.HW * nw;
+    e->use_owner = e->opt.deterministic || (double)total >= 1.0 * (double)P.HW * nw;
   else
     e->use_owner = e->opt.algo == 0 || e->opt.deterministic;
   if (e->owner()) {
