@@ -44,6 +44,20 @@ WORKLOADS = {
 HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
+def measured_traffic(workload, kernel, world):
+    """DRAM bytes (read + write) per launch of `kernel` from one committed
+    `ncu --set full` capture of this workload on 1 GPU (profiles/traffic.json);
+    None when not captured (or for N > 1, where per-GPU work is the same but the
+    capture was not repeated)."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -353,8 +367,8 @@ def cuda_arm(args, wl):
     achieved = per_kernel[dom] / (kern[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "algorithmic_bytes_per_launch": per_kernel[dom],
-                "launch_ms": kern[dom]}
+                "traffic": measured_traffic(args.workload, dom, world),
+                "algorithmic_bytes_per_launch": per_kernel[dom], "launch_ms": kern[dom]}
     step_roofline = {"algorithmic_bytes_per_step": total_bytes,
                      "achieved_GBps": total_bytes / (ms_per_step * 1e-3) / 1e9,
                      "frac": total_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
