@@ -14,13 +14,17 @@
 // BIT-IDENTICAL whatever the order of the atomics: the fast mode is
 // deterministic.
 //
-// Precision: the IWE weights w and w*tb lie in [0, 1] and use k = 50 (2^-51
-// absolute rounding per term; per-pixel sums below 2^14 per window, reference
-// and polarity). The reference's sensitive quantity is the splat_position_grad
-// factor a*inv*(tb - a), largest where C ~ eps = 1e-9; there a term's relative
-// error is ~2^-51 / 1e-9 ~ 4e-7. Gradient terms w*g use k = 49 - e with
-// 2^e > max|g| of the window (k_bwd_event). n_active is exact: a pixel is
-// active iff some contribution has w > 0, recorded as a flag.
+// Precision: the IWE weights w and w*tb lie in [0, 1] and use k = 50 fraction
+// bits (2^-51 absolute rounding per term) whenever the reference's candidate
+// count T of the owner tile is below 2^13 (T bounds every pixel's weight sum);
+// denser tiles get k = 63 - bits(T), so the sums can never wrap. The
+// reference's sensitive quantity is the splat_position_grad factor
+// a*inv*(tb - a), largest where C ~ eps = 1e-9; there a term's relative error
+// is ~2^-51 / 1e-9 ~ 4e-7. Gradient terms w*g use k = kbits - e with
+// 2^e > max|g| of the window (k_bwd_event) and kbits <= 49 chosen from the
+// largest candidate count of the CTA's groups. n_active is exact: a pixel is
+// active iff some contribution has w > 0 (weights below the fixed-point
+// resolution are flagged).
 //
 // Candidates: warp 0 stages every record range of the owner tile (a sort tile's
 // events at this reference) into shared memory with one cp.async.bulk (TMA bulk
@@ -272,6 +276,9 @@ __device__ __forceinline__ void fx_add(uint32_t a_lo, uint32_t a_hi, unsigned lo
       "r"(a_hi), "l"(q)
       : "memory");
 }
+// bits needed to count t: fixed-point sums of t terms bounded by 2^k need k + bits
+__device__ __forceinline__ int bits_for(uint32_t t) { return 32 - __clz(t); }
+
 __device__ __forceinline__ unsigned long long fx_read(const uint32_t* plo, const uint32_t* phi) {
   return ((unsigned long long)*phi << 32) | *plo;
 }
@@ -388,6 +395,7 @@ struct RoundDesc {
   uint32_t n;  // staged candidates
   int r;       // reference
   int last;    // last round of this reference
+  int fb;      // fraction bits of this reference's sums (<= 50, see below)
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
@@ -444,8 +452,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     };
     uint32_t it = 0;
     // stage the rounds of one view; `final`: its last round ends reference r
-    auto rounds = [&](const Cat& cv, int r, bool final) {
+    // fraction bits: a pixel's weight sum is bounded by the reference's candidate
+    // count T (each record adds w <= 1), so T * 2^fb < 2^64 with fb <= 50
+    const uint32_t nw_events = (uint32_t)(ev_off[w + 1] - base);
+    auto rounds = [&](const Cat& cv, int r, bool final, uint32_t tbound) {
       const FwdRec* rr = recs + (size_t)r * n_total + base;
+      const int fbits = min(50, 63 - bits_for(tbound));
       const int nl = cv.nl();
       const uint32_t total = cv.total();
       for (uint32_t rb = 0; rb < total || (rb == 0 && final); rb += kStageP) {
@@ -457,6 +469,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
           desc[b].n = n;
           desc[b].r = r;
           desc[b].last = (final && rb + kStageP >= total) ? 1 : 0;
+          desc[b].fb = fbits;
         }
         fence_proxy_async();
         __syncwarp();
@@ -478,7 +491,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
       mbar_wait(&rbar[r & 1], (r >> 1) & 1);
       const uint2* v = rv[r & 1];
       if (v[0].x != kOverflow) {
-        rounds(make_cat(v, nullptr), r, true);
+        rounds(make_cat(v, nullptr), r, true, v[0].y);
       } else {  // overflowed list: scan the sort-tile boxes batch by batch
         const size_t ws = (size_t)w * NS + r;
         if (lane == 0) bt.seg = -1;
@@ -490,7 +503,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
                         [&](int, int S) { return make_uint2(tp[S], tp[S + 1]); });
           more = bt.more;
           batch_to_view(bt, fb);
-          rounds(make_cat(fb, nullptr), r, !more);
+          rounds(make_cat(fb, nullptr), r, !more, nw_events);  // total unknown: window bound
         }
       }
     }
@@ -507,6 +520,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     const RoundDesc d = desc[b];
     const FwdRec* sb = stage + b * kStageP;
     const double esr = P.es[d.r], iwin = P.inv_window;
+    const double fsc = ldexp(1.0, d.fb);  // 2^fb, exact scaling
     // splat_bilinear corners (warp.hpp:147-160) as exact fixed-point sums
     compacted<kCons>(
         (uint32_t)cw * 32, d.n, wq[cw],
@@ -522,9 +536,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
           expand_frac(rec.fx, wx, ax);
           expand_frac(rec.fy, wy, ay);
           const double tb = fabs(dm((double)rec.dt, 1e-6) - esr) * iwin;  // engine.hpp:370
-          // polarity_index plane set; corner weights pre-scaled by 2^50 (exact)
+          // polarity_index plane set; corner weights pre-scaled by 2^fb (exact)
           const uint32_t pa = acc_s + (rec.cell >> 31) * (4 * kPlane * 4);
-          const double sx0 = ax * 0x1p50, sx1 = wx * 0x1p50;
+          const double sx0 = ax * fsc, sx1 = wx * fsc;
           const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
           const int o00 = ly * kRowW + lx;
 #pragma unroll
@@ -556,10 +570,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
       const int px = ox0 + lx, py = oy0 + ly;
       const int o = ly * kRowW + lx;
       if (px < W && py < H) {
-        const double C0 = (double)fx_read(acc + o, acc + kPlane + o) * 0x1p-50;
-        const double S0 = (double)fx_read(acc + 2 * kPlane + o, acc + 3 * kPlane + o) * 0x1p-50;
-        const double C1 = (double)fx_read(acc + 4 * kPlane + o, acc + 5 * kPlane + o) * 0x1p-50;
-        const double S1 = (double)fx_read(acc + 6 * kPlane + o, acc + 7 * kPlane + o) * 0x1p-50;
+        const double ifs = 1.0 / fsc;  // 2^-fb
+        const double C0 = (double)fx_read(acc + o, acc + kPlane + o) * ifs;
+        const double S0 = (double)fx_read(acc + 2 * kPlane + o, acc + 3 * kPlane + o) * ifs;
+        const double C1 = (double)fx_read(acc + 4 * kPlane + o, acc + 5 * kPlane + o) * ifs;
+        const double S1 = (double)fx_read(acc + 6 * kPlane + o, acc + 7 * kPlane + o) * ifs;
         const int g = py * W + px;
         actv = (flag[o] || C0 > 0.0 || C1 > 0.0) ? 1u : 0u;  // refresh_active: some w > 0
         const double i0 = 1.0 / (C0 + kLossEps), i1 = 1.0 / (C1 + kLossEps);
@@ -650,6 +665,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
   __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
   __shared__ uint16_t wq[kWarps][64];  // per-warp compaction queues
+  __shared__ int s_kbits;              // fixed-point magnitude bits of the gradient terms
   __shared__ double s_pose[2][kWarps][6];
 
   const int T = blockIdx.x, w = blockIdx.y;
@@ -794,6 +810,20 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
         rounds(kind == 0 ? make_cat(fb, nullptr) : make_cat(nullptr, fb), g, final && !more);
       }
     };
+    // fixed-point headroom: a bin tile sums terms of two groups; bound every
+    // group's candidate count (overflowed lists: the window's event count)
+    {
+      const uint32_t nwe = (uint32_t)(ev_off[w + 1] - base);
+      uint32_t tmax = 0;
+      for (int l = lane; l < 2 * B - 1; l += 32) {
+        const int slot = l < B - 1 ? l + 1 : R + (l - (B - 1));
+        const uint2 e0 = ranges[(((size_t)w * NS + slot) * TP.oT + T) * kRgCap];
+        tmax = max(tmax, e0.x == kOverflow ? nwe : e0.y);
+      }
+      for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(kFull, tmax, o));
+      if (lane == 0) s_kbits = min(49, 63 - bits_for(2u * min(tmax, 0x7fffffffu)));
+      __syncwarp();
+    }
     if (run) {
       prefetch(1);
       for (int g = 1; g <= B; ++g) {
@@ -830,15 +860,20 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   const bool dok = own_px && depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
   // backproject(x, 1.0, k) (geometry.hpp:147-149), bin-independent
   const double rx = 1.0 * ((double)px - cx) / fx, ry = 1.0 * ((double)py - cy) / fy;
-  // fixed-point scale of this window's gradient terms: |w g| <= max|g| < 2^e
+  // fixed-point scale of this window's gradient terms: |w g| <= max|g| < 2^e,
+  // scaled to 2^kbits (s_kbits is written by the producer before its first round)
   int e2 = 0;
   frexp((double)__uint_as_float(gmax[w]), &e2);
-  const double gsc = ldexp(1.0, 49 - e2), igsc = ldexp(1.0, e2 - 49);
+  double gsc = 0.0, igsc = 0.0;
   double dd = 0.0;  // d_depth of this pixel, bins summed in order
   uint32_t it = 0;
   for (int done = 0; done < B;) {
     const int b = it & 1;
     mbar_wait(&full[b], (it >> 1) & 1);
+    if (it == 0) {
+      gsc = ldexp(1.0, s_kbits - e2);
+      igsc = ldexp(1.0, e2 - s_kbits);
+    }
     const BRound d = desc[b];
     const uint4* s16 = stage16 + b * kStageQ;
     const float2* s8 = stage8 + b * kStageQ;

@@ -191,3 +191,27 @@ def test_repeatability(engine):
     gb = engine.backward(_slice(w), _flows(w), b).grad
     assert abs(la - b.loss.value) <= 1e-9 * abs(la)
     assert rel_inf(ga, gb) <= 1e-6
+
+
+def test_hot_pixel_dense(engine):
+    """A hot pixel: 20k events on one pixel (plus a sparse background) under a
+    small smooth flow, so one pixel's per-reference weight sum exceeds 2^14 --
+    the fixed-point accumulators must choose their headroom from the candidate
+    count (cmax_cells.cu) and still match the oracle."""
+    rng = np.random.default_rng(5)
+    W, H, B = 64, 48, 4
+    n_hot, n_bg = 20000, 3000
+    t = np.sort(rng.integers(0, 100000, n_hot + n_bg))
+    x = np.concatenate([np.full(n_hot, 20), rng.integers(0, W, n_bg)])
+    y = np.concatenate([np.full(n_hot, 30), rng.integers(0, H, n_bg)])
+    perm = rng.permutation(n_hot + n_bg)
+    ev = O.make_events(t, x[perm], y[perm], np.where(rng.random(n_hot + n_bg) < 0.5, 1, -1))
+    xs, ys = np.arange(W)[None, :], np.arange(H)[:, None]
+    uv = np.zeros((B, 2, H, W))
+    for b in range(B):
+        uv[b, 0] = 0.5 * np.sin(0.1 * xs + b) + 0 * ys
+        uv[b, 1] = 0.5 * np.cos(0.1 * ys - b) + 0 * xs
+    uv = uv.astype(np.float32).astype(np.float64)
+    w = O.Window(W, H, O.make_edges(0, 100000, B), ev, uv)
+    fwd, *_ = _check(engine, w)
+    assert fwd.stack.count.max() > 2 ** 14
