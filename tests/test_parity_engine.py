@@ -204,8 +204,9 @@ def test_hot_pixel_dense(engine):
     t = np.sort(rng.integers(0, 100000, n_hot + n_bg))
     x = np.concatenate([np.full(n_hot, 20), rng.integers(0, W, n_bg)])
     y = np.concatenate([np.full(n_hot, 30), rng.integers(0, H, n_bg)])
+    pol = np.concatenate([np.ones(n_hot, int), np.where(rng.random(n_bg) < 0.5, 1, -1)])
     perm = rng.permutation(n_hot + n_bg)
-    ev = O.make_events(t, x[perm], y[perm], np.where(rng.random(n_hot + n_bg) < 0.5, 1, -1))
+    ev = O.make_events(t, x[perm], y[perm], pol[perm])
     xs, ys = np.arange(W)[None, :], np.arange(H)[:, None]
     uv = np.zeros((B, 2, H, W))
     for b in range(B):
