@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
   const double em = es[(B + 1) / 2];
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
-  const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
-  const uint64_t c1 = c0 + kChunk < n ? c0 + kChunk : n;
+  const uint64_t c0 = (uint64_t)blockIdx.x * TP.chunk;
+  const uint64_t c1 = c0 + TP.chunk < n ? c0 + TP.chunk : n;
   const double2* fl = flows + (size_t)w * B * HW;
   for (uint64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
     const uint2 e = packed[base + k];
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_sort_tilescan(const uint32_t* __restri
   if (threadIdx.x == 0) tp[TP.nT] = s_carry;
 }
 
-// Stable scatter: warp `wid` of chunk c owns events [c*kChunk + wid*kChunk/nW, ...);
+// Stable scatter: warp `wid` of chunk c owns events [c*chunk + wid*chunk/nW, ...);
 // per-warp tile counts (u16) give each warp its base inside the chunk's run of
 // the tile, so the output keeps the input (time) order inside every tile.
 __global__ void __launch_bounds__(kScatterThreads) k_sort_scatter(
@@ -186,13 +186,13 @@ __global__ void __launch_bounds__(kScatterThreads) k_sort_scatter(
     uint32_t* __restrict__ sorted_keys) {
   extern __shared__ uint16_t whist[];  // [nW warps][nT]
   constexpr int nW = kScatterThreads / 32;
-  constexpr int per = kChunk / nW;
+  const int per = TP.chunk / nW;
   for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
   __syncthreads();
   const int w = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
-  const uint64_t k0 = (uint64_t)blockIdx.x * kChunk + (uint64_t)wid * per;
+  const uint64_t k0 = (uint64_t)blockIdx.x * TP.chunk + (uint64_t)wid * per;
   uint16_t* mine = whist + wid * TP.nT;
   for (int b = 0; b < per; b += 32) {  // pass 1: per-warp counts
     const uint64_t k = k0 + b + lane;
@@ -484,7 +484,14 @@ TileParams make_tiles(const WinParams& P, uint64_t max_n) {
   TP.otx = (P.W + kOwnW - 1) / kOwnW;
   TP.oty = (P.H + kOwnH - 1) / kOwnH;
   TP.oT = TP.otx * TP.oty;
-  TP.nchunks = (int)std::max<uint64_t>(1, (max_n + kChunk - 1) / kChunk);
+  // chunk size: the largest power of two <= kChunk that still gives the sort
+  // kernels >= 4 CTAs per SM over the batch (small batches, e.g. config B)
+  int chunk = kChunk;
+  while (chunk > 1024 &&
+         (double)((max_n + chunk - 1) / chunk) * P.n_windows < 4.0 * 148.0)
+    chunk /= 2;
+  TP.chunk = chunk;
+  TP.nchunks = (int)std::max<uint64_t>(1, (max_n + chunk - 1) / chunk);
   return TP;
 }
 

@@ -13,7 +13,7 @@ namespace evcm_b200 {
 constexpr int kSortTile = 8;       // sort tiles: 8x8 px of the position at the middle reference
 constexpr int kOwnW = 32;          // owner tiles: 32x16 px of the IWE stack / gradient planes
 constexpr int kOwnH = 16;
-constexpr int kChunk = 8192;       // events per sort chunk (one CTA)
+constexpr int kChunk = 8192;       // max events per sort chunk (one CTA); TileParams.chunk adapts
 constexpr int kSortThreads = 512;  // key/histogram CTA size
 constexpr int kScatterThreads = 256;  // 8 warps x 1024 events per scatter chunk
 constexpr int kMaxTiles = 12000;   // sort scatter keeps 8 x nT u16 counters in smem
@@ -23,6 +23,7 @@ struct TileParams {
   int ntx, nty, nT;  // sort tiles
   int otx, oty, oT;  // owner tiles
   int nchunks;       // sort chunks per window (max over the batch)
+  int chunk;         // events per sort chunk: 1024..kChunk, enough CTAs for the batch
 };
 
 // Per (event, reference) splat record, 16 B. cell = x0 | y0 << 16 | negative

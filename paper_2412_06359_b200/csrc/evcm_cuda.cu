@@ -319,7 +319,7 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
     if (TP.nT > kMaxTiles)
       fail(EVCM_ERR_CONFIG, "cuda backend: sensor too large (more than " +
                                 std::to_string(kMaxTiles) + " 8x8 sort tiles)");
-    if (max_n > 0xffff * (uint64_t)kChunk)
+    if ((uint64_t)TP.nchunks > 0xffffu)
       fail(EVCM_ERR_CONFIG, "cuda backend: too many events in one window");
     e->TP = TP;
     launch_stage_pack(e->stream, dev, off_d, P, max_n, packed, err);
