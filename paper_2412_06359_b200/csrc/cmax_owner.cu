@@ -68,14 +68,30 @@ __global__ void __launch_bounds__(kSortThreads) k_stage_pack(
   }
 }
 
+// Coarse flow map for the sort key: the flow of every bin sampled at the
+// centre pixel of every 8x8 sort tile, [w][B][nT] (768 KB per 640x480 window:
+// L2-resident, unlike per-event gathers from the full flow planes).
+__global__ void k_coarse_flow(const double2* __restrict__ flows, WinParams P, TileParams TP,
+                              double2* __restrict__ coarse) {
+  const size_t total = (size_t)P.n_windows * P.B * TP.nT;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int S = (int)(i % TP.nT);
+    const size_t wb = i / TP.nT;  // w * B + b
+    const int cx = min((S % TP.ntx) * kSortTile + kSortTile / 2, P.W - 1);
+    const int cy = min((S / TP.ntx) * kSortTile + kSortTile / 2, P.H - 1);
+    coarse[i] = flows[wb * P.HW + (size_t)cy * P.W + cx];
+  }
+}
+
 // Sort key: 8x8 tile of the event's approximate position at the middle
-// reference rm = (B+1)/2, extrapolated with the flow of its own bin at its own
-// (integer) pixel: x0 + u_j(x0) * (e_rm - t). One 16 B load per event; any
-// deterministic key is valid, this one keeps every tile compact at every ref.
+// reference rm = (B+1)/2, extrapolated with the coarse flow of its own bin at
+// its own tile: x0 + u_j(tile(x0)) * (e_rm - t). Any deterministic key is valid;
+// this one keeps every tile compact at every reference.
 // counts layout: [w][chunk][tile] (coalesced writes and column scans).
 __global__ void __launch_bounds__(kSortThreads) k_key_hist(
     const uint2* __restrict__ packed, const uint64_t* __restrict__ ev_off, WinParams P,
-    TileParams TP, const double2* __restrict__ flows, uint32_t* __restrict__ keys,
+    TileParams TP, const double2* __restrict__ coarse, uint32_t* __restrict__ keys,
     uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t hist[];
   __shared__ double es[kMaxRefs];
@@ -86,13 +102,13 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
     erel[i] = P.erel[i];
   }
   __syncthreads();
-  const int w = blockIdx.y, HW = P.HW, B = P.B;
+  const int w = blockIdx.y, B = P.B;
   const double em = es[(B + 1) / 2];
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
   const uint64_t c0 = (uint64_t)blockIdx.x * TP.chunk;
   const uint64_t c1 = c0 + TP.chunk < n ? c0 + TP.chunk : n;
-  const double2* fl = flows + (size_t)w * B * HW;
+  const double2* cf = coarse + (size_t)w * B * TP.nT;
   for (uint64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
     const uint2 e = packed[base + k];
     if (e.y == kDead) {
@@ -102,7 +118,7 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
     const uint32_t dtu = ev_dt(e);
     const int j = bin_of(dtu, erel, B);
     const int x0 = ev_x(e), y0 = ev_y(e);
-    const double2 u = __ldg(fl + (size_t)j * HW + y0 * P.W + x0);
+    const double2 u = __ldg(cf + (size_t)j * TP.nT + (y0 / kSortTile) * TP.ntx + x0 / kSortTile);
     const double dt = em - (double)dtu * 1e-6;
     const uint32_t key = (uint32_t)sort_tile_of(x0 + u.x * dt, y0 + u.y * dt, P, TP);
     keys[base + k] = key;
@@ -520,8 +536,11 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   set_smem(reinterpret_cast<const void*>(k_sort_scatter), sc_smem, &a2);
   const dim3 grid(TP.nchunks, P.n_windows);
   uint32_t* totals = keys + 2 * n_total;  // nw * nT scratch after the two key arrays
+  double2* coarse = reinterpret_cast<double2*>(totals + (((size_t)P.n_windows * TP.nT + 3) & ~(size_t)3));
   count_launch();
-  k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, flows,
+  k_coarse_flow<<<148 * 4, 256, 0, s>>>(flows, P, TP, coarse);
+  count_launch();
+  k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, coarse,
                                                                   keys, counts);
   count_launch();
   k_sort_colscan<<<dim3((TP.nT + 255) / 256, P.n_windows), 256, 0, s>>>(counts, TP, totals);

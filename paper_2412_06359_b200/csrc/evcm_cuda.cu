@@ -425,7 +425,9 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   uint2* sorted = e->get<uint2>("sorted", total);
   uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", (size_t)nw * (TP.nT + 1));
   e->mark(2);
-  uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total + (size_t)nw * TP.nT);
+  // keys: unsorted + sorted keys, per-tile totals, then the coarse flow map (double2)
+  uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total + (((size_t)nw * TP.nT + 3) & ~(size_t)3) +
+                                                     (size_t)nw * P.B * TP.nT * 4);
   launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
               e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
               nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
