@@ -635,6 +635,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
 // of one candidate; the slack slots of every region are flagged in a bitmask.
 
 constexpr int kStageQ = 1536;  // slots per buffer
+constexpr int kBufQ = 2;       // staging buffers (pipeline depth)
+constexpr int kBwdThreads = kCons + 64;  // two producer warps
 
 struct BRound {
   uint32_t n;      // slots
@@ -643,7 +645,7 @@ struct BRound {
   int last;        // last round of the group: bin r - 1 is complete
 };
 
-__global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
+__global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
     const FwdRec* __restrict__ recs, const float2* __restrict__ vals, uint64_t n_total,
@@ -654,16 +656,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
     double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint4* stage16 = reinterpret_cast<uint4*>(smem);                     // [2][kStageQ] records
-  float2* stage8 = reinterpret_cast<float2*>(stage16 + 2 * kStageQ);   // [2][kStageQ] values
-  uint32_t* acc = reinterpret_cast<uint32_t*>(stage8 + 2 * kStageQ);   // [tile][gu, gv][lo, hi][kPlane]
+  uint4* stage16 = reinterpret_cast<uint4*>(smem);                          // [kBufQ][kStageQ] records
+  float2* stage8 = reinterpret_cast<float2*>(stage16 + kBufQ * kStageQ);    // [kBufQ][kStageQ] values
+  uint32_t* acc = reinterpret_cast<uint32_t*>(stage8 + kBufQ * kStageQ);   // [tile][gu, gv][lo, hi][kPlane]
   __shared__ Batch bt;
-  __shared__ BRound desc[2];
-  __shared__ uint32_t roff[2 * kListCapO + 1 > kBatchCap ? 2 * kListCapO + 1 : kBatchCap];
-  __shared__ uint32_t fake[2][kStageQ / 32];  // slack slots of the staged round
+  __shared__ BRound desc[kBufQ];
+  __shared__ uint32_t roffs[2][2 * kListCapO + 1 > kBatchCap ? 2 * kListCapO + 1 : kBatchCap];
+  __shared__ uint32_t s_it;  // round counter hand-off after an overflowed group
+  __shared__ uint32_t fake[kBufQ][kStageQ / 32];  // slack slots of the staged round
   __shared__ __align__(16) uint2 rv[2][2][kRgCap];   // prefetched ranges (reference, source)
   __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
-  __shared__ __align__(8) uint64_t full[2], empty[2], rbar[2];
+  __shared__ __align__(8) uint64_t full[kBufQ], empty[kBufQ], rbar[2];
   __shared__ uint16_t wq[kWarps][64];  // per-warp compaction queues
   __shared__ int s_kbits;              // fixed-point magnitude bits of the gradient terms
   __shared__ double s_pose[2][kWarps][6];
@@ -678,24 +681,29 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool run = !no_surv[w];
 
-  for (int i = tid; i < 8 * kPlane; i += kFwdThreads) acc[i] = 0u;
+  for (int i = tid; i < 8 * kPlane; i += kBwdThreads) acc[i] = 0u;
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], kWarps);
-    mbar_init(&empty[1], kWarps);
+    for (int q = 0; q < kBufQ; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kWarps);
+    }
     mbar_init(&rbar[0], 1);
     mbar_init(&rbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (wid == 0) {
-    // ---------------- producer ----------------
+  if (wid < 2) {
+    // ---------------- producers ----------------
+    // two producer warps: warp pw stages the rounds of parity pw (the
+    // round sequence is a pure function of the prefetched ranges, so both walk
+    // it in lockstep); an overflowed list is staged by warp 0 alone.
+    const int pw = wid;
+    auto pair_sync = [] { asm volatile("bar.sync 2, 64;" ::: "memory"); };
     // group g = 1..B: the record sinks of reference g (g < B, list slot g) then
     // the source-pixel sinks of bin g - 1 (list slot R + g - 1); after group g
     // bin g - 1 is complete. Ranges are prefetched one group ahead.
-    auto prefetch = [&](int g) {
+    auto prefetch = [&](int g) {  // warp 0 only
       const size_t gref = ((size_t)w * NS + g) * TP.oT + T;
       const size_t gsrc = ((size_t)w * NS + R + g - 1) * TP.oT + T;
       fence_proxy_async();
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
       }
     };
     uint32_t it = 0;
-    auto rounds = [&](const Cat& cv, int g, bool final) {
+    auto rounds = [&](const Cat& cv, int g, bool final, bool all) {
       const FwdRec* rr = recs + (size_t)min(g, B) * n_total + base;
       const float2* v0 = vals + (size_t)(g - 1) * n_total;  // sinks at reference g
       const float2* v1 = vals + (size_t)(B - 1) * n_total;  // source-pixel sinks
@@ -717,8 +725,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
       // virtual candidates per round, leaving room for <= 3 slack slots per range
       const uint32_t capv = kStageQ - 3u * (uint32_t)nl;
       for (uint32_t rb = 0; rb < total || (rb == 0 && final); rb += capv) {
-        const int b = it & 1;
-        if (it >= 2) mbar_wait(&empty[b], ((it >> 1) - 1) & 1);
+        const int b = (int)(it % kBufQ);
+        if (!all && (int)(it & 1) != pw) {  // the other producer's round
+          ++it;
+          if (total == 0) break;
+          continue;
+        }
+        if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
+        uint32_t* const roff = roffs[pw];
         uint4* s16 = stage16 + b * kStageQ;
         float2* s8 = stage8 + b * kStageQ;
         // kind 1 packed events: upper half of the record buffer (slot v at byte
@@ -807,12 +821,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
                       });
         more = bt.more;
         batch_to_view(bt, fb);
-        rounds(kind == 0 ? make_cat(fb, nullptr) : make_cat(nullptr, fb), g, final && !more);
+        rounds(kind == 0 ? make_cat(fb, nullptr) : make_cat(nullptr, fb), g, final && !more, true);
       }
     };
     // fixed-point headroom: a bin tile sums terms of two groups; bound every
     // group's candidate count (overflowed lists: the window's event count)
-    {
+    if (pw == 0) {
       const uint32_t nwe = (uint32_t)(ev_off[w + 1] - base);
       uint32_t tmax = 0;
       for (int l = lane; l < 2 * B - 1; l += 32) {
@@ -825,32 +839,38 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
       __syncwarp();
     }
     if (run) {
-      prefetch(1);
+      if (pw == 0) prefetch(1);
       for (int g = 1; g <= B; ++g) {
-        if (g + 1 <= B) prefetch(g + 1);
+        pair_sync();  // both producers are done with the ranges of group g - 1
+        if (pw == 0 && g + 1 <= B) prefetch(g + 1);
         mbar_wait(&rbar[g & 1], ((g - 1) >> 1) & 1);
         const uint2* va = g < B ? rv[g & 1][0] : nullptr;
         const uint2* vb = rv[g & 1][1];
         const bool oa = va && va[0].x == kOverflow, ob = vb[0].x == kOverflow;
         if (!oa && !ob) {
-          rounds(make_cat(va, vb), g, true);
+          rounds(make_cat(va, vb), g, true, false);
         } else {
-          if (va) {
-            if (oa) scan_rounds(0, g, false);
-            else rounds(make_cat(va, nullptr), g, false);
+          if (pw == 0) {
+            if (va) {
+              if (oa) scan_rounds(0, g, false);
+              else rounds(make_cat(va, nullptr), g, false, true);
+            }
+            if (ob) scan_rounds(1, g, true);
+            else rounds(make_cat(nullptr, vb), g, true, true);
+            if (lane == 0) s_it = it;
           }
-          if (ob) scan_rounds(1, g, true);
-          else rounds(make_cat(nullptr, vb), g, true);
+          pair_sync();
+          it = s_it;
         }
       }
     } else {  // no survivors: every bin is zero, still finish each one
-      for (int g = 1; g <= B; ++g) rounds(make_cat(nullptr, nullptr), g, true);
+      for (int g = 1; g <= B; ++g) rounds(make_cat(nullptr, nullptr), g, true, false);
     }
     return;
   }
 
   // ---------------- consumers ----------------
-  const int ct = tid - 32, cw = wid - 1;
+  const int ct = tid - 64, cw = wid - 2;
   const uint32_t acc_s = smem_u32(acc);
   const int lxp = ct % kOwnW, lyp = ct / kOwnW;
   const int px = ox0 + lxp, py = oy0 + lyp;
@@ -868,8 +888,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_bwd_cells(
   double dd = 0.0;  // d_depth of this pixel, bins summed in order
   uint32_t it = 0;
   for (int done = 0; done < B;) {
-    const int b = it & 1;
-    mbar_wait(&full[b], (it >> 1) & 1);
+    const int b = (int)(it % kBufQ);
+    mbar_wait(&full[b], (it / kBufQ) & 1);
     if (it == 0) {
       gsc = ldexp(1.0, s_kbits - e2);
       igsc = ldexp(1.0, e2 - s_kbits);
@@ -1004,7 +1024,7 @@ static size_t fwd_cells_smem() {
   return 2 * (size_t)kStageP * sizeof(FwdRec) + 9 * kPlane * sizeof(uint32_t);
 }
 static size_t bwd_cells_smem() {
-  return 2 * (size_t)kStageQ * (16 + 8) + 8 * kPlane * sizeof(uint32_t);
+  return (size_t)kBufQ * kStageQ * (16 + 8) + 8 * kPlane * sizeof(uint32_t);
 }
 static void smem_attr(const void* fn, size_t bytes) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1037,7 +1057,7 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_bwd_cells), bwd_cells_smem());
   attr = true;
   count_launch();
-  k_bwd_cells<<<dim3(TP.oT, P.n_windows), kFwdThreads, bwd_cells_smem(), s>>>(
+  k_bwd_cells<<<dim3(TP.oT, P.n_windows), kBwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
       no_surv,
       depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
