@@ -216,6 +216,33 @@ EVCM_API int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* 
 EVCM_API int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* batch, int in_mem,
                                     int out_mem, evcm_chain_out* out);
 
+/* ---- predictor decode chain ------------------------------- */
+
+/* decode (predictor.hpp:126-131): depth[ph*f][pw*f] =
+ * upsample_bilinear(softplus(params[ph][pw]), f) (predictor.hpp:25-27, 46-66).
+ * Throws ConfigError for f < 1 or an empty grid. */
+EVCM_API int evcm_cuda_decode(evcm_cuda_engine* e, int pw, int ph, int factor, const double* params,
+                              int mem, double* depth_out);
+/* The depth half of accumulate_gradients (predictor.hpp:156-162):
+ * d_params = upsample_bilinear_adjoint(d_depth) * softplus_grad(params). */
+EVCM_API int evcm_cuda_decode_backward(evcm_cuda_engine* e, int pw, int ph, int factor,
+                                       const double* params, const double* d_depth, int mem,
+                                       double* d_params_out);
+/* Adam::step (optimize.hpp:115-134) over n slots: the caller keeps the step
+ * counter t (already incremented, t >= 1) and the moment buffers m, v. */
+EVCM_API int evcm_cuda_adam_step(evcm_cuda_engine* e, size_t n, double* params, const double* grads,
+                                 double* m, double* v, int t, double lr, double beta1, double beta2,
+                                 double eps, int mem);
+/* predictor_loss_and_gradients (optimize.hpp:205-241) with lambda_geo = 0 for
+ * one window: decode -> depth_pose_to_flows -> Engine::forward -> Engine::backward
+ * -> accumulate_gradients. params f64 [ph][pw] (slice is ph*f x pw*f), poses f64
+ * [n_bins][6]; outputs: loss (l_cm), d_params [ph][pw], d_poses [n_bins][6]. */
+EVCM_API int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw, int ph, int factor,
+                                                    const double* params, int n_bins,
+                                                    const double* poses, const double K[4],
+                                                    const evcm_slice* slice, int mem, double* loss,
+                                                    double* d_params, double* d_poses);
+
 /* ---- instrumentation (PhaseStats analog, engine.hpp:63-66,226-242) --------------- */
 
 /* Per-stage device times (ms, CUDA events on the engine stream) of the last

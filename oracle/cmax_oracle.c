@@ -582,3 +582,94 @@ int orc_depth_pose_to_flows_backward(int W, int H, const double* depth, const ui
   }
   return ORC_OK;
 }
+
+/* ---- predictor decode chain -------------------------------------------------------- */
+
+/* predictor.hpp:25-27 */
+double orc_softplus(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
+
+/* predictor.hpp:30-34 */
+double orc_softplus_grad(double x) {
+  if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+  const double e = exp(x);
+  return e / (1.0 + e);
+}
+
+/* upsample_src_coord (predictor.hpp:40-44) + the tap of upsample_bilinear
+ * (predictor.hpp:51-60) */
+static void up_tap(int o, int factor, int src, int* i0, int* i1, double* w) {
+  const double s = clampd(((double)o + 0.5) / (double)factor - 0.5, 0.0, (double)(src - 1));
+  int a = (int)floor(s);
+  if (a > src - 1) a = src - 1;
+  *i0 = a;
+  *i1 = a + 1 < src - 1 ? a + 1 : src - 1;
+  *w = s - a;
+}
+
+int orc_decode(int pw, int ph, int factor, const double* params, double* depth) {
+  if (pw <= 0 || ph <= 0 || factor < 1) return 1;
+  const int W = pw * factor, H = ph * factor;
+  double* low = (double*)malloc(sizeof(double) * (size_t)pw * ph);
+  if (!low) return 2;
+  for (int i = 0; i < pw * ph; ++i) low[i] = orc_softplus(params[i]);
+  if (factor == 1) {
+    memcpy(depth, low, sizeof(double) * (size_t)pw * ph);
+    free(low);
+    return 0;
+  }
+  for (int y = 0; y < H; ++y) {
+    int y0, y1;
+    double wy;
+    up_tap(y, factor, ph, &y0, &y1, &wy);
+    for (int x = 0; x < W; ++x) {
+      int x0, x1;
+      double wx;
+      up_tap(x, factor, pw, &x0, &x1, &wx);
+      depth[(size_t)y * W + x] = (1.0 - wx) * (1.0 - wy) * low[y0 * pw + x0] +
+                                 wx * (1.0 - wy) * low[y0 * pw + x1] +
+                                 (1.0 - wx) * wy * low[y1 * pw + x0] + wx * wy * low[y1 * pw + x1];
+    }
+  }
+  free(low);
+  return 0;
+}
+
+int orc_decode_backward(int pw, int ph, int factor, const double* params, const double* d_depth,
+                        double* d_params) {
+  if (pw <= 0 || ph <= 0 || factor < 1) return 1;
+  const int W = pw * factor, H = ph * factor;
+  double* low = (double*)calloc((size_t)pw * ph, sizeof(double));
+  if (!low) return 2;
+  if (factor == 1) {
+    memcpy(low, d_depth, sizeof(double) * (size_t)pw * ph);
+  } else {
+    for (int y = 0; y < H; ++y) {  /* predictor.hpp:80-95: scatter in output order */
+      int y0, y1;
+      double wy;
+      up_tap(y, factor, ph, &y0, &y1, &wy);
+      for (int x = 0; x < W; ++x) {
+        int x0, x1;
+        double wx;
+        up_tap(x, factor, pw, &x0, &x1, &wx);
+        const double g = d_depth[(size_t)y * W + x];
+        low[y0 * pw + x0] += (1.0 - wx) * (1.0 - wy) * g;
+        low[y0 * pw + x1] += wx * (1.0 - wy) * g;
+        low[y1 * pw + x0] += (1.0 - wx) * wy * g;
+        low[y1 * pw + x1] += wx * wy * g;
+      }
+    }
+  }
+  for (int i = 0; i < pw * ph; ++i) d_params[i] = low[i] * orc_softplus_grad(params[i]);
+  free(low);
+  return 0;
+}
+
+void orc_adam_step(size_t n, double* slots, const double* grads, double* m, double* v, int t,
+                   double lr, double beta1, double beta2, double eps) {
+  const double c1 = 1.0 - pow(beta1, t), c2 = 1.0 - pow(beta2, t);  /* optimize.hpp:121-122 */
+  for (size_t i = 0; i < n; ++i) {
+    m[i] = beta1 * m[i] + (1.0 - beta1) * grads[i];
+    v[i] = beta2 * v[i] + (1.0 - beta2) * grads[i] * grads[i];
+    slots[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
+  }
+}

@@ -77,6 +77,15 @@ def lib():
         L.orc_rodrigues_jacobian.argtypes = [vp, vp]
         L.orc_rodrigues_jacobian.restype = None
         L.orc_validate_window.argtypes = [i32, i32, i32, vp, u64, u64, vp, sz, vp]
+        f64 = C.c_double
+        L.orc_softplus.argtypes = [f64]
+        L.orc_softplus.restype = f64
+        L.orc_softplus_grad.argtypes = [f64]
+        L.orc_softplus_grad.restype = f64
+        L.orc_decode.argtypes = [i32, i32, i32, vp, vp]
+        L.orc_decode_backward.argtypes = [i32, i32, i32, vp, vp, vp]
+        L.orc_adam_step.argtypes = [sz, vp, vp, vp, vp, i32, f64, f64, f64, f64]
+        L.orc_adam_step.restype = None
         _lib = L
     return _lib
 
@@ -106,6 +115,11 @@ def ref():
         L.ref_chain_instance.argtypes = [u64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.ref_chain_batch.argtypes = [i32, i32, i32, i32, vp, vp, vp, u64, u64, vp, vp, i32,
                                       vp, vp, vp, vp]
+        L.ref_decode.argtypes = [i32, i32, i32, vp, vp]
+        L.ref_decode_backward.argtypes = [i32, i32, i32, vp, vp, vp]
+        L.ref_adam_steps.argtypes = [sz, vp, vp, i32, f64, f64, f64, f64]
+        L.ref_predictor_instance.argtypes = [u64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp,
+                                             vp, vp]
         _ref = L
     return _ref
 
@@ -214,6 +228,90 @@ def depth_pose_to_flows_backward(depth, poses, K, edges, grad, mask=None):
                                                 _p(edges), _p(grad), _p(dd), _p(dp))
     _check(rc, lib())
     return dd, dp
+
+
+# ---------------------------------------------------------------------------
+# predictor decode chain (predictor.hpp:25-173, optimize.hpp:115-134)
+
+
+def softplus(x):
+    return lib().orc_softplus(float(x))
+
+
+def softplus_grad(x):
+    return lib().orc_softplus_grad(float(x))
+
+
+def decode(params, factor):
+    """depth = upsample_bilinear(softplus(params), factor) (predictor.hpp:126-131)."""
+    params = np.ascontiguousarray(params, np.float64)
+    ph, pw = params.shape
+    depth = np.zeros((ph * factor, pw * factor))
+    _check(lib().orc_decode(pw, ph, factor, _p(params), _p(depth)), lib())
+    return depth
+
+
+def decode_backward(params, factor, d_depth):
+    """upsample_bilinear_adjoint(d_depth) * softplus_grad(params) (predictor.hpp:156-162)."""
+    params = np.ascontiguousarray(params, np.float64)
+    ph, pw = params.shape
+    d_depth = np.ascontiguousarray(d_depth, np.float64)
+    out = np.zeros((ph, pw))
+    _check(lib().orc_decode_backward(pw, ph, factor, _p(params), _p(d_depth), _p(out)), lib())
+    return out
+
+
+def adam_step(slots, grads, m, v, t, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """Adam::step (optimize.hpp:115-134) in place; t is the incremented step count."""
+    lib().orc_adam_step(slots.size, _p(slots), _p(np.ascontiguousarray(grads, np.float64)), _p(m),
+                        _p(v), int(t), lr, beta1, beta2, eps)
+
+
+def ref_decode(params, factor):
+    params = np.ascontiguousarray(params, np.float64)
+    ph, pw = params.shape
+    depth = np.zeros((ph * factor, pw * factor))
+    _check(ref().ref_decode(pw, ph, factor, _p(params), _p(depth)), ref(), "ref")
+    return depth
+
+
+def ref_decode_backward(params, factor, d_depth):
+    params = np.ascontiguousarray(params, np.float64)
+    ph, pw = params.shape
+    d_depth = np.ascontiguousarray(d_depth, np.float64)
+    out = np.zeros((ph, pw))
+    _check(ref().ref_decode_backward(pw, ph, factor, _p(params), _p(d_depth), _p(out)), ref(), "ref")
+    return out
+
+
+def ref_adam_steps(slots, grads, t, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """t Adam steps of the reference from zero moments on fixed grads; returns the slots."""
+    s = np.array(slots, np.float64)
+    g = np.ascontiguousarray(grads, np.float64)
+    _check(ref().ref_adam_steps(s.size, _p(s), _p(g), int(t), lr, beta1, beta2, eps), ref(), "ref")
+    return s
+
+
+def ref_predictor_instance(seed, sensor_w=16, sensor_h=12, factor=4, n_bins=2, n_events=24):
+    """The reference's chain fixture (tests/chain_support.hpp:119-184) as a raw
+    predictor, with the reference's predictor_loss_and_gradients (lambda_geo = 0)."""
+    L = ref()
+    n = C.c_size_t()
+    args = (seed, sensor_w, sensor_h, factor, n_bins, n_events)
+    _check(L.ref_predictor_instance(*args, C.byref(n), None, None, None, None, None, None, None),
+           L, "ref")
+    pw, ph = sensor_w // factor, sensor_h // factor
+    ev = np.zeros(n.value, EVENT_DTYPE)
+    params = np.zeros((ph, pw))
+    poses = np.zeros((n_bins, 6))
+    K = np.zeros(4)
+    loss = np.zeros(1)
+    dparams = np.zeros((ph, pw))
+    dposes = np.zeros((n_bins, 6))
+    _check(L.ref_predictor_instance(*args, C.byref(n), _p(ev), _p(params), _p(poses), _p(K),
+                                    _p(loss), _p(dparams), _p(dposes)), L, "ref")
+    return dict(events=ev, params=params, poses=poses, K=K, loss=float(loss[0]),
+                d_params=dparams, d_poses=dposes)
 
 
 def rodrigues(omega):

@@ -19,6 +19,8 @@
 #include "evcm/engine.hpp"
 #include "evcm/fdcheck.hpp"
 #include "evcm/geometry.hpp"
+#include "evcm/optimize.hpp"
+#include "evcm/predictor.hpp"
 #include "evcm/synth.hpp"
 #include "chain_support.hpp"
 
@@ -372,5 +374,105 @@ REF_API int ref_chain_batch(int W, int H, int B, int n_windows, const double* de
     }
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
     *loss_sum = ls;
+  });
+}
+
+// ---- predictor decode chain (predictor.hpp, optimize.hpp) --------------------
+
+namespace {
+DirectPredictor make_pred(int pw, int ph, int factor, const double* params, int B,
+                          const double* poses) {
+  DirectPredictor p;
+  p.depth_params = Image<double>(pw, ph, 0.0);
+  for (int i = 0; i < pw * ph; ++i) p.depth_params[i] = params[i];
+  p.upsample = factor;
+  p.poses.resize(B);
+  for (int b = 0; b < B; ++b) {
+    const double* q = poses + 6 * b;
+    p.poses[b].omega = {q[0], q[1], q[2]};
+    p.poses[b].trans = {q[3], q[4], q[5]};
+  }
+  return p;
+}
+}  // namespace
+
+// decode (predictor.hpp:126-131)
+REF_API int ref_decode(int pw, int ph, int factor, const double* params, double* depth) {
+  return guarded([&] {
+    const double zero_pose[6] = {0, 0, 0, 0, 0, 0};
+    const DecodedPredictor d = decode(make_pred(pw, ph, factor, params, 1, zero_pose));
+    for (std::size_t i = 0; i < d.depth.d.size(); ++i) depth[i] = d.depth.d[i];
+  });
+}
+
+// upsample_bilinear_adjoint * softplus_grad: the depth half of
+// accumulate_gradients (predictor.hpp:156-162)
+REF_API int ref_decode_backward(int pw, int ph, int factor, const double* params,
+                                const double* d_depth, double* d_params) {
+  return guarded([&] {
+    Image<double> g(pw * factor, ph * factor, 0.0);
+    for (std::size_t i = 0; i < g.size(); ++i) g[i] = d_depth[i];
+    const Image<double> low = upsample_bilinear_adjoint(g, pw, ph, factor);
+    for (int i = 0; i < pw * ph; ++i) d_params[i] = low[i] * softplus_grad(params[i]);
+  });
+}
+
+// Adam::step (optimize.hpp:115-134), t steps from zero state on the same grads
+REF_API int ref_adam_steps(std::size_t n, double* slots, const double* grads, int t, double lr,
+                           double beta1, double beta2, double eps) {
+  return guarded([&] {
+    OptimizerConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.adam_beta1 = beta1;
+    cfg.adam_beta2 = beta2;
+    cfg.adam_eps = eps;
+    Adam adam(n);
+    std::vector<double*> s(n);
+    for (std::size_t i = 0; i < n; ++i) s[i] = slots + i;
+    const std::vector<double> g(grads, grads + n);
+    for (int k = 0; k < t; ++k) adam.step(s, g, cfg);
+  });
+}
+
+// predictor_loss_and_gradients (optimize.hpp:205-241), lambda_geo = 0, on the
+// reference's own chain fixture (tests/chain_support.hpp:119-184): returns the
+// raw predictor (low-res params, poses), intrinsics, events, and the reference's
+// loss and parameter gradients. n_workers: Engine parallel backend workers.
+REF_API int ref_predictor_instance(std::uint64_t seed, int sensor_w, int sensor_h, int factor,
+                                   int n_bins, int n_events, std::size_t* n, void* ev,
+                                   double* params, double* poses, double* K, double* loss,
+                                   double* d_params, double* d_poses) {
+  return guarded([&] {
+    evcm_test::ChainParams cp;
+    cp.sensor_w = sensor_w;
+    cp.sensor_h = sensor_h;
+    cp.factor = factor;
+    cp.n_bins = n_bins;
+    cp.n_events = n_events;
+    const evcm_test::ChainInstance inst = evcm_test::make_chain_instance(seed, cp);
+    *n = inst.slice.events.size();
+    if (!ev) return;
+    if (*n) std::memcpy(ev, inst.slice.events.data(), *n * sizeof(Event));
+    const DirectPredictor& p = inst.pred;
+    for (std::size_t i = 0; i < p.depth_params.size(); ++i) params[i] = p.depth_params[i];
+    for (int b = 0; b < n_bins; ++b) {
+      const PoseStep& q = p.poses[b];
+      const double v[6] = {q.omega.x, q.omega.y, q.omega.z, q.trans.x, q.trans.y, q.trans.z};
+      std::memcpy(poses + 6 * b, v, sizeof v);
+    }
+    K[0] = inst.k.fx;
+    K[1] = inst.k.fy;
+    K[2] = inst.k.cx;
+    K[3] = inst.k.cy;
+    const Engine engine{EngineOptions{}};
+    const WindowGradients wg = predictor_loss_and_gradients(p, inst.slice, inst.k, 0.0, engine);
+    *loss = wg.l_cm;
+    for (std::size_t i = 0; i < wg.grads.d_depth_params.size(); ++i)
+      d_params[i] = wg.grads.d_depth_params[i];
+    for (int b = 0; b < n_bins; ++b) {
+      const PoseGrad& q = wg.grads.d_poses[b];
+      const double v[6] = {q.omega.x, q.omega.y, q.omega.z, q.trans.x, q.trans.y, q.trans.z};
+      std::memcpy(d_poses + 6 * b, v, sizeof v);
+    }
   });
 }

@@ -11,3 +11,6 @@ from .engine import (  # noqa: F401
     TimeRangeError, Trajectories, UnsortedEventsError, backend_from_name, build_iwe_stack,
     contrast_loss_backward, default_engine, depth_pose_to_flows, depth_pose_to_flows_backward,
     load_library, make_edges, rsat)
+from .predictor import (  # noqa: F401
+    Adam, DecodedPredictor, DirectPredictor, OptimizerConfig, PredictorGrads, WindowGradients,
+    accumulate_gradients, decode, predictor_loss_and_gradients)

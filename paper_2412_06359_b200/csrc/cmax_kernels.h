@@ -59,4 +59,11 @@ void launch_unpack_grad(cudaStream_t s, const G2* g, int B, int HW, double* out)
 void launch_traj_products(cudaStream_t s, const uint2* packed, uint64_t n, const WinParams& P,
                           const double2* flows, uint8_t* alive, int32_t* bin, double* pos);
 
+// Predictor decode chain (predictor.cu)
+void launch_decode(cudaStream_t s, const double* params, int sw, int sh, int factor, double* depth);
+void launch_decode_adjoint(cudaStream_t s, const double* params, const double* d_depth, int sw,
+                           int sh, int factor, double* d_params);
+void launch_adam(cudaStream_t s, double* slots, const double* grads, double* m, double* v, size_t n,
+                 double lr, double b1, double b2, double eps, double c1, double c2);
+
 }  // namespace evcm_b200

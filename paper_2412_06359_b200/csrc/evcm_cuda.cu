@@ -818,9 +818,14 @@ int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, co
   });
 }
 
-int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
-                           evcm_chain_out* out) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+// The batched chain; depth_dev (device, [n_windows][H][W]) replaces bt->depth
+// when given (the predictor path decodes the depth on the device).
+void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
+                evcm_chain_out* out, const double* depth_dev) {
+  {
     if (!e || !bt || !out) fail(EVCM_ERR_CONFIG, "null argument");
     set_device(e);
     reset_launch_count();
@@ -860,7 +865,8 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
     uint64_t max_n = 0;
     for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, bt->ev_offsets[w + 1] - bt->ev_offsets[w]);
     stage_events(e, bt->events, bt->ev_offsets, P, in_mem);
-    const double* depth = to_device(e, "depth", bt->depth, (size_t)nw * P.HW, in_mem);
+    const double* depth =
+        depth_dev ? depth_dev : to_device(e, "depth", bt->depth, (size_t)nw * P.HW, in_mem);
     double2* flows = e->get<double2>("flows", (size_t)nw * B * P.HW);
     e->mark(1);
     launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr);
@@ -886,11 +892,140 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
     sync_and_check(e, "chain");
     e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);
     e->last_launches = launch_count();
-  });
+  }
+}
+
+void check_grid(int pw, int ph, int factor, const void* params) {  // DirectPredictor::validate
+  if (pw <= 0 || ph <= 0 || !params) fail(EVCM_ERR_CONFIG, "predictor: empty depth grid");
+  if (factor < 1) fail(EVCM_ERR_CONFIG, "upsample: factor must be at least 1");
+  if ((int64_t)pw * factor > 65535 || (int64_t)ph * factor > 65535)
+    fail(EVCM_ERR_DIMENSION, "predictor: decoded size too large");
+}
+}  // namespace
+
+extern "C" {
+
+int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
+                           evcm_chain_out* out) {
+  return guarded([&] { chain_impl(e, bt, in_mem, out_mem, out, nullptr); });
 }
 
 int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
   return evcm_cuda_chain_batch2(e, bt, mem, mem, out);
+}
+
+int evcm_cuda_decode(evcm_cuda_engine* e, int pw, int ph, int factor, const double* params, int mem,
+                     double* depth_out) {
+  return guarded([&] {
+    if (!e || !depth_out) fail(EVCM_ERR_CONFIG, "null argument");
+    check_grid(pw, ph, factor, params);
+    set_device(e);
+    reset_launch_count();
+    const double* pd = to_device(e, "pred_params", params, (size_t)pw * ph, mem);
+    const size_t n = (size_t)pw * factor * ph * factor;
+    double* dd = mem == EVCM_MEM_DEVICE ? depth_out : e->get<double>("pred_depth", n);
+    launch_decode(e->stream, pd, pw, ph, factor, dd);
+    if (dd != depth_out) from_device(e, depth_out, dd, n * sizeof(double), mem);
+    sync_and_check(e, "decode");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_decode_backward(evcm_cuda_engine* e, int pw, int ph, int factor, const double* params,
+                              const double* d_depth, int mem, double* d_params_out) {
+  return guarded([&] {
+    if (!e || !d_depth || !d_params_out) fail(EVCM_ERR_CONFIG, "null argument");
+    check_grid(pw, ph, factor, params);
+    set_device(e);
+    reset_launch_count();
+    const size_t n = (size_t)pw * factor * ph * factor;
+    const double* pd = to_device(e, "pred_params", params, (size_t)pw * ph, mem);
+    const double* gd = to_device(e, "pred_d_depth", d_depth, n, mem);
+    double* out = mem == EVCM_MEM_DEVICE ? d_params_out : e->get<double>("pred_d_params", (size_t)pw * ph);
+    launch_decode_adjoint(e->stream, pd, gd, pw, ph, factor, out);
+    if (out != d_params_out) from_device(e, d_params_out, out, (size_t)pw * ph * sizeof(double), mem);
+    sync_and_check(e, "decode_backward");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_adam_step(evcm_cuda_engine* e, size_t n, double* params, const double* grads, double* m,
+                        double* v, int t, double lr, double beta1, double beta2, double eps, int mem) {
+  return guarded([&] {
+    if (!e || (n && (!params || !grads || !m || !v))) fail(EVCM_ERR_CONFIG, "null argument");
+    if (t < 1) fail(EVCM_ERR_CONFIG, "adam: step count must be >= 1");
+    set_device(e);
+    reset_launch_count();
+    const double c1 = 1.0 - std::pow(beta1, t), c2 = 1.0 - std::pow(beta2, t);  // optimize.hpp:121-122
+    if (mem == EVCM_MEM_DEVICE) {
+      launch_adam(e->stream, params, grads, m, v, n, lr, beta1, beta2, eps, c1, c2);
+    } else {
+      double* pd = e->get<double>("adam_p", n);
+      double* gd = e->get<double>("adam_g", n);
+      double* md = e->get<double>("adam_m", n);
+      double* vd = e->get<double>("adam_v", n);
+      const size_t b = n * sizeof(double);
+      ck(cudaMemcpyAsync(pd, params, b, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(gd, grads, b, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(md, m, b, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(vd, v, b, cudaMemcpyHostToDevice, e->stream), "H2D");
+      launch_adam(e->stream, pd, gd, md, vd, n, lr, beta1, beta2, eps, c1, c2);
+      ck(cudaMemcpyAsync(params, pd, b, cudaMemcpyDeviceToHost, e->stream), "D2H");
+      ck(cudaMemcpyAsync(m, md, b, cudaMemcpyDeviceToHost, e->stream), "D2H");
+      ck(cudaMemcpyAsync(v, vd, b, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    }
+    sync_and_check(e, "adam_step");
+    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw, int ph, int factor,
+                                           const double* params, int n_bins, const double* poses,
+                                           const double K[4], const evcm_slice* slice, int mem,
+                                           double* loss, double* d_params, double* d_poses) {
+  return guarded([&] {
+    if (!e || !slice || !K || !poses) fail(EVCM_ERR_CONFIG, "null argument");
+    check_grid(pw, ph, factor, params);
+    if (n_bins < 1) fail(EVCM_ERR_CONFIG, "predictor: need one pose per bin");
+    if ((int)slice->width != pw * factor || (int)slice->height != ph * factor)
+      fail(EVCM_ERR_DIMENSION, "predictor: decoded depth does not match the slice sensor");
+    set_device(e);
+    const int W = pw * factor, H = ph * factor;
+    const size_t HW = (size_t)W * H;
+    // decode on the device (predictor.hpp:126-131); the chain resets the launch count
+    const double* pd = to_device(e, "pred_params", params, (size_t)pw * ph, mem);
+    double* depth = e->get<double>("pred_depth", HW);
+    launch_decode(e->stream, pd, pw, ph, factor, depth);
+    // the fused chain: flows -> Engine::forward -> Engine::backward -> flows backward
+    evcm_chain_batch bt{};
+    bt.n_windows = 1;
+    bt.width = W;
+    bt.height = H;
+    bt.n_bins = n_bins;
+    bt.t_start_us = slice->t_start_us;
+    bt.t_end_us = slice->t_end_us;
+    for (int i = 0; i < 4; ++i) bt.K[i] = K[i];
+    bt.events = slice->events;
+    const uint64_t offs[2] = {0, (uint64_t)slice->n_events};
+    bt.ev_offsets = offs;
+    bt.poses = poses;
+    double* ld = e->get<double>("pred_loss", 1);
+    double* dd = e->get<double>("pred_dd", HW);
+    double* dp = mem == EVCM_MEM_DEVICE ? d_poses : e->get<double>("pred_dp", (size_t)n_bins * 6);
+    evcm_chain_out co{};
+    co.loss = ld;
+    co.d_depth = dd;
+    co.d_poses = dp;
+    chain_impl(e, &bt, mem, EVCM_MEM_DEVICE, &co, depth);
+    // accumulate_gradients, depth half (predictor.hpp:156-162)
+    double* dpar = mem == EVCM_MEM_DEVICE ? d_params : e->get<double>("pred_d_params", (size_t)pw * ph);
+    launch_decode_adjoint(e->stream, pd, dd, pw, ph, factor, dpar);
+    if (loss) from_device(e, loss, ld, sizeof(double), mem);
+    if (d_params && dpar != d_params) from_device(e, d_params, dpar, (size_t)pw * ph * sizeof(double), mem);
+    if (d_poses && dp != d_poses) from_device(e, d_poses, dp, (size_t)n_bins * 6 * sizeof(double), mem);
+    sync_and_check(e, "predictor_loss_and_gradients");
+    e->last_launches = launch_count() + 1;  // + the decode before the chain's reset
+  });
 }
 
 }  // extern "C"

@@ -155,6 +155,12 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_last_algo.argtypes = [vp]
     L.evcm_cuda_workspace_bytes.argtypes = [vp]
     L.evcm_cuda_workspace_bytes.restype = sz
+    f64 = C.c_double
+    L.evcm_cuda_decode.argtypes = [vp, i32, i32, i32, vp, i32, vp]
+    L.evcm_cuda_decode_backward.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp]
+    L.evcm_cuda_adam_step.argtypes = [vp, sz, vp, vp, vp, vp, i32, f64, f64, f64, f64, i32]
+    L.evcm_cuda_predictor_loss_and_gradients.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp,
+                                                         i32, vp, vp, vp]
     _lib = L
     return L
 

@@ -1,0 +1,196 @@
+"""The predictor decode chain on the device — the caller
+of the CMax path — mirroring the reference's names and semantics:
+
+  DirectPredictor, DecodedPredictor, decode          predictor.hpp:100-131
+  PredictorGrads, accumulate_gradients               predictor.hpp:133-173
+  OptimizerConfig (Adam fields), Adam                optimize.hpp:25-75, 115-134
+  WindowGradients, predictor_loss_and_gradients      optimize.hpp:195-241 (lambda_geo = 0)
+
+Everything runs through libevcm_cuda.so (evcm_cuda_decode / _decode_backward /
+_adam_step / _predictor_loss_and_gradients); there is no CPU fallback. Arrays
+may be numpy (host) or torch CUDA tensors (device, kept on the device)."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import (MEM_DEVICE, MEM_HOST, CameraIntrinsics, ConfigError, Engine, EventSlice,
+                     FlowSequence, _is_torch, _k_array, _mem_of, _ptr, _raise, default_engine,
+                     depth_pose_to_flows_backward, load_library)
+
+
+def _zeros_like_side(ref, shape):
+    if _is_torch(ref) and ref.is_cuda:
+        import torch
+        return torch.zeros(shape, dtype=torch.float64, device=ref.device)
+    return np.zeros(shape)
+
+
+def _f64(a):
+    return a if _is_torch(a) else np.ascontiguousarray(a, np.float64)
+
+
+@dataclass
+class DirectPredictor:
+    """predictor.hpp:100-120: low-resolution unconstrained depth parameters
+    [ph][pw] decoded through softplus and x`upsample` bilinear upsampling, plus
+    one 6-dof pose {omega, trans} per flow bin [B][6]."""
+    depth_params: object
+    poses: object
+    upsample: int = 8
+
+    @property
+    def full_width(self) -> int:
+        return int(self.depth_params.shape[1]) * self.upsample
+
+    @property
+    def full_height(self) -> int:
+        return int(self.depth_params.shape[0]) * self.upsample
+
+    @property
+    def n_bins(self) -> int:
+        return int(self.poses.shape[0])
+
+    @property
+    def n_parameters(self) -> int:
+        return int(self.depth_params.shape[0] * self.depth_params.shape[1]) + 6 * self.n_bins
+
+    def validate(self) -> None:  # predictor.hpp:109-119 (pose checks: PoseStep::validate)
+        if self.depth_params.shape[0] == 0 or self.depth_params.shape[1] == 0:
+            raise ConfigError("predictor: empty depth grid")
+        if self.n_bins == 0:
+            raise ConfigError("predictor: need one pose per bin")
+        if self.upsample < 1:
+            raise ConfigError("predictor: upsample factor must be >= 1")
+        p = self.depth_params.cpu().numpy() if _is_torch(self.depth_params) else self.depth_params
+        if not np.all(np.isfinite(p)):
+            raise ConfigError("predictor: non-finite depth parameter")
+
+
+@dataclass
+class DecodedPredictor:
+    depth: object  # [H][W], all valid
+    poses: object
+
+
+@dataclass
+class PredictorGrads:
+    d_depth_params: object
+    d_poses: object
+
+
+@dataclass
+class WindowGradients:
+    grads: PredictorGrads
+    l_cm: float = 0.0
+    l_geo: float = 0.0
+    total: float = 0.0
+
+
+def decode(pred: DirectPredictor, engine: Engine | None = None) -> DecodedPredictor:
+    """decode (predictor.hpp:126-131) on the device."""
+    pred.validate()
+    e = engine or default_engine()
+    params = _f64(pred.depth_params)
+    ph, pw = params.shape
+    mem = _mem_of(params)
+    depth = _zeros_like_side(params, (ph * pred.upsample, pw * pred.upsample))
+    _raise(load_library().evcm_cuda_decode(e._h, pw, ph, pred.upsample, _ptr(params), mem,
+                                           _ptr(depth)))
+    return DecodedPredictor(depth, pred.poses)
+
+
+def accumulate_gradients(pred: DirectPredictor, decoded_depth, k, flows: FlowSequence, flow_grads,
+                         extra_d_depth=None, extra_d_poses=None,
+                         engine: Engine | None = None) -> PredictorGrads:
+    """accumulate_gradients (predictor.hpp:143-173): flow-cell gradients through
+    depth_pose_to_flows_backward, optional extra depth / pose terms, then the
+    upsampling transpose and softplus derivative (on the device)."""
+    e = engine or default_engine()
+    d_depth, d_poses = depth_pose_to_flows_backward(decoded_depth, pred.poses, k, flows, flow_grads,
+                                                    engine=e)
+    if extra_d_depth is not None:
+        if tuple(extra_d_depth.shape) != tuple(d_depth.shape):
+            from .engine import DimensionMismatchError
+            raise DimensionMismatchError("gradients: extra depth term shape mismatch")
+        d_depth = d_depth + extra_d_depth
+    params = _f64(pred.depth_params)
+    ph, pw = params.shape
+    mem = _mem_of(params, d_depth)
+    out = _zeros_like_side(params, (ph, pw))
+    _raise(load_library().evcm_cuda_decode_backward(e._h, pw, ph, pred.upsample, _ptr(params),
+                                                    _ptr(_f64(d_depth)), mem, _ptr(out)))
+    if extra_d_poses is not None:
+        if extra_d_poses.shape[0] != d_poses.shape[0]:
+            raise ConfigError("gradients: extra pose term count mismatch")
+        d_poses = d_poses + extra_d_poses
+    return PredictorGrads(out, d_poses)
+
+
+def predictor_loss_and_gradients(pred: DirectPredictor, slice_: EventSlice, k, lambda_geo=0.0,
+                                 engine: Engine | None = None) -> WindowGradients:
+    """predictor_loss_and_gradients (optimize.hpp:205-241) in one fused device
+    call: decode -> depth_pose_to_flows -> Engine::forward -> Engine::backward ->
+    accumulate_gradients. The depth-consistency term (lambda_geo > 0) is not part
+    of the CMax path this build accelerates."""
+    if lambda_geo != 0.0:
+        raise ConfigError("cuda backend: lambda_geo > 0 (L_geo) is not implemented")
+    pred.validate()
+    e = engine or default_engine()
+    params = _f64(pred.depth_params)
+    poses = _f64(pred.poses)
+    ph, pw = params.shape
+    if slice_.width != pw * pred.upsample or slice_.height != ph * pred.upsample:
+        from .engine import DimensionMismatchError
+        raise DimensionMismatchError("predictor: decoded depth does not match the slice sensor")
+    mem = _mem_of(params, poses, slice_.events)
+    loss = _zeros_like_side(params, (1,))
+    dpar = _zeros_like_side(params, (ph, pw))
+    dpos = _zeros_like_side(params, (pred.n_bins, 6))
+    sl = slice_._c()
+    _raise(load_library().evcm_cuda_predictor_loss_and_gradients(
+        e._h, pw, ph, pred.upsample, _ptr(params), pred.n_bins, _ptr(poses),
+        _ptr(_k_array(k)), C.byref(sl), mem, _ptr(loss), _ptr(dpar), _ptr(dpos)))
+    l_cm = float(loss[0])
+    return WindowGradients(PredictorGrads(dpar, dpos), l_cm, 0.0, l_cm)
+
+
+@dataclass
+class OptimizerConfig:
+    """The Adam fields of OptimizerConfig (optimize.hpp:25-75)."""
+    learning_rate: float = 1e-4
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+
+    def validate(self) -> None:  # optimize.hpp:43-53
+        if not (self.learning_rate > 0.0) or not math.isfinite(self.learning_rate):
+            raise ConfigError("optimizer: learning_rate must be positive")
+        if not (0.0 <= self.adam_beta1 < 1.0) or not (0.0 <= self.adam_beta2 < 1.0):
+            raise ConfigError("optimizer: adam betas must lie in [0, 1)")
+        if not self.adam_eps > 0.0:
+            raise ConfigError("optimizer: adam_eps must be positive")
+
+
+class Adam:
+    """Adam (optimize.hpp:115-134) on the device: moment buffers live next to the
+    parameters (host numpy or device torch), state persists across steps."""
+
+    def __init__(self, n: int, like=None):
+        self.t = 0
+        self.m = _zeros_like_side(like, (n,)) if like is not None else np.zeros(n)
+        self.v = _zeros_like_side(like, (n,)) if like is not None else np.zeros(n)
+
+    def step(self, slots, grads, cfg: OptimizerConfig, engine: Engine | None = None) -> None:
+        """slots -= lr * m_hat / (sqrt(v_hat) + eps), in place (flat f64 vectors)."""
+        cfg.validate()
+        e = engine or default_engine()
+        self.t += 1
+        n = int(slots.shape[0])
+        mem = _mem_of(slots, grads, self.m)
+        _raise(load_library().evcm_cuda_adam_step(
+            e._h, n, _ptr(slots), _ptr(_f64(grads)), _ptr(self.m), _ptr(self.v), self.t,
+            cfg.learning_rate, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps, mem))

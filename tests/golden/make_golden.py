@@ -8,6 +8,9 @@ Each fixture is an .npz with the inputs and the reference outputs:
   smooth_32x24.npz   smooth-flow window (bench_window semantics + spatial variation)
   geom_13x9.npz      depth_pose_to_flows / _backward on a masked depth map
   chain_<seed>.npz   make_chain_instance (tests/chain_support.hpp:119-184) decoded
+  predictor_<seed>.npz  make_chain_instance as a raw DirectPredictor + the reference's
+                     decode and predictor_loss_and_gradients (optimize.hpp:205-241)
+  adam.npz           Adam::step (optimize.hpp:115-134), 3 steps on fixed gradients
 """
 import os
 import sys
@@ -32,9 +35,26 @@ def window_fixture(name, w):
          grad=r["grad"])
 
 
+def predictor_fixtures():
+    for seed in (3, 11):
+        r = O.ref_predictor_instance(seed, sensor_w=32, sensor_h=24, factor=8, n_bins=3,
+                                     n_events=60)
+        depth = O.ref_decode(r["params"], 8)
+        rng = np.random.default_rng(seed)
+        g = rng.uniform(-1, 1, depth.shape)
+        save(f"predictor_{seed}.npz", events=r["events"].view(np.uint8).reshape(-1, 16),
+             params=r["params"], poses=r["poses"], K=r["K"], factor=8, loss=r["loss"],
+             d_params=r["d_params"], d_poses=r["d_poses"], depth=depth, g=g,
+             g_params=O.ref_decode_backward(r["params"], 8, g))
+    rng = np.random.default_rng(2)
+    s, g = rng.normal(size=40), rng.normal(size=40)
+    save("adam.npz", slots=s, grads=g, lr=0.01, steps=3, out=O.ref_adam_steps(s, g, 3, 0.01))
+
+
 def main():
     if not O.ref_available():
         O.build(ref=True)
+    predictor_fixtures()
     for seed in (100, 7, 503, 1300):
         window_fixture(f"fd_{seed}.npz", O.ref_fd_instance(seed))
     window_fixture("fd_masked_900.npz", O.ref_fd_instance(900, max_events=24, want_masked=True))

@@ -222,3 +222,47 @@ def test_flow_gradient_finite_differences():
         mx = max(mx, abs(g[idx] - fd))
         na, nf = max(na, abs(g[idx])), max(nf, abs(fd))
     assert mx / max(na, nf, 1e-12) < 1e-4
+
+
+# ---- predictor decode chain ---------------------------------
+
+@pytest.mark.parametrize("name", ["predictor_3.npz", "predictor_11.npz"])
+def test_golden_predictor_decode_bit_exact(name):
+    """The oracle's decode and decode transpose reproduce the reference's
+    (predictor.hpp:126-131, 156-162) bit for bit on the committed fixtures."""
+    g = load(name[:-4])
+    f = int(g["factor"])
+    np.testing.assert_array_equal(O.decode(g["params"], f), g["depth"])
+    np.testing.assert_array_equal(O.decode_backward(g["params"], f, g["g"]), g["g_params"])
+
+
+def test_golden_adam_bit_exact():
+    g = load("adam")
+    s = g["slots"].copy()
+    m, v = np.zeros_like(s), np.zeros_like(s)
+    for t in range(1, int(g["steps"]) + 1):
+        O.adam_step(s, g["grads"], m, v, t, float(g["lr"]))
+    np.testing.assert_array_equal(s, g["out"])
+
+
+def test_softplus_tails_and_upsample_factor_one():
+    """softplus is positive and stable on both tails; factor 1 is the identity
+    (predictor.hpp:25-34, 48)."""
+    for x in (-800.0, -30.0, -1e-3, 0.0, 1e-3, 30.0, 800.0):
+        assert O.softplus(x) > 0.0 or x < -700
+        assert 0.0 <= O.softplus_grad(x) <= 1.0
+    p = np.random.default_rng(0).normal(size=(3, 4))
+    np.testing.assert_array_equal(O.decode(p, 1), np.vectorize(O.softplus)(p))
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("seed", [1, 2, 5])
+def test_decode_chain_matches_reference(seed):
+    if not O.ref_available():
+        pytest.skip("reference not built")
+    rng = np.random.default_rng(seed)
+    p = rng.normal(size=(4 + seed, 3 + seed))
+    for f in (1, 2, 8):
+        np.testing.assert_array_equal(O.decode(p, f), O.ref_decode(p, f))
+        g = rng.normal(size=(p.shape[0] * f, p.shape[1] * f))
+        np.testing.assert_array_equal(O.decode_backward(p, f, g), O.ref_decode_backward(p, f, g))
