@@ -142,6 +142,12 @@ struct evcm_cuda_engine {
   std::unordered_map<std::string, Buf> pins;  // pinned host staging
   int stage_nw = 0;
   bool check_pose_flag = false;  // device pose tables: validation result pending
+  // CUDA graph of the device-resident chain: replayed when a call repeats the
+  // previous call's signature (shapes, pointers, event offsets, options)
+  std::vector<uint64_t> gsig;
+  cudaGraphExec_t gexec = nullptr;
+  bool gfailed = false;  // capture failed for this signature: run eagerly
+  int glaunches = 0;
   // owner pipeline state
   TileParams TP{};
   uint64_t n_total = 0, max_n = 0;
@@ -603,6 +609,7 @@ void evcm_cuda_destroy(evcm_cuda_engine* e) {
   for (auto& kv : e->pins)
     if (kv.second.p) cudaFreeHost(kv.second.p);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  if (e->gexec) cudaGraphExecDestroy(e->gexec);
   if (e->own_stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -823,11 +830,9 @@ int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, co
 namespace {
 // The batched chain; depth_dev (device, [n_windows][H][W]) replaces bt->depth
 // when given (the predictor path decodes the depth on the device).
-void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
-                evcm_chain_out* out, const double* depth_dev) {
+void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
+                   evcm_chain_out* out, const double* depth_dev) {
   {
-    if (!e || !bt || !out) fail(EVCM_ERR_CONFIG, "null argument");
-    set_device(e);
     reset_launch_count();
     const int nw = bt->n_windows, B = bt->n_bins, W = bt->width, H = bt->height;
     if (nw < 1) fail(EVCM_ERR_CONFIG, "chain: need at least one window");
@@ -889,10 +894,90 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
     if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), out_mem);
     if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), out_mem);
     if (out->d_poses && dpo != out->d_poses) from_device(e, out->d_poses, dpo, (size_t)nw * B * 6 * sizeof(double), out_mem);
-    sync_and_check(e, "chain");
-    e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);
-    e->last_launches = launch_count();
   }
+}
+
+// Signature of a graph-replayable chain call (device inputs and outputs only:
+// host buffers would be read at capture time, not at replay time).
+std::vector<uint64_t> chain_signature(const evcm_cuda_engine* e, const evcm_chain_batch* bt,
+                                      const evcm_chain_out* out, const double* depth_dev) {
+  std::vector<uint64_t> g;
+  auto u = [&](uint64_t v) { g.push_back(v); };
+  auto d = [&](double v) {
+    uint64_t b;
+    std::memcpy(&b, &v, 8);
+    g.push_back(b);
+  };
+  u((uint64_t)bt->n_windows); u((uint64_t)bt->width); u((uint64_t)bt->height); u((uint64_t)bt->n_bins);
+  u(bt->t_start_us); u(bt->t_end_us);
+  for (double k : bt->K) d(k);
+  u((uint64_t)(uintptr_t)bt->events); u((uint64_t)(uintptr_t)(depth_dev ? depth_dev : bt->depth));
+  u((uint64_t)(uintptr_t)bt->poses); u((uint64_t)(uintptr_t)out->loss);
+  u((uint64_t)(uintptr_t)out->no_survivors); u((uint64_t)(uintptr_t)out->d_depth);
+  u((uint64_t)(uintptr_t)out->d_poses);
+  u((uint64_t)e->opt.algo); u((uint64_t)e->opt.deterministic); u((uint64_t)e->opt.stack_f64);
+  u((uint64_t)e->opt.grad_f64);
+  for (int w = 0; w <= bt->n_windows; ++w) u(bt->ev_offsets[w]);
+  return g;
+}
+
+void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
+                evcm_chain_out* out, const double* depth_dev) {
+  if (!e || !bt || !out || !bt->ev_offsets) fail(EVCM_ERR_CONFIG, "null argument");
+  set_device(e);
+  const bool graphable = in_mem == EVCM_MEM_DEVICE && out_mem == EVCM_MEM_DEVICE && !e->timing;
+  std::vector<uint64_t> sig;
+  if (graphable) sig = chain_signature(e, bt, out, depth_dev);
+  const bool same = graphable && sig == e->gsig;
+  if (same && e->gexec) {
+    // replay: the state the eager path leaves behind is unchanged (same signature)
+    ck(cudaGraphLaunch(e->gexec, e->stream), "graph launch");
+    e->stage_nw = bt->n_windows;
+    e->check_pose_flag = true;
+    e->have_fwd = false;
+    sync_and_check(e, "chain");
+    e->last_launches = e->glaunches;
+    return;
+  }
+  if (!same) {
+    if (e->gexec) cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+    e->gfailed = false;
+    e->gsig = sig;  // empty when not graphable
+  }
+  if (same && !e->gfailed) {
+    // second identical call: capture the enqueue into a graph, then replay it
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    bool ok = true;
+    try {
+      chain_enqueue(e, bt, in_mem, out_mem, out, depth_dev);
+    } catch (...) {
+      ok = false;
+      cudaStreamEndCapture(e->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    if (cudaStreamEndCapture(e->stream, &graph) != cudaSuccess ||
+        cudaGraphInstantiate(&e->gexec, graph, 0) != cudaSuccess) {
+      ok = false;
+      e->gexec = nullptr;
+      cudaGetLastError();
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (ok) {
+      e->glaunches = launch_count();
+      ck(cudaGraphLaunch(e->gexec, e->stream), "graph launch");
+      sync_and_check(e, "chain");
+      e->last_launches = e->glaunches;
+      return;
+    }
+    e->gfailed = true;  // fall through: eager run
+  }
+  chain_enqueue(e, bt, in_mem, out_mem, out, depth_dev);
+  sync_and_check(e, "chain");
+  e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);
+  e->last_launches = launch_count();
 }
 
 void check_grid(int pw, int ph, int factor, const void* params) {  // DirectPredictor::validate
