@@ -120,6 +120,8 @@ def ref():
         L.ref_adam_steps.argtypes = [sz, vp, vp, i32, f64, f64, f64, f64]
         L.ref_predictor_instance.argtypes = [u64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp,
                                              vp, vp]
+        L.ref_optimize_flow_only.argtypes = [i32, i32, u64, u64, vp, sz, i32, f64, i32, vp, vp, vp,
+                                             vp, vp]
         _ref = L
     return _ref
 
@@ -312,6 +314,20 @@ def ref_predictor_instance(seed, sensor_w=16, sensor_h=12, factor=4, n_bins=2, n
                                     _p(loss), _p(dparams), _p(dposes)), L, "ref")
     return dict(events=ev, params=params, poses=poses, K=K, loss=float(loss[0]),
                 d_params=dparams, d_poses=dposes)
+
+
+def ref_optimize_flow_only(W, H, t0, t1, events, n_bins, lr, max_updates):
+    """The reference's optimize_flow_only (optimize.hpp:385-487): (flows [B,2,H,W],
+    l_cm, rsat, grad_norm_depth per logged update)."""
+    L = ref()
+    ev = np.ascontiguousarray(events, EVENT_DTYPE)
+    flows = np.zeros((n_bins, 2, H, W))
+    l_cm, rsat, gn = np.zeros(max_updates), np.zeros(max_updates), np.zeros(max_updates)
+    nrec = C.c_int()
+    _check(L.ref_optimize_flow_only(W, H, t0, t1, _p(ev), len(ev), n_bins, lr, max_updates,
+                                    _p(flows), _p(l_cm), _p(rsat), _p(gn), C.byref(nrec)), L, "ref")
+    k = nrec.value
+    return flows, l_cm[:k], rsat[:k], gn[:k]
 
 
 def rodrigues(omega):

@@ -476,3 +476,36 @@ REF_API int ref_predictor_instance(std::uint64_t seed, int sensor_w, int sensor_
     }
   });
 }
+
+// optimize_flow_only (optimize.hpp:385-487): final (best) flows [B][2][H][W] and
+// the per-update l_cm / rsat / grad_norm_depth of the log.
+REF_API int ref_optimize_flow_only(int W, int H, std::uint64_t t0, std::uint64_t t1, const void* ev,
+                                   std::size_t n, int n_bins, double lr, int max_updates,
+                                   double* flows_out, double* l_cm, double* rsat, double* gnorm,
+                                   int* n_records) {
+  return guarded([&] {
+    EventSlice s;
+    s.width = W;
+    s.height = H;
+    s.t_start_us = t0;
+    s.t_end_us = t1;
+    s.events.resize(n);
+    if (n) std::memcpy(s.events.data(), ev, n * sizeof(Event));
+    OptimizerConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.max_updates = max_updates;
+    const FlowOnlyResult r = optimize_flow_only(s, n_bins, cfg);
+    const std::size_t HW = static_cast<std::size_t>(W) * H;
+    for (int b = 0; b < n_bins; ++b)
+      for (std::size_t i = 0; i < HW; ++i) {
+        flows_out[(2 * b) * HW + i] = r.flows.fields[b].u[i];
+        flows_out[(2 * b + 1) * HW + i] = r.flows.fields[b].v[i];
+      }
+    *n_records = static_cast<int>(r.log.records.size());
+    for (std::size_t i = 0; i < r.log.records.size(); ++i) {
+      l_cm[i] = r.log.records[i].l_cm;
+      rsat[i] = r.log.records[i].rsat;
+      gnorm[i] = r.log.records[i].grad_norm_depth;
+    }
+  });
+}

@@ -14,3 +14,4 @@ from .engine import (  # noqa: F401
 from .predictor import (  # noqa: F401
     Adam, DecodedPredictor, DirectPredictor, OptimizerConfig, PredictorGrads, WindowGradients,
     accumulate_gradients, decode, predictor_loss_and_gradients)
+from .optimize import FlowOnlyResult, TrainLog, TrainRecord, optimize_flow_only  # noqa: F401

@@ -160,19 +160,43 @@ def predictor_loss_and_gradients(pred: DirectPredictor, slice_: EventSlice, k, l
 
 @dataclass
 class OptimizerConfig:
-    """The Adam fields of OptimizerConfig (optimize.hpp:25-75)."""
+    """OptimizerConfig (optimize.hpp:25-75): the fields the device loops use
+    (Adam, stopping, divergence and FD spot-check controls)."""
     learning_rate: float = 1e-4
+    steps_per_update: int = 10
+    bins: int = 10
+    max_updates: int = 100
+    lambda_geo: float = 0.05  # kGeoWeightDefault; only lambda_geo = 0 runs on the cuda backend
     adam_beta1: float = 0.9
     adam_beta2: float = 0.999
     adam_eps: float = 1e-8
+    seed: int = 1
+    fd_check_every: int = 0
+    fd_check_tolerance: float = 0.05
+    divergence_factor: float = 10.0
+    grad_stop_tolerance: float = 1e-10
 
-    def validate(self) -> None:  # optimize.hpp:43-53
+    def validate(self) -> None:  # optimize.hpp:43-61
         if not (self.learning_rate > 0.0) or not math.isfinite(self.learning_rate):
             raise ConfigError("optimizer: learning_rate must be positive")
+        if self.steps_per_update < 1:
+            raise ConfigError("optimizer: steps_per_update must be >= 1")
+        if self.bins < 1:
+            raise ConfigError("optimizer: bins must be >= 1")
+        if self.max_updates < 0:
+            raise ConfigError("optimizer: max_updates must be >= 0")
+        if not (self.lambda_geo >= 0.0) or not math.isfinite(self.lambda_geo):
+            raise ConfigError("optimizer: lambda_geo must be >= 0")
         if not (0.0 <= self.adam_beta1 < 1.0) or not (0.0 <= self.adam_beta2 < 1.0):
             raise ConfigError("optimizer: adam betas must lie in [0, 1)")
         if not self.adam_eps > 0.0:
             raise ConfigError("optimizer: adam_eps must be positive")
+        if self.fd_check_every < 0:
+            raise ConfigError("optimizer: fd_check_every must be >= 0")
+        if not self.divergence_factor > 1.0:
+            raise ConfigError("optimizer: divergence_factor must exceed 1")
+        if not self.grad_stop_tolerance >= 0.0:
+            raise ConfigError("optimizer: grad_stop_tolerance must be >= 0")
 
 
 class Adam:
