@@ -190,7 +190,8 @@ EVCM_API int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int wid
  *   poses    f64 [n_windows][B][6]
  * Outputs (in `mem` space): loss f64 [n_windows], no_survivors i32 [n_windows]
  * (may be NULL), d_depth f64 [n_windows][H][W], d_poses f64 [n_windows][B][6].
- * ev_offsets is always a HOST array of n_windows+1 entries. */
+ * ev_offsets is always a HOST array of n_windows+1 entries. Window w's clock
+ * starts at t_start_us + w * window_stride_us (see the field). */
 typedef struct {
   int n_windows;
   int width, height, n_bins;
@@ -200,6 +201,11 @@ typedef struct {
   const uint64_t* ev_offsets;
   const double* depth;
   const double* poses;
+  /* window w's clock is shifted by w * window_stride_us: its events lie in
+   * [t_start_us + w*stride, t_end_us + w*stride). 0 (zero-initialised) = all
+   * windows on one clock; window_us = consecutive windows of one event stream
+   * (evcm_cuda_window_offsets). */
+  uint64_t window_stride_us;
 } evcm_chain_batch;
 
 typedef struct {
@@ -242,6 +248,23 @@ EVCM_API int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw,
                                                     const double* poses, const double K[4],
                                                     const evcm_slice* slice, int mem, double* loss,
                                                     double* d_params, double* d_poses);
+
+/* ---- event ingestion -------------------------------------- */
+
+/* Slice validation on the device. check_window = 1: EventSlice::validate
+ * (types.hpp:137-161) -- dimensions, t_end >= t_start, then per record coordinate,
+ * polarity, timestamp order, [t_start, t_end). check_window = 0: the record checks
+ * of read_events (io.hpp:123-144) on a freshly read EVT1 payload (window ignored).
+ * Returns the error of the first violating record (its index in *first_bad when
+ * non-null), EVCM_OK otherwise. */
+EVCM_API int evcm_cuda_validate_slice(evcm_cuda_engine* e, const evcm_slice* slice,
+                                      int check_window, int mem, uint64_t* first_bad);
+/* Window boundaries of time-sorted events for the batched chain:
+ * offsets[w] = first event with t_us >= t0 + w * window_us, w = 0..n_windows
+ * (offsets is a HOST array of n_windows + 1 entries). */
+EVCM_API int evcm_cuda_window_offsets(evcm_cuda_engine* e, const evcm_event* events, size_t n,
+                                      uint64_t t0, uint64_t window_us, int n_windows, int mem,
+                                      uint64_t* offsets);
 
 /* ---- instrumentation (PhaseStats analog, engine.hpp:63-66,226-242) --------------- */
 

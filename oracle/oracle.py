@@ -31,7 +31,8 @@ EVENT_DTYPE = np.dtype(
 
 ERR_NAMES = {1: "ConfigError", 2: "DimensionMismatchError", 3: "CoordinateRangeError",
              4: "InvalidPolarityError", 5: "UnsortedEventsError", 6: "TimeRangeError",
-             7: "EmptySliceError", 99: "Error"}
+             7: "EmptySliceError", 10: "BadMagicError", 11: "TruncatedFileError",
+             12: "IoError", 99: "Error"}
 
 
 class OracleError(RuntimeError):
@@ -122,6 +123,10 @@ def ref():
                                              vp, vp]
         L.ref_optimize_flow_only.argtypes = [i32, i32, u64, u64, vp, sz, i32, f64, i32, vp, vp, vp,
                                              vp, vp]
+        L.ref_read_events.argtypes = [C.c_char_p, vp, vp, vp, vp, vp, sz, vp]
+        L.ref_write_events.argtypes = [C.c_char_p, i32, i32, u64, u64, vp, sz]
+        L.ref_validate_slice.argtypes = [i32, i32, u64, u64, vp, sz]
+        L.ref_random_slice.argtypes = [u64, sz, vp, vp, vp, vp, vp]
         _ref = L
     return _ref
 
@@ -495,3 +500,116 @@ def ref_chain_batch(depth, poses, K, t0, t1, events, ev_off, n_workers=0, want_g
                              _p(ev_off), n_workers, C.byref(ls), _p(dd), _p(dp), C.byref(sec)),
            L, "ref")
     return dict(loss_sum=ls.value, seconds=sec.value, d_depth=dd, d_poses=dp)
+
+
+# ---------------------------------------------------------------------------
+# EVT1 event files (io.hpp:106-172): numpy restatement + the reference itself
+
+
+def read_events(path):
+    """read_events (io.hpp:115-154) restated: returns (W, H, t0, t1, events) or
+    raises OracleError with the reference's error code. Checks in the
+    reference's order: header length, magic, zero dims, count vs payload,
+    trailing bytes, then per record coordinate -> polarity -> order."""
+    data = open(path, "rb").read()
+    if len(data) < 16:  # io.hpp:120-121
+        raise OracleError(11, "EVT1: file shorter than the 16-byte header")
+    if data[:4] != b"EVT1":  # io.hpp:122-123
+        raise OracleError(10, "EVT1: bad magic")
+    W = int.from_bytes(data[4:6], "little")
+    H = int.from_bytes(data[6:8], "little")
+    count = int.from_bytes(data[8:16], "little")
+    if W == 0 or H == 0:  # io.hpp:128-129
+        raise OracleError(2, "EVT1: zero sensor dimension")
+    payload = len(data) - 16
+    if count > payload // 16:  # io.hpp:131-132
+        raise OracleError(11, "EVT1: header count exceeds payload size")
+    if payload != count * 16:  # io.hpp:133-134
+        raise OracleError(12, "EVT1: trailing bytes after last record")
+    src = np.frombuffer(data, EVENT_DTYPE, count, 16)
+    ev = np.zeros(count, EVENT_DTYPE)
+    for n in EVENT_DTYPE.names:
+        ev[n] = src[n]
+    code = first_violation(ev, W, H)  # io.hpp:137-150
+    if code:
+        raise OracleError(code[1], f"EVT1: record {code[0]}")
+    t0 = int(ev["t_us"][0]) if count else 0  # io.hpp:152-153
+    t1 = int(ev["t_us"][-1]) + 1 if count else 0
+    return W, H, t0, t1, ev
+
+
+def first_violation(ev, W, H, window=None):
+    """First record failing read_events' / EventSlice::validate's checks, as
+    (index, code), or None (io.hpp:141-149, types.hpp:146-158)."""
+    if len(ev) == 0:
+        return None
+    bad_xy = (ev["x"] >= W) | (ev["y"] >= H)
+    bad_p = (ev["p"] != 1) & (ev["p"] != -1)
+    bad_s = np.zeros(len(ev), bool)
+    bad_s[1:] = ev["t_us"][1:] < ev["t_us"][:-1]
+    bad_t = np.zeros(len(ev), bool)
+    if window is not None:
+        bad_t = (ev["t_us"] < window[0]) | (ev["t_us"] >= window[1])
+    idx = np.flatnonzero(bad_xy | bad_p | bad_s | bad_t)
+    if len(idx) == 0:
+        return None
+    k = int(idx[0])
+    return k, 3 if bad_xy[k] else 4 if bad_p[k] else 5 if bad_s[k] else 6
+
+
+def write_events(path, W, H, t0, t1, ev):
+    """write_events (io.hpp:156-172) restated (after EventSlice::validate)."""
+    if W == 0 or H == 0:
+        raise OracleError(2, "event slice: width and height must be positive")
+    if t1 < t0:
+        raise OracleError(6, "event slice: t_end precedes t_start")
+    code = first_violation(ev, W, H, (t0, t1))
+    if code:
+        raise OracleError(code[1], f"event slice: record {code[0]}")
+    rec = np.zeros(len(ev), EVENT_DTYPE)
+    for n in EVENT_DTYPE.names:
+        rec[n] = ev[n]
+    with open(path, "wb") as f:
+        f.write(b"EVT1" + int(W).to_bytes(2, "little") + int(H).to_bytes(2, "little")
+                + len(ev).to_bytes(8, "little") + rec.tobytes())
+
+
+def window_offsets(ev, t0, window_us, n_windows):
+    """offsets[w] = first event with t >= t0 + w * window_us."""
+    b = np.uint64(t0) + np.arange(n_windows + 1, dtype=np.uint64) * np.uint64(window_us)
+    return np.searchsorted(ev["t_us"], b, side="left").astype(np.uint64)
+
+
+def ref_read_events(path):
+    L = ref()
+    W, H, n = C.c_int(), C.c_int(), C.c_size_t()
+    t0, t1 = C.c_uint64(), C.c_uint64()
+    _check(L.ref_read_events(os.fspath(path).encode(), C.byref(W), C.byref(H), C.byref(t0),
+                             C.byref(t1), None, 0, C.byref(n)), L, "ref")
+    ev = np.zeros(n.value, EVENT_DTYPE)
+    _check(L.ref_read_events(os.fspath(path).encode(), C.byref(W), C.byref(H), C.byref(t0),
+                             C.byref(t1), _p(ev), len(ev), C.byref(n)), L, "ref")
+    return W.value, H.value, t0.value, t1.value, ev
+
+
+def ref_write_events(path, W, H, t0, t1, ev):
+    L = ref()
+    ev = np.ascontiguousarray(ev, EVENT_DTYPE)
+    _check(L.ref_write_events(os.fspath(path).encode(), W, H, t0, t1, _p(ev), len(ev)), L, "ref")
+
+
+def ref_validate_slice(W, H, t0, t1, ev):
+    L = ref()
+    ev = np.ascontiguousarray(ev, EVENT_DTYPE)
+    return L.ref_validate_slice(W, H, t0, t1, _p(ev), len(ev))
+
+
+def ref_random_slice(seed, n):
+    """evcm_test::random_slice(std::mt19937_64(seed), n) -> (W, H, t0, t1, events)."""
+    L = ref()
+    W, H = C.c_int(), C.c_int()
+    t0, t1 = C.c_uint64(), C.c_uint64()
+    ev = np.zeros(n, EVENT_DTYPE)
+    _check(L.ref_random_slice(seed, n, C.byref(W), C.byref(H), C.byref(t0), C.byref(t1), _p(ev)),
+           L, "ref")
+    return W.value, H.value, t0.value, t1.value, ev

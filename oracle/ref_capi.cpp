@@ -19,10 +19,12 @@
 #include "evcm/engine.hpp"
 #include "evcm/fdcheck.hpp"
 #include "evcm/geometry.hpp"
+#include "evcm/io.hpp"
 #include "evcm/optimize.hpp"
 #include "evcm/predictor.hpp"
 #include "evcm/synth.hpp"
 #include "chain_support.hpp"
+#include "test_support.hpp"
 
 #define REF_API extern "C" __attribute__((visibility("default")))
 
@@ -41,6 +43,9 @@ int code_of(const std::exception& ex) {
   if (dynamic_cast<const UnsortedEventsError*>(&ex)) return 5;
   if (dynamic_cast<const TimeRangeError*>(&ex)) return 6;
   if (dynamic_cast<const EmptySliceError*>(&ex)) return 7;
+  if (dynamic_cast<const BadMagicError*>(&ex)) return 10;
+  if (dynamic_cast<const TruncatedFileError*>(&ex)) return 11;
+  if (dynamic_cast<const IoError*>(&ex)) return 12;
   return 99;
 }
 
@@ -129,6 +134,47 @@ DepthMap make_depth(int W, int H, const double* d, const std::uint8_t* mask) {
 }  // namespace
 
 REF_API const char* ref_last_error() { return g_err.c_str(); }
+
+// read_events / write_events (io.hpp:115-172). ref_read_events fills at most
+// `cap` records; *n receives the file's count.
+REF_API int ref_read_events(const char* path, int* W, int* H, std::uint64_t* t0, std::uint64_t* t1,
+                            void* ev, std::size_t cap, std::size_t* n) {
+  return guarded([&] {
+    const EventSlice s = read_events(path);
+    *W = s.width;
+    *H = s.height;
+    *t0 = s.t_start_us;
+    *t1 = s.t_end_us;
+    *n = s.events.size();
+    if (ev && s.events.size() <= cap && !s.events.empty())
+      std::memcpy(ev, s.events.data(), s.events.size() * sizeof(Event));
+  });
+}
+
+REF_API int ref_write_events(const char* path, int W, int H, std::uint64_t t0, std::uint64_t t1,
+                             const void* ev, std::size_t n) {
+  return guarded([&] { write_events(make_slice(W, H, t0, t1, ev, n), path); });
+}
+
+// evcm_test::random_slice (tests/test_support.hpp:36-58) with std::mt19937_64(seed):
+// the generator of the reference's Evt1.RandomRoundTrip10kEvents test.
+REF_API int ref_random_slice(std::uint64_t seed, std::size_t n, int* W, int* H, std::uint64_t* t0,
+                             std::uint64_t* t1, void* ev) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    const EventSlice s = evcm_test::random_slice(rng, n);
+    *W = s.width;
+    *H = s.height;
+    *t0 = s.t_start_us;
+    *t1 = s.t_end_us;
+    if (n) std::memcpy(ev, s.events.data(), n * sizeof(Event));
+  });
+}
+
+REF_API int ref_validate_slice(int W, int H, std::uint64_t t0, std::uint64_t t1, const void* ev,
+                               std::size_t n) {
+  return guarded([&] { make_slice(W, H, t0, t1, ev, n).validate(); });
+}
 
 REF_API unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
 

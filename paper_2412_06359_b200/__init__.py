@@ -5,13 +5,14 @@ See DESIGN.md for the kernels, the HBM layout and the roofline; include/evcm_cud
 for the C-ABI; INTEGRATION.md for the reference-side binding.
 """
 from .engine import (  # noqa: F401
-    BACKENDS, EVENT_DTYPE, BackwardResult, CameraIntrinsics, ConfigError, CoordinateRangeError,
+    BACKENDS, EVENT_DTYPE, BackwardResult, BadMagicError, CameraIntrinsics, ConfigError, CoordinateRangeError,
     DimensionMismatchError, EmptySliceError, Engine, EngineOptions, Error, EventSlice,
     FlowSequence, ForwardResult, GeometryFlows, InvalidPolarityError, IweStack, LossResult,
-    TimeRangeError, Trajectories, UnsortedEventsError, backend_from_name, build_iwe_stack,
+    TimeRangeError, Trajectories, TruncatedFileError, IoError, UnsortedEventsError, backend_from_name, build_iwe_stack,
     contrast_loss_backward, default_engine, depth_pose_to_flows, depth_pose_to_flows_backward,
     load_library, make_edges, rsat)
 from .predictor import (  # noqa: F401
     Adam, DecodedPredictor, DirectPredictor, OptimizerConfig, PredictorGrads, WindowGradients,
     accumulate_gradients, decode, predictor_loss_and_gradients)
+from .io import Windows, read_events, slice_windows, write_events  # noqa: F401
 from .optimize import FlowOnlyResult, TrainLog, TrainRecord, optimize_flow_only  # noqa: F401

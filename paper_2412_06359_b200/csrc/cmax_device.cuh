@@ -28,7 +28,8 @@ struct WinParams {
                      // forward AND the backward, so count/tsum cancel exactly as in fp64
   double es[kMaxRefs];      // edge times on the window clock, s (engine.hpp:244-249)
   uint32_t erel[kMaxRefs];  // edges_us[i] - edges_us[0]
-  uint64_t t0, t_end;       // slice window [t0, t_end)
+  uint64_t t0, t_end;       // slice window [t0, t_end) of window 0
+  uint64_t stride_us;       // window w spans [t0, t_end) + w * stride_us
 };
 
 // Packed event, 8 B: x = (t_us - t0) | (negative polarity << 31), y = x | y << 16.

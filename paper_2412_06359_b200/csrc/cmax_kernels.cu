@@ -73,6 +73,7 @@ __global__ void k_stage(const evcm_event* __restrict__ ev, const uint64_t* __res
   const int w = blockIdx.y;
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
+  const uint64_t t0 = P.t0 + (uint64_t)w * P.stride_us, t_end = P.t_end + (uint64_t)w * P.stride_us;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
     const evcm_event e = ev[base + k];
@@ -80,12 +81,12 @@ __global__ void k_stage(const evcm_event* __restrict__ ev, const uint64_t* __res
     if (e.x >= P.W || e.y >= P.H) code = 3;
     else if (e.p != 1 && e.p != -1) code = 4;
     else if (k > 0 && e.t_us < ev[base + k - 1].t_us) code = 5;
-    else if (e.t_us < P.t0 || e.t_us >= P.t_end) code = 6;
+    else if (e.t_us < t0 || e.t_us >= t_end) code = 6;
     if (code) {
       atomicMin(err + w, ((unsigned long long)k << 4) | code);
       continue;
     }
-    const uint32_t dt = (uint32_t)(e.t_us - P.t0);
+    const uint32_t dt = (uint32_t)(e.t_us - t0);
     packed[base + k] = make_uint2(dt | (e.p > 0 ? 0u : 0x80000000u),
                                   (uint32_t)e.x | ((uint32_t)e.y << 16));
   }

@@ -66,4 +66,11 @@ void launch_decode_adjoint(cudaStream_t s, const double* params, const double* d
 void launch_adam(cudaStream_t s, double* slots, const double* grads, double* m, double* v, size_t n,
                  double lr, double b1, double b2, double eps, double c1, double c2);
 
+// Event ingestion (ingest.cu)
+void launch_validate_events(cudaStream_t s, const evcm_event* ev, uint64_t n, int W, int H,
+                            int check_window, uint64_t t_lo, uint64_t t_hi,
+                            unsigned long long* first);
+void launch_window_offsets(cudaStream_t s, const evcm_event* ev, uint64_t n, uint64_t t0,
+                           uint64_t window_us, int n_windows, uint64_t* offsets);
+
 }  // namespace evcm_b200

@@ -257,6 +257,7 @@ WinParams make_params(int W, int H, const uint64_t* edges, int B, int n_windows,
   P.inv_window = 1.0 / P.window_s;
   P.t0 = t0;
   P.t_end = t_end;
+  P.stride_us = 0;
   return P;
 }
 
@@ -841,6 +842,7 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
       fail(EVCM_ERR_CONFIG, "chain: window must be nonempty and shorter than 2^31 us");
     const std::vector<uint64_t> edges = zeros_edges(bt->t_start_us, bt->t_end_us, B);
     WinParams P = make_params(W, H, edges.data(), B, nw, bt->t_start_us, bt->t_end_us);
+    P.stride_us = bt->window_stride_us;
     e->have_fwd = false;
     e->mark(0);
     // Rotation tables: host poses -> built on the host with the reference's own
@@ -909,7 +911,7 @@ std::vector<uint64_t> chain_signature(const evcm_cuda_engine* e, const evcm_chai
     g.push_back(b);
   };
   u((uint64_t)bt->n_windows); u((uint64_t)bt->width); u((uint64_t)bt->height); u((uint64_t)bt->n_bins);
-  u(bt->t_start_us); u(bt->t_end_us);
+  u(bt->t_start_us); u(bt->t_end_us); u(bt->window_stride_us);
   for (double k : bt->K) d(k);
   u((uint64_t)(uintptr_t)bt->events); u((uint64_t)(uintptr_t)(depth_dev ? depth_dev : bt->depth));
   u((uint64_t)(uintptr_t)bt->poses); u((uint64_t)(uintptr_t)out->loss);
@@ -997,6 +999,59 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
 
 int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
   return evcm_cuda_chain_batch2(e, bt, mem, mem, out);
+}
+
+int evcm_cuda_validate_slice(evcm_cuda_engine* e, const evcm_slice* sl, int check_window, int mem,
+                             uint64_t* first_bad) {
+  return guarded([&] {
+    if (!e || !sl || (sl->n_events && !sl->events)) fail(EVCM_ERR_CONFIG, "null argument");
+    const std::string what = check_window ? "event slice: " : "EVT1: ";
+    if (sl->width == 0 || sl->height == 0) fail(EVCM_ERR_DIMENSION, what + "zero sensor dimension");
+    if (check_window && sl->t_end_us < sl->t_start_us)
+      fail(EVCM_ERR_TIME_RANGE, "event slice: t_end precedes t_start");
+    set_device(e);
+    reset_launch_count();
+    const size_t n = sl->n_events;
+    if (n == 0) {
+      e->last_launches = 0;
+      return;
+    }
+    const evcm_event* d = to_device(e, "ingest_events", sl->events, n, mem);
+    unsigned long long* first = e->get<unsigned long long>("ingest_first", 1);
+    ck(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), e->stream), "memset");
+    launch_validate_events(e->stream, d, n, sl->width, sl->height, check_window, sl->t_start_us,
+                           sl->t_end_us, first);
+    unsigned long long* h = e->pinned<unsigned long long>("ingest_first_h", 1);
+    ck(cudaMemcpyAsync(h, first, sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "validate_slice");
+    e->last_launches = launch_count();
+    if (*h == ~0ull) return;
+    const uint64_t k = *h >> 4;
+    const int code = (int)(*h & 0xf);
+    if (first_bad) *first_bad = k;
+    const std::string rec = what + "record " + std::to_string(k);
+    if (code == EVCM_ERR_COORDINATE) fail(code, rec + " coordinate out of range");
+    if (code == EVCM_ERR_POLARITY) fail(code, rec + " bad polarity");
+    if (code == EVCM_ERR_UNSORTED) fail(code, rec + " breaks timestamp order");
+    fail(code, rec + " timestamp outside [t_start, t_end)");
+  });
+}
+
+int evcm_cuda_window_offsets(evcm_cuda_engine* e, const evcm_event* events, size_t n, uint64_t t0,
+                             uint64_t window_us, int n_windows, int mem, uint64_t* offsets) {
+  return guarded([&] {
+    if (!e || !offsets || (n && !events)) fail(EVCM_ERR_CONFIG, "null argument");
+    if (n_windows < 1 || window_us == 0) fail(EVCM_ERR_CONFIG, "windows: need n_windows >= 1 and a nonzero length");
+    set_device(e);
+    reset_launch_count();
+    const evcm_event* d = to_device(e, "ingest_events", events, n, mem);
+    uint64_t* od = e->get<uint64_t>("ingest_offsets", (size_t)n_windows + 1);
+    launch_window_offsets(e->stream, d, n, t0, window_us, n_windows, od);
+    ck(cudaMemcpyAsync(offsets, od, ((size_t)n_windows + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                       e->stream), "D2H offsets");
+    ck(cudaStreamSynchronize(e->stream), "window_offsets");
+    e->last_launches = launch_count();
+  });
 }
 
 int evcm_cuda_decode(evcm_cuda_engine* e, int pw, int ph, int factor, const double* params, int mem,

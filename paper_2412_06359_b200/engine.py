@@ -36,6 +36,14 @@ class IoError(Error):
     pass
 
 
+class BadMagicError(IoError):
+    """File does not start with the expected format magic (types.hpp:28-31)."""
+
+
+class TruncatedFileError(IoError):
+    """File ends mid-header or mid-record (types.hpp:33-36)."""
+
+
 class UnsortedEventsError(Error):
     pass
 
@@ -106,7 +114,7 @@ class _ChainBatch(C.Structure):
     _fields_ = [("n_windows", C.c_int), ("width", C.c_int), ("height", C.c_int),
                 ("n_bins", C.c_int), ("t_start_us", C.c_uint64), ("t_end_us", C.c_uint64),
                 ("K", C.c_double * 4), ("events", C.c_void_p), ("ev_offsets", C.c_void_p),
-                ("depth", C.c_void_p), ("poses", C.c_void_p)]
+                ("depth", C.c_void_p), ("poses", C.c_void_p), ("window_stride_us", C.c_uint64)]
 
 
 class _ChainOut(C.Structure):
@@ -159,6 +167,8 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_decode.argtypes = [vp, i32, i32, i32, vp, i32, vp]
     L.evcm_cuda_decode_backward.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp]
     L.evcm_cuda_adam_step.argtypes = [vp, sz, vp, vp, vp, vp, i32, f64, f64, f64, f64, i32]
+    L.evcm_cuda_validate_slice.argtypes = [vp, vp, i32, i32, vp]
+    L.evcm_cuda_window_offsets.argtypes = [vp, vp, sz, u64, u64, i32, i32, vp]
     L.evcm_cuda_predictor_loss_and_gradients.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp,
                                                          i32, vp, vp, vp]
     _lib = L
@@ -512,6 +522,28 @@ class Engine:
         if int(e[0]) != slice_.t_start_us or int(e[-1]) != slice_.t_end_us:
             raise ConfigError("engine: flow bin edges do not span the slice window")
 
+    # -- event ingestion (io.py)
+    def validate_slice(self, slice_: EventSlice, check_window: bool = True) -> None:
+        """EventSlice::validate (types.hpp:137-161) on the device; with
+        ``check_window=False`` only read_events' record checks (io.hpp:123-144)."""
+        s = slice_._c()
+        mem = _mem_of(slice_.events if slice_.n_events else None)
+        _raise(load_library().evcm_cuda_validate_slice(self._h, C.byref(s), int(check_window),
+                                                       mem, None))
+
+    def window_offsets(self, events, t0_us: int, window_us: int, n_windows: int) -> np.ndarray:
+        """offsets[w] = first event with t_us >= t0 + w * window_us (w = 0..n_windows)
+        over time-sorted events (numpy EVENT_DTYPE or a torch cuda [n, 16] uint8
+        tensor): the ev_offsets of ``chain_batch``."""
+        if not _is_torch(events):
+            events = np.ascontiguousarray(events, EVENT_DTYPE)
+        n = events.numel() // 16 if _is_torch(events) else len(events)
+        offs = np.zeros(int(n_windows) + 1, np.uint64)
+        _raise(load_library().evcm_cuda_window_offsets(
+            self._h, _ptr(events) if n else None, n, int(t0_us), int(window_us), int(n_windows),
+            _mem_of(events if n else None), offs.ctypes.data_as(C.c_void_p)))
+        return offs
+
     # -- instrumentation
     def set_timing(self, on: bool = True):
         _raise(load_library().evcm_cuda_set_timing(self._h, int(on)))
@@ -539,7 +571,7 @@ class Engine:
 
     # -- batched chain (optimize.hpp:205-241 composition over many windows)
     def chain_batch(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out=None,
-                    out_device=None):
+                    out_device=None, window_stride_us: int = 0):
         """Per window w: depth_pose_to_flows(depth[w], poses[w]) -> forward ->
         backward -> depth_pose_to_flows_backward (the predictor_loss_and_gradients
         composition, optimize.hpp:205-241, without decode / L_geo).
@@ -548,7 +580,9 @@ class Engine:
         records), ev_offsets [n+1] (host). Returns (loss [n], d_depth [n, H, W],
         d_poses [n, B, 6]). Inputs may be host (numpy / pinned torch) or device
         (torch cuda); outputs live on the device when ``out_device`` (default:
-        same side as the inputs)."""
+        same side as the inputs). Window w spans [t_start_us, t_end_us) +
+        w * window_stride_us (0: one clock for all windows; the window length:
+        consecutive windows of one stream, see io.slice_windows)."""
         nw, H, W = depth.shape
         B = poses.shape[1]
         in_mem = _mem_of(depth, poses, events)
@@ -574,7 +608,8 @@ class Engine:
             if not _is_torch(events):
                 events = np.ascontiguousarray(events, EVENT_DTYPE)
         bt = _ChainBatch(nw, W, H, B, int(t_start_us), int(t_end_us), (C.c_double * 4)(*K),
-                         _ptr(events), offs.ctypes.data_as(C.c_void_p), _ptr(depth), _ptr(poses))
+                         _ptr(events), offs.ctypes.data_as(C.c_void_p), _ptr(depth), _ptr(poses),
+                         int(window_stride_us))
         co = _ChainOut(_ptr(out[0]), None, _ptr(out[1]), _ptr(out[2]))
         _raise(load_library().evcm_cuda_chain_batch2(self._h, C.byref(bt), in_mem, out_mem,
                                                      C.byref(co)))

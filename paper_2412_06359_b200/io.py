@@ -1,0 +1,172 @@
+"""Event ingestion: the EVT1 event files of the reference
+(io.hpp:106-172) and the cut of one event stream into the windows of the
+batched chain.
+
+EVT1 = a 16-byte header ("EVT1", u16 width, u16 height, u64 count, little
+endian) followed by ``count`` 16-byte records (u64 t_us, u16 x, u16 y, i8 p, 3
+pad bytes) -- byte-identical to evcm::Event, so a payload is read straight into
+the record layout (pinned host memory and one H2D copy for device slices) and
+never re-packed on the host. The header checks run on the host in the
+reference's order (they need no payload); the per-record checks of read_events
+(coordinate, polarity, timestamp order, io.hpp:134-144) run on the device
+(``Engine.validate_slice``), reporting the FIRST violating record with the
+reference's error class, so a file the reference rejects is rejected here with
+the same exception type.
+
+The reference has no window slicer (its callers pass std::vector<EventSlice>
+to run_window, train.hpp); ``slice_windows`` cuts a time-sorted stream into
+consecutive ``window_us`` windows with one device binary search per boundary
+and hands ``Engine.chain_batch`` its ``ev_offsets`` and ``window_stride_us``.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .engine import (EVENT_DTYPE, BadMagicError, ConfigError, DimensionMismatchError, Engine,
+                     EventSlice, IoError, TruncatedFileError, _is_torch, default_engine)
+
+EVT1_MAGIC = b"EVT1"
+EVT1_HEADER_BYTES = 16  # io.hpp:117
+EVT1_RECORD_BYTES = 16  # io.hpp:118
+
+
+def _parse_header(head: bytes, file_bytes: int, path) -> tuple:
+    """read_events' header checks, in the reference's order (io.hpp:120-132)."""
+    if file_bytes < EVT1_HEADER_BYTES:
+        raise TruncatedFileError("EVT1: file shorter than the 16-byte header")
+    if head[:4] != EVT1_MAGIC:
+        raise BadMagicError(f"EVT1: bad magic in {path}")
+    width = int.from_bytes(head[4:6], "little")
+    height = int.from_bytes(head[6:8], "little")
+    count = int.from_bytes(head[8:16], "little")
+    if width == 0 or height == 0:
+        raise DimensionMismatchError("EVT1: zero sensor dimension")
+    payload = file_bytes - EVT1_HEADER_BYTES
+    if count > payload // EVT1_RECORD_BYTES:
+        raise TruncatedFileError("EVT1: header count exceeds payload size")
+    if payload != count * EVT1_RECORD_BYTES:
+        raise IoError("EVT1: trailing bytes after last record")
+    return width, height, count
+
+
+def read_events(path, device: bool = False, engine: Optional[Engine] = None) -> EventSlice:
+    """read_events (io.hpp:115-154). ``device=True`` returns the events as a torch
+    cuda uint8 tensor [n, 16] (one pinned H2D copy); otherwise a numpy
+    EVENT_DTYPE array. The window is the tightest one holding every event:
+    [first t, last t + 1) (empty file: [0, 0))."""
+    path = os.fspath(path)
+    try:
+        size = os.path.getsize(path)
+        f = open(path, "rb")
+    except OSError as e:
+        raise IoError(f"cannot open {path}: {e}") from None
+    with f:
+        head = f.read(EVT1_HEADER_BYTES)
+        width, height, count = _parse_header(head, size, path)
+        nbytes = count * EVT1_RECORD_BYTES
+        if device:
+            import torch
+            eng = engine or default_engine()
+            host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            if nbytes and f.readinto(memoryview(host.numpy())) != nbytes:
+                raise TruncatedFileError("EVT1: short read")
+            raw = host.numpy().view(EVENT_DTYPE) if nbytes else np.zeros(0, EVENT_DTYPE)
+            events = host.view(-1, EVT1_RECORD_BYTES).to(
+                torch.device("cuda", eng.opts.device), non_blocking=True) if nbytes else \
+                torch.empty((0, EVT1_RECORD_BYTES), dtype=torch.uint8,
+                            device=torch.device("cuda", eng.opts.device))
+        else:
+            buf = bytearray(nbytes)
+            if nbytes and f.readinto(buf) != nbytes:
+                raise TruncatedFileError("EVT1: short read")
+            # copy into a zero-padded array: the reference rebuilds each Event,
+            # so the 3 pad bytes of a record never survive a read (io.hpp:137-140)
+            src = np.frombuffer(buf, EVENT_DTYPE)
+            events = np.zeros(count, EVENT_DTYPE)
+            for name in EVENT_DTYPE.names:
+                events[name] = src[name]
+            raw = events
+    t0 = int(raw["t_us"][0]) if count else 0
+    t1 = int(raw["t_us"][-1]) + 1 if count else 0
+    s = EventSlice(width, height, t0, t1, events)
+    if count:
+        (engine or default_engine()).validate_slice(s, check_window=False)
+    return s
+
+
+def _host_events(slice_: EventSlice) -> np.ndarray:
+    ev = slice_.events
+    if _is_torch(ev):
+        ev = ev.reshape(-1).cpu().numpy().view(EVENT_DTYPE)
+    return np.asarray(ev, EVENT_DTYPE)
+
+
+def write_events(slice_: EventSlice, path, engine: Optional[Engine] = None) -> None:
+    """write_events (io.hpp:156-172): EventSlice::validate (on the device), then
+    the header and zero-padded records."""
+    eng = engine or default_engine()
+    eng.validate_slice(slice_, check_window=True)
+    ev = _host_events(slice_)
+    rec = np.zeros(len(ev), EVENT_DTYPE)  # pad bytes written as 0 (io.hpp:170)
+    for name in EVENT_DTYPE.names:
+        rec[name] = ev[name]
+    head = (EVT1_MAGIC + int(slice_.width).to_bytes(2, "little")
+            + int(slice_.height).to_bytes(2, "little") + len(ev).to_bytes(8, "little"))
+    try:
+        with open(os.fspath(path), "wb") as f:
+            f.write(head)
+            f.write(rec.tobytes())
+    except OSError as e:
+        raise IoError(f"cannot write {path}: {e}") from None
+
+
+@dataclass
+class Windows:
+    """Consecutive windows [t0 + w*window_us, t0 + (w+1)*window_us) of one slice:
+    events of window w = events[offsets[w] : offsets[w+1]]."""
+    slice: EventSlice
+    t0_us: int
+    window_us: int
+    offsets: np.ndarray  # uint64 [n_windows + 1]
+
+    @property
+    def n_windows(self) -> int:
+        return len(self.offsets) - 1
+
+    def window(self, w: int) -> EventSlice:
+        """Window w as an EventSlice (a view of the events, no copy)."""
+        if not 0 <= w < self.n_windows:
+            raise ConfigError(f"window {w} outside [0, {self.n_windows})")
+        a, b = int(self.offsets[w]), int(self.offsets[w + 1])
+        t = self.t0_us + w * self.window_us
+        return EventSlice(self.slice.width, self.slice.height, t, t + self.window_us,
+                          self.slice.events[a:b])
+
+    def chain_batch(self, engine: Engine, depth, poses, k, out=None, out_device=None):
+        """Engine.chain_batch over every window (one clock shift per window)."""
+        return engine.chain_batch(depth, poses, k, self.t0_us, self.t0_us + self.window_us,
+                                  self.slice.events, self.offsets, out=out,
+                                  out_device=out_device, window_stride_us=self.window_us)
+
+
+def slice_windows(slice_: EventSlice, window_us: int, n_windows: Optional[int] = None,
+                  t0_us: Optional[int] = None, engine: Optional[Engine] = None) -> Windows:
+    """Cuts a time-sorted slice into consecutive ``window_us`` windows from
+    ``t0_us`` (default: the slice's t_start); ``n_windows`` defaults to the
+    windows needed to cover [t0, t_end). Boundaries come from a device binary
+    search over the events (Engine.window_offsets)."""
+    if window_us <= 0:
+        raise ConfigError("windows: window length must be positive")
+    t0 = int(slice_.t_start_us if t0_us is None else t0_us)
+    if n_windows is None:
+        span = max(0, int(slice_.t_end_us) - t0)
+        n_windows = max(1, -(-span // int(window_us)))
+    if n_windows < 1:
+        raise ConfigError("windows: need at least one window")
+    eng = engine or default_engine()
+    offs = eng.window_offsets(slice_.events, t0, int(window_us), int(n_windows))
+    return Windows(slice_, t0, int(window_us), offs)

@@ -11,6 +11,10 @@ Each fixture is an .npz with the inputs and the reference outputs:
   predictor_<seed>.npz  make_chain_instance as a raw DirectPredictor + the reference's
                      decode and predictor_loss_and_gradients (optimize.hpp:205-241)
   adam.npz           Adam::step (optimize.hpp:115-134), 3 steps on fixed gradients
+  evt1/*.evt1        EVT1 files written by the reference's write_events (io.hpp:156-172),
+                     plus the byte-patched variants of tests/test_core_io.cpp:73-137;
+  evt1.npz           the reference's read_events outcome for each (error code or
+                     W, H, t0, t1, events)
 """
 import os
 import sys
@@ -51,9 +55,51 @@ def predictor_fixtures():
     save("adam.npz", slots=s, grads=g, lr=0.01, steps=3, out=O.ref_adam_steps(s, g, 3, 0.01))
 
 
+EVT1_FILES = ["empty", "three", "random_2k", "bad_magic", "trunc_record", "trunc_header",
+              "unsorted", "coord_at_width", "zero_polarity", "trailing", "zero_width"]
+
+
+def evt1_fixtures():
+    """The reference's EVT1 tests (tests/test_core_io.cpp:45-150) as files."""
+    d = os.path.join(HERE, "evt1")
+    os.makedirs(d, exist_ok=True)
+    f = lambda n: os.path.join(d, n + ".evt1")  # noqa: E731
+    three = O.make_events([100, 250, 400], [1, 3, 9], [2, 4, 7], [1, -1, 1])  # :33-41
+    O.ref_write_events(f("empty"), 32, 24, 0, 0, np.zeros(0, O.EVENT_DTYPE))
+    O.ref_write_events(f("three"), 10, 8, 100, 401, three)
+    W, H, t0, t1, ev = O.ref_random_slice(7, 2000)
+    O.ref_write_events(f("random_2k"), W, H, t0, t1, ev)
+    base = open(f("three"), "rb").read()
+
+    def patched(name, fn):
+        b = bytearray(base)
+        b = fn(b) or b
+        open(f(name), "wb").write(bytes(b))
+
+    patched("bad_magic", lambda b: b.__setitem__(0, ord("X")))
+    patched("trunc_record", lambda b: b[:-7])
+    patched("trunc_header", lambda b: b[:10])
+    patched("unsorted", lambda b: b.__setitem__(slice(16, 19), b"\xff\xff\xff"))
+    patched("coord_at_width", lambda b: b.__setitem__(slice(24, 26), b"\x0a\x00"))
+    patched("zero_polarity", lambda b: b.__setitem__(28, 0))
+    patched("trailing", lambda b: b + b"\x00")
+    patched("zero_width", lambda b: b.__setitem__(slice(4, 6), b"\x00\x00"))
+    out = {}
+    for n in EVT1_FILES:
+        try:
+            W, H, t0, t1, ev = O.ref_read_events(f(n))
+            out[n + "_code"] = 0
+            out[n + "_hdr"] = np.array([W, H, t0, t1], np.uint64)
+            out[n + "_events"] = ev.view(np.uint8).reshape(-1, 16)
+        except O.OracleError as e:
+            out[n + "_code"] = e.code
+    save("evt1.npz", **out)
+
+
 def main():
     if not O.ref_available():
         O.build(ref=True)
+    evt1_fixtures()
     predictor_fixtures()
     for seed in (100, 7, 503, 1300):
         window_fixture(f"fd_{seed}.npz", O.ref_fd_instance(seed))
