@@ -249,6 +249,47 @@ EVCM_API int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw,
                                                     const evcm_slice* slice, int mem, double* loss,
                                                     double* d_params, double* d_poses);
 
+/* predictor_loss_and_gradients (optimize.hpp:205-241) with the depth-consistency
+ * term: losses[3] = {l_cm, l_geo, total = l_cm + lambda_geo * l_geo}; with
+ * lambda_geo > 0, L_geo runs per bin on (depth, depth) with upstream
+ * lambda_geo / B and its gradients add onto the CMax ones (optimize.hpp:219-236,
+ * predictor.hpp:153-171); lambda_geo <= 0 switches the term off, as in the
+ * reference (total = l_cm + lambda_geo * 0). */
+EVCM_API int evcm_cuda_predictor_loss_and_gradients_geo(
+    evcm_cuda_engine* e, int pw, int ph, int factor, const double* params, int n_bins,
+    const double* poses, const double K[4], const evcm_slice* slice, double lambda_geo, int mem,
+    double* losses, double* d_params, double* d_poses);
+
+/* ---- geometry-consistency loss L_geo ---------------------- */
+
+/* Outputs of evcm_cuda_geometry_consistency_loss, all in `mem` space; any may be
+ * NULL. Per-pose arrays are [n_poses][...]; d_poses rows are {omega xyz, trans xyz}. */
+typedef struct {
+  double* value;         /* [n_poses] GeoLossTerms::value (0 when the valid set is empty) */
+  int64_t* n_valid;      /* [n_poses] GeoLossTerms::n_valid */
+  double* projected;     /* [n_poses][H][W] GeoLossTerms::projected */
+  double* interpolated;  /* [n_poses][H][W] GeoLossTerms::interpolated */
+  uint8_t* valid;        /* [n_poses][H][W] GeoLossTerms::valid */
+  double* d_d0;          /* [n_poses][H][W] GeoLossGrad::d_d0 (want_grad) */
+  double* d_d1;          /* [n_poses][H][W] GeoLossGrad::d_d1 (want_grad) */
+  double* d_poses;       /* [n_poses][6]    GeoLossGrad::d_omega, d_trans (want_grad) */
+  double* d_depth_sum;   /* [H][W] sum_i (d_d0_i + d_d1_i), the predictor's extra depth
+                            term (optimize.hpp:229-230) (want_grad) */
+} evcm_geo_out;
+
+/* geometry_consistency_loss (want_grad = 0, geometry.hpp:416-453) or
+ * geometry_consistency_loss_backward (want_grad = 1, :458-534, scaled by
+ * `upstream`) of depth maps d0 -> d1 (masks may be NULL = all valid) for each of
+ * n_poses poses {omega, trans}. Membership (projection, z-min winners, target
+ * depth, valid set) is bit-identical to the reference; sums over pixels differ
+ * only by rounding order. */
+EVCM_API int evcm_cuda_geometry_consistency_loss(evcm_cuda_engine* e, int W, int H, const double* d0,
+                                                 const uint8_t* mask0, const double* d1,
+                                                 const uint8_t* mask1, int n_poses,
+                                                 const double* poses, const double K[4],
+                                                 double upstream, int want_grad, int mem,
+                                                 evcm_geo_out* out);
+
 /* ---- event ingestion -------------------------------------- */
 
 /* Slice validation on the device. check_window = 1: EventSlice::validate

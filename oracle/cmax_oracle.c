@@ -583,6 +583,156 @@ int orc_depth_pose_to_flows_backward(int W, int H, const double* depth, const ui
   return ORC_OK;
 }
 
+/* ---- geometry-consistency loss (geometry.hpp:329-534) ------------------------------ */
+
+/* reproject (geometry.hpp:157-166): returns valid (z > 0); px, py, z out. */
+static int reproject(double x, double y, double d, const double* R, const double* tr,
+                     const double* K, double* px, double* py, double* z) {
+  const double fx = K[0], fy = K[1], cx = K[2], cy = K[3];
+  const double bp[3] = {d * (x - cx) / fx, d * (y - cy) / fy, d}; /* backproject :147-149 */
+  double p[3];
+  mat3_vec(R, bp, p);
+  p[0] = p[0] + tr[0];
+  p[1] = p[1] + tr[1];
+  p[2] = p[2] + tr[2];
+  *z = p[2];
+  if (!(p[2] > 0.0)) return 0;
+  *px = fx * p[0] / p[2] + cx;
+  *py = fy * p[1] / p[2] + cy;
+  return 1;
+}
+
+int orc_geo_loss(int W, int H, const double* d0, const uint8_t* m0, const double* d1,
+                 const uint8_t* m1, const double* pose, const double* K, double upstream,
+                 int want_grad, double* value, int64_t* n_valid_out, double* projected,
+                 double* interpolated, uint8_t* valid, double* d_d0, double* d_d1,
+                 double* d_pose) {
+  const size_t HW = (size_t)W * H;
+  const double fx = K[0], fy = K[1], cx = K[2], cy = K[3];
+  double R[9], dR[27];
+  orc_rodrigues(pose, R);
+  orc_rodrigues_jacobian(pose, dR);
+  const double* tr = pose + 3;
+  double* ppx = malloc(sizeof(double) * HW);
+  double* ppy = malloc(sizeof(double) * HW);
+  double* pz = malloc(sizeof(double) * HW);
+  int* pcell = malloc(sizeof(int) * HW);
+  double* zbuf = malloc(sizeof(double) * HW);
+  int64_t* winner = malloc(sizeof(int64_t) * HW);
+  if (projected) memset(projected, 0, sizeof(double) * HW);
+  if (interpolated) memset(interpolated, 0, sizeof(double) * HW);
+  if (valid) memset(valid, 0, HW);
+  if (d_d0) memset(d_d0, 0, sizeof(double) * HW);
+  if (d_d1) memset(d_d1, 0, sizeof(double) * HW);
+  if (d_pose) memset(d_pose, 0, sizeof(double) * 6);
+  *value = 0.0;
+  *n_valid_out = 0;
+  /* project_with_zmin (geometry.hpp:359-390) */
+  int any = 0;
+  for (size_t q = 0; q < HW; ++q) {
+    zbuf[q] = INFINITY;
+    winner[q] = -1;
+    pcell[q] = -1;
+  }
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const size_t q = idx(x, y, W);
+      if (m0 && !m0[q]) continue;
+      const double d = d0[q];
+      if (!(d > 0.0)) continue;
+      double px, py, z;
+      if (!reproject((double)x, (double)y, d, R, tr, K, &px, &py, &z)) continue;
+      if (!in_bounds(px, py, W, H)) continue;
+      const int nx = (int)lround(px), ny = (int)lround(py);
+      ppx[q] = px;
+      ppy[q] = py;
+      pz[q] = z;
+      pcell[q] = (int)idx(nx, ny, W);
+      any = 1;
+      if (z < zbuf[pcell[q]]) {
+        zbuf[pcell[q]] = z;
+        winner[pcell[q]] = (int64_t)q;
+      }
+    }
+  double sum = 0.0;
+  int64_t n_valid = 0;
+  double dom[3] = {0, 0, 0}, dtr[3] = {0, 0, 0};
+  for (int y = 0; any && y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      const size_t q = idx(x, y, W);
+      if (pcell[q] < 0 || winner[pcell[q]] != (int64_t)q) continue;
+      /* sample_target_depth (geometry.hpp:394-409) */
+      const cell_t c = bilin_cell(ppx[q], ppy[q], W, H);
+      if (m1 && !(m1[idx(c.x0, c.y0, W)] && m1[idx(c.x1, c.y0, W)] && m1[idx(c.x0, c.y1, W)] &&
+                  m1[idx(c.x1, c.y1, W)]))
+        continue;
+      const double v00 = d1[idx(c.x0, c.y0, W)], v10 = d1[idx(c.x1, c.y0, W)];
+      const double v01 = d1[idx(c.x0, c.y1, W)], v11 = d1[idx(c.x1, c.y1, W)];
+      const double b = w00(&c) * v00 + w10(&c) * v10 + w01(&c) * v01 + w11(&c) * v11;
+      if (!(b > 0.0)) continue;
+      const double dbx = (1.0 - c.wy) * (v10 - v00) + c.wy * (v11 - v01);
+      const double dby = (1.0 - c.wx) * (v01 - v00) + c.wx * (v11 - v10);
+      const double a = pz[q];
+      if (projected) projected[q] = a;
+      if (interpolated) interpolated[q] = b;
+      if (valid) valid[q] = 1;
+      ++n_valid;
+      sum += fabs(a - b) / (a + b);
+      if (!want_grad) continue;
+      /* geometry.hpp:479-516 */
+      const double s = (a > b) ? 1.0 : (a < b ? -1.0 : 0.0);
+      const double inv_ab = 1.0 / ((a + b) * (a + b));
+      const double ga = 2.0 * s * b * inv_ab;
+      const double gb = -2.0 * s * a * inv_ab;
+      /* reproject_with_grads (geometry.hpp:185-209) */
+      const double d = d0[q];
+      const double ray[3] = {1.0 * ((double)x - cx) / fx, 1.0 * ((double)y - cy) / fy, 1.0};
+      double rray[3];
+      mat3_vec(R, ray, rray);
+      const double p[3] = {d * rray[0] + tr[0], d * rray[1] + tr[1], d * rray[2] + tr[2]};
+      const double iz = 1.0 / p[2];
+      const double ju[3] = {fx * iz, 0.0, -fx * p[0] * iz * iz};
+      const double jv[3] = {0.0, fy * iz, -fy * p[1] * iz * iz};
+      const double dpdx = dot3(ju, rray), dpdy = dot3(jv, rray);
+      d_d0[q] += ga * rray[2] + gb * (dbx * dpdx + dby * dpdy);
+      d_d1[idx(c.x0, c.y0, W)] += gb * w00(&c);
+      d_d1[idx(c.x1, c.y0, W)] += gb * w10(&c);
+      d_d1[idx(c.x0, c.y1, W)] += gb * w01(&c);
+      d_d1[idx(c.x1, c.y1, W)] += gb * w11(&c);
+      for (int k = 0; k < 3; ++k) {
+        double m[3], q3[3];
+        mat3_vec(dR + 9 * k, ray, m);
+        q3[0] = d * m[0];
+        q3[1] = d * m[1];
+        q3[2] = d * m[2];
+        dtr[k] += ga * (k == 2 ? 1.0 : 0.0) + gb * (dbx * ju[k] + dby * jv[k]);
+        dom[k] += ga * q3[2] + gb * (dbx * dot3(ju, q3) + dby * dot3(jv, q3));
+      }
+    }
+  if (n_valid > 0) {
+    *value = sum / (double)n_valid;
+    *n_valid_out = n_valid;
+    if (want_grad) {
+      const double scale = upstream / (double)n_valid;
+      for (size_t q = 0; q < HW; ++q) {
+        d_d0[q] *= scale;
+        d_d1[q] *= scale;
+      }
+      for (int k = 0; k < 3; ++k) {
+        d_pose[k] = scale * dom[k];
+        d_pose[3 + k] = scale * dtr[k];
+      }
+    }
+  }
+  free(ppx);
+  free(ppy);
+  free(pz);
+  free(pcell);
+  free(zbuf);
+  free(winner);
+  return ORC_OK;
+}
+
 /* ---- predictor decode chain -------------------------------------------------------- */
 
 /* predictor.hpp:25-27 */

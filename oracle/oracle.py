@@ -87,6 +87,8 @@ def lib():
         L.orc_decode_backward.argtypes = [i32, i32, i32, vp, vp, vp]
         L.orc_adam_step.argtypes = [sz, vp, vp, vp, vp, i32, f64, f64, f64, f64]
         L.orc_adam_step.restype = None
+        L.orc_geo_loss.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp,
+                                   vp, vp, vp]
         _lib = L
     return _lib
 
@@ -127,6 +129,10 @@ def ref():
         L.ref_write_events.argtypes = [C.c_char_p, i32, i32, u64, u64, vp, sz]
         L.ref_validate_slice.argtypes = [i32, i32, u64, u64, vp, sz]
         L.ref_random_slice.argtypes = [u64, sz, vp, vp, vp, vp, vp]
+        L.ref_geo_loss.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp,
+                                   vp, vp, vp, vp]
+        L.ref_predictor_loss.argtypes = [i32, i32, i32, vp, i32, vp, vp, u64, u64, vp, sz, f64, vp,
+                                         vp, vp]
         _ref = L
     return _ref
 
@@ -613,3 +619,67 @@ def ref_random_slice(seed, n):
     _check(L.ref_random_slice(seed, n, C.byref(W), C.byref(H), C.byref(t0), C.byref(t1), _p(ev)),
            L, "ref")
     return W.value, H.value, t0.value, t1.value, ev
+
+
+# ---------------------------------------------------------------------------
+# geometry-consistency loss L_geo (geometry.hpp:329-543)
+
+
+def _geo_outputs(H, W):
+    return dict(value=np.zeros(1), n_valid=np.zeros(1, np.int64), projected=np.zeros((H, W)),
+                interpolated=np.zeros((H, W)), valid=np.zeros((H, W), np.uint8),
+                d_d0=np.zeros((H, W)), d_d1=np.zeros((H, W)), d_pose=np.zeros(6))
+
+
+def geo_loss(d0, d1, pose, K, m0=None, m1=None, upstream=1.0, want_grad=True):
+    """orc_geo_loss: the restatement (one pose). Returns a dict of the terms and,
+    with want_grad, d_d0 / d_d1 / d_pose (omega, trans)."""
+    L = lib()
+    H, W = d0.shape
+    o = _geo_outputs(H, W)
+    c = lambda a, t=np.float64: None if a is None else np.ascontiguousarray(a, t)  # noqa: E731
+    d0, d1, pose, K = c(d0), c(d1), c(pose), c(K)
+    m0, m1 = c(m0, np.uint8), c(m1, np.uint8)
+    _check(L.orc_geo_loss(W, H, _p(d0), _p(m0), _p(d1), _p(m1), _p(pose), _p(K), upstream,
+                          int(want_grad), _p(o["value"]), _p(o["n_valid"]), _p(o["projected"]),
+                          _p(o["interpolated"]), _p(o["valid"]), _p(o["d_d0"]), _p(o["d_d1"]),
+                          _p(o["d_pose"])), L)
+    o["value"], o["n_valid"] = float(o["value"][0]), int(o["n_valid"][0])
+    o["empty"] = o["n_valid"] == 0
+    return o
+
+
+def ref_geo_loss(d0, d1, pose, K, m0=None, m1=None, upstream=1.0, want_grad=True):
+    """The reference's geometry_consistency_loss[_backward] (one pose)."""
+    L = ref()
+    H, W = d0.shape
+    o = _geo_outputs(H, W)
+    empty = np.zeros(1, np.int32)
+    c = lambda a, t=np.float64: None if a is None else np.ascontiguousarray(a, t)  # noqa: E731
+    d0, d1, pose, K = c(d0), c(d1), c(pose), c(K)
+    m0, m1 = c(m0, np.uint8), c(m1, np.uint8)
+    _check(L.ref_geo_loss(W, H, _p(d0), _p(m0), _p(d1), _p(m1), _p(pose), _p(K), upstream,
+                          int(want_grad), _p(o["value"]), _p(o["n_valid"]), _p(empty),
+                          _p(o["projected"]), _p(o["interpolated"]), _p(o["valid"]),
+                          _p(o["d_d0"]), _p(o["d_d1"]), _p(o["d_pose"])), L, "ref")
+    o["value"], o["n_valid"] = float(o["value"][0]), int(o["n_valid"][0])
+    o["empty"] = bool(empty[0])
+    return o
+
+
+def ref_predictor_loss(params, factor, poses, K, t0, t1, events, lambda_geo):
+    """The reference's predictor_loss_and_gradients with any lambda_geo:
+    ((l_cm, l_geo, total), d_params, d_poses)."""
+    L = ref()
+    ph, pw = params.shape
+    B = poses.shape[0]
+    losses = np.zeros(3)
+    dpar = np.zeros((ph, pw))
+    dpo = np.zeros((B, 6))
+    params = np.ascontiguousarray(params, np.float64)
+    poses = np.ascontiguousarray(poses, np.float64)
+    K = np.ascontiguousarray(K, np.float64)
+    ev = np.ascontiguousarray(events, EVENT_DTYPE)
+    _check(L.ref_predictor_loss(pw, ph, factor, _p(params), B, _p(poses), _p(K), t0, t1, _p(ev),
+                                len(ev), lambda_geo, _p(losses), _p(dpar), _p(dpo)), L, "ref")
+    return tuple(losses), dpar, dpo

@@ -523,6 +523,74 @@ REF_API int ref_predictor_instance(std::uint64_t seed, int sensor_w, int sensor_
   });
 }
 
+// geometry_consistency_loss (want_grad = 0) / _backward (geometry.hpp:416-534) for
+// one pose. Output pointers may be NULL (d_pose = {omega, trans}).
+REF_API int ref_geo_loss(int W, int H, const double* d0, const std::uint8_t* m0, const double* d1,
+                         const std::uint8_t* m1, const double* pose, const double* K,
+                         double upstream, int want_grad, double* value, std::int64_t* n_valid,
+                         int* empty, double* projected, double* interpolated, std::uint8_t* valid,
+                         double* d_d0, double* d_d1, double* d_pose) {
+  return guarded([&] {
+    const DepthMap a = make_depth(W, H, d0, m0), b = make_depth(W, H, d1, m1);
+    const PoseStep ps = make_poses(1, pose)[0];
+    const CameraIntrinsics k{K[0], K[1], K[2], K[3]};
+    auto dump_terms = [&](const GeoLossTerms& t) {
+      *value = t.value;
+      *n_valid = t.n_valid;
+      *empty = t.empty_valid_set ? 1 : 0;
+      for (std::size_t i = 0; i < static_cast<std::size_t>(W) * H; ++i) {
+        if (projected) projected[i] = t.projected[i];
+        if (interpolated) interpolated[i] = t.interpolated[i];
+        if (valid) valid[i] = t.valid[i];
+      }
+    };
+    if (!want_grad) {
+      dump_terms(geometry_consistency_loss(a, b, ps, k));
+      return;
+    }
+    const GeoLossGrad g = geometry_consistency_loss_backward(a, b, ps, k, upstream);
+    dump_terms(g.terms);
+    for (std::size_t i = 0; i < static_cast<std::size_t>(W) * H; ++i) {
+      if (d_d0) d_d0[i] = g.d_d0[i];
+      if (d_d1) d_d1[i] = g.d_d1[i];
+    }
+    if (d_pose) {
+      const double v[6] = {g.d_omega.x, g.d_omega.y, g.d_omega.z,
+                           g.d_trans.x, g.d_trans.y, g.d_trans.z};
+      std::memcpy(d_pose, v, sizeof v);
+    }
+  });
+}
+
+// predictor_loss_and_gradients (optimize.hpp:205-241) of a DirectPredictor with
+// any lambda_geo: losses = {l_cm, l_geo, total}.
+REF_API int ref_predictor_loss(int pw, int ph, int factor, const double* params, int n_bins,
+                               const double* poses, const double* K, std::uint64_t t0,
+                               std::uint64_t t1, const void* ev, std::size_t n, double lambda_geo,
+                               double* losses, double* d_params, double* d_poses) {
+  return guarded([&] {
+    DirectPredictor p;
+    p.depth_params = Image<double>(pw, ph, 0.0);
+    for (std::size_t i = 0; i < p.depth_params.size(); ++i) p.depth_params[i] = params[i];
+    p.poses = make_poses(n_bins, poses);
+    p.upsample = factor;
+    const EventSlice s = make_slice(pw * factor, ph * factor, t0, t1, ev, n);
+    const Engine engine{EngineOptions{}};
+    const WindowGradients wg = predictor_loss_and_gradients(
+        p, s, CameraIntrinsics{K[0], K[1], K[2], K[3]}, lambda_geo, engine);
+    losses[0] = wg.l_cm;
+    losses[1] = wg.l_geo;
+    losses[2] = wg.total;
+    for (std::size_t i = 0; i < wg.grads.d_depth_params.size(); ++i)
+      d_params[i] = wg.grads.d_depth_params[i];
+    for (int b = 0; b < n_bins; ++b) {
+      const PoseGrad& q = wg.grads.d_poses[b];
+      const double v[6] = {q.omega.x, q.omega.y, q.omega.z, q.trans.x, q.trans.y, q.trans.z};
+      std::memcpy(d_poses + 6 * b, v, sizeof v);
+    }
+  });
+}
+
 // optimize_flow_only (optimize.hpp:385-487): final (best) flows [B][2][H][W] and
 // the per-update l_cm / rsat / grad_norm_depth of the log.
 REF_API int ref_optimize_flow_only(int W, int H, std::uint64_t t0, std::uint64_t t1, const void* ev,

@@ -14,5 +14,8 @@ from .engine import (  # noqa: F401
 from .predictor import (  # noqa: F401
     Adam, DecodedPredictor, DirectPredictor, OptimizerConfig, PredictorGrads, WindowGradients,
     accumulate_gradients, decode, predictor_loss_and_gradients)
+from .geo import (  # noqa: F401
+    GEO_WEIGHT_DEFAULT, GeoBatch, GeoLossGrad, GeoLossTerms, geometry_consistency_loss,
+    geometry_consistency_loss_backward, geometry_consistency_loss_batch, total_loss)
 from .io import Windows, read_events, slice_windows, write_events  # noqa: F401
 from .optimize import FlowOnlyResult, TrainLog, TrainRecord, optimize_flow_only  # noqa: F401

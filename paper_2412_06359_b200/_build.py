@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libevcm_cuda.so")
-SOURCES = ["cmax_kernels.cu", "cmax_owner.cu", "cmax_cells.cu", "predictor.cu", "ingest.cu", "evcm_cuda.cu"]
+SOURCES = ["cmax_kernels.cu", "cmax_owner.cu", "cmax_cells.cu", "predictor.cu", "ingest.cu", "geo.cu", "evcm_cuda.cu"]
 HEADERS = ["cmax_device.cuh", "cmax_kernels.h", "cmax_owner.h", "cmax_owner_dev.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

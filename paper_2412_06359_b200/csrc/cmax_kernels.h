@@ -73,4 +73,42 @@ void launch_validate_events(cudaStream_t s, const evcm_event* ev, uint64_t n, in
 void launch_window_offsets(cudaStream_t s, const evcm_event* ev, uint64_t n, uint64_t t0,
                            uint64_t window_us, int n_windows, uint64_t* offsets);
 
+// Geometry-consistency loss (geo.cu)
+struct GeoArgs {
+  int W, H, n_poses, want_grad;
+  const double* d0;
+  const uint8_t* m0;  // may be null (all valid)
+  const double* d1;
+  const uint8_t* m1;
+  const double* tab;  // pose table [n_poses][kPoseTab]
+  double K[4];
+  double upstream;
+  // workspace
+  unsigned long long* zkey;  // [n_poses][HW]
+  unsigned* winner;          // [n_poses][HW]
+  double* dd0_raw;           // [n_poses][HW]   (want_grad)
+  double* gb_src;            // [n_poses][HW]   (want_grad)
+  double2* land;             // [n_poses][HW]   (want_grad)
+  double* parts;             // [n_poses][geo_parts][8]
+  double* scale;             // [n_poses]
+  // outputs (device; null = not wanted)
+  double* value;             // [n_poses]
+  long long* n_valid;        // [n_poses]
+  double* projected;         // [n_poses][HW]
+  double* interpolated;      // [n_poses][HW]
+  uint8_t* valid;            // [n_poses][HW]
+  double* d_d0;              // [n_poses][HW]
+  double* d_d1;              // [n_poses][HW]
+  double* d_poses;           // [n_poses][6]
+  const double* add_poses;   // d_poses = add_poses + scale * g (may alias d_poses)
+  double* d_depth_sum;       // [HW] sum_i (d_d0_i + d_d1_i)
+  const double* add_depth;   // d_depth_sum = add_depth + extra (may alias)
+  const double* l_cm;        // predictor: losses = {l_cm, l_geo, l_cm + lambda * l_geo}
+  double lambda;
+  double* losses;
+};
+int geo_parts(int W, int H);
+void launch_geo(cudaStream_t s, const GeoArgs& g);
+void launch_geo_losses_off(cudaStream_t s, const double* l_cm, double lambda, double* losses);
+
 }  // namespace evcm_b200

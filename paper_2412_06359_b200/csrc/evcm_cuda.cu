@@ -400,6 +400,22 @@ const double* upload_pose_table(evcm_cuda_engine* e, const double* poses_h, int 
   return d;
 }
 
+// Workspace of the L_geo kernels (geo.cu) for g.n_poses poses of a W x H pair.
+void geo_workspace(evcm_cuda_engine* e, GeoArgs& g) {
+  const size_t n = (size_t)g.W * g.H * g.n_poses;
+  g.zkey = e->get<unsigned long long>("geo_zkey", n);
+  g.winner = e->get<unsigned>("geo_winner", n);
+  if (g.want_grad) {
+    g.dd0_raw = e->get<double>("geo_dd0_raw", n);
+    g.gb_src = e->get<double>("geo_gb", n);
+    g.land = e->get<double2>("geo_land", n);
+  }
+  g.parts = e->get<double>("geo_parts", (size_t)geo_parts(g.W, g.H) * g.n_poses * 8);
+  g.scale = e->get<double>("geo_scale", (size_t)g.n_poses);
+  g.value = e->get<double>("geo_value_ws", (size_t)g.n_poses);
+  g.n_valid = (long long*)e->get<int64_t>("geo_nvalid_ws", (size_t)g.n_poses);
+}
+
 template <typename S2>
 void run_forward_t(evcm_cuda_engine* e, const WinParams& P, uint64_t max_n, const double2* flows) {
   const size_t R = P.B + 1;
@@ -1119,10 +1135,11 @@ int evcm_cuda_adam_step(evcm_cuda_engine* e, size_t n, double* params, const dou
   });
 }
 
-int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw, int ph, int factor,
-                                           const double* params, int n_bins, const double* poses,
-                                           const double K[4], const evcm_slice* slice, int mem,
-                                           double* loss, double* d_params, double* d_poses) {
+int evcm_cuda_predictor_loss_and_gradients_geo(evcm_cuda_engine* e, int pw, int ph, int factor,
+                                               const double* params, int n_bins,
+                                               const double* poses, const double K[4],
+                                               const evcm_slice* slice, double lambda_geo, int mem,
+                                               double* losses, double* d_params, double* d_poses) {
   return guarded([&] {
     if (!e || !slice || !K || !poses) fail(EVCM_ERR_CONFIG, "null argument");
     check_grid(pw, ph, factor, params);
@@ -1157,14 +1174,144 @@ int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw, int ph, 
     co.d_depth = dd;
     co.d_poses = dp;
     chain_impl(e, &bt, mem, EVCM_MEM_DEVICE, &co, depth);
+    int launches = launch_count() + 1;  // + the decode before the chain's reset
+    double* lo = e->get<double>("pred_losses", 3);
+    if (lambda_geo > 0.0) {
+      // optimize.hpp:219-236: L_geo per bin on (depth, depth), upstream lambda / B;
+      // both halves of the depth gradient and the pose gradient add onto the
+      // CMax gradients before the decode adjoint (predictor.hpp:153-171)
+      GeoArgs g{};
+      g.W = W;
+      g.H = H;
+      g.n_poses = n_bins;
+      g.want_grad = 1;
+      g.d0 = g.d1 = depth;
+      g.tab = e->get<double>("pose_tab", (size_t)n_bins * kPoseTab);  // built by the chain
+      for (int i = 0; i < 4; ++i) g.K[i] = K[i];
+      g.upstream = lambda_geo / (double)n_bins;
+      geo_workspace(e, g);
+      g.d_poses = dp;
+      g.add_poses = dp;
+      g.d_depth_sum = dd;
+      g.add_depth = dd;
+      g.l_cm = ld;
+      g.lambda = lambda_geo;
+      g.losses = lo;
+      reset_launch_count();
+      launch_geo(e->stream, g);
+      launches += launch_count();
+    } else {
+      launch_geo_losses_off(e->stream, ld, lambda_geo, lo);
+      ++launches;
+    }
     // accumulate_gradients, depth half (predictor.hpp:156-162)
     double* dpar = mem == EVCM_MEM_DEVICE ? d_params : e->get<double>("pred_d_params", (size_t)pw * ph);
     launch_decode_adjoint(e->stream, pd, dd, pw, ph, factor, dpar);
-    if (loss) from_device(e, loss, ld, sizeof(double), mem);
+    ++launches;
+    if (losses) from_device(e, losses, lo, 3 * sizeof(double), mem);
     if (d_params && dpar != d_params) from_device(e, d_params, dpar, (size_t)pw * ph * sizeof(double), mem);
     if (d_poses && dp != d_poses) from_device(e, d_poses, dp, (size_t)n_bins * 6 * sizeof(double), mem);
     sync_and_check(e, "predictor_loss_and_gradients");
-    e->last_launches = launch_count() + 1;  // + the decode before the chain's reset
+    e->last_launches = launches;
+  });
+}
+
+int evcm_cuda_predictor_loss_and_gradients(evcm_cuda_engine* e, int pw, int ph, int factor,
+                                           const double* params, int n_bins, const double* poses,
+                                           const double K[4], const evcm_slice* slice, int mem,
+                                           double* loss, double* d_params, double* d_poses) {
+  double l3[3];
+  double* dl = nullptr;
+  if (loss && mem == EVCM_MEM_DEVICE) {
+    // device losses land in a scratch triple; the caller's scalar receives l_cm
+    const int rc = guarded([&] { dl = e ? e->get<double>("pred_losses_user", 3) : nullptr; });
+    if (rc) return rc;
+  }
+  const int rc = evcm_cuda_predictor_loss_and_gradients_geo(e, pw, ph, factor, params, n_bins, poses,
+                                                           K, slice, 0.0, mem,
+                                                           loss ? (dl ? dl : l3) : nullptr,
+                                                           d_params, d_poses);
+  if (rc || !loss) return rc;
+  if (dl)
+    return guarded([&] {
+      ck(cudaMemcpyAsync(loss, dl, sizeof(double), cudaMemcpyDeviceToDevice, e->stream), "loss");
+      ck(cudaStreamSynchronize(e->stream), "loss");
+    });
+  *loss = l3[0];
+  return rc;
+}
+
+int evcm_cuda_geometry_consistency_loss(evcm_cuda_engine* e, int W, int H, const double* d0,
+                                        const uint8_t* mask0, const double* d1,
+                                        const uint8_t* mask1, int n_poses, const double* poses,
+                                        const double K[4], double upstream, int want_grad, int mem,
+                                        evcm_geo_out* out) {
+  return guarded([&] {
+    if (!e || !out || !K || !poses || !d0 || !d1) fail(EVCM_ERR_CONFIG, "null argument");
+    if (W <= 0 || H <= 0) fail(EVCM_ERR_DIMENSION, "depth consistency: depth maps must share a shape");
+    if (n_poses < 1) fail(EVCM_ERR_CONFIG, "depth consistency: need at least one pose");
+    set_device(e);
+    reset_launch_count();
+    const size_t HW = (size_t)W * H, nP = (size_t)n_poses;
+    std::vector<double> ph(6 * nP);
+    if (mem == EVCM_MEM_DEVICE)
+      ck(cudaMemcpy(ph.data(), poses, ph.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H poses");
+    else
+      std::memcpy(ph.data(), poses, ph.size() * sizeof(double));
+    std::vector<uint64_t> unit_edges(nP + 1);  // inv_dt is not used by L_geo
+    for (size_t i = 0; i <= nP; ++i) unit_edges[i] = i;
+    GeoArgs g{};
+    g.W = W;
+    g.H = H;
+    g.n_poses = n_poses;
+    g.want_grad = want_grad ? 1 : 0;
+    // geometry_consistency_loss does not validate the pose (geometry.hpp:423)
+    g.tab = upload_pose_table(e, ph.data(), 1, n_poses, unit_edges.data(), false);
+    g.d0 = to_device(e, "geo_d0", d0, HW, mem);
+    g.m0 = mask0 ? to_device(e, "geo_m0", mask0, HW, mem) : nullptr;
+    g.d1 = d1 == d0 ? g.d0 : to_device(e, "geo_d1", d1, HW, mem);
+    g.m1 = !mask1 ? nullptr : mask1 == mask0 ? g.m0 : to_device(e, "geo_m1", mask1, HW, mem);
+    for (int i = 0; i < 4; ++i) g.K[i] = K[i];
+    g.upstream = upstream;
+    geo_workspace(e, g);
+    const bool dev = mem == EVCM_MEM_DEVICE;
+    auto outp = [&](auto* user, const char* name, size_t n) {
+      using T = std::remove_pointer_t<decltype(user)>;
+      return (T*)(user == nullptr ? nullptr : dev ? user : e->get<T>(name, n));
+    };
+    g.value = outp(out->value, "geo_value", nP);
+    if (!g.value) g.value = e->get<double>("geo_value", nP);
+    g.n_valid = (long long*)outp((int64_t*)out->n_valid, "geo_nvalid", nP);
+    if (!g.n_valid) g.n_valid = (long long*)e->get<int64_t>("geo_nvalid", nP);
+    g.projected = outp(out->projected, "geo_proj", nP * HW);
+    g.interpolated = outp(out->interpolated, "geo_interp", nP * HW);
+    g.valid = outp(out->valid, "geo_valid", nP * HW);
+    if (want_grad) {
+      g.d_d0 = outp(out->d_d0, "geo_dd0", nP * HW);
+      g.d_d1 = outp(out->d_d1, "geo_dd1", nP * HW);
+      g.d_poses = outp(out->d_poses, "geo_dposes", nP * 6);
+      g.d_depth_sum = outp(out->d_depth_sum, "geo_dsum", HW);
+    }
+    launch_geo(e->stream, g);
+    if (!dev) {
+      auto back = [&](void* user, const void* d, size_t bytes) {
+        if (user) from_device(e, user, d, bytes, mem);
+      };
+      back(out->value, g.value, nP * sizeof(double));
+      back(out->n_valid, g.n_valid, nP * sizeof(int64_t));
+      back(out->projected, g.projected, nP * HW * sizeof(double));
+      back(out->interpolated, g.interpolated, nP * HW * sizeof(double));
+      back(out->valid, g.valid, nP * HW);
+      if (want_grad) {
+        back(out->d_d0, g.d_d0, nP * HW * sizeof(double));
+        back(out->d_d1, g.d_d1, nP * HW * sizeof(double));
+        back(out->d_poses, g.d_poses, nP * 6 * sizeof(double));
+        back(out->d_depth_sum, g.d_depth_sum, HW * sizeof(double));
+      }
+    }
+    e->stage_nw = 0;
+    sync_and_check(e, "geometry_consistency_loss");
+    e->last_launches = launch_count();
   });
 }
 

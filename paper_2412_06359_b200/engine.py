@@ -167,6 +167,10 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_decode.argtypes = [vp, i32, i32, i32, vp, i32, vp]
     L.evcm_cuda_decode_backward.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp]
     L.evcm_cuda_adam_step.argtypes = [vp, sz, vp, vp, vp, vp, i32, f64, f64, f64, f64, i32]
+    L.evcm_cuda_predictor_loss_and_gradients_geo.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp,
+                                                             vp, f64, i32, vp, vp, vp]
+    L.evcm_cuda_geometry_consistency_loss.argtypes = [vp, i32, i32, vp, vp, vp, vp, i32, vp, vp,
+                                                      f64, i32, i32, vp]
     L.evcm_cuda_validate_slice.argtypes = [vp, vp, i32, i32, vp]
     L.evcm_cuda_window_offsets.argtypes = [vp, vp, sz, u64, u64, i32, i32, vp]
     L.evcm_cuda_predictor_loss_and_gradients.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp,

@@ -4,10 +4,10 @@ of the CMax path — mirroring the reference's names and semantics:
   DirectPredictor, DecodedPredictor, decode          predictor.hpp:100-131
   PredictorGrads, accumulate_gradients               predictor.hpp:133-173
   OptimizerConfig (Adam fields), Adam                optimize.hpp:25-75, 115-134
-  WindowGradients, predictor_loss_and_gradients      optimize.hpp:195-241 (lambda_geo = 0)
+  WindowGradients, predictor_loss_and_gradients      optimize.hpp:195-241 (with L_geo)
 
 Everything runs through libevcm_cuda.so (evcm_cuda_decode / _decode_backward /
-_adam_step / _predictor_loss_and_gradients); there is no CPU fallback. Arrays
+_adam_step / _predictor_loss_and_gradients_geo); there is no CPU fallback. Arrays
 may be numpy (host) or torch CUDA tensors (device, kept on the device)."""
 from __future__ import annotations
 
@@ -134,10 +134,8 @@ def predictor_loss_and_gradients(pred: DirectPredictor, slice_: EventSlice, k, l
                                  engine: Engine | None = None) -> WindowGradients:
     """predictor_loss_and_gradients (optimize.hpp:205-241) in one fused device
     call: decode -> depth_pose_to_flows -> Engine::forward -> Engine::backward ->
-    accumulate_gradients. The depth-consistency term (lambda_geo > 0) is not part
-    of the CMax path this build accelerates."""
-    if lambda_geo != 0.0:
-        raise ConfigError("cuda backend: lambda_geo > 0 (L_geo) is not implemented")
+    [lambda_geo > 0: L_geo per bin on (depth, depth), upstream lambda_geo / B] ->
+    accumulate_gradients."""
     pred.validate()
     e = engine or default_engine()
     params = _f64(pred.depth_params)
@@ -147,15 +145,16 @@ def predictor_loss_and_gradients(pred: DirectPredictor, slice_: EventSlice, k, l
         from .engine import DimensionMismatchError
         raise DimensionMismatchError("predictor: decoded depth does not match the slice sensor")
     mem = _mem_of(params, poses, slice_.events)
-    loss = _zeros_like_side(params, (1,))
+    losses = _zeros_like_side(params, (3,))
     dpar = _zeros_like_side(params, (ph, pw))
     dpos = _zeros_like_side(params, (pred.n_bins, 6))
     sl = slice_._c()
-    _raise(load_library().evcm_cuda_predictor_loss_and_gradients(
+    _raise(load_library().evcm_cuda_predictor_loss_and_gradients_geo(
         e._h, pw, ph, pred.upsample, _ptr(params), pred.n_bins, _ptr(poses),
-        _ptr(_k_array(k)), C.byref(sl), mem, _ptr(loss), _ptr(dpar), _ptr(dpos)))
-    l_cm = float(loss[0])
-    return WindowGradients(PredictorGrads(dpar, dpos), l_cm, 0.0, l_cm)
+        _ptr(_k_array(k)), C.byref(sl), float(lambda_geo), mem, _ptr(losses), _ptr(dpar),
+        _ptr(dpos)))
+    l = [float(v) for v in losses.tolist()]
+    return WindowGradients(PredictorGrads(dpar, dpos), l[0], l[1], l[2])
 
 
 @dataclass
@@ -166,7 +165,7 @@ class OptimizerConfig:
     steps_per_update: int = 10
     bins: int = 10
     max_updates: int = 100
-    lambda_geo: float = 0.05  # kGeoWeightDefault; only lambda_geo = 0 runs on the cuda backend
+    lambda_geo: float = 0.05  # kGeoWeightDefault (geometry.hpp:538)
     adam_beta1: float = 0.9
     adam_beta2: float = 0.999
     adam_eps: float = 1e-8

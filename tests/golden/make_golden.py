@@ -15,6 +15,9 @@ Each fixture is an .npz with the inputs and the reference outputs:
                      plus the byte-patched variants of tests/test_core_io.cpp:73-137;
   evt1.npz           the reference's read_events outcome for each (error code or
                      W, H, t0, t1, events)
+  geo_<case>.npz     geometry_consistency_loss_backward (geometry.hpp:458-534) on
+                     masked / occluding / tied / empty cases
+  predictor_geo_3.npz  predictor_loss_and_gradients with lambda_geo = 0.05 and 0.5
 """
 import os
 import sys
@@ -53,6 +56,59 @@ def predictor_fixtures():
     rng = np.random.default_rng(2)
     s, g = rng.normal(size=40), rng.normal(size=40)
     save("adam.npz", slots=s, grads=g, lr=0.01, steps=3, out=O.ref_adam_steps(s, g, 3, 0.01))
+
+
+GEO_CASES = ["masked", "occlusion", "ties", "empty"]
+
+
+def geo_inputs(case):
+    """Inputs of the L_geo fixtures (also used by the tests for the restatement)."""
+    rng = np.random.default_rng({"masked": 1, "occlusion": 2, "ties": 3, "empty": 4}[case])
+    H, W = 24, 32
+    K = np.array([0.9 * W, 0.9 * W, (W - 1) / 2, (H - 1) / 2])
+    m0 = m1 = None
+    if case == "masked":
+        d0 = rng.uniform(1, 3, (H, W))
+        d1 = d0 * rng.uniform(0.95, 1.05, (H, W))
+        m0 = (rng.uniform(size=(H, W)) > 0.1).astype(np.uint8)
+        m1 = (rng.uniform(size=(H, W)) > 0.1).astype(np.uint8)
+        pose = np.array([0.01, -0.02, 0.015, 0.05, -0.03, 0.02])
+    elif case == "occlusion":  # near plane slides over the far one
+        d0 = np.full((H, W), 4.0)
+        d0[:, W // 3: W // 2] = 1.0
+        d0 *= rng.uniform(0.99, 1.01, (H, W))
+        d1 = d0.copy()
+        pose = np.array([0.0, 0.03, 0.0, 0.25, 0.0, 0.0])
+    elif case == "ties":  # constant depth, forward motion: equal z in every cell
+        d0 = np.full((H, W), 2.0)
+        d1 = np.full((H, W), 2.0)
+        pose = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 0.3])
+    else:  # everything leaves the view
+        d0 = rng.uniform(1, 2, (H, W))
+        d1 = d0.copy()
+        pose = np.array([0.0, 0.0, 0.0, 50.0, 0.0, 0.0])
+    return d0, d1, m0, m1, pose, K
+
+
+def geo_fixtures():
+    for case in GEO_CASES:
+        d0, d1, m0, m1, pose, K = geo_inputs(case)
+        r = O.ref_geo_loss(d0, d1, pose, K, m0, m1, upstream=0.7)
+        extra = {} if m0 is None else dict(m0=m0, m1=m1)
+        save(f"geo_{case}.npz", d0=d0, d1=d1, pose=pose, K=K, upstream=0.7, value=r["value"],
+             n_valid=r["n_valid"], empty=r["empty"], projected=r["projected"],
+             interpolated=r["interpolated"], valid=r["valid"], d_d0=r["d_d0"], d_d1=r["d_d1"],
+             d_pose=r["d_pose"], **extra)
+    g = np.load(os.path.join(HERE, "predictor_3.npz"))
+    ev = np.ascontiguousarray(g["events"]).view(O.EVENT_DTYPE).reshape(-1)
+    out = {}
+    for lam in (0.05, 0.5):
+        losses, dpar, dpo = O.ref_predictor_loss(g["params"], int(g["factor"]), g["poses"], g["K"],
+                                                 0, 100000, ev, lam)
+        key = str(lam).replace(".", "p")
+        out.update({f"losses_{key}": np.array(losses), f"d_params_{key}": dpar,
+                    f"d_poses_{key}": dpo})
+    save("predictor_geo_3.npz", **out)
 
 
 EVT1_FILES = ["empty", "three", "random_2k", "bad_magic", "trunc_record", "trunc_header",
@@ -101,6 +157,7 @@ def main():
         O.build(ref=True)
     evt1_fixtures()
     predictor_fixtures()
+    geo_fixtures()
     for seed in (100, 7, 503, 1300):
         window_fixture(f"fd_{seed}.npz", O.ref_fd_instance(seed))
     window_fixture("fd_masked_900.npz", O.ref_fd_instance(900, max_events=24, want_masked=True))

@@ -127,9 +127,6 @@ def test_predictor_errors():
     f = int(g["factor"])
     ph, pw = g["params"].shape
     pred = P.DirectPredictor(g["params"], g["poses"], f)
-    with pytest.raises(P.ConfigError):
-        P.predictor_loss_and_gradients(pred, _slice(events_of(g), pw * f, ph * f), g["K"],
-                                       lambda_geo=0.05)
     with pytest.raises(P.DimensionMismatchError):
         P.predictor_loss_and_gradients(pred, _slice(events_of(g), pw * f + 1, ph * f), g["K"])
     with pytest.raises(P.ConfigError):
