@@ -129,6 +129,10 @@ def ref():
         L.ref_write_events.argtypes = [C.c_char_p, i32, i32, u64, u64, vp, sz]
         L.ref_validate_slice.argtypes = [i32, i32, u64, u64, vp, sz]
         L.ref_random_slice.argtypes = [u64, sz, vp, vp, vp, vp, vp]
+        L.ref_format_number.argtypes = [f64, C.c_char_p]
+        L.ref_format_number.restype = None
+        L.ref_run_window.argtypes = [i32, vp, vp, vp, i32, i32, i32, vp, i32, vp, vp, f64, i32, i32,
+                                     f64, vp, vp, vp, vp]
         L.ref_geo_loss.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp,
                                    vp, vp, vp, vp]
         L.ref_predictor_loss.argtypes = [i32, i32, i32, vp, i32, vp, vp, u64, u64, vp, sz, f64, vp,
@@ -683,3 +687,34 @@ def ref_predictor_loss(params, factor, poses, K, t0, t1, events, lambda_geo):
     _check(L.ref_predictor_loss(pw, ph, factor, _p(params), B, _p(poses), _p(K), t0, t1, _p(ev),
                                 len(ev), lambda_geo, _p(losses), _p(dpar), _p(dpo)), L, "ref")
     return tuple(losses), dpar, dpo
+
+
+def ref_format_number(v):
+    buf = C.create_string_buffer(64)
+    ref().ref_format_number(float(v), buf)
+    return buf.value.decode()
+
+
+def ref_run_window(windows, params, factor, poses, K, lr, steps_per_update, max_updates,
+                   lambda_geo):
+    """The reference's run_window; windows = [(t0, t1, events), ...]. Returns
+    (params, poses, records [n, 6] = l_cm, l_geo, total, rsat, gnd, gnp)."""
+    L = ref()
+    nw = len(windows)
+    t01 = np.array([[w[0], w[1]] for w in windows], np.uint64).reshape(-1)
+    evs = [np.ascontiguousarray(w[2], EVENT_DTYPE) for w in windows]
+    offs = np.zeros(nw + 1, np.uint64)
+    offs[1:] = np.cumsum([len(e) for e in evs])
+    ev = np.concatenate(evs).astype(EVENT_DTYPE) if nw else np.zeros(0, EVENT_DTYPE)
+    ph, pw = params.shape
+    B = poses.shape[0]
+    po, qo = np.zeros((ph, pw)), np.zeros((B, 6))
+    rec = np.zeros((max(max_updates, 1), 6))
+    n = C.c_int()
+    params = np.ascontiguousarray(params, np.float64)
+    poses = np.ascontiguousarray(poses, np.float64)
+    K = np.ascontiguousarray(K, np.float64)
+    _check(L.ref_run_window(nw, _p(t01), _p(ev), _p(offs), pw, ph, factor, _p(params), B, _p(poses),
+                            _p(K), lr, steps_per_update, max_updates, lambda_geo, _p(po), _p(qo),
+                            _p(rec), C.byref(n)), L, "ref")
+    return po, qo, rec[: n.value]

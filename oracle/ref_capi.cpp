@@ -591,6 +591,54 @@ REF_API int ref_predictor_loss(int pw, int ph, int factor, const double* params,
   });
 }
 
+// format_number (io.hpp:295-299) into buf (>= 64 bytes).
+REF_API void ref_format_number(double v, char* buf) {
+  const std::string s = format_number(v);
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+// run_window (optimize.hpp:297-375) over nw windows (events concatenated,
+// window w = events[offs[w], offs[w+1]) on [t01[2w], t01[2w+1])). Returns the
+// trained params / poses and per record {l_cm, l_geo, total, rsat, gnd, gnp}.
+REF_API int ref_run_window(int nw, const std::uint64_t* t01, const void* ev,
+                           const std::uint64_t* offs, int pw, int ph, int factor,
+                           const double* params, int n_bins, const double* poses, const double* K,
+                           double lr, int steps_per_update, int max_updates, double lambda_geo,
+                           double* params_out, double* poses_out, double* rec, int* n_rec) {
+  return guarded([&] {
+    std::vector<EventSlice> wins;
+    const auto* e = static_cast<const Event*>(ev);
+    for (int w = 0; w < nw; ++w)
+      wins.push_back(make_slice(pw * factor, ph * factor, t01[2 * w], t01[2 * w + 1], e + offs[w],
+                                offs[w + 1] - offs[w]));
+    DirectPredictor p;
+    p.depth_params = Image<double>(pw, ph, 0.0);
+    for (std::size_t i = 0; i < p.depth_params.size(); ++i) p.depth_params[i] = params[i];
+    p.poses = make_poses(n_bins, poses);
+    p.upsample = factor;
+    OptimizerConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.steps_per_update = steps_per_update;
+    cfg.bins = n_bins;
+    cfg.max_updates = max_updates;
+    cfg.lambda_geo = lambda_geo;
+    const RunResult r = run_window(wins, p, CameraIntrinsics{K[0], K[1], K[2], K[3]}, cfg);
+    for (std::size_t i = 0; i < r.predictor.depth_params.size(); ++i)
+      params_out[i] = r.predictor.depth_params[i];
+    for (int b = 0; b < n_bins; ++b) {
+      const PoseStep& q = r.predictor.poses[b];
+      const double v[6] = {q.omega.x, q.omega.y, q.omega.z, q.trans.x, q.trans.y, q.trans.z};
+      std::memcpy(poses_out + 6 * b, v, sizeof v);
+    }
+    *n_rec = static_cast<int>(r.log.records.size());
+    for (std::size_t i = 0; i < r.log.records.size(); ++i) {
+      const TrainRecord& t = r.log.records[i];
+      const double v[6] = {t.l_cm, t.l_geo, t.total, t.rsat, t.grad_norm_depth, t.grad_norm_pose};
+      std::memcpy(rec + 6 * i, v, sizeof v);
+    }
+  });
+}
+
 // optimize_flow_only (optimize.hpp:385-487): final (best) flows [B][2][H][W] and
 // the per-update l_cm / rsat / grad_norm_depth of the log.
 REF_API int ref_optimize_flow_only(int W, int H, std::uint64_t t0, std::uint64_t t1, const void* ev,

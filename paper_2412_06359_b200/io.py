@@ -124,6 +124,37 @@ def write_events(slice_: EventSlice, path, engine: Optional[Engine] = None) -> N
         raise IoError(f"cannot write {path}: {e}") from None
 
 
+def format_number(v: float) -> str:
+    """format_number (io.hpp:295-299): std::to_chars(double) -- the shortest
+    round-trip digits, printed fixed or scientific, whichever is shorter (fixed
+    on a tie; a fixed integer keeps its exact digits)."""
+    import decimal
+    import math
+    v = float(v)
+    if math.isnan(v):
+        return "-nan" if math.copysign(1.0, v) < 0 else "nan"
+    if math.isinf(v):
+        return "-inf" if v < 0 else "inf"
+    sign = "-" if math.copysign(1.0, v) < 0 else ""
+    if v == 0.0:
+        return sign + "0"
+    t = decimal.Decimal(repr(abs(v))).as_tuple()  # repr = shortest round-trip digits
+    digits = "".join(map(str, t.digits)).lstrip("0")
+    exp = t.exponent + (len(t.digits) - len("".join(map(str, t.digits)).rstrip("0")))
+    digits = digits.rstrip("0")
+    n = len(digits)
+    sci_e = exp + n - 1
+    sci = digits[0] + ("." + digits[1:] if n > 1 else "") + \
+        ("e-" if sci_e < 0 else "e+") + f"{abs(sci_e):02d}"
+    if exp >= 0:  # an integer: printf-style fixed prints all its exact digits
+        fixed = str(int(abs(v)))
+    elif sci_e >= 0:
+        fixed = digits[: n + exp] + "." + digits[n + exp:]
+    else:
+        fixed = "0." + "0" * (-sci_e - 1) + digits
+    return sign + (fixed if len(fixed) <= len(sci) else sci)
+
+
 @dataclass
 class Windows:
     """Consecutive windows [t0 + w*window_us, t0 + (w+1)*window_us) of one slice:

@@ -18,6 +18,7 @@ Each fixture is an .npz with the inputs and the reference outputs:
   geo_<case>.npz     geometry_consistency_loss_backward (geometry.hpp:458-534) on
                      masked / occluding / tied / empty cases
   predictor_geo_3.npz  predictor_loss_and_gradients with lambda_geo = 0.05 and 0.5
+  run_window.npz     run_window (optimize.hpp:297-375) over 3 windows, 12 updates
 """
 import os
 import sys
@@ -111,6 +112,29 @@ def geo_fixtures():
     save("predictor_geo_3.npz", **out)
 
 
+def run_window_fixture():
+    base = O.ref_predictor_instance(3, sensor_w=32, sensor_h=24, factor=8, n_bins=3, n_events=60)
+    wins = []
+    for w, seed in enumerate([3, 4, 5]):
+        rr = O.ref_predictor_instance(seed, sensor_w=32, sensor_h=24, factor=8, n_bins=3,
+                                      n_events=60)
+        ev = rr["events"].copy()
+        ev["t_us"] += np.uint64(w * 100000)
+        wins.append((w * 100000, (w + 1) * 100000, ev))
+    out = {}
+    for lam in (0.0, 0.05):
+        po, qo, rec = O.ref_run_window(wins, base["params"], 8, base["poses"], base["K"], 1e-3, 1,
+                                       12, lam)
+        key = str(lam).replace(".", "p")
+        out.update({f"params_{key}": po, f"poses_{key}": qo, f"rec_{key}": rec})
+    ev = np.concatenate([w[2] for w in wins]).astype(O.EVENT_DTYPE)
+    offs = np.cumsum([0] + [len(w[2]) for w in wins]).astype(np.uint64)
+    save("run_window.npz", events=ev.view(np.uint8).reshape(-1, 16), offs=offs,
+         t01=np.array([[w[0], w[1]] for w in wins], np.uint64), params=base["params"],
+         poses=base["poses"], K=base["K"], factor=8, lr=1e-3, steps_per_update=1, max_updates=12,
+         **out)
+
+
 EVT1_FILES = ["empty", "three", "random_2k", "bad_magic", "trunc_record", "trunc_header",
               "unsorted", "coord_at_width", "zero_polarity", "trailing", "zero_width"]
 
@@ -158,6 +182,7 @@ def main():
     evt1_fixtures()
     predictor_fixtures()
     geo_fixtures()
+    run_window_fixture()
     for seed in (100, 7, 503, 1300):
         window_fixture(f"fd_{seed}.npz", O.ref_fd_instance(seed))
     window_fixture("fd_masked_900.npz", O.ref_fd_instance(900, max_events=24, want_masked=True))
