@@ -8,6 +8,8 @@
 //   evcm::cuda::Engine            ~ evcm::Engine              (engine.hpp:134-213)
 //   evcm::cuda::depth_pose_to_flows / _backward               (geometry.hpp:229-325)
 //   evcm::cuda::contrast_loss_backward / build_iwe_stack / rsat (engine.hpp:606-631)
+//   evcm::cuda::geometry_consistency_loss[_backward]            (geometry.hpp:416-534)
+//   evcm::cuda::predictor_loss_and_gradients                    (optimize.hpp:205-241)
 //
 // Requires the reference headers on the include path (it reuses EventSlice,
 // FlowSequence, ForwardResult, ... from evcm).
@@ -21,6 +23,8 @@
 
 #include "evcm/engine.hpp"
 #include "evcm/geometry.hpp"
+#include "evcm/optimize.hpp"
+#include "evcm/predictor.hpp"
 #include "evcm_cuda.h"
 
 namespace evcm::cuda {
@@ -233,6 +237,75 @@ inline double rsat(const EventSlice& s, const FlowSequence& f, CudaOptions o = {
   const LossResult base = e.forward(s, f.zeros_like()).loss;
   if (base.no_survivors || base.value == 0.0) throw EmptySliceError("rsat: zero-flow loss is zero");
   return with_flow / base.value;
+}
+
+// geometry_consistency_loss_backward (geometry.hpp:458-534); want_grad = false
+// gives geometry_consistency_loss (:416-453) with zero gradients.
+inline GeoLossGrad geometry_consistency_loss_backward(const Engine& e, const DepthMap& d0,
+                                                      const DepthMap& d1, const PoseStep& pose,
+                                                      const CameraIntrinsics& k,
+                                                      double upstream = 1.0,
+                                                      bool want_grad = true) {
+  if (!d0.d.same_shape(d1.d))
+    throw DimensionMismatchError("depth consistency: depth maps must share a shape");
+  const int W = d0.width(), H = d0.height();
+  const double p[6] = {pose.omega.x, pose.omega.y, pose.omega.z,
+                       pose.trans.x, pose.trans.y, pose.trans.z};
+  const double K[4] = {k.fx, k.fy, k.cx, k.cy};
+  GeoLossGrad out;
+  out.terms.projected = Image<double>(W, H, 0.0);
+  out.terms.interpolated = Image<double>(W, H, 0.0);
+  out.terms.valid = Image<std::uint8_t>(W, H, 0);
+  out.d_d0 = Image<double>(W, H, 0.0);
+  out.d_d1 = Image<double>(W, H, 0.0);
+  double value = 0.0, dp[6] = {0, 0, 0, 0, 0, 0};
+  std::int64_t n_valid = 0;
+  evcm_geo_out o{&value, &n_valid, &out.terms.projected[0], &out.terms.interpolated[0],
+                 &out.terms.valid[0], want_grad ? &out.d_d0[0] : nullptr,
+                 want_grad ? &out.d_d1[0] : nullptr, want_grad ? dp : nullptr, nullptr};
+  check(evcm_cuda_geometry_consistency_loss(
+      e.handle(), W, H, &d0.d[0], d0.has_mask() ? &d0.valid[0] : nullptr, &d1.d[0],
+      d1.has_mask() ? &d1.valid[0] : nullptr, 1, p, K, upstream, want_grad ? 1 : 0,
+      EVCM_MEM_HOST, &o));
+  out.terms.value = value;
+  out.terms.n_valid = n_valid;
+  out.terms.empty_valid_set = n_valid == 0;
+  out.d_omega = Vec3{dp[0], dp[1], dp[2]};
+  out.d_trans = Vec3{dp[3], dp[4], dp[5]};
+  return out;
+}
+
+inline GeoLossTerms geometry_consistency_loss(const Engine& e, const DepthMap& d0,
+                                              const DepthMap& d1, const PoseStep& pose,
+                                              const CameraIntrinsics& k) {
+  return geometry_consistency_loss_backward(e, d0, d1, pose, k, 1.0, false).terms;
+}
+
+// predictor_loss_and_gradients (optimize.hpp:205-241) as one device call:
+// decode -> depth_pose_to_flows -> forward -> backward -> [L_geo] -> adjoint.
+inline WindowGradients predictor_loss_and_gradients(const Engine& e, const DirectPredictor& pred,
+                                                    const EventSlice& slice,
+                                                    const CameraIntrinsics& k,
+                                                    double lambda_geo) {
+  pred.validate();
+  const int pw = pred.depth_params.width(), ph = pred.depth_params.height();
+  const std::vector<double> p = pack_poses(pred.poses);
+  const double K[4] = {k.fx, k.fy, k.cx, k.cy};
+  const evcm_slice cs = c_slice(slice);
+  double losses[3];
+  WindowGradients out;
+  out.grads.d_depth_params = Image<double>(pw, ph, 0.0);
+  std::vector<double> dp(6 * pred.poses.size());
+  check(evcm_cuda_predictor_loss_and_gradients_geo(
+      e.handle(), pw, ph, pred.upsample, &pred.depth_params[0], pred.n_bins(), p.data(), K, &cs,
+      lambda_geo, EVCM_MEM_HOST, losses, &out.grads.d_depth_params[0], dp.data()));
+  out.l_cm = losses[0];
+  out.l_geo = losses[1];
+  out.total = losses[2];
+  for (std::size_t b = 0; b < pred.poses.size(); ++b)
+    out.grads.d_poses.push_back(PoseGrad{{dp[6 * b], dp[6 * b + 1], dp[6 * b + 2]},
+                                         {dp[6 * b + 3], dp[6 * b + 4], dp[6 * b + 5]}});
+  return out;
 }
 
 }  // namespace evcm::cuda

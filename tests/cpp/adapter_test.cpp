@@ -9,6 +9,7 @@
 
 #include "evcm/fdcheck.hpp"
 #include "evcm/geometry.hpp"
+#include "chain_support.hpp"
 #include "evcm_cuda_backend.hpp"
 
 using namespace evcm;
@@ -102,6 +103,47 @@ int main() {
     CHECK(std::abs(gb.d_poses[b].trans.x - rb.d_poses[b].trans.x) <=
               1e-10 * (1 + std::abs(rb.d_poses[b].trans.x)),
           "d_pose");
+  // L_geo: membership bit-exact, sums within rounding
+  {
+    Image<double> d1img = dimg;
+    for (std::size_t i = 0; i < d1img.size(); ++i) d1img[i] *= 1.0 + 0.02 * std::sin(0.3 * i);
+    const DepthMap d1(d1img);
+    const PoseStep pose{{0.01, -0.015, 0.02}, {0.12, -0.05, 0.03}};
+    const GeoLossGrad r = geometry_consistency_loss_backward(depth, d1, pose, k, 0.7);
+    const GeoLossGrad c = cuda::geometry_consistency_loss_backward(gpu, depth, d1, pose, k, 0.7);
+    CHECK(r.terms.n_valid == c.terms.n_valid && r.terms.valid == c.terms.valid &&
+              r.terms.projected == c.terms.projected && r.terms.interpolated == c.terms.interpolated,
+          "L_geo membership");
+    CHECK(std::abs(r.terms.value - c.terms.value) <= 1e-13 * r.terms.value, "L_geo value");
+    double m = 0, mr = 0;
+    for (std::size_t i = 0; i < r.d_d0.size(); ++i) {
+      m = std::max({m, std::abs(r.d_d0[i] - c.d_d0[i]), std::abs(r.d_d1[i] - c.d_d1[i])});
+      mr = std::max({mr, std::abs(r.d_d0[i]), std::abs(r.d_d1[i])});
+    }
+    CHECK(m <= 1e-10 * mr, "L_geo depth gradients %g", m / mr);
+    CHECK(std::abs(r.d_trans.x - c.d_trans.x) <= 1e-10 * (1 + std::abs(r.d_trans.x)), "L_geo pose");
+  }
+  // predictor_loss_and_gradients with L_geo on the reference's chain fixture
+  {
+    evcm_test::ChainParams cp;
+    cp.sensor_w = 32;
+    cp.sensor_h = 24;
+    cp.factor = 8;
+    cp.n_bins = 3;
+    cp.n_events = 60;
+    const evcm_test::ChainInstance inst = evcm_test::make_chain_instance(3, cp);
+    const Engine eng{EngineOptions{}};
+    const WindowGradients r = predictor_loss_and_gradients(inst.pred, inst.slice, inst.k, 0.05, eng);
+    const WindowGradients c = cuda::predictor_loss_and_gradients(gpu, inst.pred, inst.slice, inst.k, 0.05);
+    CHECK(std::abs(r.total - c.total) <= 1e-5 * std::abs(r.total), "predictor total");
+    CHECK(std::abs(r.l_geo - c.l_geo) <= 1e-12 * std::abs(r.l_geo), "predictor l_geo");
+    double m = 0, mr = 0;
+    for (std::size_t i = 0; i < r.grads.d_depth_params.size(); ++i) {
+      m = std::max(m, std::abs(r.grads.d_depth_params[i] - c.grads.d_depth_params[i]));
+      mr = std::max(mr, std::abs(r.grads.d_depth_params[i]));
+    }
+    CHECK(m <= 1e-5 * mr, "predictor d_params %g", m / mr);
+  }
   std::printf("OK %d\n", g_checks);
   return 0;
 }
