@@ -286,6 +286,46 @@ __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __re
 // ---------------------------------------------------------------------------
 // trajectories -> splat records + per-(sort tile, slot) cell boxes
 
+__device__ __forceinline__ uint4 make_rec(const Cell& c, uint32_t dt, int pol) {
+  return make_uint4((uint32_t)c.x0 | ((uint32_t)c.y0 << 16) | ((uint32_t)pol << 31), dt,
+                    __float_as_uint(compress_frac(c.wx)), __float_as_uint(compress_frac(c.wy)));
+}
+
+// trajectory (cmax_device.cuh, build_trajectory warp.hpp:257-281) emitting the
+// splat record of every reference instead of its position: the bilinear cells
+// of the interior references 1..B-1 are the ones the flow sampling of the next
+// step computes anyway, so only references 0 and B need their own bilin_cell.
+// rec[r * stride] receives the record of reference r. Returns alive.
+__device__ __forceinline__ bool trajectory_records(double x0, double y0, double t, int j,
+                                                   const double2* __restrict__ flows,
+                                                   const WinParams& P, const double* es,
+                                                   uint4* rec, int stride, uint32_t dtu, int pol) {
+  const int W = P.W, H = P.H, B = P.B, HW = P.HW;
+  const Cell c0 = bilin_cell(x0, y0, W, H);
+  const double2 u0 = sample_flow(flows + (size_t)j * HW, c0);
+  const double db = ds(es[j], t), df = ds(es[j + 1], t);
+  double2 pb = make_double2(da(x0, dm(db, u0.x)), da(y0, dm(db, u0.y)));
+  double2 pf = make_double2(da(x0, dm(df, u0.x)), da(y0, dm(df, u0.y)));
+  bool ok = in_bounds(pb.x, pb.y, W, H) && in_bounds(pf.x, pf.y, W, H);
+  for (int s = 0; s < B - 1; ++s) {
+    const bool back = s < j;
+    // backward leg: bin i = j-1-s sampled at pos[i+1] (reference i+1), writes pos[i]
+    // forward leg:  bin i = s+1     sampled at pos[i]   (reference i),   writes pos[i+1]
+    const int i = back ? j - 1 - s : s + 1;
+    const double2 p = back ? pb : pf;
+    const double dt = back ? ds(es[i], es[i + 1]) : ds(es[i + 1], es[i]);
+    const Cell c = bilin_cell(p.x, p.y, W, H);
+    rec[(back ? i + 1 : i) * stride] = make_rec(c, dtu, pol);
+    const double2 u = sample_flow(flows + (size_t)i * HW, c);
+    const double2 q = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
+    ok = ok && in_bounds(q.x, q.y, W, H);
+    if (back) pb = q; else pf = q;
+  }
+  rec[0] = make_rec(bilin_cell(pb.x, pb.y, W, H), dtu, pol);  // pb = pos[0]
+  rec[B * stride] = make_rec(bilin_cell(pf.x, pf.y, W, H), dtu, pol);  // pf = pos[B]
+  return ok;
+}
+
 __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ sorted_keys,
@@ -294,7 +334,7 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
   extern __shared__ __align__(16) unsigned char smem[];
   double* es = reinterpret_cast<double*>(smem);
   uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
-  double2* pos = reinterpret_cast<double2*>(smem + kEvSmemHeader) + threadIdx.x;
+  uint4* srec = reinterpret_cast<uint4*>(smem + kEvSmemHeader) + threadIdx.x;  // [r][thread]
   for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
     es[i] = P.es[i];
     erel[i] = P.erel[i];
@@ -315,8 +355,9 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     const uint32_t dt = ev_dt(e);
     const double t = dm((double)dt, 1e-6);
     j = bin_of(dt, erel, P.B);
-    alive = trajectory((double)ev_x(e), (double)ev_y(e), t, j,
-                       flows + (size_t)w * P.B * P.HW, P, es, pos, blockDim.x);
+    alive = trajectory_records((double)ev_x(e), (double)ev_y(e), t, j,
+                               flows + (size_t)w * P.B * P.HW, P, es, srec, blockDim.x, dt,
+                               ev_pol(e));
     S = (int)sorted_keys[base + k];  // sort tile of this slot
   }
   const unsigned amask = __ballot_sync(kFull, alive);
@@ -335,25 +376,11 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
       atomicMin(&b->w, cmy);
     }
   };
+  const uint4 dead = make_uint4(kDead, 0u, 0u, 0u);
   for (int r = 0; r < R; ++r) {
-    FwdRec rec;
-    uint32_t x0 = 0, y0 = 0;
-    if (alive) {
-      const double2 p = pos[r * blockDim.x];
-      const Cell c = bilin_cell(p.x, p.y, P.W, P.H);
-      x0 = (uint32_t)c.x0;
-      y0 = (uint32_t)c.y0;
-      rec.cell = x0 | (y0 << 16) | ((uint32_t)ev_pol(e) << 31);
-      rec.dt = ev_dt(e);
-      rec.fx = compress_frac(c.wx);
-      rec.fy = compress_frac(c.wy);
-    } else {
-      rec.cell = kDead;
-      rec.dt = 0;
-      rec.fx = rec.fy = 0.f;
-    }
-    if (valid) recs[(size_t)r * n_total + base + k] = rec;
-    if (alive) box_update(peers, leader, r, x0, y0);
+    const uint4 rv = alive ? srec[r * blockDim.x] : dead;
+    if (valid) reinterpret_cast<uint4*>(recs)[(size_t)r * n_total + base + k] = rv;
+    if (alive) box_update(peers, leader, r, rv.x & 0xffffu, (rv.x >> 16) & 0x7fffu);
   }
   // source-pixel boxes per bin (the partial steps of the backward sink at x0)
   if (alive) {
@@ -561,7 +588,7 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                          uint64_t n_total, FwdRec* recs, uint4* bbox, uint32_t* lcount,
                          uint16_t* lists) {
   static size_t a = 0;
-  const size_t smem = kEvSmemHeader + sizeof(double2) * (size_t)(P.B + 1) * kEvBlock;
+  const size_t smem = kEvSmemHeader + sizeof(uint4) * (size_t)(P.B + 1) * kEvBlock;
   set_smem(reinterpret_cast<const void*>(k_traj_records), smem, &a);
   if (max_n > 0) {
     count_launch();
