@@ -86,10 +86,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// wait for phase `parity`; back off between polls so that waiting warps leave
-// the issue slots to the CTAs that still compute
+// try_wait with a suspend-time hint: the waiting warp is parked by the hardware
+// until the phase completes (or the hint expires), instead of polling -- waiting
+// warps leave the issue slots to the CTAs that still compute
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
 }
 // global -> shared bulk copy (16 B aligned, size a multiple of 16) completing on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -899,6 +914,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const float2* s8 = stage8 + b * kStageQ;
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
+    const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
     // record sinks of reference d.r (slots < split)
     compacted<kCons>(
         (uint32_t)cw * 32, d.split, wq[cw],
@@ -914,9 +930,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           const uint4 rec = s16[v];
           const int lx = (int)(rec.x & 0xffffu) - ox0, ly = (int)((rec.x >> 16) & 0x7fffu) - oy0;
           const float2 g = s8[v];
-          // the bin this sink belongs to (bin_of on the record's time, warp.hpp:284-288)
-          const int j = bin_of(rec.y, P.erel, B);
-          const int bin = (d.r <= j) ? d.r - 1 : d.r;
+          // the bin this sink belongs to: r - 1 if r <= j else r, and for
+          // 1 <= r <= B-1, r <= bin_of(t) (warp.hpp:284-288) iff erel[r] <= dt
+          const int bin = (rec.y >= er) ? d.r - 1 : d.r;
           const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
           double wx, ax, wy, ay;
           expand_frac(__uint_as_float(rec.z), wx, ax);
