@@ -392,30 +392,40 @@ def cuda_arm(args, wl):
         h_poses = torch.from_numpy(poses).pin_memory()
         h_ev = torch.from_numpy(ev.view(np.uint8)).pin_memory()
         h_red = torch.empty_like(red, device="cpu").pin_memory()
+        # the public pipelined feed (paper_2412_06359_b200/pipeline.py): batch
+        # i+1's pinned host -> device copy overlaps batch i's compute; every
+        # batch's reduced result is read back by the host. The L2 flush (160 MB
+        # > 126 MB L2) runs inside the timed region, after each batch.
+        pipe = P.ChainPipeline(eng, compute_stream=stream)
+        flush160 = flush[: 160 * 1024 * 1024 // 4]
 
-        def e2e_step():
-            eng.chain_batch(h_depth, h_poses, K, 0, wl["window_us"], h_ev, offs, out=out,
-                            out_device=True)
-            reduce_and_allreduce()
-            h_red.copy_(red, non_blocking=True)
+        def post(loss, dd, dp):
+            pack_window_sums(loss, dd, dp, out=red)
+            allreduce_window_sums(red)
+            flush160.zero_()
+            return red
 
-        with torch.cuda.stream(stream):
-            for _ in range(max(1, args.warmup)):
-                e2e_step()
-            stream.synchronize()
-            es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-            ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize(dev)
-            for i in range(args.steps):
-                flush.zero_()
-                es[i].record(stream)
-                e2e_step()
-                ee[i].record(stream)
-                stream.synchronize()  # the host reads the result every step
-            torch.cuda.synchronize(dev)
-        e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
+        def batches(n):
+            for _ in range(n):
+                yield (h_depth, h_poses, h_ev, offs)
+
+        for _ in pipe.run(batches(max(4, args.warmup)), K, 0, wl["window_us"], post=post,
+                          host_out=h_red):
+            pass
+        t0e = torch.cuda.Event(enable_timing=True)
+        t1e = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0e.record(stream)
+        pipe.copy.wait_event(t0e)  # the first batch's copy is inside the timed region
+        n_done = 0
+        for _ in pipe.run(batches(args.steps), K, 0, wl["window_us"], post=post, host_out=h_red):
+            n_done += 1
+        t1e.record(stream)
+        torch.cuda.synchronize(dev)
+        assert n_done == args.steps
+        e2e_ms = t0e.elapsed_time(t1e)
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -423,7 +433,9 @@ def cuda_arm(args, wl):
         e2e = {"value": events_per_step * args.steps / (e2e_ms * 1e-3) / 1e6, "unit": "Mevents/s",
                "h2d_bytes_per_step": int(h_depth.numel() * 8 + h_poses.numel() * 8 + h_ev.numel()),
                "d2h_bytes_per_step": int(h_red.numel() * 8),
-               "ms_per_step": e2e_ms / args.steps}
+               "ms_per_step": e2e_ms / args.steps,
+               "api": "ChainPipeline.run (double-buffered H2D overlapping compute; "
+                      "result read back every batch; 160 MB L2 flush per batch inside the timing)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

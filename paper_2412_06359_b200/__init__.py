@@ -17,6 +17,7 @@ from .predictor import (  # noqa: F401
 from .geo import (  # noqa: F401
     GEO_WEIGHT_DEFAULT, GeoBatch, GeoLossGrad, GeoLossTerms, geometry_consistency_loss,
     geometry_consistency_loss_backward, geometry_consistency_loss_batch, total_loss)
+from .pipeline import ChainPipeline  # noqa: F401
 from .io import Windows, format_number, read_events, slice_windows, write_events  # noqa: F401
 from .optimize import (  # noqa: F401
     FlowOnlyResult, RunResult, TrainLog, TrainRecord, optimize_flow_only, predictor_total_loss,

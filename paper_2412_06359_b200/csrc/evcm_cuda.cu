@@ -2,6 +2,7 @@
 // error taxonomy, workspace management, host<->device staging, and the stage
 // sequencing of Engine::forward / backward, the motion field and the batched
 // chain. Kernels live in cmax_kernels.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -142,12 +143,22 @@ struct evcm_cuda_engine {
   std::unordered_map<std::string, Buf> pins;  // pinned host staging
   int stage_nw = 0;
   bool check_pose_flag = false;  // device pose tables: validation result pending
-  // CUDA graph of the device-resident chain: replayed when a call repeats the
-  // previous call's signature (shapes, pointers, event offsets, options)
-  std::vector<uint64_t> gsig;
-  cudaGraphExec_t gexec = nullptr;
-  bool gfailed = false;  // capture failed for this signature: run eagerly
-  int glaunches = 0;
+  // CUDA graphs of the device-resident chain, keyed by the call signature
+  // (shapes, pointers, event offsets, options): the first call of a signature
+  // runs eagerly, the second is captured, later ones replay. A few signatures
+  // are kept (e.g. double-buffered inputs of a pipelined caller); every entry
+  // is dropped when a workspace buffer is reallocated (alloc_gen), since its
+  // graph would reference the freed memory.
+  struct GraphEntry {
+    std::vector<uint64_t> sig;
+    cudaGraphExec_t exec = nullptr;
+    bool failed = false;  // capture failed for this signature: run eagerly
+    int launches = 0;
+    uint64_t gen = 0, last_use = 0;
+  };
+  static constexpr size_t kGraphCache = 4;
+  std::vector<GraphEntry> graphs;
+  uint64_t alloc_gen = 0, use_clock = 0;
   // owner pipeline state
   TileParams TP{};
   uint64_t n_total = 0, max_n = 0;
@@ -172,6 +183,7 @@ struct evcm_cuda_engine {
       b.p = nullptr;
       ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
       b.cap = bytes;
+      ++alloc_gen;
     }
     return static_cast<T*>(b.p);
   }
@@ -626,7 +638,8 @@ void evcm_cuda_destroy(evcm_cuda_engine* e) {
   for (auto& kv : e->pins)
     if (kv.second.p) cudaFreeHost(kv.second.p);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
-  if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  for (auto& g : e->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (e->own_stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -946,25 +959,63 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
   const bool graphable = in_mem == EVCM_MEM_DEVICE && out_mem == EVCM_MEM_DEVICE && !e->timing;
   std::vector<uint64_t> sig;
   if (graphable) sig = chain_signature(e, bt, out, depth_dev);
-  const bool same = graphable && sig == e->gsig;
-  if (same && e->gexec) {
+  using GE = evcm_cuda_engine::GraphEntry;
+  GE* g = nullptr;
+  if (graphable) {
+    for (GE& x : e->graphs)
+      if (x.sig == sig) g = &x;
+    if (g && g->gen != e->alloc_gen) {  // workspace moved since the capture
+      if (g->exec) cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+      g->failed = false;
+      g->gen = e->alloc_gen;
+      g->last_use = ++e->use_clock;
+      g = nullptr;  // this call runs eagerly (and re-sizes nothing); the next captures
+      for (GE& x : e->graphs)
+        if (x.sig == sig) x.gen = e->alloc_gen;
+      goto eager;
+    }
+  }
+  if (g && g->exec) {
     // replay: the state the eager path leaves behind is unchanged (same signature)
-    ck(cudaGraphLaunch(e->gexec, e->stream), "graph launch");
+    g->last_use = ++e->use_clock;
+    ck(cudaGraphLaunch(g->exec, e->stream), "graph launch");
     e->stage_nw = bt->n_windows;
     e->check_pose_flag = true;
     e->have_fwd = false;
     sync_and_check(e, "chain");
-    e->last_launches = e->glaunches;
+    e->last_launches = g->launches;
     return;
   }
-  if (!same) {
-    if (e->gexec) cudaGraphExecDestroy(e->gexec);
-    e->gexec = nullptr;
-    e->gfailed = false;
-    e->gsig = sig;  // empty when not graphable
+  if (graphable && !g) {  // first call of this signature: remember it, run eagerly
+    if (e->graphs.size() >= evcm_cuda_engine::kGraphCache) {
+      auto lru = std::min_element(e->graphs.begin(), e->graphs.end(),
+                                  [](const GE& x, const GE& y) { return x.last_use < y.last_use; });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      e->graphs.erase(lru);
+    }
+    GE ne;
+    ne.sig = sig;
+    ne.last_use = ++e->use_clock;
+    e->graphs.push_back(ne);
+    // sized by this eager run; the capture of the next identical call must not
+    // see a reallocation, so the entry's generation is taken after it
+    chain_enqueue(e, bt, in_mem, out_mem, out, depth_dev);
+    sync_and_check(e, "chain");
+    e->graphs.back().gen = e->alloc_gen;
+    for (GE& x : e->graphs)  // earlier entries survive only if nothing moved
+      if (x.gen != e->alloc_gen && x.exec) {
+        cudaGraphExecDestroy(x.exec);
+        x.exec = nullptr;
+        x.gen = e->alloc_gen;
+      }
+    e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);
+    e->last_launches = launch_count();
+    return;
   }
-  if (same && !e->gfailed) {
+  if (g && !g->failed) {
     // second identical call: capture the enqueue into a graph, then replay it
+    g->last_use = ++e->use_clock;
     cudaGraph_t graph = nullptr;
     ck(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
     bool ok = true;
@@ -977,21 +1028,28 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
       throw;
     }
     if (cudaStreamEndCapture(e->stream, &graph) != cudaSuccess ||
-        cudaGraphInstantiate(&e->gexec, graph, 0) != cudaSuccess) {
+        cudaGraphInstantiate(&g->exec, graph, 0) != cudaSuccess) {
       ok = false;
-      e->gexec = nullptr;
+      g->exec = nullptr;
       cudaGetLastError();
     }
     if (graph) cudaGraphDestroy(graph);
-    if (ok) {
-      e->glaunches = launch_count();
-      ck(cudaGraphLaunch(e->gexec, e->stream), "graph launch");
+    if (ok && g->gen == e->alloc_gen) {
+      g->launches = launch_count();
+      ck(cudaGraphLaunch(g->exec, e->stream), "graph launch");
       sync_and_check(e, "chain");
-      e->last_launches = e->glaunches;
+      e->last_launches = g->launches;
       return;
     }
-    e->gfailed = true;  // fall through: eager run
+    if (ok) {  // a buffer moved during the capture: the graph is stale
+      cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+      g->gen = e->alloc_gen;
+    } else {
+      g->failed = true;  // fall through: eager run
+    }
   }
+eager:
   chain_enqueue(e, bt, in_mem, out_mem, out, depth_dev);
   sync_and_check(e, "chain");
   e->collect_range(0, e->owner() ? 9 : M_FWD0 + 6);

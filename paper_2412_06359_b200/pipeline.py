@@ -1,0 +1,103 @@
+"""Pipelined host -> device feeding of the batched chain (Engine.chain_batch).
+
+A training or serving loop that receives its event batches in host memory pays
+the PCIe copy of every batch (16 B per event plus the depth maps and poses).
+``ChainPipeline`` hides it behind the compute of the previous batch: two device
+input buffer sets, a copy stream that stages batch i+1 (pinned host -> device)
+while the engine stream runs batch i, and an event that makes batch i+1's
+compute wait for its own copy. Each batch still returns its result to the host
+(the caller's ``post`` reduction, read back every step). The engine caches one
+CUDA graph per input buffer set, so both alternating calls replay graphs.
+"""
+from __future__ import annotations
+
+from typing import Callable, Iterable, Iterator, Optional
+
+import numpy as np
+
+from .engine import ConfigError, Engine, _is_torch
+
+
+class ChainPipeline:
+    """Double-buffered ``chain_batch`` over a stream of host batches.
+
+    ``engine`` must run on a torch CUDA stream (EngineOptions(stream=...)) or its
+    own stream; the pipeline uses ``compute_stream`` (default: the current torch
+    stream of the engine's device) for the waits and the result read-back."""
+
+    def __init__(self, engine: Engine, compute_stream=None):
+        import torch
+        self.engine = engine
+        self.dev = torch.device("cuda", engine.opts.device)
+        if compute_stream is None:
+            if engine.opts.stream is None:
+                raise ConfigError("ChainPipeline: the engine needs an explicit stream "
+                                  "(EngineOptions(stream=torch_stream.cuda_stream))")
+            compute_stream = torch.cuda.ExternalStream(engine.opts.stream, device=self.dev)
+        self.compute = compute_stream
+        self.copy = torch.cuda.Stream(self.dev)
+        self.sets = [None, None]
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.out = None
+
+    def _stage(self, slot: int, depth, poses, events):
+        import torch
+        cur = self.sets[slot]
+        if cur is None or cur[0].shape != depth.shape or cur[1].shape != poses.shape or \
+                cur[2].shape != events.shape:
+            cur = (torch.empty(depth.shape, dtype=torch.float64, device=self.dev),
+                   torch.empty(poses.shape, dtype=torch.float64, device=self.dev),
+                   torch.empty(events.shape, dtype=torch.uint8, device=self.dev))
+            self.sets[slot] = cur
+        with torch.cuda.stream(self.copy):
+            cur[0].copy_(depth, non_blocking=True)
+            cur[1].copy_(poses, non_blocking=True)
+            cur[2].copy_(events, non_blocking=True)
+            self.copied[slot].record(self.copy)
+        return cur
+
+    def run(self, batches: Iterable, k, t_start_us: int, t_end_us: int,
+            post: Optional[Callable] = None, host_out=None,
+            window_stride_us: int = 0) -> Iterator:
+        """For each host batch ``(depth [n,H,W] f64, poses [n,B,6] f64, events
+        uint8 [N,16], ev_offsets [n+1])`` -- pinned torch CPU tensors -- run the
+        chain and yield the host result: ``post(loss, d_depth, d_poses)`` (a
+        device tensor, e.g. a data-parallel reduction) copied into ``host_out``
+        (pinned), or the three outputs copied to the host when ``post`` is None."""
+        import torch
+        it = iter(batches)
+        cur = next(it, None)
+        if cur is None:
+            return
+        for a in cur[:3]:
+            if not (_is_torch(a) and not a.is_cuda):
+                raise ConfigError("ChainPipeline: batches must be host (pinned) torch tensors")
+        staged = self._stage(0, *cur[:3])
+        slot = 0
+        while cur is not None:
+            nxt = next(it, None)
+            if nxt is not None:  # batch i+1 copies while batch i computes
+                staged_next = self._stage(1 - slot, *nxt[:3])
+            self.compute.wait_event(self.copied[slot])
+            nw = staged[0].shape[0]
+            if self.out is None or self.out[1].shape != staged[0].shape or \
+                    self.out[2].shape != staged[1].shape:
+                self.out = (torch.empty(nw, dtype=torch.float64, device=self.dev),
+                            torch.empty(tuple(staged[0].shape), dtype=torch.float64, device=self.dev),
+                            torch.empty(tuple(staged[1].shape), dtype=torch.float64, device=self.dev))
+            with torch.cuda.stream(self.compute):
+                self.engine.chain_batch(staged[0], staged[1], k, t_start_us, t_end_us, staged[2],
+                                        np.asarray(cur[3], np.uint64), out=self.out,
+                                        out_device=True, window_stride_us=window_stride_us)
+                if post is not None:
+                    r = post(*self.out)
+                    dst = host_out if host_out is not None else \
+                        torch.empty(r.shape, dtype=r.dtype).pin_memory()
+                    dst.copy_(r, non_blocking=True)
+                else:
+                    dst = tuple(o.to("cpu", non_blocking=True) for o in self.out)
+            self.compute.synchronize()  # the host reads every batch's result
+            yield dst
+            cur = nxt
+            if nxt is not None:
+                staged, slot = staged_next, 1 - slot

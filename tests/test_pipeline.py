@@ -1,0 +1,52 @@
+"""ChainPipeline (pipeline.py): double-buffered host -> device feeding of the
+batched chain gives, batch by batch, exactly what a direct chain_batch call on
+the same inputs gives (same engine path, graphs replayed per buffer set)."""
+import numpy as np
+import pytest
+
+import paper_2412_06359_b200 as P
+from tests.helpers import chain_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipeline_matches_direct_calls():
+    import torch
+    s = torch.cuda.Stream()
+    eng = P.Engine(P.EngineOptions(stream=s.cuda_stream))
+    ref_eng = P.Engine(P.EngineOptions())
+    batches, refs = [], []
+    for seed in range(7):  # 7 batches: both buffer sets replay their graphs
+        depth, poses, K, ev, offs = chain_inputs(64, 48, 6, 3, 4000, seed=seed % 3)
+        batches.append((torch.from_numpy(depth).pin_memory(), torch.from_numpy(poses).pin_memory(),
+                        torch.from_numpy(ev.view(np.uint8)).pin_memory(), offs))
+        # device-resident inputs: the pipeline's path (device pose tables)
+        r = ref_eng.chain_batch(torch.from_numpy(depth).cuda(), torch.from_numpy(poses).cuda(), K, 0,
+                                100000, torch.from_numpy(ev.view(np.uint8)).cuda(), offs)
+        refs.append(tuple(x.cpu().numpy() for x in r))
+    pipe = P.ChainPipeline(eng, compute_stream=s)
+    outs = list(pipe.run(iter(batches), K, 0, 100000))
+    assert len(outs) == len(batches)
+    for (loss, dd, dp), (rl, rd, rp) in zip(outs, refs):
+        assert np.array_equal(loss.numpy(), rl)
+        assert np.array_equal(dd.numpy(), rd) and np.array_equal(dp.numpy(), rp)
+
+
+def test_pipeline_post_reduction_and_errors():
+    import torch
+    s = torch.cuda.Stream()
+    eng = P.Engine(P.EngineOptions(stream=s.cuda_stream))
+    depth, poses, K, ev, offs = chain_inputs(32, 24, 4, 2, 500, seed=4)
+    b = (torch.from_numpy(depth).pin_memory(), torch.from_numpy(poses).pin_memory(),
+         torch.from_numpy(ev.view(np.uint8)).pin_memory(), offs)
+    host = torch.empty(1, dtype=torch.float64).pin_memory()
+    got = [float(r[0]) for r in P.ChainPipeline(eng, s).run(
+        [b, b, b], K, 0, 100000, post=lambda l, d, p: l.sum().reshape(1), host_out=host)]
+    ref = float(P.Engine().chain_batch(torch.from_numpy(depth).cuda(), torch.from_numpy(poses).cuda(),
+                                       K, 0, 100000, torch.from_numpy(ev.view(np.uint8)).cuda(),
+                                       offs)[0].sum())
+    assert got == [ref] * 3
+    with pytest.raises(P.ConfigError):
+        next(P.ChainPipeline(eng, s).run([(depth, poses, ev, offs)], K, 0, 100000))
+    with pytest.raises(P.ConfigError):
+        P.ChainPipeline(P.Engine())  # no explicit stream
