@@ -409,8 +409,7 @@ def cuda_arm(args, wl):
             for _ in range(n):
                 yield (h_depth, h_poses, h_ev, offs)
 
-        for _ in pipe.run(batches(max(4, args.warmup)), K, 0, wl["window_us"], post=post,
-                          host_out=h_red):
+        for _ in pipe.run(batches(max(4, args.warmup)), K, 0, wl["window_us"], post=post):
             pass
         t0e = torch.cuda.Event(enable_timing=True)
         t1e = torch.cuda.Event(enable_timing=True)
@@ -420,8 +419,9 @@ def cuda_arm(args, wl):
         t0e.record(stream)
         pipe.copy.wait_event(t0e)  # the first batch's copy is inside the timed region
         n_done = 0
-        for _ in pipe.run(batches(args.steps), K, 0, wl["window_us"], post=post, host_out=h_red):
+        for res in pipe.run(batches(args.steps), K, 0, wl["window_us"], post=post):
             n_done += 1
+            assert res.numel() == h_red.numel()
         t1e.record(stream)
         torch.cuda.synchronize(dev)
         assert n_done == args.steps

@@ -222,6 +222,18 @@ EVCM_API int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* 
 EVCM_API int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* batch, int in_mem,
                                     int out_mem, evcm_chain_out* out);
 
+/* Asynchronous form for pipelined callers: enqueues the batch on the engine's
+ * stream and returns; when the call replays a captured graph (device inputs and
+ * outputs, third and later calls of a signature) it does not wait, and the
+ * batch's validation result is delivered by evcm_cuda_chain_wait(slot). Slots
+ * 0..3 carry separate error words, so batch i+1 can be queued before batch i
+ * is waited for. Calls that run eagerly complete (and report) synchronously. */
+EVCM_API int evcm_cuda_chain_batch_async(evcm_cuda_engine* e, const evcm_chain_batch* batch,
+                                         int in_mem, int out_mem, evcm_chain_out* out, int slot);
+/* Waits for the batch queued on `slot` and raises its validation errors (the
+ * same codes a synchronous call returns). No-op for a slot with nothing pending. */
+EVCM_API int evcm_cuda_chain_wait(evcm_cuda_engine* e, int slot);
+
 /* ---- predictor decode chain ------------------------------- */
 
 /* decode (predictor.hpp:126-131): depth[ph*f][pw*f] =

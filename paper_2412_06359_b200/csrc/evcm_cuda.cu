@@ -159,6 +159,20 @@ struct evcm_cuda_engine {
   static constexpr size_t kGraphCache = 4;
   std::vector<GraphEntry> graphs;
   uint64_t alloc_gen = 0, use_clock = 0;
+  // asynchronous chain calls (evcm_cuda_chain_batch_async): each of kSlots
+  // slots has its own pinned error words, completion event and pending checks,
+  // so a caller can keep the next batch queued while it waits for this one
+  static constexpr int kSlots = 4;
+  int slot = 0;
+  struct Pending {
+    bool active = false;
+    int nw = 0;
+    bool pose = false;
+    cudaEvent_t done = nullptr;
+  } pending[kSlots];
+  std::string slot_name(const char* base) const {
+    return slot ? std::string(base) + "#" + std::to_string(slot) : std::string(base);
+  }
   // owner pipeline state
   TileParams TP{};
   uint64_t n_total = 0, max_n = 0;
@@ -345,7 +359,7 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   } else {
     launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
   }
-  unsigned long long* err_h = e->pinned<unsigned long long>("stage_err_h", nw);
+  unsigned long long* err_h = e->pinned<unsigned long long>(e->slot_name("stage_err_h"), nw);
   ck(cudaMemcpyAsync(err_h, err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream),
      "D2H err");
   e->stage_nw = nw;
@@ -354,7 +368,7 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
 // After the stream sync: raise the reference's error for the first invalid
 // event of the first bad window (EventSlice::validate order, types.hpp:143-155).
 void check_stage_errors(evcm_cuda_engine* e) {
-  const unsigned long long* h = e->pinned<unsigned long long>("stage_err_h", e->stage_nw);
+  const unsigned long long* h = e->pinned<unsigned long long>(e->slot_name("stage_err_h"), e->stage_nw);
   for (int w = 0; w < e->stage_nw; ++w) {
     if (h[w] == ~0ull) continue;
     const int code = static_cast<int>(h[w] & 0xf);
@@ -376,7 +390,7 @@ void sync_and_check(evcm_cuda_engine* e, const char* what) {
   // (optimize.hpp:211-213), so a bad pose wins over a bad event.
   if (e->check_pose_flag) {
     e->check_pose_flag = false;
-    if (*e->pinned<int>("pose_bad_h", 1))
+    if (*e->pinned<int>(e->slot_name("pose_bad_h"), 1))
       fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi and components finite");
   }
   check_stage_errors(e);
@@ -640,6 +654,8 @@ void evcm_cuda_destroy(evcm_cuda_engine* e) {
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   for (auto& g : e->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& q : e->pending)
+    if (q.done) cudaEventDestroy(q.done);
   if (e->own_stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -888,7 +904,7 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
       ck(cudaMemsetAsync(bad, 0, sizeof(int), e->stream), "memset");
       double* tab_d = e->get<double>("pose_tab", (size_t)nw * B * kPoseTab);
       launch_pose_table(e->stream, bt->poses, nw, B, inv_d, tab_d, bad);
-      ck(cudaMemcpyAsync(e->pinned<int>("pose_bad_h", 1), bad, sizeof(int), cudaMemcpyDeviceToHost,
+      ck(cudaMemcpyAsync(e->pinned<int>(e->slot_name("pose_bad_h"), 1), bad, sizeof(int), cudaMemcpyDeviceToHost,
                          e->stream), "D2H");
       e->check_pose_flag = true;
       tab = tab_d;
@@ -939,6 +955,7 @@ std::vector<uint64_t> chain_signature(const evcm_cuda_engine* e, const evcm_chai
     std::memcpy(&b, &v, 8);
     g.push_back(b);
   };
+  u((uint64_t)e->slot);  // the slot's pinned error words are baked into the graph
   u((uint64_t)bt->n_windows); u((uint64_t)bt->width); u((uint64_t)bt->height); u((uint64_t)bt->n_bins);
   u(bt->t_start_us); u(bt->t_end_us); u(bt->window_stride_us);
   for (double k : bt->K) d(k);
@@ -953,7 +970,7 @@ std::vector<uint64_t> chain_signature(const evcm_cuda_engine* e, const evcm_chai
 }
 
 void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int out_mem,
-                evcm_chain_out* out, const double* depth_dev) {
+                evcm_chain_out* out, const double* depth_dev, bool async = false) {
   if (!e || !bt || !out || !bt->ev_offsets) fail(EVCM_ERR_CONFIG, "null argument");
   set_device(e);
   const bool graphable = in_mem == EVCM_MEM_DEVICE && out_mem == EVCM_MEM_DEVICE && !e->timing;
@@ -980,11 +997,20 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
     // replay: the state the eager path leaves behind is unchanged (same signature)
     g->last_use = ++e->use_clock;
     ck(cudaGraphLaunch(g->exec, e->stream), "graph launch");
+    e->have_fwd = false;
+    e->last_launches = g->launches;
+    if (async) {  // checked by evcm_cuda_chain_wait(slot)
+      auto& q = e->pending[e->slot];
+      if (!q.done) ck(cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(q.done, e->stream), "event record");
+      q.active = true;
+      q.nw = bt->n_windows;
+      q.pose = true;  // graphs only exist for device inputs: device pose tables
+      return;
+    }
     e->stage_nw = bt->n_windows;
     e->check_pose_flag = true;
-    e->have_fwd = false;
     sync_and_check(e, "chain");
-    e->last_launches = g->launches;
     return;
   }
   if (graphable && !g) {  // first call of this signature: remember it, run eagerly
@@ -1073,6 +1099,43 @@ int evcm_cuda_chain_batch2(evcm_cuda_engine* e, const evcm_chain_batch* bt, int 
 
 int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* bt, int mem, evcm_chain_out* out) {
   return evcm_cuda_chain_batch2(e, bt, mem, mem, out);
+}
+
+int evcm_cuda_chain_batch_async(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem,
+                                int out_mem, evcm_chain_out* out, int slot) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    if (slot < 0 || slot >= evcm_cuda_engine::kSlots) fail(EVCM_ERR_CONFIG, "chain: slot out of range");
+    if (e->pending[slot].active) fail(EVCM_ERR_STATE, "chain: slot still pending (call evcm_cuda_chain_wait)");
+    struct Restore {
+      evcm_cuda_engine* e;
+      ~Restore() { e->slot = 0; }
+    } restore{e};
+    e->slot = slot;
+    chain_impl(e, bt, in_mem, out_mem, out, nullptr, true);
+  });
+}
+
+int evcm_cuda_chain_wait(evcm_cuda_engine* e, int slot) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    if (slot < 0 || slot >= evcm_cuda_engine::kSlots) fail(EVCM_ERR_CONFIG, "chain: slot out of range");
+    auto& q = e->pending[slot];
+    if (!q.active) return;  // the call already completed synchronously
+    q.active = false;
+    set_device(e);
+    ck(cudaEventSynchronize(q.done), "chain wait");
+    struct Restore {
+      evcm_cuda_engine* e;
+      ~Restore() { e->slot = 0; }
+    } restore{e};
+    e->slot = slot;
+    if (q.pose && *e->pinned<int>(e->slot_name("pose_bad_h"), 1))
+      fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi and components finite");
+    e->stage_nw = q.nw;
+    check_stage_errors(e);
+    ck(cudaGetLastError(), "chain wait");
+  });
 }
 
 int evcm_cuda_validate_slice(evcm_cuda_engine* e, const evcm_slice* sl, int check_window, int mem,

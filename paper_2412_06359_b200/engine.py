@@ -157,6 +157,8 @@ def load_library(build_if_missing: bool = True):
                                                          vp, i32, vp, vp]
     L.evcm_cuda_chain_batch.argtypes = [vp, vp, i32, vp]
     L.evcm_cuda_chain_batch2.argtypes = [vp, vp, i32, i32, vp]
+    L.evcm_cuda_chain_batch_async.argtypes = [vp, vp, i32, i32, vp, i32]
+    L.evcm_cuda_chain_wait.argtypes = [vp, i32]
     L.evcm_cuda_set_timing.argtypes = [vp, i32]
     L.evcm_cuda_stage_times.argtypes = [vp, vp, i32]
     L.evcm_cuda_last_launch_count.argtypes = [vp]
@@ -587,6 +589,28 @@ class Engine:
         same side as the inputs). Window w spans [t_start_us, t_end_us) +
         w * window_stride_us (0: one clock for all windows; the window length:
         consecutive windows of one stream, see io.slice_windows)."""
+        out, args = self._chain_args(depth, poses, k, t_start_us, t_end_us, events, ev_offsets,
+                                     out, out_device, window_stride_us)
+        _raise(load_library().evcm_cuda_chain_batch2(self._h, *args))
+        return out
+
+    def chain_batch_async(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out,
+                          slot: int, window_stride_us: int = 0):
+        """chain_batch that does not wait when it replays a captured graph (device
+        inputs/outputs): the batch is queued on the engine's stream and its
+        validation result is raised by ``chain_wait(slot)``. ``out`` (device
+        tensors) must be given; slots 0..3 may be in flight together."""
+        out, args = self._chain_args(depth, poses, k, t_start_us, t_end_us, events, ev_offsets,
+                                     out, True, window_stride_us)
+        _raise(load_library().evcm_cuda_chain_batch_async(self._h, *args, int(slot)))
+        return out
+
+    def chain_wait(self, slot: int) -> None:
+        """Waits for the batch queued on ``slot`` and raises its errors."""
+        _raise(load_library().evcm_cuda_chain_wait(self._h, int(slot)))
+
+    def _chain_args(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out,
+                    out_device, window_stride_us):
         nw, H, W = depth.shape
         B = poses.shape[1]
         in_mem = _mem_of(depth, poses, events)
@@ -615,9 +639,9 @@ class Engine:
                          _ptr(events), offs.ctypes.data_as(C.c_void_p), _ptr(depth), _ptr(poses),
                          int(window_stride_us))
         co = _ChainOut(_ptr(out[0]), None, _ptr(out[1]), _ptr(out[2]))
-        _raise(load_library().evcm_cuda_chain_batch2(self._h, C.byref(bt), in_mem, out_mem,
-                                                     C.byref(co)))
-        return out
+        # keep the (possibly converted) inputs alive until the call has enqueued them
+        self._keep = (bt, co, offs, depth, poses, events, K)
+        return out, (C.byref(bt), in_mem, out_mem, C.byref(co))
 
 
 # ---------------------------------------------------------------------------

@@ -7,7 +7,10 @@ input buffer sets, a copy stream that stages batch i+1 (pinned host -> device)
 while the engine stream runs batch i, and an event that makes batch i+1's
 compute wait for its own copy. Each batch still returns its result to the host
 (the caller's ``post`` reduction, read back every step). The engine caches one
-CUDA graph per input buffer set, so both alternating calls replay graphs.
+CUDA graph per input buffer set, so both alternating calls replay graphs, and
+the calls are asynchronous (Engine.chain_batch_async): batch i+1 is already
+queued on the GPU while the host waits for batch i's result, so the device
+never idles between batches.
 """
 from __future__ import annotations
 
@@ -57,13 +60,15 @@ class ChainPipeline:
         return cur
 
     def run(self, batches: Iterable, k, t_start_us: int, t_end_us: int,
-            post: Optional[Callable] = None, host_out=None,
+            post: Optional[Callable] = None,
             window_stride_us: int = 0) -> Iterator:
         """For each host batch ``(depth [n,H,W] f64, poses [n,B,6] f64, events
         uint8 [N,16], ev_offsets [n+1])`` -- pinned torch CPU tensors -- run the
         chain and yield the host result: ``post(loss, d_depth, d_poses)`` (a
-        device tensor, e.g. a data-parallel reduction) copied into ``host_out``
-        (pinned), or the three outputs copied to the host when ``post`` is None."""
+        device tensor, e.g. a data-parallel reduction) copied into a pinned host
+        buffer owned by the pipeline (valid until two batches later), or the
+        three outputs copied to the host when ``post`` is None. A batch's
+        validation error is raised when its result is collected."""
         import torch
         it = iter(batches)
         cur = next(it, None)
@@ -72,11 +77,23 @@ class ChainPipeline:
         for a in cur[:3]:
             if not (_is_torch(a) and not a.is_cuda):
                 raise ConfigError("ChainPipeline: batches must be host (pinned) torch tensors")
+        if not hasattr(self, "consumed"):
+            self.consumed = [torch.cuda.Event(), torch.cuda.Event()]
+            self.done = [torch.cuda.Event(), torch.cuda.Event()]
+            self.host = [None, None]
         staged = self._stage(0, *cur[:3])
         slot = 0
+        prev = None  # (slot, host result) of the batch queued before this one
+
+        def finish(p):
+            self.engine.chain_wait(p[0])  # raises the batch's validation errors
+            self.done[p[0]].synchronize()  # its result is in host memory
+            return p[1]
+
         while cur is not None:
             nxt = next(it, None)
             if nxt is not None:  # batch i+1 copies while batch i computes
+                self.copy.wait_event(self.consumed[1 - slot])  # batch i-1 read that set
                 staged_next = self._stage(1 - slot, *nxt[:3])
             self.compute.wait_event(self.copied[slot])
             nw = staged[0].shape[0]
@@ -86,18 +103,25 @@ class ChainPipeline:
                             torch.empty(tuple(staged[0].shape), dtype=torch.float64, device=self.dev),
                             torch.empty(tuple(staged[1].shape), dtype=torch.float64, device=self.dev))
             with torch.cuda.stream(self.compute):
-                self.engine.chain_batch(staged[0], staged[1], k, t_start_us, t_end_us, staged[2],
-                                        np.asarray(cur[3], np.uint64), out=self.out,
-                                        out_device=True, window_stride_us=window_stride_us)
+                self.engine.chain_batch_async(staged[0], staged[1], k, t_start_us, t_end_us,
+                                              staged[2], np.asarray(cur[3], np.uint64), self.out,
+                                              slot, window_stride_us=window_stride_us)
+                self.consumed[slot].record(self.compute)
                 if post is not None:
                     r = post(*self.out)
-                    dst = host_out if host_out is not None else \
-                        torch.empty(r.shape, dtype=r.dtype).pin_memory()
+                    h = self.host[slot]
+                    if h is None or h.shape != r.shape or h.dtype != r.dtype:
+                        h = torch.empty(r.shape, dtype=r.dtype).pin_memory()
+                        self.host[slot] = h
+                    dst = h
                     dst.copy_(r, non_blocking=True)
                 else:
                     dst = tuple(o.to("cpu", non_blocking=True) for o in self.out)
-            self.compute.synchronize()  # the host reads every batch's result
-            yield dst
+                self.done[slot].record(self.compute)
+            if prev is not None:
+                yield finish(prev)
+            prev = (slot, dst)
             cur = nxt
             if nxt is not None:
                 staged, slot = staged_next, 1 - slot
+        yield finish(prev)

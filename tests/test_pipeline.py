@@ -39,14 +39,31 @@ def test_pipeline_post_reduction_and_errors():
     depth, poses, K, ev, offs = chain_inputs(32, 24, 4, 2, 500, seed=4)
     b = (torch.from_numpy(depth).pin_memory(), torch.from_numpy(poses).pin_memory(),
          torch.from_numpy(ev.view(np.uint8)).pin_memory(), offs)
-    host = torch.empty(1, dtype=torch.float64).pin_memory()
     got = [float(r[0]) for r in P.ChainPipeline(eng, s).run(
-        [b, b, b], K, 0, 100000, post=lambda l, d, p: l.sum().reshape(1), host_out=host)]
+        [b, b, b, b, b], K, 0, 100000, post=lambda l, d, p: l.sum().reshape(1))]
     ref = float(P.Engine().chain_batch(torch.from_numpy(depth).cuda(), torch.from_numpy(poses).cuda(),
                                        K, 0, 100000, torch.from_numpy(ev.view(np.uint8)).cuda(),
                                        offs)[0].sum())
-    assert got == [ref] * 3
+    assert got == [ref] * 5
     with pytest.raises(P.ConfigError):
         next(P.ChainPipeline(eng, s).run([(depth, poses, ev, offs)], K, 0, 100000))
     with pytest.raises(P.ConfigError):
         P.ChainPipeline(P.Engine())  # no explicit stream
+
+
+def test_pipeline_reports_a_bad_batch():
+    """An invalid event in a later (graph-replayed, asynchronous) batch raises the
+    reference's error class when that batch's result is collected."""
+    import torch
+    s = torch.cuda.Stream()
+    eng = P.Engine(P.EngineOptions(stream=s.cuda_stream))
+    depth, poses, K, ev, offs = chain_inputs(32, 24, 4, 2, 500, seed=5)
+    bad = ev.copy()
+    bad["x"][7] = 32
+    mk = lambda e: (torch.from_numpy(depth).pin_memory(), torch.from_numpy(poses).pin_memory(),
+                    torch.from_numpy(e.view(np.uint8)).pin_memory(), offs)
+    seen = 0
+    with pytest.raises(P.CoordinateRangeError):
+        for _ in P.ChainPipeline(eng, s).run([mk(ev)] * 6 + [mk(bad)], K, 0, 100000):
+            seen += 1
+    assert seen == 6
