@@ -135,17 +135,13 @@ __device__ void rodrigues_dev(const double* w, double* R) {
   for (int i = 0; i < 9; ++i) R[i] = ((i % 4 == 0 ? 1.0 : 0.0) + a * S[i]) + b * S2[i];
 }
 
-__global__ void k_pose_table(const double* __restrict__ poses, int n, int B,
-                             const double* __restrict__ inv_dt, double* __restrict__ tab,
-                             int* __restrict__ bad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (window, bin)
-  if (i >= n) return;
-  const double* p = poses + 6 * (size_t)i;
+// One (window, bin) entry of the pose table: R[9], dR[27], t[3], inv_dt.
+// Returns true when the pose fails PoseStep::validate (types.hpp:362-368).
+__device__ bool pose_entry(const double* __restrict__ p, double inv_dt, double* __restrict__ t) {
   const double pi = 3.14159265358979323846;
-  if (!(sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]) < pi) || !isfinite(p[0]) || !isfinite(p[1]) ||
-      !isfinite(p[2]) || !isfinite(p[3]) || !isfinite(p[4]) || !isfinite(p[5]))
-    atomicExch(bad, 1);
-  double* t = tab + (size_t)i * kPoseTab;
+  const bool bad = !(sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]) < pi) || !isfinite(p[0]) ||
+                   !isfinite(p[1]) || !isfinite(p[2]) || !isfinite(p[3]) || !isfinite(p[4]) ||
+                   !isfinite(p[5]);
   double R[9], S[9];
   rodrigues_dev(p, R);
   for (int q = 0; q < 9; ++q) t[q] = R[q];
@@ -174,7 +170,16 @@ __global__ void k_pose_table(const double* __restrict__ poses, int n, int B,
   t[36] = p[3];
   t[37] = p[4];
   t[38] = p[5];
-  t[39] = inv_dt[i % B];
+  t[39] = inv_dt;
+  return bad;
+}
+
+__global__ void k_pose_table(const double* __restrict__ poses, int n, int B,
+                             const double* __restrict__ inv_dt, double* __restrict__ tab,
+                             int* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (window, bin)
+  if (i >= n) return;
+  if (pose_entry(poses + 6 * (size_t)i, inv_dt[i % B], tab + (size_t)i * kPoseTab)) atomicExch(bad, 1);
 }
 
 void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B,
@@ -182,6 +187,31 @@ void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B
   const int n = n_windows * B;
   ++g_launches;
   k_pose_table<<<(n + 63) / 64, 64, 0, s>>>(poses, n, B, inv_dt, tab, bad);
+}
+
+// The chain's prologue in one launch (instead of two host->device copies, two
+// memsets and the pose-table kernel): the window offsets (kernel parameters)
+// into device memory, the per-window validation words to "no error", and --
+// for device poses -- the pose table with FlowSequence::zeros bin durations
+// (types.hpp:303-304, the host expression) and the validation flag in word nw.
+__global__ void __launch_bounds__(256) k_chain_init(ChainInit a, WinParams P) {
+  const int tid = threadIdx.x, nw = a.nw, B = a.B;
+  for (int i = tid; i <= nw; i += blockDim.x) a.ev_off[i] = a.off[i];
+  for (int i = tid; i < nw; i += blockDim.x) a.err[i] = ~0ull;
+  int bad = 0;
+  if (a.poses)
+    for (int i = tid; i < nw * B; i += blockDim.x) {
+      const int b = i % B;
+      const double dur = dm(ds((double)(P.t0 + P.erel[b + 1]), (double)(P.t0 + P.erel[b])), 1e-6);
+      bad |= pose_entry(a.poses + 6 * (size_t)i, dd(1.0, dur), a.tab + (size_t)i * kPoseTab) ? 1 : 0;
+    }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) a.err[nw] = bad ? 1ull : 0ull;
+}
+
+void launch_chain_init(cudaStream_t s, const ChainInit& a, const WinParams& P) {
+  ++g_launches;
+  k_chain_init<<<1, 256, 0, s>>>(a, P);
 }
 
 // --------------------------------------------------------------------------

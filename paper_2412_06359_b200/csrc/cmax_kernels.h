@@ -32,6 +32,17 @@ void launch_stage(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, 
                   uint64_t max_n, uint2* packed, unsigned long long* err);
 void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B,
                        const double* inv_dt, double* tab, int* bad);
+// Chain prologue (k_chain_init): offsets, validation words, device pose table.
+constexpr int kInitMaxWin = 256;  // windows whose offsets fit the kernel parameters
+struct ChainInit {
+  uint64_t off[kInitMaxWin + 1];
+  int nw, B;
+  const double* poses;       // device poses [nw][B][6], or null (host-built table)
+  double* tab;               // pose table out [nw][B][kPoseTab]
+  uint64_t* ev_off;          // device offsets out [nw + 1]
+  unsigned long long* err;   // [nw]: ~0 (no error); [nw]: pose validation flag
+};
+void launch_chain_init(cudaStream_t s, const ChainInit& a, const WinParams& P);
 void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out);
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,

@@ -323,21 +323,25 @@ const char* code_name(int c) {
 // Stage + validate events of n_windows windows (offsets on host). Asynchronous:
 // the per-window first-violation keys land in pinned host memory and are
 // checked by check_stage_errors() after the call's final stream sync.
+// prepared: k_chain_init already wrote the device offsets ("ev_off") and reset
+// the validation words ("stage_err", nw + 1 words); the caller copies them back.
 void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off_h, const WinParams& P,
-                  int mem) {
+                  int mem, bool prepared = false) {
   const int nw = P.n_windows;
   const uint64_t total = off_h[nw];
   uint64_t max_n = 0;
   for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, off_h[w + 1] - off_h[w]);
   const evcm_event* dev = to_device(e, "events_aos", ev, total, mem);
-  uint64_t* off_pin = e->pinned<uint64_t>("ev_off_h", nw + 1);
-  std::memcpy(off_pin, off_h, (nw + 1) * sizeof(uint64_t));
   uint64_t* off_d = e->get<uint64_t>("ev_off", nw + 1);
-  ck(cudaMemcpyAsync(off_d, off_pin, (nw + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream),
-     "H2D offsets");
+  unsigned long long* err = e->get<unsigned long long>("stage_err", nw + 1);
+  if (!prepared) {
+    uint64_t* off_pin = e->pinned<uint64_t>("ev_off_h", nw + 1);
+    std::memcpy(off_pin, off_h, (nw + 1) * sizeof(uint64_t));
+    ck(cudaMemcpyAsync(off_d, off_pin, (nw + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream),
+       "H2D offsets");
+    ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
+  }
   uint2* packed = e->get<uint2>("packed", total);
-  unsigned long long* err = e->get<unsigned long long>("stage_err", nw);
-  ck(cudaMemsetAsync(err, 0xff, nw * sizeof(unsigned long long), e->stream), "memset");
   e->n_total = (total + 1) & ~1ull;  // even plane stride (16 B-aligned 8 B sub-arrays)
   e->max_n = max_n;
   // algo auto: the owner pipeline (deterministic, fixed-point) ties the atomic one
@@ -359,8 +363,10 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   } else {
     launch_stage(e->stream, dev, off_d, P, max_n, packed, err);
   }
-  unsigned long long* err_h = e->pinned<unsigned long long>(e->slot_name("stage_err_h"), nw);
-  ck(cudaMemcpyAsync(err_h, err, nw * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream),
+  // one read-back: the window words and, after them, the chain's pose flag
+  const int nwords = nw + 1;
+  unsigned long long* err_h = e->pinned<unsigned long long>(e->slot_name("stage_err_h"), nw + 1);
+  ck(cudaMemcpyAsync(err_h, err, nwords * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream),
      "D2H err");
   e->stage_nw = nw;
 }
@@ -390,7 +396,7 @@ void sync_and_check(evcm_cuda_engine* e, const char* what) {
   // (optimize.hpp:211-213), so a bad pose wins over a bad event.
   if (e->check_pose_flag) {
     e->check_pose_flag = false;
-    if (*e->pinned<int>(e->slot_name("pose_bad_h"), 1))
+    if (e->pinned<unsigned long long>(e->slot_name("stage_err_h"), e->stage_nw + 1)[e->stage_nw])
       fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi and components finite");
   }
   check_stage_errors(e);
@@ -894,18 +900,39 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
     // expression order (bit-identical flows); device poses -> k_pose_table (no
     // host round trip; validation reported through a device flag).
     const double* tab;
-    if (in_mem == EVCM_MEM_DEVICE) {
+    const bool prepared = nw <= kInitMaxWin;
+    if (prepared) {
+      // offsets, validation words and (device poses) the pose table in one launch
+      ChainInit a;
+      for (int w = 0; w <= nw; ++w) a.off[w] = bt->ev_offsets[w];
+      a.nw = nw;
+      a.B = B;
+      a.ev_off = e->get<uint64_t>("ev_off", nw + 1);
+      a.err = e->get<unsigned long long>("stage_err", nw + 1);
+      a.poses = in_mem == EVCM_MEM_DEVICE ? bt->poses : nullptr;
+      a.tab = e->get<double>("pose_tab", (size_t)nw * B * kPoseTab);
+      if (in_mem != EVCM_MEM_DEVICE) {  // host poses: host-built table (bit-identical R)
+        const size_t np = (size_t)nw * B * 6;
+        double* ph = e->pinned<double>("poses_h", np);
+        std::memcpy(ph, bt->poses, np * sizeof(double));
+        tab = upload_pose_table(e, ph, nw, B, edges.data(), true);
+      } else {
+        tab = a.tab;
+        e->check_pose_flag = true;
+      }
+      launch_chain_init(e->stream, a, P);
+    } else if (in_mem == EVCM_MEM_DEVICE) {
       double* inv = e->pinned<double>("inv_dt_h", B);
       for (int b = 0; b < B; ++b)
         inv[b] = 1.0 / ((static_cast<double>(edges[b + 1]) - static_cast<double>(edges[b])) * 1e-6);
       double* inv_d = e->get<double>("inv_dt", B);
       ck(cudaMemcpyAsync(inv_d, inv, B * sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D");
-      int* bad = e->get<int>("pose_bad", 1);
-      ck(cudaMemsetAsync(bad, 0, sizeof(int), e->stream), "memset");
+      // the pose flag lives in validation word nw (copied back by stage_events)
+      unsigned long long* errw = e->get<unsigned long long>("stage_err", nw + 1);
+      ck(cudaMemsetAsync(errw + nw, 0, sizeof(unsigned long long), e->stream), "memset");
       double* tab_d = e->get<double>("pose_tab", (size_t)nw * B * kPoseTab);
-      launch_pose_table(e->stream, bt->poses, nw, B, inv_d, tab_d, bad);
-      ck(cudaMemcpyAsync(e->pinned<int>(e->slot_name("pose_bad_h"), 1), bad, sizeof(int), cudaMemcpyDeviceToHost,
-                         e->stream), "D2H");
+      launch_pose_table(e->stream, bt->poses, nw, B, inv_d, tab_d,
+                        reinterpret_cast<int*>(errw + nw));
       e->check_pose_flag = true;
       tab = tab_d;
     } else {
@@ -916,7 +943,7 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
     }
     uint64_t max_n = 0;
     for (int w = 0; w < nw; ++w) max_n = std::max<uint64_t>(max_n, bt->ev_offsets[w + 1] - bt->ev_offsets[w]);
-    stage_events(e, bt->events, bt->ev_offsets, P, in_mem);
+    stage_events(e, bt->events, bt->ev_offsets, P, in_mem, prepared);
     const double* depth =
         depth_dev ? depth_dev : to_device(e, "depth", bt->depth, (size_t)nw * P.HW, in_mem);
     double2* flows = e->get<double2>("flows", (size_t)nw * B * P.HW);
@@ -1130,7 +1157,7 @@ int evcm_cuda_chain_wait(evcm_cuda_engine* e, int slot) {
       ~Restore() { e->slot = 0; }
     } restore{e};
     e->slot = slot;
-    if (q.pose && *e->pinned<int>(e->slot_name("pose_bad_h"), 1))
+    if (q.pose && e->pinned<unsigned long long>(e->slot_name("stage_err_h"), q.nw + 1)[q.nw])
       fail(EVCM_ERR_CONFIG, "pose step: rotation angle must stay below pi and components finite");
     e->stage_nw = q.nw;
     check_stage_errors(e);
