@@ -1002,11 +1002,29 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
       }
     }
     if (pose_part) {
+      // six warp sums by transposition: each halving step trades half of the
+      // remaining components with the partner lane (9 double shuffles, not 30);
+      // lane 4c ends up holding component c (fixed order: deterministic)
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+      double a4[4];
 #pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double v = warp_sum(c6[a]);
-        if (lane == 0) s_pose[i & 1][cw][a] = v;
+      for (int k = 0; k < 4; ++k) {
+        const double mine = h16 ? (k < 2 ? c6[4 + k] : 0.0) : c6[k];
+        const double other = h16 ? c6[k] : (k < 2 ? c6[4 + k] : 0.0);
+        a4[k] = mine + __shfl_xor_sync(kFull, other, 16);
       }
+      double a2[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double mine = h8 ? a4[2 + k] : a4[k];
+        const double other = h8 ? a4[k] : a4[2 + k];
+        a2[k] = mine + __shfl_xor_sync(kFull, other, 8);
+      }
+      double v = (h4 ? a2[1] : a2[0]) + __shfl_xor_sync(kFull, h4 ? a2[0] : a2[1], 4);
+      v += __shfl_xor_sync(kFull, v, 2);
+      v += __shfl_xor_sync(kFull, v, 1);
+      const int comp = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+      if ((lane & 3) == 0 && comp < 6) s_pose[i & 1][cw][comp] = v;
     }
     consumer_sync(kCons);  // also: the zeroed tile is ready for bin i + 2
     if (pose_part && ct < 6) {
