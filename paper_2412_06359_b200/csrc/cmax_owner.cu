@@ -131,26 +131,37 @@ __global__ void __launch_bounds__(kSortThreads) k_key_hist(
 }
 
 // Per tile: exclusive prefix over chunks (in place, counts -> offsets inside the
-// tile) and the tile total. One thread per (window, tile); reads are coalesced
-// across tiles.
-__global__ void k_sort_colscan(uint32_t* __restrict__ counts, TileParams TP,
-                               uint32_t* __restrict__ totals) {
-  const int w = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= TP.nT) return;
+// tile) and the tile total. A CTA covers 32 tiles x kColSeg chunk segments: each
+// thread sums its segment (independent, coalesced loads across the 32 tiles),
+// the segment sums are scanned in shared memory, then each thread writes its
+// segment's running offsets -- two load round trips instead of nchunks / 8.
+constexpr int kColSeg = 8;
+__global__ void __launch_bounds__(32 * kColSeg) k_sort_colscan(uint32_t* __restrict__ counts,
+                                                               TileParams TP,
+                                                               uint32_t* __restrict__ totals) {
+  __shared__ uint32_t seg_sum[kColSeg][32];
+  const int w = blockIdx.y, lane = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int per = (TP.nchunks + kColSeg - 1) / kColSeg;
+  const int c0 = sg * per, c1 = min(TP.nchunks, c0 + per);
   uint32_t* c = counts + (size_t)w * TP.nchunks * TP.nT + t;
-  uint32_t run = 0;
-  constexpr int U = 8;  // independent loads in flight per thread
-  for (int ch0 = 0; ch0 < TP.nchunks; ch0 += U) {
-    uint32_t v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ch0 + u < TP.nchunks ? c[(size_t)(ch0 + u) * TP.nT] : 0u;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (ch0 + u < TP.nchunks) c[(size_t)(ch0 + u) * TP.nT] = run;
-      run += v[u];
-    }
+  uint32_t sum = 0;
+  if (t < TP.nT) {
+#pragma unroll 8
+    for (int ch = c0; ch < c1; ++ch) sum += c[(size_t)ch * TP.nT];
   }
-  totals[(size_t)w * TP.nT + t] = run;
+  seg_sum[sg][lane] = sum;
+  __syncthreads();
+  uint32_t run = 0;
+  for (int q = 0; q < sg; ++q) run += seg_sum[q][lane];
+  if (t < TP.nT) {
+    for (int ch = c0; ch < c1; ++ch) {
+      const uint32_t v = c[(size_t)ch * TP.nT];
+      c[(size_t)ch * TP.nT] = run;
+      run += v;
+    }
+    if (sg == kColSeg - 1) totals[(size_t)w * TP.nT + t] = run;
+  }
 }
 
 // Exclusive scan of the tile totals: tile_ptr[w][t] = first sorted slot of tile
@@ -260,26 +271,32 @@ __global__ void __launch_bounds__(kScatterThreads) k_sort_scatter(
 }
 
 // bin_ptr[w][S][b] = first sorted slot of tile S whose event bin is >= b
-// (the stable sort keeps events time-ordered inside a tile).
+// (the stable sort keeps events time-ordered inside a tile, so bins are
+// non-decreasing along the tile's run): one warp per tile, lane b runs the
+// binary search for the first slot with dt >= erel[b] -- the B-1 searches of a
+// tile proceed in parallel instead of one after another.
 __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off,
                           WinParams P, TileParams TP, const uint32_t* __restrict__ tile_ptr,
                           uint32_t* __restrict__ bin_ptr) {
-  const int w = blockIdx.y;
-  const int S = blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = blockIdx.y, lane = threadIdx.x & 31;
+  const int S = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (S >= TP.nT) return;
+  const int B = P.B;
   const uint64_t base = ev_off[w];
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t lo = tp[S], hi = tp[S + 1];
-  uint32_t* out = bin_ptr + ((size_t)w * TP.nT + S) * (P.B + 1);
-  out[0] = lo;
-  out[P.B] = hi;
-  for (int b = 1; b < P.B; ++b) {
-    uint32_t a = lo, z = hi;  // first slot with dt >= erel[b]
+  uint32_t* out = bin_ptr + ((size_t)w * TP.nT + S) * (B + 1);
+  if (lane == 0) {
+    out[0] = lo;
+    out[B] = hi;
+  } else if (lane < B) {
+    const uint32_t th = P.erel[lane];
+    uint32_t a = lo, z = hi;  // first slot with dt >= erel[lane]
     while (a < z) {
       const uint32_t m = (a + z) >> 1;
-      if ((sorted[base + m].x & 0x7fffffffu) >= P.erel[b]) z = m; else a = m + 1;
+      if ((__ldg(&sorted[base + m].x) & 0x7fffffffu) >= th) z = m; else a = m + 1;
     }
-    out[b] = a;
+    out[lane] = a;
   }
 }
 
@@ -571,14 +588,14 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, coarse,
                                                                   keys, counts);
   count_launch();
-  k_sort_colscan<<<dim3((TP.nT + 255) / 256, P.n_windows), 256, 0, s>>>(counts, TP, totals);
+  k_sort_colscan<<<dim3((TP.nT + 31) / 32, P.n_windows), 32 * kColSeg, 0, s>>>(counts, TP, totals);
   count_launch();
   k_sort_tilescan<<<P.n_windows, 1024, 0, s>>>(totals, TP, tile_ptr);
   count_launch();
   k_sort_scatter<<<grid, kScatterThreads, sc_smem, s>>>(packed, keys, ev_off, TP, counts, tile_ptr,
                                                         sorted, perm, keys + n_total);
   count_launch();
-  k_bin_ptr<<<dim3((TP.nT + 127) / 128, P.n_windows), 128, 0, s>>>(sorted, ev_off, P, TP,
+  k_bin_ptr<<<dim3((TP.nT + 7) / 8, P.n_windows), 256, 0, s>>>(sorted, ev_off, P, TP,
                                                                     tile_ptr, bin_ptr);
 }
 
