@@ -211,6 +211,7 @@ struct evcm_cuda_engine {
       b.p = nullptr;
       ck(cudaMallocHost(&b.p, bytes), "cudaMallocHost");
       b.cap = bytes;
+      ++alloc_gen;  // captured graphs may copy from / into the old buffer
     }
     return static_cast<T*>(b.p);
   }
@@ -1000,7 +1001,10 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
                 evcm_chain_out* out, const double* depth_dev, bool async = false) {
   if (!e || !bt || !out || !bt->ev_offsets) fail(EVCM_ERR_CONFIG, "null argument");
   set_device(e);
-  const bool graphable = in_mem == EVCM_MEM_DEVICE && out_mem == EVCM_MEM_DEVICE && !e->timing;
+  // graphs only where every host-side input of the enqueue is baked into kernel
+  // parameters: device inputs and outputs, and offsets that fit k_chain_init
+  const bool graphable = in_mem == EVCM_MEM_DEVICE && out_mem == EVCM_MEM_DEVICE && !e->timing &&
+                         bt->n_windows <= kInitMaxWin;
   std::vector<uint64_t> sig;
   if (graphable) sig = chain_signature(e, bt, out, depth_dev);
   using GE = evcm_cuda_engine::GraphEntry;
