@@ -85,3 +85,36 @@ def test_chain_graph_replay():
     for w in range(nw):
         assert abs(float(out[0][w]) - ref2[w][0]) <= 1e-5 * abs(ref2[w][0])
         assert rel_inf(out[1][w].cpu().numpy(), ref2[w][1]) <= 1e-5
+
+
+def test_graph_cache_survives_reallocation():
+    """Two alternating signatures keep their graphs; a larger call in between
+    reallocates the workspace, which must invalidate (not replay) the old graphs.
+    The owner pipeline is bit-deterministic, so every call must match bit for bit."""
+    import torch
+    eng = P.Engine(P.EngineOptions(deterministic=True))
+    dev = torch.device("cuda:0")
+
+    def batch(W, H, nw, n, seed):
+        depth, poses, K, ev, offs = chain_inputs(W, H, 6, nw, n, seed=seed)
+        return (torch.from_numpy(depth).to(dev), torch.from_numpy(poses).to(dev),
+                torch.from_numpy(ev.view(np.uint8)).to(dev), K, offs)
+
+    a, b, big = batch(64, 48, 2, 3000, 1), batch(64, 48, 2, 3000, 2), batch(160, 120, 4, 60000, 3)
+
+    def run(x):
+        d, p, e, K, offs = x
+        r = eng.chain_batch(d, p, K, 0, 100000, e, offs)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy().copy() for t in r]
+
+    first_a, first_b = run(a), run(b)
+    for _ in range(3):  # eager, capture, replay for both signatures
+        for x, ref in ((a, first_a), (b, first_b)):
+            got = run(x)
+            assert all(np.array_equal(g, r) for g, r in zip(got, ref))
+    run(big)  # grows the workspace
+    for _ in range(3):
+        for x, ref in ((a, first_a), (b, first_b)):
+            got = run(x)
+            assert all(np.array_equal(g, r) for g, r in zip(got, ref))
