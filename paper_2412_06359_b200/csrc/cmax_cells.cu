@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         const double S1 = (double)fx_read(acc + 6 * kPlane + o, acc + 7 * kPlane + o) * ifs;
         const int g = py * W + px;
         actv = (flag[o] || C0 > 0.0 || C1 > 0.0) ? 1u : 0u;  // refresh_active: some w > 0
-        const double i0 = 1.0 / (C0 + kLossEps), i1 = 1.0 / (C1 + kLossEps);
+        // correctly rounded reciprocals (== 1.0 / x, without the general divide)
+        const double i0 = __drcp_rn(C0 + kLossEps), i1 = __drcp_rn(C1 + kLossEps);
         const double c0 = S0 * i0, c1 = S1 * i1;
         lsum = c0 * c0 + c1 * c1;
         double2* cwp = coef + ((size_t)w * R + r) * 2 * HW;
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
       for (int k = 0; k < 9; ++k) acc[k * kPlane + o] = 0u;  // this pixel's words, next reference
     }
     lsum = warp_sum(lsum);
-    actv = warp_sum_u32(actv);
+    actv = __reduce_add_sync(kFull, actv);
     if (lane == 0) {
       s_red[r & 1][cw] = lsum;
       s_act[r & 1][cw] = actv;
