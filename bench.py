@@ -39,7 +39,14 @@ WORKLOADS = {
     "C": dict(W=640, H=480, B=10, n_events=1_000_000, batch=16, window_us=100_000,
               name="DSEC-shape 640x480 windows, 1M events/window, batch 16 per GPU, "
                    "10 bins (11 refs), 0.1 s windows"),
+    # SURVEY.md §8(d) scaling config: a fixed batch of 64 DSEC-shape windows split
+    # over the GPUs (strong scaling)
+    "S": dict(W=640, H=480, B=10, n_events=1_000_000, batch_total=64, window_us=100_000,
+              name="DSEC-shape 640x480 windows, 1M events/window, batch 64 split over the "
+                   "GPUs, 10 bins (11 refs), 0.1 s windows"),
 }
+# SURVEY.md §8(d) sweep: one 346x260 window, N events
+SWEEP_N = (10_000, 30_000, 100_000, 300_000, 1_000_000, 3_000_000, 10_000_000)
 
 HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
@@ -82,7 +89,7 @@ def make_inputs(wl, rank, n_windows):
     depth = np.empty((H, W))
     depth[:, : W // 2] = 1.0
     depth[:, W // 2:] = 3.0
-    depth = np.ascontiguousarray(np.broadcast_to(depth, (n_windows, H, W)))
+    depth = np.broadcast_to(depth, (n_windows, H, W)).copy()
     poses = np.tile(np.array([0.001, -0.002, 0.003, 0.02, 0.01, 0.005]), (n_windows, B, 1))
     poses = poses.astype(np.float32).astype(np.float64)
     K = np.array([0.9 * W, 0.9 * W, (W - 1) / 2, (H - 1) / 2]).astype(np.float32).astype(np.float64)
@@ -229,17 +236,18 @@ def reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    depth, poses, K, ev, offs = make_inputs(wl, 0, wl["batch"])
+    nb = wl.get("batch", 4)  # windows sampled (one per step)
+    depth, poses, K, ev, offs = make_inputs(wl, 0, nb)
     from oracle import oracle as O
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libevcm_ref.so not built"}))
         return
     cores = int(O.ref().ref_hardware_concurrency())
     for i in range(args.warmup):
-        run_reference_chain(wl, depth, poses, K, ev, offs, [i % wl["batch"]])
+        run_reference_chain(wl, depth, poses, K, ev, offs, [i % nb])
     times, n_ev = [], 0
     for i in range(args.steps):
-        s, n = run_reference_chain(wl, depth, poses, K, ev, offs, [i % wl["batch"]])
+        s, n = run_reference_chain(wl, depth, poses, K, ev, offs, [i % nb])
         times.append(s)
         n_ev += n
     total = sum(times)
@@ -247,7 +255,8 @@ def reference_arm(args, wl):
     line = {
         "impl": "reference", "metric": "CMax loss fwd+bwd throughput", "value": value,
         "unit": "Mevents/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if "batch_total" in wl else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["name"], "step": "one window per step (bounded sample)",
                    "events_per_window": wl["n_events"]},
@@ -287,7 +296,12 @@ def cuda_arm(args, wl):
 
     import paper_2412_06359_b200 as P
 
-    nwin = wl["batch"]
+    if "batch_total" in wl:  # strong scaling: the fixed batch is split over the ranks
+        if wl["batch_total"] % world:
+            raise SystemExit(f"--workload S needs a GPU count dividing {wl['batch_total']}")
+        nwin = wl["batch_total"] // world
+    else:
+        nwin = wl["batch"]
     depth, poses, K, ev, offs = make_inputs(wl, rank, nwin)
     stream = torch.cuda.Stream(dev)
     eng = P.Engine(P.EngineOptions(device=local, stream=stream.cuda_stream,
@@ -445,7 +459,8 @@ def cuda_arm(args, wl):
         line = {
             "metric": "CMax loss fwd+bwd throughput", "value": value, "unit": "Mevents/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if "batch_total" in wl else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl["name"], "windows_per_gpu_per_step": nwin,
                        "events_per_window": wl["n_events"], "sensor": [wl["W"], wl["H"]],
@@ -470,6 +485,41 @@ def cuda_arm(args, wl):
         dist.destroy_process_group()
 
 
+def sweep(args):
+    """SURVEY.md §8(d) sweep: one 346x260 window with N events, device-resident
+    chain (graph replay), L2 flushed between steps; one JSON line per N."""
+    import torch
+    import paper_2412_06359_b200 as P
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    eng = P.Engine(P.EngineOptions(stream=stream.cuda_stream, algo=args.algo))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for n in SWEEP_N:
+        wl = dict(WORKLOADS["B"], n_events=n)
+        depth, poses, K, ev, offs = make_inputs(wl, 0, 1)
+        with torch.cuda.stream(stream):
+            d_depth = torch.from_numpy(depth).to(dev)
+            d_poses = torch.from_numpy(poses).to(dev)
+            d_ev = torch.from_numpy(ev.view(np.uint8)).to(dev)
+            out = (torch.empty(1, dtype=torch.float64, device=dev),
+                   torch.empty((1, wl["H"], wl["W"]), dtype=torch.float64, device=dev),
+                   torch.empty((1, wl["B"], 6), dtype=torch.float64, device=dev))
+            for _ in range(max(3, args.warmup)):
+                eng.chain_batch(d_depth, d_poses, K, 0, wl["window_us"], d_ev, offs, out=out)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                flush.zero_()
+                a.record(stream)
+                eng.chain_batch(d_depth, d_poses, K, 0, wl["window_us"], d_ev, offs, out=out)
+                b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+        print(json.dumps({"sweep": "346x260, 1 window, 10 bins", "n_events": n,
+                          "ms_per_window": ms, "Mevents_per_s": n / (ms * 1e-3) / 1e6,
+                          "algo": eng.last_algo(), "steps": args.steps}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -484,7 +534,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
+    ap.add_argument("--sweep", action="store_true",
+                    help="SURVEY §8(d) sweep (346x260, 1 window, 1e4..1e7 events); not the contract line")
     args = ap.parse_args()
+    if args.sweep:
+        sweep(args)
+        return
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, wl)
