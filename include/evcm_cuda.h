@@ -213,6 +213,11 @@ typedef struct {
   int32_t* no_survivors;
   double* d_depth;
   double* d_poses;
+  /* optional (may be NULL): the batch's data-parallel payload [sum_w loss,
+   * sum_w d_depth (H*W), sum_w d_poses (B*6)], summed over the windows in window
+   * order (deterministic) inside the chain -- the buffer a multi-GPU caller
+   * all-reduces */
+  double* sums;
 } evcm_chain_out;
 
 EVCM_API int evcm_cuda_chain_batch(evcm_cuda_engine* e, const evcm_chain_batch* batch, int mem,

@@ -189,6 +189,38 @@ void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B
   k_pose_table<<<(n + 63) / 64, 64, 0, s>>>(poses, n, B, inv_dt, tab, bad);
 }
 
+// Packed window sums [sum_w loss, sum_w d_depth, sum_w d_poses], each entry
+// summed over the windows in window order (deterministic).
+__global__ void k_window_sums(const double* __restrict__ loss, const double* __restrict__ d_depth,
+                              const double* __restrict__ d_poses, int nw, int HW, int B6,
+                              double* __restrict__ out) {
+  const int n = 1 + HW + B6;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double* src;
+    size_t stride;
+    if (i == 0) {
+      src = loss;
+      stride = 1;
+    } else if (i <= HW) {
+      src = d_depth + (i - 1);
+      stride = HW;
+    } else {
+      src = d_poses + (i - 1 - HW);
+      stride = B6;
+    }
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += src[(size_t)w * stride];
+    out[i] = s;
+  }
+}
+
+void launch_window_sums(cudaStream_t s, const double* loss, const double* d_depth,
+                        const double* d_poses, int nw, int HW, int B6, double* out) {
+  ++g_launches;
+  const int n = 1 + HW + B6;
+  k_window_sums<<<(n + 255) / 256, 256, 0, s>>>(loss, d_depth, d_poses, nw, HW, B6, out);
+}
+
 // The chain's prologue in one launch (instead of two host->device copies, two
 // memsets and the pose-table kernel): the window offsets (kernel parameters)
 // into device memory, the per-window validation words to "no error", and --

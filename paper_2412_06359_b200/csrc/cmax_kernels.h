@@ -43,6 +43,8 @@ struct ChainInit {
   unsigned long long* err;   // [nw]: ~0 (no error); [nw]: pose validation flag
 };
 void launch_chain_init(cudaStream_t s, const ChainInit& a, const WinParams& P);
+void launch_window_sums(cudaStream_t s, const double* loss, const double* d_depth,
+                        const double* d_poses, int nw, int HW, int B6, double* out);
 void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out);
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,

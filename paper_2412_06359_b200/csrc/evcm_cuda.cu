@@ -965,6 +965,12 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
         launch_flows_bwd<float2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<float2*>(g), ddo, pp, dpo);
       e->mark(M_FWD0 + 6);
     }
+    if (out->sums) {  // the data-parallel payload, summed in window order
+      const size_t ns = 1 + (size_t)P.HW + (size_t)B * 6;
+      double* sd = direct ? out->sums : e->get<double>("sums", ns);
+      launch_window_sums(e->stream, e->get<double>("loss", nw), ddo, dpo, nw, P.HW, B * 6, sd);
+      if (!direct) from_device(e, out->sums, sd, ns * sizeof(double), out_mem);
+    }
     if (out->loss) from_device(e, out->loss, e->get<double>("loss", nw), nw * sizeof(double), out_mem);
     if (out->no_survivors) from_device(e, out->no_survivors, e->get<int>("no_surv", nw), nw * sizeof(int), out_mem);
     if (out->d_depth && ddo != out->d_depth) from_device(e, out->d_depth, ddo, (size_t)nw * P.HW * sizeof(double), out_mem);
@@ -990,7 +996,7 @@ std::vector<uint64_t> chain_signature(const evcm_cuda_engine* e, const evcm_chai
   u((uint64_t)(uintptr_t)bt->events); u((uint64_t)(uintptr_t)(depth_dev ? depth_dev : bt->depth));
   u((uint64_t)(uintptr_t)bt->poses); u((uint64_t)(uintptr_t)out->loss);
   u((uint64_t)(uintptr_t)out->no_survivors); u((uint64_t)(uintptr_t)out->d_depth);
-  u((uint64_t)(uintptr_t)out->d_poses);
+  u((uint64_t)(uintptr_t)out->d_poses); u((uint64_t)(uintptr_t)out->sums);
   u((uint64_t)e->opt.algo); u((uint64_t)e->opt.deterministic); u((uint64_t)e->opt.stack_f64);
   u((uint64_t)e->opt.grad_f64);
   for (int w = 0; w <= bt->n_windows; ++w) u(bt->ev_offsets[w]);

@@ -119,7 +119,7 @@ class _ChainBatch(C.Structure):
 
 class _ChainOut(C.Structure):
     _fields_ = [("loss", C.c_void_p), ("no_survivors", C.c_void_p), ("d_depth", C.c_void_p),
-                ("d_poses", C.c_void_p)]
+                ("d_poses", C.c_void_p), ("sums", C.c_void_p)]
 
 
 _lib = None
@@ -577,7 +577,7 @@ class Engine:
 
     # -- batched chain (optimize.hpp:205-241 composition over many windows)
     def chain_batch(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out=None,
-                    out_device=None, window_stride_us: int = 0):
+                    out_device=None, window_stride_us: int = 0, sums=None):
         """Per window w: depth_pose_to_flows(depth[w], poses[w]) -> forward ->
         backward -> depth_pose_to_flows_backward (the predictor_loss_and_gradients
         composition, optimize.hpp:205-241, without decode / L_geo).
@@ -588,20 +588,22 @@ class Engine:
         (torch cuda); outputs live on the device when ``out_device`` (default:
         same side as the inputs). Window w spans [t_start_us, t_end_us) +
         w * window_stride_us (0: one clock for all windows; the window length:
-        consecutive windows of one stream, see io.slice_windows)."""
+        consecutive windows of one stream, see io.slice_windows). ``sums`` (optional,
+        same side as the outputs, 1 + H*W + B*6 float64): receives [sum_w loss,
+        sum_w d_depth, sum_w d_poses] computed inside the chain (dist.py's payload)."""
         out, args = self._chain_args(depth, poses, k, t_start_us, t_end_us, events, ev_offsets,
-                                     out, out_device, window_stride_us)
+                                     out, out_device, window_stride_us, sums)
         _raise(load_library().evcm_cuda_chain_batch2(self._h, *args))
         return out
 
     def chain_batch_async(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out,
-                          slot: int, window_stride_us: int = 0):
+                          slot: int, window_stride_us: int = 0, sums=None):
         """chain_batch that does not wait when it replays a captured graph (device
         inputs/outputs): the batch is queued on the engine's stream and its
         validation result is raised by ``chain_wait(slot)``. ``out`` (device
         tensors) must be given; slots 0..3 may be in flight together."""
         out, args = self._chain_args(depth, poses, k, t_start_us, t_end_us, events, ev_offsets,
-                                     out, True, window_stride_us)
+                                     out, True, window_stride_us, sums)
         _raise(load_library().evcm_cuda_chain_batch_async(self._h, *args, int(slot)))
         return out
 
@@ -610,7 +612,7 @@ class Engine:
         _raise(load_library().evcm_cuda_chain_wait(self._h, int(slot)))
 
     def _chain_args(self, depth, poses, k, t_start_us, t_end_us, events, ev_offsets, out,
-                    out_device, window_stride_us):
+                    out_device, window_stride_us, sums=None):
         nw, H, W = depth.shape
         B = poses.shape[1]
         in_mem = _mem_of(depth, poses, events)
@@ -638,9 +640,12 @@ class Engine:
         bt = _ChainBatch(nw, W, H, B, int(t_start_us), int(t_end_us), (C.c_double * 4)(*K),
                          _ptr(events), offs.ctypes.data_as(C.c_void_p), _ptr(depth), _ptr(poses),
                          int(window_stride_us))
-        co = _ChainOut(_ptr(out[0]), None, _ptr(out[1]), _ptr(out[2]))
+        if sums is not None and (sums.shape[0] != 1 + H * W + B * 6 or
+                                 _mem_of(sums) != out_mem):
+            raise ConfigError("chain: sums must hold 1 + H*W + B*6 values on the output side")
+        co = _ChainOut(_ptr(out[0]), None, _ptr(out[1]), _ptr(out[2]), _ptr(sums))
         # keep the (possibly converted) inputs alive until the call has enqueued them
-        self._keep = (bt, co, offs, depth, poses, events, K)
+        self._keep = (bt, co, offs, depth, poses, events, K, sums)
         return out, (C.byref(bt), in_mem, out_mem, C.byref(co))
 
 

@@ -61,14 +61,17 @@ class ChainPipeline:
 
     def run(self, batches: Iterable, k, t_start_us: int, t_end_us: int,
             post: Optional[Callable] = None,
-            window_stride_us: int = 0) -> Iterator:
+            window_stride_us: int = 0, window_sums: bool = False) -> Iterator:
         """For each host batch ``(depth [n,H,W] f64, poses [n,B,6] f64, events
         uint8 [N,16], ev_offsets [n+1])`` -- pinned torch CPU tensors -- run the
         chain and yield the host result: ``post(loss, d_depth, d_poses)`` (a
         device tensor, e.g. a data-parallel reduction) copied into a pinned host
         buffer owned by the pipeline (valid until two batches later), or the
-        three outputs copied to the host when ``post`` is None. A batch's
-        validation error is raised when its result is collected."""
+        three outputs copied to the host when ``post`` is None. With
+        ``window_sums`` the chain also writes the packed [sum loss, sum d_depth,
+        sum d_poses] payload (Engine.chain_batch ``sums``) and ``post(sums)``
+        (default: the payload itself) is what comes back. A batch's validation
+        error is raised when its result is collected."""
         import torch
         it = iter(batches)
         cur = next(it, None)
@@ -102,13 +105,22 @@ class ChainPipeline:
                 self.out = (torch.empty(nw, dtype=torch.float64, device=self.dev),
                             torch.empty(tuple(staged[0].shape), dtype=torch.float64, device=self.dev),
                             torch.empty(tuple(staged[1].shape), dtype=torch.float64, device=self.dev))
+            if window_sums:
+                H, W, B = staged[0].shape[1], staged[0].shape[2], staged[1].shape[1]
+                n_s = 1 + H * W + B * 6
+                if getattr(self, "sums", None) is None or self.sums.shape[0] != n_s:
+                    self.sums = torch.empty(n_s, dtype=torch.float64, device=self.dev)
             with torch.cuda.stream(self.compute):
                 self.engine.chain_batch_async(staged[0], staged[1], k, t_start_us, t_end_us,
                                               staged[2], np.asarray(cur[3], np.uint64), self.out,
-                                              slot, window_stride_us=window_stride_us)
+                                              slot, window_stride_us=window_stride_us,
+                                              sums=self.sums if window_sums else None)
                 self.consumed[slot].record(self.compute)
-                if post is not None:
-                    r = post(*self.out)
+                if window_sums or post is not None:
+                    if window_sums:
+                        r = post(self.sums) if post is not None else self.sums
+                    else:
+                        r = post(*self.out)
                     h = self.host[slot]
                     if h is None or h.shape != r.shape or h.dtype != r.dtype:
                         h = torch.empty(r.shape, dtype=r.dtype).pin_memory()

@@ -118,3 +118,25 @@ def test_graph_cache_survives_reallocation():
         for x, ref in ((a, first_a), (b, first_b)):
             got = run(x)
             assert all(np.array_equal(g, r) for g, r in zip(got, ref))
+
+
+def test_chain_window_sums_match_torch():
+    """The chain's packed window sums equal dist.pack_window_sums of its outputs
+    (window-order sums vs torch's reduction: rounding only), host and device."""
+    import torch
+    from paper_2412_06359_b200.dist import pack_window_sums
+    eng = P.Engine(P.EngineOptions(deterministic=True))
+    depth, poses, K, ev, offs = chain_inputs(64, 48, 5, 4, 6000, seed=9)
+    n_s = 1 + 64 * 48 + 5 * 6
+    sums_h = np.zeros(n_s)
+    out = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs, sums=sums_h)
+    ref = pack_window_sums(*(torch.from_numpy(np.ascontiguousarray(o)) for o in out)).numpy()
+    assert rel_inf(sums_h, ref) <= 1e-14
+    dev = torch.device("cuda:0")
+    sums_d = torch.empty(n_s, dtype=torch.float64, device=dev)
+    outd = eng.chain_batch(torch.from_numpy(depth).to(dev), torch.from_numpy(poses).to(dev), K, 0,
+                           100000, torch.from_numpy(ev.view(np.uint8)).to(dev), offs, sums=sums_d)
+    refd = pack_window_sums(*outd).cpu().numpy()
+    assert rel_inf(sums_d.cpu().numpy(), refd) <= 1e-14
+    with pytest.raises(P.ConfigError):
+        eng.chain_batch(depth, poses, K, 0, 100000, ev, offs, sums=np.zeros(5))
