@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kSortThreads) k_stage_pack(
 // centre pixel of every 8x8 sort tile, [w][B][nT] (768 KB per 640x480 window:
 // L2-resident, unlike per-event gathers from the full flow planes).
 __global__ void k_coarse_flow(const double2* __restrict__ flows, WinParams P, TileParams TP,
-                              double2* __restrict__ coarse) {
+                              double2* __restrict__ coarse, uint4* __restrict__ bbox, size_t n_bbox,
+                              uint32_t* __restrict__ lcount, size_t n_lcount){
   const size_t total = (size_t)P.n_windows * P.B * TP.nT;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -83,6 +84,14 @@ __global__ void k_coarse_flow(const double2* __restrict__ flows, WinParams P, Ti
     const int cy = min((S / TP.ntx) * kSortTile + kSortTile / 2, P.H - 1);
     coarse[i] = flows[wb * P.HW + (size_t)cy * P.W + cx];
   }
+  // the empty cell boxes and list counts of k_traj_records / k_build_lists
+  // (folded in here instead of two memset nodes)
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bbox;
+       i += (size_t)gridDim.x * blockDim.x)
+    bbox[i] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_lcount;
+       i += (size_t)gridDim.x * blockDim.x)
+    lcount[i] = 0u;
 }
 
 // Sort key: 8x8 tile of the event's approximate position at the middle
@@ -574,7 +583,7 @@ void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
                  const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
-                 uint32_t* bin_ptr) {
+                 uint32_t* bin_ptr, uint4* bbox, size_t n_bbox, uint32_t* lcount, size_t n_lcount) {
   static size_t a1 = 0, a2 = 0;
   const size_t sc_smem = (size_t)(kScatterThreads / 32) * TP.nT * 2;
   set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
@@ -583,7 +592,7 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   uint32_t* totals = keys + 2 * n_total;  // nw * nT scratch after the two key arrays
   double2* coarse = reinterpret_cast<double2*>(totals + (((size_t)P.n_windows * TP.nT + 3) & ~(size_t)3));
   count_launch();
-  k_coarse_flow<<<148 * 4, 256, 0, s>>>(flows, P, TP, coarse);
+  k_coarse_flow<<<148 * 4, 256, 0, s>>>(flows, P, TP, coarse, bbox, n_bbox, lcount, n_lcount);
   count_launch();
   k_key_hist<<<grid, kSortThreads, TP.nT * sizeof(uint32_t), s>>>(packed, ev_off, P, TP, coarse,
                                                                   keys, counts);

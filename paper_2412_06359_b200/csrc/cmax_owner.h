@@ -43,7 +43,8 @@ void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
                  const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
-                 uint32_t* bin_ptr);
+                 uint32_t* bin_ptr, uint4* bbox = nullptr, size_t n_bbox = 0,
+                 uint32_t* lcount = nullptr, size_t n_lcount = 0);
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                          const uint32_t* sorted_keys, uint64_t max_n, const double2* flows,

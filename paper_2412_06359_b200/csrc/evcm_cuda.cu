@@ -484,16 +484,16 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   // keys: unsorted + sorted keys, per-tile totals, then the coarse flow map (double2)
   uint32_t* keys = e->get<uint32_t>("sort_keys", 2 * total + (((size_t)nw * TP.nT + 3) & ~(size_t)3) +
                                                      (size_t)nw * P.B * TP.nT * 4);
-  launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
-              e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
-              nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)));
-  e->mark(3);
-  FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
   uint4* bbox = e->get<uint4>("bbox", (size_t)nw * NS * TP.nT);
-  ck(cudaMemsetAsync(bbox, 0xff, (size_t)nw * NS * TP.nT * sizeof(uint4), e->stream), "memset");
   const size_t nl = (size_t)nw * NS * TP.oT;
   uint32_t* lcount = e->get<uint32_t>("lcount", nl);
-  ck(cudaMemsetAsync(lcount, 0, nl * sizeof(uint32_t), e->stream), "memset");
+  // the sort's first kernel also resets the cell boxes and list counts
+  launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
+              e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
+              nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)), bbox,
+              (size_t)nw * NS * TP.nT, lcount, nl);
+  e->mark(3);
+  FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
   uint16_t* lists = e->get<uint16_t>("lists", nl * kListCapO);
   launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, keys + total, e->max_n, flows,
                       total, recs, bbox, lcount, lists);
