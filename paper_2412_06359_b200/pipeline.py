@@ -93,47 +93,64 @@ class ChainPipeline:
             self.done[p[0]].synchronize()  # its result is in host memory
             return p[1]
 
-        while cur is not None:
-            nxt = next(it, None)
-            if nxt is not None:  # batch i+1 copies while batch i computes
-                self.copy.wait_event(self.consumed[1 - slot])  # batch i-1 read that set
-                staged_next = self._stage(1 - slot, *nxt[:3])
-            self.compute.wait_event(self.copied[slot])
-            nw = staged[0].shape[0]
-            if self.out is None or self.out[1].shape != staged[0].shape or \
-                    self.out[2].shape != staged[1].shape:
-                self.out = (torch.empty(nw, dtype=torch.float64, device=self.dev),
-                            torch.empty(tuple(staged[0].shape), dtype=torch.float64, device=self.dev),
-                            torch.empty(tuple(staged[1].shape), dtype=torch.float64, device=self.dev))
-            if window_sums:
-                H, W, B = staged[0].shape[1], staged[0].shape[2], staged[1].shape[1]
-                n_s = 1 + H * W + B * 6
-                if getattr(self, "sums", None) is None or self.sums.shape[0] != n_s:
-                    self.sums = torch.empty(n_s, dtype=torch.float64, device=self.dev)
-            with torch.cuda.stream(self.compute):
-                self.engine.chain_batch_async(staged[0], staged[1], k, t_start_us, t_end_us,
-                                              staged[2], np.asarray(cur[3], np.uint64), self.out,
-                                              slot, window_stride_us=window_stride_us,
-                                              sums=self.sums if window_sums else None)
-                self.consumed[slot].record(self.compute)
-                if window_sums or post is not None:
-                    if window_sums:
-                        r = post(self.sums) if post is not None else self.sums
+        queued = []  # slots with a batch in flight
+        try:
+            while cur is not None:
+                nxt = next(it, None)
+                if nxt is not None:  # batch i+1 copies while batch i computes
+                    self.copy.wait_event(self.consumed[1 - slot])  # batch i-1 read that set
+                    staged_next = self._stage(1 - slot, *nxt[:3])
+                self.compute.wait_event(self.copied[slot])
+                nw = staged[0].shape[0]
+                if self.out is None or self.out[1].shape != staged[0].shape or \
+                        self.out[2].shape != staged[1].shape:
+                    self.out = (torch.empty(nw, dtype=torch.float64, device=self.dev),
+                                torch.empty(tuple(staged[0].shape), dtype=torch.float64,
+                                            device=self.dev),
+                                torch.empty(tuple(staged[1].shape), dtype=torch.float64,
+                                            device=self.dev))
+                if window_sums:
+                    H, W, B = staged[0].shape[1], staged[0].shape[2], staged[1].shape[1]
+                    n_s = 1 + H * W + B * 6
+                    if getattr(self, "sums", None) is None or self.sums.shape[0] != n_s:
+                        self.sums = torch.empty(n_s, dtype=torch.float64, device=self.dev)
+                with torch.cuda.stream(self.compute):
+                    self.engine.chain_batch_async(staged[0], staged[1], k, t_start_us, t_end_us,
+                                                  staged[2], np.asarray(cur[3], np.uint64),
+                                                  self.out, slot,
+                                                  window_stride_us=window_stride_us,
+                                                  sums=self.sums if window_sums else None)
+                    queued.append(slot)
+                    self.consumed[slot].record(self.compute)
+                    if window_sums or post is not None:
+                        if window_sums:
+                            r = post(self.sums) if post is not None else self.sums
+                        else:
+                            r = post(*self.out)
+                        h = self.host[slot]
+                        if h is None or h.shape != r.shape or h.dtype != r.dtype:
+                            h = torch.empty(r.shape, dtype=r.dtype).pin_memory()
+                            self.host[slot] = h
+                        dst = h
+                        dst.copy_(r, non_blocking=True)
                     else:
-                        r = post(*self.out)
-                    h = self.host[slot]
-                    if h is None or h.shape != r.shape or h.dtype != r.dtype:
-                        h = torch.empty(r.shape, dtype=r.dtype).pin_memory()
-                        self.host[slot] = h
-                    dst = h
-                    dst.copy_(r, non_blocking=True)
-                else:
-                    dst = tuple(o.to("cpu", non_blocking=True) for o in self.out)
-                self.done[slot].record(self.compute)
-            if prev is not None:
-                yield finish(prev)
-            prev = (slot, dst)
-            cur = nxt
-            if nxt is not None:
-                staged, slot = staged_next, 1 - slot
-        yield finish(prev)
+                        dst = tuple(o.to("cpu", non_blocking=True) for o in self.out)
+                    self.done[slot].record(self.compute)
+                if prev is not None:
+                    queued.remove(prev[0])
+                    yield finish(prev)
+                prev = (slot, dst)
+                cur = nxt
+                if nxt is not None:
+                    staged, slot = staged_next, 1 - slot
+            queued.remove(prev[0])
+            yield finish(prev)
+        finally:
+            # an error or an early stop leaves batches in flight: collect them so
+            # the engine's slots are free for the next run (their errors, if any,
+            # are secondary to the one being raised)
+            for q in queued:
+                try:
+                    self.engine.chain_wait(q)
+                except Exception:
+                    pass

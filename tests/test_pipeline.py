@@ -67,3 +67,20 @@ def test_pipeline_reports_a_bad_batch():
         for _ in P.ChainPipeline(eng, s).run([mk(ev)] * 6 + [mk(bad)], K, 0, 100000):
             seen += 1
     assert seen == 6
+
+
+def test_pipeline_early_stop_frees_the_slots():
+    """Breaking out of a run leaves a batch in flight; the pipeline collects it so
+    the next run on the same engine can use every slot."""
+    import torch
+    s = torch.cuda.Stream()
+    eng = P.Engine(P.EngineOptions(stream=s.cuda_stream))
+    depth, poses, K, ev, offs = chain_inputs(32, 24, 4, 2, 500, seed=6)
+    b = (torch.from_numpy(depth).pin_memory(), torch.from_numpy(poses).pin_memory(),
+         torch.from_numpy(ev.view(np.uint8)).pin_memory(), offs)
+    pipe = P.ChainPipeline(eng, s)
+    for i, _ in enumerate(pipe.run([b] * 8, K, 0, 100000)):
+        if i == 4:
+            break
+    got = list(pipe.run([b] * 5, K, 0, 100000))
+    assert len(got) == 5
