@@ -734,7 +734,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           if (total == 0) break;
           continue;
         }
-        if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
+        // everything that does not touch buffer b is prepared before waiting
+        // for it: the region offsets (this producer's own array) and the byte count
         uint32_t* const roff = roffs[pw];
         uint4* s16 = stage16 + b * kStageQ;
         float2* s8 = stage8 + b * kStageQ;
@@ -742,7 +743,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         // 8 * (kStageQ + v) > 16 * v for every record slot v < split)
         uint2* s8e = reinterpret_cast<uint2*>(s16) + kStageQ;
         uint32_t* fk = fake[b];
-        for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
         // region offsets: exclusive scan of roundup2(len + 2) over the ranges
         uint32_t carry = 0;
         for (int l0 = 0; l0 < nl; l0 += 32) {
@@ -767,17 +767,25 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
-          const uint32_t par = (uint32_t)((base + k0) & 1ull);  // n_total is even
-          const uint32_t s0 = roff[l], sz = (uint32_t)((len + 3) & ~1ull);
           const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
-          // slack slots (no candidate of this range): s0 if par, [s0+par+len, s0+sz)
-          if (par) atomicOr(fk + (s0 >> 5), 1u << (s0 & 31));
-          for (uint32_t q = s0 + par + (uint32_t)len; q < s0 + sz; ++q)
-            atomicOr(fk + (q >> 5), 1u << (q & 31));
           bytes += (uint32_t)(l < n0 ? len * sizeof(FwdRec) : (a1 - a0) * 8);
           bytes += (uint32_t)((a1 - a0) * 8);
         }
         bytes = warp_sum_u32(bytes);
+        if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
+        for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
+        __syncwarp();
+        for (int l = lane; l < nl; l += 32) {
+          const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
+          if (lo >= hi) continue;
+          const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
+          const uint32_t par = (uint32_t)((base + k0) & 1ull);  // n_total is even
+          const uint32_t s0 = roff[l], sz = (uint32_t)((len + 3) & ~1ull);
+          // slack slots (no candidate of this range): s0 if par, [s0+par+len, s0+sz)
+          if (par) atomicOr(fk + (s0 >> 5), 1u << (s0 & 31));
+          for (uint32_t q = s0 + par + (uint32_t)len; q < s0 + sz; ++q)
+            atomicOr(fk + (q >> 5), 1u << (q & 31));
+        }
         if (lane == 0) {
           desc[b].n = nslots;
           desc[b].split = n0 < nl ? roff[n0] : nslots;
