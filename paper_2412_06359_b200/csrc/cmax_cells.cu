@@ -477,7 +477,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         __syncwarp();
         if (lane == 0) mbar_arrive_expect_tx(&full[b], n * (uint32_t)sizeof(FwdRec));
         __syncwarp();
-        for (int l = lane; l < nl; l += 32) {
+        int la = 0;  // first range ending after rb (prefixes are monotone)
+        {
+          int z = nl;
+          while (la < z) {
+            const int m = (la + z) >> 1;
+            if (cv.pre(m + 1) > rb) z = m; else la = m + 1;
+          }
+        }
+        for (int l = la + lane; l < nl && cv.pre(l) < rb + kStageP; l += 32) {
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + kStageP);
           if (lo < hi)
             bulk_g2s(sb + (lo - rb), rr + cv.rng(l) + (lo - cv.pre(l)),
@@ -743,12 +751,28 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         // 8 * (kStageQ + v) > 16 * v for every record slot v < split)
         uint2* s8e = reinterpret_cast<uint2*>(s16) + kStageQ;
         uint32_t* fk = fake[b];
+        // the ranges that intersect this round: [la, lb) (prefixes are monotone)
+        int la = 0, lb = nl;
+        {
+          int a = 0, z = nl;  // first l with pre(l + 1) > rb
+          while (a < z) {
+            const int m = (a + z) >> 1;
+            if (cv.pre(m + 1) > rb) z = m; else a = m + 1;
+          }
+          la = a;
+          z = nl;  // first l >= la with pre(l) >= rb + capv
+          while (a < z) {
+            const int m = (a + z) >> 1;
+            if (cv.pre(m) >= rb + capv) z = m; else a = m + 1;
+          }
+          lb = a;
+        }
         // region offsets: exclusive scan of roundup2(len + 2) over the ranges
         uint32_t carry = 0;
-        for (int l0 = 0; l0 < nl; l0 += 32) {
+        for (int l0 = la; l0 < lb; l0 += 32) {
           const int l = l0 + lane;
           uint32_t sz = 0;
-          if (l < nl) {
+          if (l < lb) {
             const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
             sz = lo < hi ? ((hi - lo + 3) & ~1u) : 0u;
           }
@@ -757,13 +781,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             const uint32_t y = __shfl_up_sync(kFull, x, o);
             if (lane >= o) x += y;
           }
-          if (l < nl) roff[l] = carry + x - sz;
+          if (l < lb) roff[l] = carry + x - sz;
           carry += __shfl_sync(kFull, x, 31);
         }
         __syncwarp();
         const uint32_t nslots = carry;
         uint32_t bytes = 0;
-        for (int l = lane; l < nl; l += 32) {
+        for (int l = la + lane; l < lb; l += 32) {
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
@@ -775,7 +799,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
         for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
         __syncwarp();
-        for (int l = lane; l < nl; l += 32) {
+        for (int l = la + lane; l < lb; l += 32) {
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
@@ -788,7 +812,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         }
         if (lane == 0) {
           desc[b].n = nslots;
-          desc[b].split = n0 < nl ? roff[n0] : nslots;
+          desc[b].split = n0 < la ? 0u : (n0 < lb ? roff[n0] : nslots);
           desc[b].r = g;
           desc[b].last = (final && rb + capv >= total) ? 1 : 0;
         }
@@ -796,7 +820,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         __syncwarp();
         if (lane == 0) mbar_arrive_expect_tx(&full[b], bytes);
         __syncwarp();
-        for (int l = lane; l < nl; l += 32) {
+        for (int l = la + lane; l < lb; l += 32) {
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
