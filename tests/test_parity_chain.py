@@ -140,3 +140,29 @@ def test_chain_window_sums_match_torch():
     assert rel_inf(sums_d.cpu().numpy(), refd) <= 1e-14
     with pytest.raises(P.ConfigError):
         eng.chain_batch(depth, poses, K, 0, 100000, ev, offs, sums=np.zeros(5))
+
+
+def test_chain_many_windows_and_async_host_inputs():
+    """More windows than the chain prologue's parameter block holds (offsets
+    copied from pinned memory, no graph) and an asynchronous call with host
+    inputs (runs eagerly, its slot has nothing pending) give the per-window
+    results of small batches."""
+    import torch
+    eng = P.Engine(P.EngineOptions(deterministic=True))
+    nw = 300
+    depth, poses, K, ev, offs = chain_inputs(16, 12, 3, nw, 40, seed=3)
+    loss, dd, dp = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    for w in (0, 137, 299):
+        o = np.array([0, offs[w + 1] - offs[w]], np.uint64)
+        l1, d1, p1 = eng.chain_batch(depth[w:w + 1], poses[w:w + 1], K, 0, 100000,
+                                     ev[int(offs[w]):int(offs[w + 1])], o)
+        assert np.array_equal(l1, loss[w:w + 1])
+        assert np.array_equal(d1[0], dd[w]) and rel_inf(p1[0], dp[w]) <= 1e-12
+    out = (torch.empty(nw, dtype=torch.float64, device="cuda"),
+           torch.empty((nw, 12, 16), dtype=torch.float64, device="cuda"),
+           torch.empty((nw, 3, 6), dtype=torch.float64, device="cuda"))
+    eng.chain_batch_async(depth, poses, K, 0, 100000, ev, offs, out, 1)
+    eng.chain_wait(1)
+    assert np.array_equal(out[0].cpu().numpy(), loss)
+    with pytest.raises(P.ConfigError):
+        eng.chain_wait(7)
