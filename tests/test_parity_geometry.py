@@ -70,3 +70,57 @@ def test_rejects_bad_pose(engine):
     with pytest.raises(P.ConfigError):
         engine.depth_pose_to_flows(np.ones((4, 4)), np.array([[4.0, 0, 0, 0, 0, 0]]),
                                    np.array([4.0, 4.0, 1.5, 1.5]), 0, 1000)
+
+
+def test_translational_flow_scales_inversely_with_depth(engine):
+    """DepthPoseToFlows.TranslationalFlowScalesInverselyWithDepth (test_geometry.cpp:303-322)."""
+    K = np.array([64.0, 64.0, 4.5, 3.5])
+    lateral = np.array([[0.0, 0.0, 0.0, 0.03, -0.02, 0.0]])
+    far = engine.depth_pose_to_flows(np.full((8, 10), 2.0), lateral, K, 0, 50000).flows.uv
+    near = engine.depth_pose_to_flows(np.full((8, 10), 1.0), lateral, K, 0, 50000).flows.uv
+    assert np.all(np.abs(near - 2.0 * far) <= 1e-10)
+    rot = np.array([[0.01, -0.02, 0.03, 0.0, 0.0, 0.0]])  # pure rotation: depth-independent
+    rf = engine.depth_pose_to_flows(np.full((8, 10), 2.0), rot, K, 0, 50000).flows.uv
+    rn = engine.depth_pose_to_flows(np.full((8, 10), 1.0), rot, K, 0, 50000).flows.uv
+    assert np.all(np.abs(rn - rf) <= 1e-10)
+
+
+def test_depth_translation_scale_family(engine):
+    """DepthPoseToFlows.DepthAndTranslationScaleFamilyLeavesFlowUnchanged (:324-346)."""
+    rng = np.random.default_rng(17)
+    base = rng.uniform(1.0, 3.0, (7, 11))
+    K = np.array([60.0, 58.0, 5.0, 3.5])
+    poses = np.array([[0.01, -0.015, 0.02, 0.04, 0.02, 0.01],
+                      [-0.02, 0.01, 0.005, -0.03, 0.01, -0.02]])
+    s = 3.7
+    sp = poses.copy()
+    sp[:, 3:] *= s
+    a = engine.depth_pose_to_flows(base, poses, K, 0, 100000)
+    b = engine.depth_pose_to_flows(base * s, sp, K, 0, 100000)
+    assert np.array_equal(a.valid, b.valid)
+    assert np.all(np.abs(a.flows.uv - b.flows.uv) <= 1e-10)
+
+
+def test_behind_camera_pixels_zero_flow_clear_bit(engine):
+    """DepthPoseToFlows.BehindCameraPixelsGetZeroFlowAndClearBit (:348-366)."""
+    H, W = 8, 6
+    d = np.repeat((0.55 + 0.25 * np.arange(H))[:, None], W, axis=1)
+    gf = engine.depth_pose_to_flows(d, np.array([[0, 0, 0, 0, 0, -1.0]]),
+                                    np.array([50.0, 50.0, 2.5, 3.5]), 0, 40000)
+    expect = (d > 1.0)
+    assert np.array_equal(gf.valid[0] != 0, expect)
+    assert np.all(gf.flows.uv[0][:, ~expect] == 0.0)
+
+
+def test_rsat_true_flow_and_zero_flow(engine):
+    """ContrastLoss.TrueFlowBeatsZeroFlowOnLinearTrajectory (test_warp.cpp:164-186):
+    rsat(zero flow) is exactly 1 and the true flow scores below 1."""
+    ev = O.make_events([k * 20000 for k in range(5)], [2 + (80 * k) // 100 for k in range(5)],
+                       [4] * 5, [1] * 5)
+    s = P.EventSlice(12, 8, 0, 100000, ev)
+    truth = P.FlowSequence.zeros(12, 8, 0, 100000, 2)
+    truth.uv[:, 0] = 40.0
+    zero = truth.zeros_like()
+    assert engine.forward(s, truth).loss.value < engine.forward(s, zero).loss.value
+    assert P.rsat(s, truth) < 1.0
+    assert P.rsat(s, zero) == 1.0
