@@ -129,6 +129,9 @@ def ref():
         L.ref_write_events.argtypes = [C.c_char_p, i32, i32, u64, u64, vp, sz]
         L.ref_validate_slice.argtypes = [i32, i32, u64, u64, vp, sz]
         L.ref_random_slice.argtypes = [u64, sz, vp, vp, vp, vp, vp]
+        L.ref_save_predictor.argtypes = [i32, i32, i32, vp, i32, vp, C.c_char_p, C.c_char_p]
+        L.ref_load_predictor.argtypes = [C.c_char_p, C.c_char_p, vp, vp, vp, vp, vp, sz, vp, i32]
+        L.ref_read_pfm.argtypes = [C.c_char_p, vp, vp, vp, sz]
         L.ref_format_number.argtypes = [f64, C.c_char_p]
         L.ref_format_number.restype = None
         L.ref_run_window.argtypes = [i32, vp, vp, vp, i32, i32, i32, vp, i32, vp, vp, f64, i32, i32,
@@ -718,3 +721,36 @@ def ref_run_window(windows, params, factor, poses, K, lr, steps_per_update, max_
                             _p(K), lr, steps_per_update, max_updates, lambda_geo, _p(po), _p(qo),
                             _p(rec), C.byref(n)), L, "ref")
     return po, qo, rec[: n.value]
+
+
+def ref_save_predictor(params, factor, poses, pfm, csv):
+    L = ref()
+    ph, pw = params.shape
+    params = np.ascontiguousarray(params, np.float64)
+    poses = np.ascontiguousarray(poses, np.float64)
+    _check(L.ref_save_predictor(pw, ph, factor, _p(params), poses.shape[0], _p(poses),
+                                os.fspath(pfm).encode(), os.fspath(csv).encode()), L, "ref")
+
+
+def ref_load_predictor(pfm, csv):
+    """-> (params [ph, pw], factor, poses [B, 6]) or OracleError."""
+    L = ref()
+    pw, ph, f, nb = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    args = (os.fspath(pfm).encode(), os.fspath(csv).encode())
+    _check(L.ref_load_predictor(*args, C.byref(pw), C.byref(ph), C.byref(f), C.byref(nb), None, 0,
+                                None, 0), L, "ref")
+    params = np.zeros((ph.value, pw.value))
+    poses = np.zeros((nb.value, 6))
+    _check(L.ref_load_predictor(*args, C.byref(pw), C.byref(ph), C.byref(f), C.byref(nb),
+                                _p(params), params.size, _p(poses), nb.value), L, "ref")
+    return params, f.value, poses
+
+
+def ref_read_pfm(path):
+    L = ref()
+    w, h = C.c_int(), C.c_int()
+    _check(L.ref_read_pfm(os.fspath(path).encode(), C.byref(w), C.byref(h), None, 0), L, "ref")
+    out = np.zeros((h.value, w.value), np.float32)
+    _check(L.ref_read_pfm(os.fspath(path).encode(), C.byref(w), C.byref(h), _p(out), out.size),
+           L, "ref")
+    return out

@@ -591,6 +591,50 @@ REF_API int ref_predictor_loss(int pw, int ph, int factor, const double* params,
   });
 }
 
+// save_predictor / load_predictor (predictor.hpp:178-218) and the PFM codec
+// (io.hpp:178-236) for the checkpoint fixtures.
+REF_API int ref_save_predictor(int pw, int ph, int factor, const double* params, int n_bins,
+                               const double* poses, const char* pfm, const char* csv) {
+  return guarded([&] {
+    DirectPredictor p;
+    p.depth_params = Image<double>(pw, ph, 0.0);
+    for (std::size_t i = 0; i < p.depth_params.size(); ++i) p.depth_params[i] = params[i];
+    p.poses = make_poses(n_bins, poses);
+    p.upsample = factor;
+    save_predictor(p, pfm, csv);
+  });
+}
+
+REF_API int ref_load_predictor(const char* pfm, const char* csv, int* pw, int* ph, int* factor,
+                               int* n_bins, double* params, std::size_t cap_params, double* poses,
+                               int cap_bins) {
+  return guarded([&] {
+    const DirectPredictor p = load_predictor(pfm, csv);
+    *pw = p.depth_params.width();
+    *ph = p.depth_params.height();
+    *factor = p.upsample;
+    *n_bins = static_cast<int>(p.poses.size());
+    if (params && p.depth_params.size() <= cap_params)
+      for (std::size_t i = 0; i < p.depth_params.size(); ++i) params[i] = p.depth_params[i];
+    if (poses && *n_bins <= cap_bins)
+      for (int b = 0; b < *n_bins; ++b) {
+        const PoseStep& q = p.poses[b];
+        const double v[6] = {q.omega.x, q.omega.y, q.omega.z, q.trans.x, q.trans.y, q.trans.z};
+        std::memcpy(poses + 6 * b, v, sizeof v);
+      }
+  });
+}
+
+REF_API int ref_read_pfm(const char* path, int* w, int* h, float* out, std::size_t cap) {
+  return guarded([&] {
+    const Image<float> img = read_pfm(path);
+    *w = img.width();
+    *h = img.height();
+    if (out && img.size() <= cap)
+      for (std::size_t i = 0; i < img.size(); ++i) out[i] = img[i];
+  });
+}
+
 // format_number (io.hpp:295-299) into buf (>= 64 bytes).
 REF_API void ref_format_number(double v, char* buf) {
   const std::string s = format_number(v);

@@ -13,12 +13,14 @@ from .engine import (  # noqa: F401
     load_library, make_edges, rsat)
 from .predictor import (  # noqa: F401
     Adam, DecodedPredictor, DirectPredictor, OptimizerConfig, PredictorGrads, WindowGradients,
-    accumulate_gradients, decode, predictor_loss_and_gradients)
+    accumulate_gradients, decode, load_predictor, predictor_loss_and_gradients, save_predictor)
 from .geo import (  # noqa: F401
     GEO_WEIGHT_DEFAULT, GeoBatch, GeoLossGrad, GeoLossTerms, geometry_consistency_loss,
     geometry_consistency_loss_backward, geometry_consistency_loss_batch, total_loss)
 from .pipeline import ChainPipeline  # noqa: F401
-from .io import Windows, format_number, read_events, slice_windows, write_events  # noqa: F401
+from .io import (  # noqa: F401
+    Windows, format_number, read_csv, read_events, read_pfm, slice_windows, write_events,
+    write_pfm)
 from .optimize import (  # noqa: F401
     FlowOnlyResult, RunResult, TrainLog, TrainRecord, optimize_flow_only, predictor_total_loss,
     run_window)

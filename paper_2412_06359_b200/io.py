@@ -155,6 +155,100 @@ def format_number(v: float) -> str:
     return sign + (fixed if len(fixed) <= len(sci) else sci)
 
 
+# ---- PFM float maps (io.hpp:178-236), used by the predictor checkpoints -------
+
+_WS = b" \t\n\v\f\r"  # std::isspace in the "C" locale
+
+
+def _next_token(data: bytes, pos: int, what: str):
+    while pos < len(data) and data[pos] in _WS:
+        pos += 1
+    if pos >= len(data):
+        raise TruncatedFileError(f"{what}: unexpected end of header")
+    start = pos
+    while pos < len(data) and data[pos] not in _WS:
+        pos += 1
+    return data[start:pos].decode("latin-1"), pos
+
+
+def _parse_int(tok: str, what: str) -> int:  # std::from_chars over the whole token
+    import re
+    if not re.fullmatch(r"-?[0-9]+", tok):
+        raise IoError(f"{what}: bad integer '{tok}'")
+    v = int(tok)
+    if not -2**31 <= v < 2**31:
+        raise IoError(f"{what}: bad integer '{tok}'")
+    return v
+
+
+def _strtod(tok: str) -> float:  # std::strtod: the longest valid prefix, 0 if none
+    import re
+    m = re.match(r"[+-]?(?:(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?|inf(?:inity)?|nan)",
+                 tok, re.IGNORECASE)
+    return float(m.group(0)) if m else 0.0
+
+
+def read_pfm(path) -> np.ndarray:
+    """read_pfm (io.hpp:181-217): a grayscale "Pf" map as float32 [H, W], top row
+    first (the file stores the bottom row first; a negative scale means little
+    endian, a magnitude != 1 scales the values)."""
+    try:
+        data = open(os.fspath(path), "rb").read()
+    except OSError as e:
+        raise IoError(f"cannot open {path}: {e}") from None
+    magic, pos = _next_token(data, 0, "PFM")
+    if magic != "Pf":
+        raise BadMagicError(f"PFM: expected grayscale magic 'Pf' in {path}")
+    tok, pos = _next_token(data, pos, "PFM")
+    w = _parse_int(tok, "PFM width")
+    tok, pos = _next_token(data, pos, "PFM")
+    h = _parse_int(tok, "PFM height")
+    tok, pos = _next_token(data, pos, "PFM")
+    scale = _strtod(tok)
+    if scale == 0.0:
+        raise IoError("PFM: zero scale")
+    if w <= 0 or h <= 0:
+        raise DimensionMismatchError("PFM: non-positive dimensions")
+    pos += 1  # exactly one whitespace byte separates header and raster
+    need = w * h * 4
+    if len(data) - pos < need:
+        raise TruncatedFileError("PFM: raster shorter than w*h")
+    if len(data) - pos > need:
+        raise IoError("PFM: trailing bytes after raster")
+    little = scale < 0.0
+    img = np.frombuffer(data, "<f4" if little else ">f4", w * h, pos).astype(np.float32)
+    mag = np.float32(-scale if little else scale)
+    if mag != np.float32(1.0):
+        img = img * mag
+    return img.reshape(h, w)[::-1].copy()
+
+
+def write_pfm(img, path) -> None:
+    """write_pfm (io.hpp:219-228): little-endian float32, bottom row first."""
+    a = np.asarray(img, np.float32)
+    if a.ndim != 2 or a.size == 0:
+        raise DimensionMismatchError("PFM: refusing to write empty image")
+    h, w = a.shape
+    try:
+        with open(os.fspath(path), "wb") as f:
+            f.write(f"Pf\n{w} {h}\n-1.0\n".encode())
+            f.write(np.ascontiguousarray(a[::-1]).astype("<f4").tobytes())
+    except OSError as e:
+        raise IoError(f"cannot open {path} for writing: {e}") from None
+
+
+def read_csv(path):
+    """read_csv (io.hpp:323-345): no quoting, comma-separated, '\r' stripped."""
+    try:
+        text = open(os.fspath(path), "rb").read().decode("latin-1")
+    except OSError as e:
+        raise IoError(f"cannot open {path}: {e}") from None
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()  # std::getline: a final newline ends the last line
+    return [ln[:-1].split(",") if ln.endswith("\r") else ln.split(",") for ln in lines]
+
+
 @dataclass
 class Windows:
     """Consecutive windows [t0 + w*window_us, t0 + (w+1)*window_us) of one slice:

@@ -3,6 +3,7 @@ of the CMax path — mirroring the reference's names and semantics:
 
   DirectPredictor, DecodedPredictor, decode          predictor.hpp:100-131
   PredictorGrads, accumulate_gradients               predictor.hpp:133-173
+  save_predictor, load_predictor (checkpoints)      predictor.hpp:175-218
   OptimizerConfig (Adam fields), Adam                optimize.hpp:25-75, 115-134
   WindowGradients, predictor_loss_and_gradients      optimize.hpp:195-241 (with L_geo)
 
@@ -68,6 +69,12 @@ class DirectPredictor:
         p = self.depth_params.cpu().numpy() if _is_torch(self.depth_params) else self.depth_params
         if not np.all(np.isfinite(p)):
             raise ConfigError("predictor: non-finite depth parameter")
+        q = self.poses.cpu().numpy() if _is_torch(self.poses) else np.asarray(self.poses)
+        for row in np.asarray(q, np.float64).reshape(-1, 6):  # PoseStep::validate (types.hpp:362-368)
+            if not (np.sqrt(row[0] * row[0] + row[1] * row[1] + row[2] * row[2]) < np.pi):
+                raise ConfigError("pose step: rotation angle must stay below pi")
+            if not np.all(np.isfinite(row)):
+                raise ConfigError("pose step: non-finite component")
 
 
 @dataclass
@@ -217,3 +224,66 @@ class Adam:
         _raise(load_library().evcm_cuda_adam_step(
             e._h, n, _ptr(slots), _ptr(_f64(grads)), _ptr(self.m), _ptr(self.v), self.t,
             cfg.learning_rate, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps, mem))
+
+
+# ---- checkpoints (predictor.hpp:175-218): depth parameters as PFM (float32), poses
+# and the upsample factor as CSV; host files, nothing on the device
+
+
+def save_predictor(pred: DirectPredictor, params_pfm, poses_csv) -> None:
+    """save_predictor (predictor.hpp:178-193)."""
+    from .io import format_number, write_pfm
+    pred.validate()
+    params = pred.depth_params.cpu().numpy() if _is_torch(pred.depth_params) else pred.depth_params
+    poses = pred.poses.cpu().numpy() if _is_torch(pred.poses) else np.asarray(pred.poses)
+    write_pfm(np.asarray(params, np.float64).astype(np.float32), params_pfm)
+    lines = ["bin,upsample,wx,wy,wz,tx,ty,tz"]
+    for i, p in enumerate(np.asarray(poses, np.float64).reshape(-1, 6)):
+        lines.append(",".join([str(i), str(pred.upsample)] + [format_number(v) for v in p]))
+    try:
+        with open(poses_csv, "w", newline="") as f:
+            f.write("\n".join(lines) + "\n")
+    except OSError as e:
+        from .engine import IoError
+        raise IoError(f"cannot open {poses_csv} for writing: {e}") from None
+
+
+def _stoi(tok: str) -> int:  # std::stoi: leading whitespace, sign, digits prefix
+    import re
+    m = re.match(r"\s*[+-]?[0-9]+", tok)
+    if not m:
+        from .engine import Error
+        raise Error(f"stoi: no conversion of '{tok}'")
+    return int(m.group(0))
+
+
+def _stod(tok: str) -> float:  # std::stod: the longest valid prefix
+    from .io import _strtod
+    import re
+    if not re.match(r"\s*[+-]?(?:[0-9]|\.[0-9]|inf|nan)", tok, re.IGNORECASE):
+        from .engine import Error
+        raise Error(f"stod: no conversion of '{tok}'")
+    return _strtod(tok.lstrip())
+
+
+def load_predictor(params_pfm, poses_csv) -> DirectPredictor:
+    """load_predictor (predictor.hpp:195-218)."""
+    from .io import read_csv, read_pfm
+    params = read_pfm(params_pfm).astype(np.float64)
+    rows = read_csv(poses_csv)
+    if len(rows) < 2 or len(rows[0]) != 8:
+        raise ConfigError("predictor checkpoint: malformed pose table")
+    upsample = 0
+    poses = []
+    for r in rows[1:]:
+        if len(r) != 8:
+            raise ConfigError("predictor checkpoint: malformed pose row")
+        factor = _stoi(r[1])
+        if upsample == 0:
+            upsample = factor
+        elif factor != upsample:
+            raise ConfigError("predictor checkpoint: inconsistent upsample factor")
+        poses.append([_stod(c) for c in r[2:8]])
+    pred = DirectPredictor(params, np.array(poses, np.float64), upsample)
+    pred.validate()
+    return pred
