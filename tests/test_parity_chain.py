@@ -166,3 +166,24 @@ def test_chain_many_windows_and_async_host_inputs():
     assert np.array_equal(out[0].cpu().numpy(), loss)
     with pytest.raises(P.ConfigError):
         eng.chain_wait(7)
+
+
+@pytest.mark.parametrize("B", [1, 32])
+def test_chain_bin_extremes_and_ragged_batch(engine_det, B):
+    """B = 1 and B = 32 (the cuda backend's limit), a batch with an empty window
+    and windows of very different sizes, against the oracle composition."""
+    W, H = 48, 36
+    depth, poses, K, ev, offs = chain_inputs(W, H, B, 4, 3000, seed=40 + B)
+    # ragged: window 1 empty, window 2 keeps 40 events, window 3 all of its own
+    keep = np.concatenate([np.arange(int(offs[0]), int(offs[1])),
+                           np.arange(int(offs[2]), int(offs[2]) + 40),
+                           np.arange(int(offs[3]), int(offs[4]))])
+    ev2 = ev[keep].copy()
+    offs2 = np.array([0, 3000, 3000, 3040, 6040], np.uint64)
+    loss, dd, dp = engine_det.chain_batch(depth, poses, K, 0, 100000, ev2, offs2)
+    ref = _oracle_chain(depth, poses, K, ev2, offs2)
+    for w in range(4):
+        assert abs(loss[w] - ref[w][0]) <= 1e-5 * max(abs(ref[w][0]), 1e-300)
+        assert rel_inf(dd[w], ref[w][1]) <= 1e-5
+        assert rel_inf(dp[w], ref[w][2]) <= 1e-5
+    assert loss[1] == 0.0 and not np.any(dd[1]) and not np.any(dp[1])  # empty window
