@@ -391,7 +391,7 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
 
 constexpr int kCons = kThreads;                 // consumer threads (16 warps)
 constexpr int kFwdThreads = kCons + 32;         // + producer warp
-constexpr int kStageP = 2048;                   // candidates per buffer
+constexpr int kStageP = 2304;                   // candidates per buffer
 
 struct RoundDesc {
   uint32_t n;  // staged candidates
