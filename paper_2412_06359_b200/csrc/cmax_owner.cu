@@ -216,13 +216,14 @@ __global__ void __launch_bounds__(1024) k_sort_tilescan(const uint32_t* __restri
 // Stable scatter: warp `wid` of chunk c owns events [c*chunk + wid*chunk/nW, ...);
 // per-warp tile counts (u16) give each warp its base inside the chunk's run of
 // the tile, so the output keeps the input (time) order inside every tile.
-__global__ void __launch_bounds__(kScatterThreads) k_sort_scatter(
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_sort_scatter(
     const uint2* __restrict__ packed, const uint32_t* __restrict__ keys,
     const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
     const uint32_t* __restrict__ tile_ptr, uint2* __restrict__ sorted, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ sorted_keys) {
   extern __shared__ uint16_t whist[];  // [nW warps][nT]
-  constexpr int nW = kScatterThreads / 32;
+  constexpr int nW = NW;  // 8 warps, or 4 for many tiles (launch_sort)
   const int per = TP.chunk / nW;
   for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
   __syncthreads();
@@ -585,9 +586,16 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
                  uint32_t* bin_ptr, uint4* bbox, size_t n_bbox, uint32_t* lcount, size_t n_lcount) {
   static size_t a1 = 0, a2 = 0;
-  const size_t sc_smem = (size_t)(kScatterThreads / 32) * TP.nT * 2;
+  // many sort tiles: 4 warps per CTA, so the per-warp tile counts (2 B per tile)
+  // leave room for more resident CTAs (measured: -9 % sort at 640x480)
+  const int sc_threads = TP.nT > 2048 ? kScatterThreads / 2 : kScatterThreads;
+  const size_t sc_smem = (size_t)(sc_threads / 32) * TP.nT * 2;
   set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
-  set_smem(reinterpret_cast<const void*>(k_sort_scatter), sc_smem, &a2);
+  static size_t a3 = 0;
+  if (sc_threads == kScatterThreads)
+    set_smem(reinterpret_cast<const void*>(k_sort_scatter<kScatterThreads / 32>), sc_smem, &a2);
+  else
+    set_smem(reinterpret_cast<const void*>(k_sort_scatter<kScatterThreads / 64>), sc_smem, &a3);
   const dim3 grid(TP.nchunks, P.n_windows);
   uint32_t* totals = keys + 2 * n_total;  // nw * nT scratch after the two key arrays
   double2* coarse = reinterpret_cast<double2*>(totals + (((size_t)P.n_windows * TP.nT + 3) & ~(size_t)3));
@@ -601,7 +609,11 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   count_launch();
   k_sort_tilescan<<<P.n_windows, 1024, 0, s>>>(totals, TP, tile_ptr);
   count_launch();
-  k_sort_scatter<<<grid, kScatterThreads, sc_smem, s>>>(packed, keys, ev_off, TP, counts, tile_ptr,
+if (sc_threads == kScatterThreads)
+    k_sort_scatter<kScatterThreads / 32><<<grid, sc_threads, sc_smem, s>>>(packed, keys, ev_off, TP, counts, tile_ptr,
+                                                        sorted, perm, keys + n_total);
+  else
+    k_sort_scatter<kScatterThreads / 64><<<grid, sc_threads, sc_smem, s>>>(packed, keys, ev_off, TP, counts, tile_ptr,
                                                         sorted, perm, keys + n_total);
   count_launch();
   k_bin_ptr<<<dim3((TP.nT + 7) / 8, P.n_windows), 256, 0, s>>>(sorted, ev_off, P, TP,
