@@ -31,6 +31,10 @@ EVENT_DTYPE = np.dtype({"names": ["t_us", "x", "y", "p"], "formats": ["<u8", "<u
                         "offsets": [0, 8, 10, 12], "itemsize": 16})
 
 WORKLOADS = {
+    # BASELINE.json configs[0]: the reference's own CPU-runnable case, one window
+    "A": dict(W=128, H=128, B=10, n_events=20_000, batch=1, window_us=100_000,
+              name="128x128 window (drone-downsampled), 20k events, batch 1, "
+                   "10 bins (11 refs), 0.1 s windows"),
     # BASELINE.json configs[1]: MVSEC-shape windows, ~100k events each, batch 8, 1 B200
     "B": dict(W=346, H=260, B=10, n_events=100_000, batch=8, window_us=100_000,
               name="MVSEC-shape 346x260 windows, 100k events/window, batch 8 per GPU, "
