@@ -547,11 +547,17 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     ap.add_argument("--sweep", action="store_true",
                     help="SURVEY §8(d) sweep (346x260, 1 window, 1e4..1e7 events); not the contract line")
+    ap.add_argument("--events", type=int, default=0, help="override events per window (exploration)")
+    ap.add_argument("--batch", type=int, default=0, help="override windows per GPU (exploration)")
     args = ap.parse_args()
     if args.sweep:
         sweep(args)
         return
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.events:
+        wl.update(n_events=args.events, name=wl["name"] + f" [events/window overridden: {args.events}]")
+    if args.batch:
+        wl.update(batch=args.batch, name=wl["name"] + f" [batch overridden: {args.batch}]")
     if args.impl == "reference":
         reference_arm(args, wl)
     else:

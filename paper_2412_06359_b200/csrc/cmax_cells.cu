@@ -37,6 +37,8 @@
 // BufferGradSink::add warp.hpp:391-407, depth_pose_to_flows_backward
 // geometry.hpp:279-325.
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 
 #include "cmax_device.cuh"
 #include "cmax_kernels.h"
@@ -381,8 +383,10 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
 }
 
 // ---------------------------------------------------------------------------
-// forward: one CTA per (owner tile, window), references in order, warp
-// specialised. Warp 0 (producer) builds each round's candidate ranges and
+// forward: one CTA per (owner tile, window, reference group), the group's
+// references [r0, r1) in order, warp specialised. References are independent
+// here, so the groups only add CTAs when the tiles x windows alone leave SMs
+// idle (owner_groups); the outputs do not depend on the grouping. Warp 0 (producer) builds each round's candidate ranges and
 // stages them with cp.async.bulk into one of two buffers (full/empty mbarrier
 // pair per buffer), running up to two rounds ahead; warps 1..16 (consumers, one
 // pixel each in the pixel phase) accumulate a round, release its buffer and,
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
   const int T = blockIdx.x, w = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int R = P.B + 1, NS = 2 * P.B + 1, W = P.W, H = P.H, HW = P.HW;
+  const int r0 = (int)blockIdx.z * R / (int)gridDim.z, r1 = ((int)blockIdx.z + 1) * R / (int)gridDim.z;
   const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const uint64_t base = ev_off[w];
@@ -445,11 +450,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     // ranges of reference r: precomputed list (prefetched one reference ahead)
     auto prefetch = [&](int r) {
       const size_t gid = ((size_t)w * NS + r) * TP.oT + T;
+      const int q = (r - r0) & 1;
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&rbar[r & 1], kRgCap * (uint32_t)sizeof(uint2));
-        bulk_g2s(rv[r & 1], ranges + gid * kRgCap, kRgCap * (uint32_t)sizeof(uint2), &rbar[r & 1]);
+        mbar_arrive_expect_tx(&rbar[q], kRgCap * (uint32_t)sizeof(uint2));
+        bulk_g2s(rv[q], ranges + gid * kRgCap, kRgCap * (uint32_t)sizeof(uint2), &rbar[q]);
       }
     };
     uint32_t it = 0;
@@ -495,11 +501,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         if (total == 0) break;
       }
     };
-    prefetch(0);
-    for (int r = 0; r < R; ++r) {
-      if (r + 1 < R) prefetch(r + 1);
-      mbar_wait(&rbar[r & 1], (r >> 1) & 1);
-      const uint2* v = rv[r & 1];
+    prefetch(r0);
+    for (int r = r0; r < r1; ++r) {
+      if (r + 1 < r1) prefetch(r + 1);
+      mbar_wait(&rbar[(r - r0) & 1], ((r - r0) >> 1) & 1);
+      const uint2* v = rv[(r - r0) & 1];
       if (v[0].x != kOverflow) {
         rounds(make_cat(v, nullptr), r, true, v[0].y);
       } else {  // overflowed list: scan the sort-tile boxes batch by batch
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
   const int ct = tid - 32, cw = wid - 1;  // consumer thread / warp
   const uint32_t acc_s = smem_u32(acc);
   uint32_t it = 0;
-  for (int r = 0; r < R;) {
+  for (int r = r0; r < r1;) {
     const int b = it & 1;
     mbar_wait(&full[b], (it >> 1) & 1);
     const RoundDesc d = desc[b];
@@ -644,10 +650,19 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
 // bulk-copied as the 16 B-aligned superset starting at the region, and its
 // records at the same slot offset, so slot s holds the record, value and event
 // of one candidate; the slack slots of every region are flagged in a bitmask.
+//
+// Bin groups (gridDim.z > 1, owner_groups): CTA z owns bins [i0, i1) and
+// streams groups i0..i1, where group i0 (i0 > 0) only primes bin i0 with the
+// record sinks of reference i0 that belong to it. Every bin tile is then built
+// from exactly the same terms as without groups (bit-identical, fixed point),
+// and each bin's d_depth term is stored (dbin) for k_depth_bins to sum in bin
+// order -- the same sum the single-group CTA forms in registers.
 
 constexpr int kStageQ = 1536;  // slots per buffer
 constexpr int kBufQ = 2;       // staging buffers (pipeline depth)
 constexpr int kBwdThreads = kCons + 64;  // two producer warps
+// each extra bin group re-streams one reference's records (its prime group)
+constexpr int kMaxBwdGroups = 3;
 
 struct BRound {
   uint32_t n;      // slots
@@ -665,7 +680,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint2* __restrict__ ranges, const int* __restrict__ no_surv,
     const double* __restrict__ depth, const uint8_t* __restrict__ mask,
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
-    double* __restrict__ d_depth, double* __restrict__ pose_part, double* __restrict__ grad_out) {
+    double* __restrict__ d_depth, double* __restrict__ dbin, double* __restrict__ pose_part,
+    double* __restrict__ grad_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* stage16 = reinterpret_cast<uint4*>(smem);                          // [kBufQ][kStageQ] records
   float2* stage8 = reinterpret_cast<float2*>(stage16 + kBufQ * kStageQ);    // [kBufQ][kStageQ] values
@@ -691,6 +707,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool run = !no_surv[w];
+  // this CTA's bins [i0, i1); group gs = max(i0, 1) primes bin i0 when i0 > 0
+  const int i0 = (int)blockIdx.z * B / (int)gridDim.z, i1 = ((int)blockIdx.z + 1) * B / (int)gridDim.z;
+  const int gs = i0 > 0 ? i0 : 1, prime_r = i0 > 0 ? i0 : -1;
 
   for (int i = tid; i < 8 * kPlane; i += kBwdThreads) acc[i] = 0u;
   if (tid == 0) {
@@ -717,13 +736,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     auto prefetch = [&](int g) {  // warp 0 only
       const size_t gref = ((size_t)w * NS + g) * TP.oT + T;
       const size_t gsrc = ((size_t)w * NS + R + g - 1) * TP.oT + T;
+      const int q = (g - gs) & 1;
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
         const uint32_t one = kRgCap * (uint32_t)sizeof(uint2);
-        mbar_arrive_expect_tx(&rbar[g & 1], g < B ? 2 * one : one);
-        if (g < B) bulk_g2s(rv[g & 1][0], ranges + gref * kRgCap, one, &rbar[g & 1]);
-        bulk_g2s(rv[g & 1][1], ranges + gsrc * kRgCap, one, &rbar[g & 1]);
+        mbar_arrive_expect_tx(&rbar[q], g < B ? 2 * one : one);
+        if (g < B) bulk_g2s(rv[q][0], ranges + gref * kRgCap, one, &rbar[q]);
+        bulk_g2s(rv[q][1], ranges + gsrc * kRgCap, one, &rbar[q]);
       }
     };
     uint32_t it = 0;
@@ -874,24 +894,28 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
       __syncwarp();
     }
     if (run) {
-      if (pw == 0) prefetch(1);
-      for (int g = 1; g <= B; ++g) {
+      if (pw == 0) prefetch(gs);
+      for (int g = gs; g <= i1; ++g) {
         pair_sync();  // both producers are done with the ranges of group g - 1
-        if (pw == 0 && g + 1 <= B) prefetch(g + 1);
-        mbar_wait(&rbar[g & 1], ((g - 1) >> 1) & 1);
-        const uint2* va = g < B ? rv[g & 1][0] : nullptr;
-        const uint2* vb = rv[g & 1][1];
-        const bool oa = va && va[0].x == kOverflow, ob = vb[0].x == kOverflow;
+        if (pw == 0 && g + 1 <= i1) prefetch(g + 1);
+        const int q = (g - gs) & 1;
+        mbar_wait(&rbar[q], ((g - gs) >> 1) & 1);
+        const bool prime = g == prime_r;  // record sinks of reference g only, bin g not complete
+        const uint2* va = g < B ? rv[q][0] : nullptr;
+        const uint2* vb = prime ? nullptr : rv[q][1];
+        const bool oa = va && va[0].x == kOverflow, ob = vb && vb[0].x == kOverflow;
         if (!oa && !ob) {
-          rounds(make_cat(va, vb), g, true, false);
+          rounds(make_cat(va, vb), g, !prime, false);
         } else {
           if (pw == 0) {
             if (va) {
               if (oa) scan_rounds(0, g, false);
               else rounds(make_cat(va, nullptr), g, false, true);
             }
-            if (ob) scan_rounds(1, g, true);
-            else rounds(make_cat(nullptr, vb), g, true, true);
+            if (vb) {
+              if (ob) scan_rounds(1, g, true);
+              else rounds(make_cat(nullptr, vb), g, true, true);
+            }
             if (lane == 0) s_it = it;
           }
           pair_sync();
@@ -899,7 +923,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         }
       }
     } else {  // no survivors: every bin is zero, still finish each one
-      for (int g = 1; g <= B; ++g) rounds(make_cat(nullptr, nullptr), g, true, false);
+      for (int g = i0 + 1; g <= i1; ++g) rounds(make_cat(nullptr, nullptr), g, true, false);
     }
     return;
   }
@@ -922,7 +946,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   double gsc = 0.0, igsc = 0.0;
   double dd = 0.0;  // d_depth of this pixel, bins summed in order
   uint32_t it = 0;
-  for (int done = 0; done < B;) {
+  for (int done = 0; done < i1 - i0;) {
     const int b = (int)(it % kBufQ);
     mbar_wait(&full[b], (it / kBufQ) & 1);
     if (it == 0) {
@@ -935,6 +959,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
     const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
+    const int lo_bin = d.r == prime_r ? d.r : 0;
     // record sinks of reference d.r (slots < split)
     compacted<kCons>(
         (uint32_t)cw * 32, d.split, wq[cw],
@@ -953,6 +978,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           // the bin this sink belongs to: r - 1 if r <= j else r, and for
           // 1 <= r <= B-1, r <= bin_of(t) (warp.hpp:284-288) iff erel[r] <= dt
           const int bin = (rec.y >= er) ? d.r - 1 : d.r;
+          if (bin < lo_bin) return;  // a sink of bin i0 - 1 (another CTA's)
           const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
           double wx, ax, wy, ay;
           expand_frac(__uint_as_float(rec.z), wx, ax);
@@ -996,6 +1022,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const int i = d.r - 1;
     consumer_sync(kCons);
     double c6[6] = {0, 0, 0, 0, 0, 0};
+    double ddi = 0.0;  // this bin's d_depth term
     {
       const uint32_t* at = acc + (i & 1) * 4 * kPlane;
       const double gu = (double)(long long)fx_read(at + op, at + kPlane + op) * igsc;
@@ -1017,7 +1044,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             const double inv_dt = ptab[39], iz = 1.0 / p2;
             const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
             const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-            dd += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
+            // explicit roundings: k_depth_bins re-forms this sum from the stored terms
+            ddi = __dmul_rn(gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2), inv_dt);
             c6[3] = gu * ju0 * inv_dt;
             c6[4] = gv * jv1 * inv_dt;
             c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
@@ -1034,6 +1062,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         }
       }
     }
+    if (dbin && own_px) dbin[((size_t)w * B + i) * HW + gq] = ddi;
+    dd = __dadd_rn(dd, ddi);
     if (pose_part) {
       // six warp sums by transposition: each halving step trades half of the
       // remaining components with the partner lane (9 double shuffles, not 30);
@@ -1067,8 +1097,21 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     }
     ++done;
   }
-  if (d_depth && own_px) d_depth[(size_t)w * HW + gq] = dd;
+  if (d_depth && !dbin && own_px) d_depth[(size_t)w * HW + gq] = dd;
   (void)H;
+}
+
+// d_depth of grouped backward CTAs: each pixel's bin terms summed in bin order
+// from 0.0, exactly the register sum of an ungrouped CTA
+__global__ void k_depth_bins(const double* __restrict__ dbin, int B, int HW, int n_windows,
+                             double* __restrict__ d_depth) {
+  const size_t n = (size_t)n_windows * HW;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    const size_t w = k / HW, p = k % HW;
+    double dd = 0.0;
+    for (int i = 0; i < B; ++i) dd = __dadd_rn(dd, dbin[(w * B + i) * HW + p]);
+    d_depth[k] = dd;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1088,12 +1131,12 @@ void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, const uint2* ranges, double2* coef, double2* stack_out,
-                      double* part_acc, unsigned long long* part_act) {
+                      double* part_acc, unsigned long long* part_act, int groups) {
   static bool attr = false;
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_fwd_cells), fwd_cells_smem());
   attr = true;
   count_launch();
-  k_fwd_cells<<<dim3(TP.oT, P.n_windows), kFwdThreads, fwd_cells_smem(), s>>>(
+  k_fwd_cells<<<dim3(TP.oT, P.n_windows, std::max(1, std::min(groups, P.B + 1))), kFwdThreads, fwd_cells_smem(), s>>>(
       ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, ranges, coef, stack_out,
       part_acc, part_act);
 }
@@ -1105,16 +1148,40 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
                       const int* no_surv, const double* depth, const uint8_t* mask,
                       const double* pose_tab, const double* K, double* d_depth, double* pose_part,
-                      double* grad_out) {
+                      double* grad_out, int groups, double* dbin) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   static bool attr = false;
   if (!attr) smem_attr(reinterpret_cast<const void*>(k_bwd_cells), bwd_cells_smem());
   attr = true;
   count_launch();
-  k_bwd_cells<<<dim3(TP.oT, P.n_windows), kBwdThreads, bwd_cells_smem(), s>>>(
+  groups = std::max(1, std::min(groups, P.B));
+  if (groups == 1 || !d_depth) dbin = nullptr;
+  k_bwd_cells<<<dim3(TP.oT, P.n_windows, groups), kBwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
-      no_surv,
-      depth, mask, pose_tab, k0, k1, k2, k3, d_depth, pose_part, grad_out);
+      no_surv, depth, mask, pose_tab, k0, k1, k2, k3, d_depth, dbin, pose_part, grad_out);
+  if (dbin) {
+    count_launch();
+    const size_t n = (size_t)P.n_windows * P.HW;
+    k_depth_bins<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(dbin, P.B, P.HW,
+                                                                                    P.n_windows, d_depth);
+  }
+}
+
+static int env_int(const char* name) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : 0;
+}
+
+int owner_groups(const TileParams& TP, const WinParams& P, bool backward) {
+  static const int env_f = env_int("EVCM_FWD_GROUPS"), env_b = env_int("EVCM_BWD_GROUPS");
+  const int env = backward ? env_b : env_f;
+  const int max_groups = backward ? P.B : P.B + 1;
+  const long ctas = (long)TP.oT * P.n_windows;
+  const long target = 4L * 2 * 148;
+  int g = (int)std::min<long>((target + ctas - 1) / ctas, max_groups);
+  if (backward) g = std::min(g, kMaxBwdGroups);
+  if (env > 0) g = env;
+  return std::max(1, std::min(g, max_groups));
 }
 
 void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,

@@ -34,6 +34,7 @@ void launch_pose_table(cudaStream_t s, const double* poses, int n_windows, int B
                        const double* inv_dt, double* tab, int* bad);
 // Chain prologue (k_chain_init): offsets, validation words, device pose table.
 constexpr int kInitMaxWin = 256;  // windows whose offsets fit the kernel parameters
+constexpr uint64_t kOwnerMinEvents = 250000;  // algo auto: smaller calls take the atomic pipeline
 struct ChainInit {
   uint64_t off[kInitMaxWin + 1];
   int nw, B;

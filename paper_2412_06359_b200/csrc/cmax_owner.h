@@ -60,7 +60,12 @@ void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
                       uint64_t n_total, const uint4* bbox, const uint32_t* lcount,
                       const uint16_t* lists, const uint2* ranges, double2* coef, double2* stack_out,
-                      double* part_acc, unsigned long long* part_act);
+                      double* part_acc, unsigned long long* part_act, int groups);
+// CTA groups of the owner kernels: split the references (forward) / bins
+// (backward) over `groups` CTAs per (tile, window) when tiles x windows alone
+// fill fewer than ~4 waves of 2 CTAs per SM (EVCM_FWD_GROUPS / EVCM_BWD_GROUPS
+// override, for measurements)
+int owner_groups(const TileParams& TP, const WinParams& P, bool backward);
 void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
@@ -68,7 +73,7 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
                       const int* no_surv, const double* depth, const uint8_t* mask,
                       const double* pose_tab, const double* K, double* d_depth, double* pose_part,
-                      double* grad_out);
+                      double* grad_out, int groups, double* dbin);
 // Per (window, slot, owner tile) list: precomputed candidate ranges (kListCapO + 2
 // uint2 entries; see cmax_cells.cu)
 void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,

@@ -346,9 +346,12 @@ void stage_events(evcm_cuda_engine* e, const evcm_event* ev, const uint64_t* off
   e->n_total = (total + 1) & ~1ull;  // even plane stride (16 B-aligned 8 B sub-arrays)
   e->max_n = max_n;
   // algo auto: the owner pipeline (deterministic, fixed-point) ties the atomic one
-  // at ~1 event per pixel and window and wins above (measured)
+  // at ~1 event per pixel and window and wins above, once the call carries
+  // ~2.5e5 events (below, its fixed per-stage latency dominates; measured,
+  // DESIGN.md)
   if (e->opt.algo == 2)
-    e->use_owner = e->opt.deterministic || (double)total >= 1.0 * (double)P.HW * nw;
+    e->use_owner = e->opt.deterministic ||
+                   ((double)total >= 1.0 * (double)P.HW * nw && total >= kOwnerMinEvents);
   else
     e->use_owner = e->opt.algo == 0 || e->opt.deterministic;
   if (e->owner()) {
@@ -505,7 +508,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   // fixed-point accumulation: bit-deterministic in both modes
   launch_fwd_cells(e->stream, ev_off, P, TP, tile_ptr, recs, total, bbox, lcount, lists, ranges,
                    e->get<double2>("coef", (size_t)nw * R * 2 * P.HW), stack,
-                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np));
+                   e->get<double>("part_acc", np), e->get<unsigned long long>("part_act", np),
+                   owner_groups(TP, P, false));
   e->mark(5);
   launch_loss_finalize(e->stream, e->get<double>("part_acc", np),
                        e->get<unsigned long long>("part_act", np), TP.oT, P,
@@ -535,11 +539,13 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
                    bwd, gmax);
   e->mark(7);
   double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * 6) : nullptr;
+  const int bgroups = owner_groups(TP, P, true);
   launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
                    e->get<uint16_t>("lists", 1), e->get<uint2>("ranges", 1), e->get<int>("no_surv", 1),
                    depth, mask, pose_tab,
-                   K, depth ? d_depth : nullptr, pose_part, grad_out);
+                   K, depth ? d_depth : nullptr, pose_part, grad_out, bgroups,
+                   bgroups > 1 && depth ? e->get<double>("dbin", (size_t)nw * P.B * P.HW) : nullptr);
   e->mark(8);
   if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
   e->mark(9);

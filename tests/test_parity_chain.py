@@ -56,7 +56,7 @@ def test_chain_graph_replay():
     (fixed-point accumulation is order-independent), and the replay must read the
     CURRENT contents of the (same) input buffers."""
     import torch
-    eng = P.Engine()
+    eng = P.Engine(P.EngineOptions(algo="owner"))  # deterministic pipeline
     W, H, B, nw, n = 96, 64, 6, 3, 8000
     depth, poses, K, ev, offs = chain_inputs(W, H, B, nw, n, seed=3)
     d_depth = torch.from_numpy(depth).cuda()
