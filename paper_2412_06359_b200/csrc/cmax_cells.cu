@@ -404,6 +404,7 @@ struct RoundDesc {
   int fb;      // fraction bits of this reference's sums (<= 50, see below)
 };
 
+template <bool kGrouped>
 __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     const uint64_t* __restrict__ ev_off, WinParams P, TileParams TP,
     const uint32_t* __restrict__ tile_ptr, const FwdRec* __restrict__ recs, uint64_t n_total,
@@ -427,7 +428,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
   const int T = blockIdx.x, w = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int R = P.B + 1, NS = 2 * P.B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int r0 = (int)blockIdx.z * R / (int)gridDim.z, r1 = ((int)blockIdx.z + 1) * R / (int)gridDim.z;
+  const int r0 = kGrouped ? (int)blockIdx.z * R / (int)gridDim.z : 0;
+  const int r1 = kGrouped ? ((int)blockIdx.z + 1) * R / (int)gridDim.z : R;
   const int ox0 = (T % TP.otx) * kOwnW, oy0 = (T / TP.otx) * kOwnH;
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const uint64_t base = ev_off[w];
@@ -671,6 +673,7 @@ struct BRound {
   int last;        // last round of the group: bin r - 1 is complete
 };
 
+template <bool kGrouped>
 __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
@@ -708,8 +711,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool run = !no_surv[w];
   // this CTA's bins [i0, i1); group gs = max(i0, 1) primes bin i0 when i0 > 0
-  const int i0 = (int)blockIdx.z * B / (int)gridDim.z, i1 = ((int)blockIdx.z + 1) * B / (int)gridDim.z;
-  const int gs = i0 > 0 ? i0 : 1, prime_r = i0 > 0 ? i0 : -1;
+  const int i0 = kGrouped ? (int)blockIdx.z * B / (int)gridDim.z : 0;
+  const int i1 = kGrouped ? ((int)blockIdx.z + 1) * B / (int)gridDim.z : B;
+  const int gs = i0 > 0 ? i0 : 1, prime_r = kGrouped && i0 > 0 ? i0 : -1;
 
   for (int i = tid; i < 8 * kPlane; i += kBwdThreads) acc[i] = 0u;
   if (tid == 0) {
@@ -959,7 +963,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
     const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
-    const int lo_bin = d.r == prime_r ? d.r : 0;
+    const int lo_bin = kGrouped && d.r == prime_r ? d.r : 0;
     // record sinks of reference d.r (slots < split)
     compacted<kCons>(
         (uint32_t)cw * 32, d.split, wq[cw],
@@ -978,7 +982,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           // the bin this sink belongs to: r - 1 if r <= j else r, and for
           // 1 <= r <= B-1, r <= bin_of(t) (warp.hpp:284-288) iff erel[r] <= dt
           const int bin = (rec.y >= er) ? d.r - 1 : d.r;
-          if (bin < lo_bin) return;  // a sink of bin i0 - 1 (another CTA's)
+          if (kGrouped && bin < lo_bin) return;  // a sink of bin i0 - 1 (another CTA's)
           const uint32_t pt = acc_s + (uint32_t)(bin & 1) * (4 * kPlane * 4);
           double wx, ax, wy, ay;
           expand_frac(__uint_as_float(rec.z), wx, ax);
@@ -1046,6 +1050,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
             // explicit roundings: k_depth_bins re-forms this sum from the stored terms
             ddi = __dmul_rn(gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2), inv_dt);
+            dd = __dadd_rn(dd, ddi);
             c6[3] = gu * ju0 * inv_dt;
             c6[4] = gv * jv1 * inv_dt;
             c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
@@ -1062,8 +1067,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         }
       }
     }
-    if (dbin && own_px) dbin[((size_t)w * B + i) * HW + gq] = ddi;
-    dd = __dadd_rn(dd, ddi);
+    if (kGrouped && dbin && own_px) dbin[((size_t)w * B + i) * HW + gq] = ddi;
     if (pose_part) {
       // six warp sums by transposition: each halving step trades half of the
       // remaining components with the partner lane (9 double shuffles, not 30);
@@ -1097,7 +1101,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     }
     ++done;
   }
-  if (d_depth && !dbin && own_px) d_depth[(size_t)w * HW + gq] = dd;
+  if (d_depth && !(kGrouped && dbin) && own_px) d_depth[(size_t)w * HW + gq] = dd;
   (void)H;
 }
 
@@ -1133,10 +1137,15 @@ void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P
                       const uint16_t* lists, const uint2* ranges, double2* coef, double2* stack_out,
                       double* part_acc, unsigned long long* part_act, int groups) {
   static bool attr = false;
-  if (!attr) smem_attr(reinterpret_cast<const void*>(k_fwd_cells), fwd_cells_smem());
+  if (!attr) {
+    smem_attr(reinterpret_cast<const void*>(k_fwd_cells<false>), fwd_cells_smem());
+    smem_attr(reinterpret_cast<const void*>(k_fwd_cells<true>), fwd_cells_smem());
+  }
   attr = true;
   count_launch();
-  k_fwd_cells<<<dim3(TP.oT, P.n_windows, std::max(1, std::min(groups, P.B + 1))), kFwdThreads, fwd_cells_smem(), s>>>(
+  groups = std::max(1, std::min(groups, P.B + 1));
+  auto* kern = groups > 1 ? k_fwd_cells<true> : k_fwd_cells<false>;
+  kern<<<dim3(TP.oT, P.n_windows, groups), kFwdThreads, fwd_cells_smem(), s>>>(
       ev_off, P, TP, tile_ptr, recs, n_total, bbox, lcount, lists, ranges, coef, stack_out,
       part_acc, part_act);
 }
@@ -1151,12 +1160,16 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       double* grad_out, int groups, double* dbin) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   static bool attr = false;
-  if (!attr) smem_attr(reinterpret_cast<const void*>(k_bwd_cells), bwd_cells_smem());
+  if (!attr) {
+    smem_attr(reinterpret_cast<const void*>(k_bwd_cells<false>), bwd_cells_smem());
+    smem_attr(reinterpret_cast<const void*>(k_bwd_cells<true>), bwd_cells_smem());
+  }
   attr = true;
   count_launch();
   groups = std::max(1, std::min(groups, P.B));
   if (groups == 1 || !d_depth) dbin = nullptr;
-  k_bwd_cells<<<dim3(TP.oT, P.n_windows, groups), kBwdThreads, bwd_cells_smem(), s>>>(
+  auto* kern = groups > 1 ? k_bwd_cells<true> : k_bwd_cells<false>;
+  kern<<<dim3(TP.oT, P.n_windows, groups), kBwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
       no_surv, depth, mask, pose_tab, k0, k1, k2, k3, d_depth, dbin, pose_part, grad_out);
   if (dbin) {
