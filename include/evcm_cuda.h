@@ -97,8 +97,9 @@ typedef struct {
   void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
   int algo;            /* 0: owner-computes tiles (no global atomics; the only path with
                           deterministic = 1); 1: per-event global atomics (honours
-                          stack_f64 / grad_f64); 2 (default): auto — owner when the
-                          batch has >= 2 events per pixel per window or deterministic */
+                          stack_f64 / grad_f64); 2 (default): auto — owner when
+                          deterministic, or when the call carries >= 1 event per pixel
+                          per window and >= 2.5e5 events in total (measured crossover) */
 } evcm_cuda_options;
 
 /* EventSlice (types.hpp:121-126). */
