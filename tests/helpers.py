@@ -56,3 +56,27 @@ def chain_inputs(W, H, B, n_windows, events_per_window, seed=7, window_us=100000
                                  np.where(np.arange(n) % 2 == 0, 1, -1)))
         offs.append(offs[-1] + n)
     return depth, poses, K, np.concatenate(evs).astype(O.EVENT_DTYPE), np.array(offs, np.uint64)
+
+
+def contraction_window(W, H, B, n, factor=0.2, seed=11, window_us=100000):
+    """Still first half, then a radial flow that shrinks the sensor toward its
+    centre by `factor` over the second half: events keep their spread at the
+    middle reference (the sort key), and at the last references one 32x16 owner
+    tile gathers ~(1/factor)^2 x 8 sort tiles, more than a precomputed list
+    holds (kListCapO = 128), so the owner kernels take their overflow
+    (box-scan) path."""
+    rng = np.random.default_rng(seed)
+    t = np.sort(rng.integers(0, window_us, n)).astype(np.uint64)
+    ev = O.make_events(t, rng.integers(0, W, n), rng.integers(0, H, n),
+                       np.where(np.arange(n) % 2 == 0, 1, -1))
+    edges = O.make_edges(0, window_us, B)
+    nb = B - B // 2  # the trajectory compounds one linear step per bin
+    k = -(1.0 - factor ** (1.0 / nb)) / (window_us * 1e-6 / B)  # 1/s
+    xs = np.arange(W)[None, :] - (W - 1) / 2
+    ys = np.arange(H)[:, None] - (H - 1) / 2
+    uv = np.zeros((B, 2, H, W))
+    for b in range(B // 2, B):
+        uv[b, 0] = k * xs + 0 * ys
+        uv[b, 1] = k * ys + 0 * xs
+    uv = uv.astype(np.float32).astype(np.float64)
+    return O.Window(W, H, edges, ev, uv)

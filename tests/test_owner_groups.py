@@ -18,7 +18,7 @@ SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, {root!r})
 import paper_2412_06359_b200 as P
-from tests.helpers import chain_inputs, smooth_window
+from tests.helpers import chain_inputs, contraction_window, smooth_window
 out = {{}}
 eng = P.Engine(P.EngineOptions(algo="owner"))
 for (W, H, B, nw, n, seed) in [(128, 128, 10, 1, 20000, 1), (200, 150, 7, 3, 60000, 2),
@@ -37,6 +37,12 @@ g = eng.backward(sl, fl, f)
 out["loss"] = np.array([f.loss.value])
 out["stack"] = np.concatenate([np.ravel(f.stack.count), np.ravel(f.stack.tsum)])
 out["grad"] = np.ravel(g.grad)
+w = contraction_window(256, 192, 6, 40000, factor=0.15)  # overflowed owner lists
+sl = P.EventSlice(w.W, w.H, int(w.edges[0]), int(w.edges[-1]), w.events)
+fl = P.FlowSequence(w.edges.copy(), w.flows.copy())
+f = eng.forward(sl, fl)
+out["c_loss"] = np.array([f.loss.value])
+out["c_grad"] = np.ravel(eng.backward(sl, fl, f).grad)
 np.savez(sys.argv[1], **out)
 """
 

@@ -216,3 +216,12 @@ def test_hot_pixel_dense(engine):
     w = O.Window(W, H, O.make_edges(0, 100000, B), ev, uv)
     fwd, *_ = _check(engine, w)
     assert fwd.stack.count.max() > 2 ** 14
+
+
+@pytest.mark.parametrize("factor", [0.5, 0.15])
+def test_overflowing_owner_lists(factor):
+    """Strong contraction: owner tiles near the centre gather from more sort tiles
+    than their precomputed lists hold; the box-scan path must give the same parity."""
+    from tests.helpers import contraction_window
+    w = contraction_window(256, 192, 6, 40000, factor=factor)
+    _check(P.Engine(P.EngineOptions(algo="owner")), w)
