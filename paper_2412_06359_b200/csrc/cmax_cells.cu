@@ -1045,7 +1045,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           const double rr2 = ptab[6] * rx + ptab[7] * ry + ptab[8];
           const double p0 = dpx * rr0 + ptab[36], p1 = dpx * rr1 + ptab[37], p2 = dpx * rr2 + ptab[38];
           if (p2 > 0.0) {
-            const double inv_dt = ptab[39], iz = 1.0 / p2;
+            const double inv_dt = ptab[39], iz = __drcp_rn(p2);  // == 1.0 / p2 (correctly rounded)
             const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
             const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
             // explicit roundings: k_depth_bins re-forms this sum from the stored terms

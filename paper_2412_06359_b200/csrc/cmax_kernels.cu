@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kPxBlock) k_loss_reduce(const S2* __restrict__
     const double a0 = v0.y / (v0.x + kLossEps), a1 = v1.y / (v1.x + kLossEps);
     acc += a0 * a0 + a1 * a1;
     // splat_position_grad's per-pixel factors (warp.hpp:346-349)
-    const double i0 = 1.0 / (v0.x + kLossEps), i1 = 1.0 / (v1.x + kLossEps);
+    const double i0 = __drcp_rn(v0.x + kLossEps), i1 = __drcp_rn(v1.x + kLossEps);  // == 1.0 / x
     const double b0 = v0.y * i0, b1 = v1.y * i1;
     store2(coef + plane0 + q, b0, b0 * i0);
     store2(coef + plane0 + HW + q, b1, b1 * i1);
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
       const double p0 = d * rr0 + pt[36], p1 = d * rr1 + pt[37], p2 = d * rr2 + pt[38];
       if (!(p2 > 0.0)) continue;
       const double inv_dt = pt[39];
-      const double iz = 1.0 / p2;
+      const double iz = __drcp_rn(p2);  // == 1.0 / p2 (correctly rounded)
       const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
       const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
       dd[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
