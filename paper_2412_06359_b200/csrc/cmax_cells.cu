@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   __shared__ __align__(8) uint64_t full[kBufQ], empty[kBufQ], rbar[2];
   __shared__ uint16_t wq[kWarps][64];  // per-warp compaction queues
   __shared__ int s_kbits;              // fixed-point magnitude bits of the gradient terms
-  __shared__ double s_pose[2][kWarps][6];
+  __shared__ double s_pose[2][kWarps][kPoseSums];
 
   const int T = blockIdx.x, w = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1025,7 +1025,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     // bin i = d.r - 1 complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
     const int i = d.r - 1;
     consumer_sync(kCons);
-    double c6[6] = {0, 0, 0, 0, 0, 0};
+    // pose sums of this pixel (see kPoseSums): N = d v r^T (0..8), v (9..11)
+    double c6[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c6[k] = 0.0;
     double ddi = 0.0;  // this bin's d_depth term
     {
       const uint32_t* at = acc + (i & 1) * 4 * kPlane;
@@ -1051,53 +1054,49 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             // explicit roundings: k_depth_bins re-forms this sum from the stored terms
             ddi = __dmul_rn(gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2), inv_dt);
             dd = __dadd_rn(dd, ddi);
-            c6[3] = gu * ju0 * inv_dt;
-            c6[4] = gv * jv1 * inv_dt;
-            c6[5] = (gu * ju2 + gv * jv2) * inv_dt;
+            // d_t = v = (gu ju0, gv jv1, gu ju2 + gv jv2) / dt, and d_omega_a =
+            // d v . (dR_a r^), r^ = (rx, ry, 1): summed as the moments N = sum d v r^T,
+            // contracted with dR_a once per (window, bin) (k_pose_contract)
+            const double v0 = gu * ju0 * inv_dt, v1 = gv * jv1 * inv_dt;
+            const double v2 = (gu * ju2 + gv * jv2) * inv_dt;
+            const double dv[3] = {dpx * v0, dpx * v1, dpx * v2};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-              const double* dR = ptab + 9 + 9 * a;
-              const double m0 = dR[0] * rx + dR[1] * ry + dR[2];
-              const double m1 = dR[3] * rx + dR[4] * ry + dR[5];
-              const double m2 = dR[6] * rx + dR[7] * ry + dR[8];
-              c6[a] = (gu * (ju0 * dpx * m0 + ju2 * dpx * m2) + gv * (jv1 * dpx * m1 + jv2 * dpx * m2)) *
-                      inv_dt;
+              c6[3 * a] = dv[a] * rx;
+              c6[3 * a + 1] = dv[a] * ry;
+              c6[3 * a + 2] = dv[a];
             }
+            c6[9] = v0;
+            c6[10] = v1;
+            c6[11] = v2;
           }
         }
       }
     }
     if (kGrouped && dbin && own_px) dbin[((size_t)w * B + i) * HW + gq] = ddi;
     if (pose_part) {
-      // six warp sums by transposition: each halving step trades half of the
-      // remaining components with the partner lane (9 double shuffles, not 30);
-      // lane 4c ends up holding component c (fixed order: deterministic)
-      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-      double a4[4];
+      // sixteen warp sums by transposition: each halving step trades half of
+      // the remaining components with the partner lane (15 double shuffles, not
+      // 60); lane 2c ends up holding component c (fixed order: deterministic)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double mine = h16 ? (k < 2 ? c6[4 + k] : 0.0) : c6[k];
-        const double other = h16 ? c6[k] : (k < 2 ? c6[4 + k] : 0.0);
-        a4[k] = mine + __shfl_xor_sync(kFull, other, 16);
-      }
-      double a2[2];
+      for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
+        const bool up = lane & off;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const double mine = h8 ? a4[2 + k] : a4[k];
-        const double other = h8 ? a4[k] : a4[2 + k];
-        a2[k] = mine + __shfl_xor_sync(kFull, other, 8);
+        for (int k = 0; k < h; ++k) {
+          const double mine = up ? c6[h + k] : c6[k], other = up ? c6[k] : c6[h + k];
+          c6[k] = mine + __shfl_xor_sync(kFull, other, off);
+        }
       }
-      double v = (h4 ? a2[1] : a2[0]) + __shfl_xor_sync(kFull, h4 ? a2[0] : a2[1], 4);
-      v += __shfl_xor_sync(kFull, v, 2);
-      v += __shfl_xor_sync(kFull, v, 1);
-      const int comp = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
-      if ((lane & 3) == 0 && comp < 6) s_pose[i & 1][cw][comp] = v;
+      const double v = c6[0] + __shfl_xor_sync(kFull, c6[0], 1);
+      const int comp = ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) +
+                       ((lane & 2) ? 1 : 0);
+      if ((lane & 1) == 0 && comp < kPoseSums) s_pose[i & 1][cw][comp] = v;
     }
     consumer_sync(kCons);  // also: the zeroed tile is ready for bin i + 2
-    if (pose_part && ct < 6) {
+    if (pose_part && ct < kPoseSums) {
       double sum = 0.0;
       for (int m = 0; m < kWarps; ++m) sum += s_pose[i & 1][m][ct];
-      pose_part[(((size_t)w * TP.oT + T) * B + i) * 6 + ct] = sum;
+      pose_part[(((size_t)w * TP.oT + T) * B + i) * kPoseSums + ct] = sum;
     }
     ++done;
   }

@@ -651,6 +651,35 @@ __global__ void k_pose_finalize(const double* __restrict__ pose_part, int n_part
   if (lane == 0) d_poses[o] = v;
 }
 
+// Owner backward pose gradients: one block per (window, bin); warp c sums moment
+// c over the parts (lane-strided + shuffle tree, fixed order), then
+// d_omega_a = sum_ij dR_a[i][j] N[i][j] and d_t = v (see k_bwd_cells).
+__global__ void k_pose_contract(const double* __restrict__ pose_part, int n_parts, int B,
+                                const double* __restrict__ pose_tab, double* __restrict__ d_poses) {
+  __shared__ double s[kPoseSums];
+  const int wb = blockIdx.x, w = wb / B, i = wb % B;
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  if (c < kPoseSums) {
+    double v = 0.0;
+    for (int p = lane; p < n_parts; p += 32) v += pose_part[(((size_t)w * n_parts + p) * B + i) * kPoseSums + c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s[c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int a = threadIdx.x;
+    double r;
+    if (a < 3) {
+      const double* dR = pose_tab + (size_t)wb * kPoseTab + 9 + 9 * a;
+      r = 0.0;
+      for (int k = 0; k < 9; ++k) r += dR[k] * s[k];
+    } else {
+      r = s[9 + a - 3];
+    }
+    d_poses[(size_t)wb * 6 + a] = r;
+  }
+}
+
 // --------------------------------------------------------------------------
 // products / format conversion
 
@@ -773,6 +802,12 @@ void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned
   k_loss_finalize<<<P.n_windows, 32 * std::min(P.B + 1, 32), 0, s>>>(part_acc, part_act, n_parts,
                                                                      P, loss, no_surv, n_active,
                                                                      scale);
+}
+
+void launch_pose_contract(cudaStream_t s, const double* pose_part, int n_parts, int B, int n_windows,
+                          const double* pose_tab, double* d_poses) {
+  ++g_launches;
+  k_pose_contract<<<n_windows * B, 32 * kPoseSums, 0, s>>>(pose_part, n_parts, B, pose_tab, d_poses);
 }
 
 void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,

@@ -20,6 +20,11 @@ void count_launch();
 void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned long long* part_act,
                           int n_parts, const WinParams& P, double* loss, int* no_surv,
                           long long* n_active, double* scale);
+// owner backward: per-part pose moments (kPoseSums per (window, bin)) summed in
+// part order, then contracted with the pose table's dR into d_poses [w][B][6]
+constexpr int kPoseSums = 12;
+void launch_pose_contract(cudaStream_t s, const double* pose_part, int n_parts, int B, int n_windows,
+                          const double* pose_tab, double* d_poses);
 void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
                           int n_windows, double* d_poses);
 int launch_count();

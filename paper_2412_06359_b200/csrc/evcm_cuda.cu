@@ -538,7 +538,8 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
                    e->get<double2>("coef", 1), e->get<double>("scale", 1), e->get<int>("no_surv", 1),
                    bwd, gmax);
   e->mark(7);
-  double* pose_part = depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * 6) : nullptr;
+  double* pose_part =
+      depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * kPoseSums) : nullptr;
   const int bgroups = owner_groups(TP, P, true);
   launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
@@ -547,7 +548,7 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
                    K, depth ? d_depth : nullptr, pose_part, grad_out, bgroups,
                    bgroups > 1 && depth ? e->get<double>("dbin", (size_t)nw * P.B * P.HW) : nullptr);
   e->mark(8);
-  if (depth) launch_pose_finalize(e->stream, pose_part, TP.oT, P.B, nw, d_poses);
+  if (depth) launch_pose_contract(e->stream, pose_part, TP.oT, P.B, nw, pose_tab, d_poses);
   e->mark(9);
 }
 
