@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
                                                         double* __restrict__ d_depth,
                                                         double* __restrict__ pose_part) {
   __shared__ double s_pose[kMaxBins * kPoseTab];
-  __shared__ double s_red[kPxBlock / 32][kMaxBins][6];
+  __shared__ double s_red[kPxBlock / 32][kMaxBins][kPoseSums];
   const int w = blockIdx.y;
   const int B = P.B, HW = P.HW;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -585,7 +585,9 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
   const G2* gw = grad + (size_t)w * B * HW;
   for (int b = 0; b < B; ++b) {
     const double* pt = s_pose + b * kPoseTab;
-    double c6[6] = {0, 0, 0, 0, 0, 0};
+    double c6[16];  // pose moments (k_bwd_cells): N = sum d v r^T (0..8), v (9..11)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c6[k] = 0.0;
 #pragma unroll
     for (int m = 0; m < kK5Px; ++m) {
       const int q = q0 + m * blockDim.x;
@@ -604,24 +606,33 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
       const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
       const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
       dd[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-      c6[3] += gu * ju0 * inv_dt;
-      c6[4] += gv * jv1 * inv_dt;
-      c6[5] += (gu * ju2 + gv * jv2) * inv_dt;
+      const double v0 = gu * ju0 * inv_dt, v1 = gv * jv1 * inv_dt;
+      const double v2 = (gu * ju2 + gv * jv2) * inv_dt;
+      const double dv[3] = {d * v0, d * v1, d * v2};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        const double* dR = pt + 9 + 9 * a;
-        const double m0 = dR[0] * rx[m] + dR[1] * ry[m] + dR[2];
-        const double m1 = dR[3] * rx[m] + dR[4] * ry[m] + dR[5];
-        const double m2 = dR[6] * rx[m] + dR[7] * ry[m] + dR[8];
-        c6[a] += (gu * (ju0 * d * m0 + ju2 * d * m2) + gv * (jv1 * d * m1 + jv2 * d * m2)) * inv_dt;
+        c6[3 * a] += dv[a] * rx[m];
+        c6[3 * a + 1] += dv[a] * ry[m];
+        c6[3 * a + 2] += dv[a];
+      }
+      c6[9] += v0;
+      c6[10] += v1;
+      c6[11] += v2;
+    }
+    // transposed warp sums (fixed order), lane 2c holds moment c
+#pragma unroll
+    for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
+      const bool up = lane & off;
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const double mine = up ? c6[h + k] : c6[k], other = up ? c6[k] : c6[h + k];
+        c6[k] = mine + __shfl_xor_sync(0xffffffffu, other, off);
       }
     }
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      double v = c6[a];
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s_red[wid][b][a] = v;
-    }
+    const double v = c6[0] + __shfl_xor_sync(0xffffffffu, c6[0], 1);
+    const int comp = ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) +
+                     ((lane & 2) ? 1 : 0);
+    if ((lane & 1) == 0 && comp < kPoseSums) s_red[wid][b][comp] = v;
   }
 #pragma unroll
   for (int m = 0; m < kK5Px; ++m) {
@@ -629,11 +640,11 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
     if (q < HW) d_depth[(size_t)w * HW + q] = dd[m];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < B * 6; i += blockDim.x) {
-    const int b = i / 6, a = i % 6;
+  for (int i = threadIdx.x; i < B * kPoseSums; i += blockDim.x) {
+    const int b = i / kPoseSums, a = i % kPoseSums;
     double v = 0.0;
     for (int q = 0; q < kPxBlock / 32; ++q) v += s_red[q][b][a];  // warp order
-    pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * 6 + a] = v;
+    pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * kPoseSums + a] = v;
   }
 }
 
@@ -854,9 +865,7 @@ void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,
   ++g_launches;
   k_flows_bwd<G2><<<dim3(parts, P.n_windows), kPxBlock, 0, s>>>(
       depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
-  const int total = P.n_windows * P.B * 6;
-  ++g_launches;
-  k_pose_finalize<<<(total + 3) / 4, 128, 0, s>>>(pose_part, parts, P.B, P.n_windows, d_poses);
+  launch_pose_contract(s, pose_part, parts, P.B, P.n_windows, pose_tab, d_poses);
 }
 
 template <typename S2>

@@ -874,7 +874,7 @@ int evcm_cuda_depth_pose_to_flows_backward(evcm_cuda_engine* e, int W, int H, co
     double2* g2 = e->get<double2>("grad_in", (size_t)B * P.HW);
     launch_interleave_flows(e->stream, gp, B, P.HW, g2);
     double* ddo = e->get<double>("d_depth", (size_t)P.HW);
-    double* pp = e->get<double>("pose_part", (size_t)flows_bwd_parts(P) * B * 6);
+    double* pp = e->get<double>("pose_part", (size_t)flows_bwd_parts(P) * B * kPoseSums);
     double* dpo = e->get<double>("d_poses", (size_t)B * 6);
     launch_flows_bwd<double2>(e->stream, dd, md, tab_d, P, K, g2, ddo, pp, dpo);
     from_device(e, d_depth, ddo, (size_t)P.HW * sizeof(double), mem);
@@ -965,7 +965,7 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
       run_backward_owner(e, P, flows, depth, nullptr, tab, bt->K, ddo, dpo, nullptr);
     } else {
       void* g = run_backward(e, P, max_n, flows);
-      double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * 6);
+      double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * kPoseSums);
       if (e->opt.grad_f64)
         launch_flows_bwd<double2>(e->stream, depth, nullptr, tab, P, bt->K, static_cast<double2*>(g), ddo, pp, dpo);
       else
