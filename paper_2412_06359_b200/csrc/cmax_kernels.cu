@@ -546,9 +546,9 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd(const uint2* __restrict__ pack
 // the 6 pose partials of a bin stay in registers and are reduced once per warp
 // per bin; d_depth accumulates over bins in registers (bin order, as the
 // reference's outer loop, geometry.hpp:293-323).
-constexpr int kK5Px = 2;
+constexpr int kK5Px = 2;  // pixels per thread (1 when that leaves SMs idle)
 
-template <typename G2>
+template <typename G2, int kPx>
 __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict__ depth,
                                                         const uint8_t* __restrict__ mask,
                                                         const double* __restrict__ pose_tab,
@@ -565,11 +565,11 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
   for (int i = threadIdx.x; i < B * kPoseTab; i += blockDim.x)
     s_pose[i] = pose_tab[(size_t)w * B * kPoseTab + i];
   __syncthreads();
-  const int q0 = blockIdx.x * blockDim.x * kK5Px + threadIdx.x;
-  double dd[kK5Px], dep[kK5Px], rx[kK5Px], ry[kK5Px];
-  bool ok[kK5Px];
+  const int q0 = blockIdx.x * blockDim.x * kPx + threadIdx.x;
+  double dd[kPx], dep[kPx], rx[kPx], ry[kPx];
+  bool ok[kPx];
 #pragma unroll
-  for (int m = 0; m < kK5Px; ++m) {
+  for (int m = 0; m < kPx; ++m) {
     const int q = q0 + m * blockDim.x;
     dd[m] = 0.0;
     ok[m] = false;
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
 #pragma unroll
     for (int k = 0; k < 16; ++k) c6[k] = 0.0;
 #pragma unroll
-    for (int m = 0; m < kK5Px; ++m) {
+    for (int m = 0; m < kPx; ++m) {
       const int q = q0 + m * blockDim.x;
       if (!ok[m]) continue;
       const auto gg = gw[(size_t)b * HW + q];
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
     if ((lane & 1) == 0 && comp < kPoseSums) s_red[wid][b][comp] = v;
   }
 #pragma unroll
-  for (int m = 0; m < kK5Px; ++m) {
+  for (int m = 0; m < kPx; ++m) {
     const int q = q0 + m * blockDim.x;
     if (q < HW) d_depth[(size_t)w * HW + q] = dd[m];
   }
@@ -855,16 +855,27 @@ void launch_bwd(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, con
       packed, ev_off, P, flows, coef, scale, no_surv, grad);
 }
 
-int flows_bwd_parts(const WinParams& P) { return (P.HW + kPxBlock * kK5Px - 1) / (kPxBlock * kK5Px); }
+// parts at kK5Px pixels per thread, or at one when that fills fewer than two
+// blocks per SM; flows_bwd_parts is the allocation bound (the larger count)
+static int flows_bwd_px(const WinParams& P) {
+  const int parts2 = (P.HW + kPxBlock * kK5Px - 1) / (kPxBlock * kK5Px);
+  return (long)parts2 * P.n_windows < 2L * 148 ? 1 : kK5Px;
+}
+int flows_bwd_parts(const WinParams& P) { return (P.HW + kPxBlock - 1) / kPxBlock; }
 
 template <typename G2>
 void launch_flows_bwd(cudaStream_t s, const double* depth, const uint8_t* mask,
                       const double* pose_tab, const WinParams& P, const double* K, const G2* grad,
                       double* d_depth, double* pose_part, double* d_poses) {
-  const int parts = flows_bwd_parts(P);
+  const int px = flows_bwd_px(P);
+  const int parts = (P.HW + kPxBlock * px - 1) / (kPxBlock * px);
   ++g_launches;
-  k_flows_bwd<G2><<<dim3(parts, P.n_windows), kPxBlock, 0, s>>>(
-      depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
+  if (px == 1)
+    k_flows_bwd<G2, 1><<<dim3(parts, P.n_windows), kPxBlock, 0, s>>>(
+        depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
+  else
+    k_flows_bwd<G2, kK5Px><<<dim3(parts, P.n_windows), kPxBlock, 0, s>>>(
+        depth, mask, pose_tab, P, K[0], K[1], K[2], K[3], grad, d_depth, pose_part);
   launch_pose_contract(s, pose_part, parts, P.B, P.n_windows, pose_tab, d_poses);
 }
 
