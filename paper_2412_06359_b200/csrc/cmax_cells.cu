@@ -1049,16 +1049,18 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           const double p0 = dpx * rr0 + ptab[36], p1 = dpx * rr1 + ptab[37], p2 = dpx * rr2 + ptab[38];
           if (p2 > 0.0) {
             const double inv_dt = ptab[39], iz = __drcp_rn(p2);  // == 1.0 / p2 (correctly rounded)
-            const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-            const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-            // explicit roundings: k_depth_bins re-forms this sum from the stored terms
-            ddi = __dmul_rn(gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2), inv_dt);
+            // reproject_with_grads (geometry.hpp:185-209) folded into the adjoint:
+            // v = (gu du/dX, gv dv/dY, gu du/dZ + gv dv/dZ) / dt with du/dX = fx/Z,
+            // du/dZ = -fx X/Z^2 (dv alike) -- the translation gradient; d_depth adds
+            // v . (R r^) and d_omega_a = d v . (dR_a r^), r^ = (rx, ry, 1), summed as
+            // the moments N = sum d v r^T, contracted with dR_a once per (window,
+            // bin) (k_pose_contract)
+            const double sc = iz * inv_dt;
+            const double v0 = gu * fx * sc, v1 = gv * fy * sc;
+            const double v2 = -(v0 * p0 + v1 * p1) * iz;
+            // the add is explicitly rounded: k_depth_bins re-forms this sum from the stored terms
+            ddi = v0 * rr0 + v1 * rr1 + v2 * rr2;
             dd = __dadd_rn(dd, ddi);
-            // d_t = v = (gu ju0, gv jv1, gu ju2 + gv jv2) / dt, and d_omega_a =
-            // d v . (dR_a r^), r^ = (rx, ry, 1): summed as the moments N = sum d v r^T,
-            // contracted with dR_a once per (window, bin) (k_pose_contract)
-            const double v0 = gu * ju0 * inv_dt, v1 = gv * jv1 * inv_dt;
-            const double v2 = (gu * ju2 + gv * jv2) * inv_dt;
             const double dv[3] = {dpx * v0, dpx * v1, dpx * v2};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
