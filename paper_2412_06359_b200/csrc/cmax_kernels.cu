@@ -603,11 +603,11 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
       if (!(p2 > 0.0)) continue;
       const double inv_dt = pt[39];
       const double iz = __drcp_rn(p2);  // == 1.0 / p2 (correctly rounded)
-      const double ju0 = fx * iz, ju2 = -fx * p0 * iz * iz;
-      const double jv1 = fy * iz, jv2 = -fy * p1 * iz * iz;
-      dd[m] += (gu * (ju0 * rr0 + ju2 * rr2) + gv * (jv1 * rr1 + jv2 * rr2)) * inv_dt;
-      const double v0 = gu * ju0 * inv_dt, v1 = gv * jv1 * inv_dt;
-      const double v2 = (gu * ju2 + gv * jv2) * inv_dt;
+      // the Jacobian folded into the adjoint, as in k_bwd_cells: v = d_t of this pixel
+      const double sc = iz * inv_dt;
+      const double v0 = gu * fx * sc, v1 = gv * fy * sc;
+      const double v2 = -(v0 * p0 + v1 * p1) * iz;
+      dd[m] += v0 * rr0 + v1 * rr1 + v2 * rr2;
       const double dv[3] = {d * v0, d * v1, d * v2};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
