@@ -280,6 +280,16 @@ __device__ __forceinline__ void fx_add(uint32_t a_lo, uint32_t a_hi, unsigned lo
       "r"(a_hi), "l"(q)
       : "memory");
 }
+// round-to-nearest-even integer conversions by the 2^52 "magic number": adding
+// 2^52 (1.5 * 2^52) to x leaves round(x) in the low mantissa bits -- one DADD and
+// an integer subtract instead of the F2I.64 conversion (a quarter-rate pipe).
+// Identical to __double2ull_rn / __double2ll_rn on the stated ranges.
+__device__ __forceinline__ unsigned long long fx_q(double x) {  // 0 <= x < 2^52
+  return (unsigned long long)__double_as_longlong(__dadd_rn(x, 0x1.0p52)) - 0x4330000000000000ull;
+}
+__device__ __forceinline__ unsigned long long fx_qs(double x) {  // |x| < 2^51, two's complement
+  return (unsigned long long)__double_as_longlong(__dadd_rn(x, 0x1.8p52)) - 0x4338000000000000ull;
+}
 // bits needed to count t: fixed-point sums of t terms bounded by 2^k need k + bits
 __device__ __forceinline__ int bits_for(uint32_t t) { return 32 - __clz(t); }
 
@@ -566,10 +576,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
             if (in && wqq > 0.0) {
               const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
               const uint32_t a = pa + 4u * (uint32_t)o;
-              const unsigned long long qc = __double2ull_rn(wqq);
+              const unsigned long long qc = fx_q(wqq);  // wqq <= 2^50
               if (qc == 0ull) flag[o] = 1u;  // w > 0 below the fixed-point resolution
               fx_add(a, a + 4 * kPlane, qc);
-              fx_add(a + 8 * kPlane, a + 12 * kPlane, __double2ull_rn(wqq * tb));
+              fx_add(a + 8 * kPlane, a + 12 * kPlane, fx_q(wqq * tb));
             }
           }
         });
@@ -997,8 +1007,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             if (in && wqq != 0.0) {
               const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
               const uint32_t a = pt + 4u * (uint32_t)o;
-              fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn(wqq * gx));
-              fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn(wqq * gy));
+              fx_add(a, a + 4 * kPlane, fx_qs(wqq * gx));
+              fx_add(a + 8 * kPlane, a + 12 * kPlane, fx_qs(wqq * gy));
             }
           }
         });
@@ -1013,8 +1023,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         const float2 g = s8[v];
         if (g.x == 0.f && g.y == 0.f) continue;
         const uint32_t a = pt + 4u * (uint32_t)(ly * kRowW + lx);
-        fx_add(a, a + 4 * kPlane, (unsigned long long)__double2ll_rn((double)g.x * gsc));
-        fx_add(a + 8 * kPlane, a + 12 * kPlane, (unsigned long long)__double2ll_rn((double)g.y * gsc));
+        fx_add(a, a + 4 * kPlane, fx_qs((double)g.x * gsc));
+        fx_add(a + 8 * kPlane, a + 12 * kPlane, fx_qs((double)g.y * gsc));
       }
     }
     __syncwarp();
