@@ -232,19 +232,49 @@ __global__ void __launch_bounds__(NW * 32) k_sort_scatter(
   const uint64_t n = ev_off[w + 1] - base;
   const uint64_t k0 = (uint64_t)blockIdx.x * TP.chunk + (uint64_t)wid * per;
   uint16_t* mine = whist + wid * TP.nT;
-  for (int b = 0; b < per; b += 32) {  // pass 1: per-warp counts
-    const uint64_t k = k0 + b + lane;
-    int t = -1;
-    if (k < n) {
-      const uint32_t key = keys[base + k];
-      if (key != kDead) t = (int)key;
+  // pass 1: per-warp counts. Many-tile chunks (NW = 4, e.g. 640x480) pipeline
+  // the key loads by hand (see pass 3); the 8-warp form measured faster as is.
+  if constexpr (NW <= 4) {
+    int tn = -1;  // the next step's key in flight
+    {
+      const uint64_t k = k0 + lane;
+      if (per > 0 && k < n) {
+        const uint32_t key = keys[base + k];
+        if (key != kDead) tn = (int)key;
+      }
     }
-    const unsigned act = __ballot_sync(kFull, t >= 0);
-    if (t >= 0) {
-      const unsigned peers = __match_any_sync(act, t);
-      if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+    for (int b = 0; b < per; b += 32) {
+      const int t = tn;
+      tn = -1;
+      {
+        const uint64_t k = k0 + b + 32 + lane;
+        if (b + 32 < per && k < n) {
+          const uint32_t key = keys[base + k];
+          if (key != kDead) tn = (int)key;
+        }
+      }
+      const unsigned act = __ballot_sync(kFull, t >= 0);
+      if (t >= 0) {
+        const unsigned peers = __match_any_sync(act, t);
+        if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+      }
+      __syncwarp();
     }
-    __syncwarp();
+  } else {
+    for (int b = 0; b < per; b += 32) {  // pass 1: per-warp counts
+      const uint64_t k = k0 + b + lane;
+      int t = -1;
+      if (k < n) {
+        const uint32_t key = keys[base + k];
+        if (key != kDead) t = (int)key;
+      }
+      const unsigned act = __ballot_sync(kFull, t >= 0);
+      if (t >= 0) {
+        const unsigned peers = __match_any_sync(act, t);
+        if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+      }
+      __syncwarp();
+    }
   }
   __syncthreads();
   const uint32_t* off = offsets + ((size_t)w * TP.nchunks + blockIdx.x) * TP.nT;
@@ -258,25 +288,67 @@ __global__ void __launch_bounds__(NW * 32) k_sort_scatter(
     }
   }
   __syncthreads();
-  for (int b = 0; b < per; b += 32) {  // pass 3: place in order
-    const uint64_t k = k0 + b + lane;
-    int t = -1;
-    if (k < n) {
+  if constexpr (NW <= 4) {
+    // pass 3: place in order. Software-pipelined by hand (the warp syncs keep the
+    // compiler from hoisting loads): the key of step i + 2 and the event and tile
+    // base (tile_ptr + chunk offset) of step i + 1 are in flight while step i places.
+    auto key_at = [&](int b) -> int {
+      const uint64_t k = k0 + b + lane;
+      if (b >= per || k >= n) return -1;
       const uint32_t key = keys[base + k];
-      if (key != kDead) t = (int)key;
+      return key != kDead ? (int)key : -1;
+    };
+    auto ev_at = [&](int b) -> uint2 {
+      const uint64_t k = k0 + b + lane;
+      return (b < per && k < n) ? packed[base + k] : make_uint2(0u, 0u);
+    };
+    auto base_of = [&](int t) -> uint32_t { return t >= 0 ? tp[t] + off[t] : 0u; };
+    int t1 = key_at(0), t2 = key_at(32);
+    uint32_t g1 = base_of(t1);
+    uint2 e1 = ev_at(0);
+    for (int b = 0; b < per; b += 32) {
+      const int t = t1;
+      const uint32_t gb = g1;
+      const uint2 ev = e1;
+      t1 = t2;
+      g1 = base_of(t2);
+      e1 = ev_at(b + 32);
+      t2 = key_at(b + 64);
+      const uint64_t k = k0 + b + lane;
+      const unsigned act = __ballot_sync(kFull, t >= 0);
+      if (t >= 0) {
+        const unsigned peers = __match_any_sync(act, t);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        const uint32_t dst = gb + mine[t] + rank;
+        sorted[base + dst] = ev;
+        sorted_keys[base + dst] = (uint32_t)t;
+        if (perm) perm[base + dst] = (uint32_t)k;
+        __syncwarp(peers);
+        if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+      }
+      __syncwarp();
     }
-    const unsigned act = __ballot_sync(kFull, t >= 0);
-    if (t >= 0) {
-      const unsigned peers = __match_any_sync(act, t);
-      const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-      const uint32_t dst = tp[t] + off[t] + mine[t] + rank;
-      sorted[base + dst] = packed[base + k];
-      sorted_keys[base + dst] = (uint32_t)t;
-      if (perm) perm[base + dst] = (uint32_t)k;
-      __syncwarp(peers);
-      if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+  } else {
+    for (int b = 0; b < per; b += 32) {  // pass 3: place in order
+      const uint64_t k = k0 + b + lane;
+      int t = -1;
+      if (k < n) {
+        const uint32_t key = keys[base + k];
+        if (key != kDead) t = (int)key;
+      }
+      const unsigned act = __ballot_sync(kFull, t >= 0);
+      if (t >= 0) {
+        const unsigned peers = __match_any_sync(act, t);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        const uint32_t dst = tp[t] + off[t] + mine[t] + rank;
+        sorted[base + dst] = packed[base + k];
+        sorted_keys[base + dst] = (uint32_t)t;
+        if (perm) perm[base + dst] = (uint32_t)k;
+        __syncwarp(peers);
+        if (lane == __ffs(peers) - 1) mine[t] = (uint16_t)(mine[t] + __popc(peers));
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
