@@ -187,3 +187,19 @@ def test_chain_bin_extremes_and_ragged_batch(engine_det, B):
         assert rel_inf(dd[w], ref[w][1]) <= 1e-5
         assert rel_inf(dp[w], ref[w][2]) <= 1e-5
     assert loss[1] == 0.0 and not np.any(dd[1]) and not np.any(dp[1])  # empty window
+
+
+def test_chain_batch_many_tiles():
+    """640 x 480 (4800 sort tiles > 2048): the counting sort takes its 4-warp,
+    hand-pipelined scatter; parity against the oracle composition, and the
+    owner pipeline is bit-stable run to run."""
+    eng = P.Engine(P.EngineOptions(algo="owner"))
+    depth, poses, K, ev, offs = chain_inputs(640, 480, 10, 2, 150000, seed=21)
+    loss, dd, dp = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    ref = _oracle_chain(depth, poses, K, ev, offs)
+    for w in range(2):
+        assert abs(loss[w] - ref[w][0]) <= 1e-5 * abs(ref[w][0])
+        assert rel_inf(dd[w], ref[w][1]) <= 1e-5, rel_inf(dd[w], ref[w][1])
+        assert rel_inf(dp[w], ref[w][2]) <= 1e-5, rel_inf(dp[w], ref[w][2])
+    l2, dd2, dp2 = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    assert np.array_equal(l2, loss) and np.array_equal(dd2, dd) and np.array_equal(dp2, dp)
