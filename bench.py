@@ -140,7 +140,7 @@ def algorithmic_bytes(wl, n_windows, algo="owner"):
 # evcm_cuda_stage_times order per pipeline (include/evcm_cuda.h)
 STAGES_BY_ALGO = {
     "owner": ["staging", "motion_field", "sort", "traj_records", "fwd_owner", "loss_finalize",
-              "bwd_event", "bwd_owner", "pose_finalize"],
+              "bwd_event", "bwd_owner", "pose_contract"],
     "atomic": ["staging", "motion_field", "stack_memset", "warp_splat", "loss_reduce",
                "grad_memset", "backward", "flows_backward", "unused"],
 }

@@ -648,20 +648,6 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
   }
 }
 
-// Fixed-order (lane-strided + shuffle tree) sum of the per-block pose partials;
-// one warp per (window, bin, component).
-__global__ void k_pose_finalize(const double* __restrict__ pose_part, int n_parts, int B,
-                                int n_windows, double* __restrict__ d_poses) {
-  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (o >= n_windows * B * 6) return;
-  const int w = o / (B * 6), rem = o % (B * 6);
-  double v = 0.0;
-  for (int p = lane; p < n_parts; p += 32) v += pose_part[((size_t)w * n_parts + p) * B * 6 + rem];
-  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-  if (lane == 0) d_poses[o] = v;
-}
-
 // Owner backward pose gradients: one block per (window, bin); warp c sums moment
 // c over the parts (lane-strided + shuffle tree, fixed order), then
 // d_omega_a = sum_ij dR_a[i][j] N[i][j] and d_t = v (see k_bwd_cells).
@@ -819,13 +805,6 @@ void launch_pose_contract(cudaStream_t s, const double* pose_part, int n_parts, 
                           const double* pose_tab, double* d_poses) {
   ++g_launches;
   k_pose_contract<<<n_windows * B, 32 * kPoseSums, 0, s>>>(pose_part, n_parts, B, pose_tab, d_poses);
-}
-
-void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
-                          int n_windows, double* d_poses) {
-  const int total = n_windows * B * 6;
-  ++g_launches;
-  k_pose_finalize<<<(total + 3) / 4, 128, 0, s>>>(pose_part, n_parts, B, n_windows, d_poses);
 }
 
 int loss_parts(const WinParams& P) { return std::max(1, std::min((P.HW + kPxBlock - 1) / kPxBlock, 64)); }

@@ -25,8 +25,6 @@ void launch_loss_finalize(cudaStream_t s, const double* part_acc, const unsigned
 constexpr int kPoseSums = 12;
 void launch_pose_contract(cudaStream_t s, const double* pose_part, int n_parts, int B, int n_windows,
                           const double* pose_tab, double* d_poses);
-void launch_pose_finalize(cudaStream_t s, const double* pose_part, int n_parts, int B,
-                          int n_windows, double* d_poses);
 int launch_count();
 
 size_t ev_smem_bytes(const WinParams& P);
