@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     if (pose_part && ct < kPoseSums) {
       double sum = 0.0;
       for (int m = 0; m < kWarps; ++m) sum += s_pose[i & 1][m][ct];
-      pose_part[(((size_t)w * TP.oT + T) * B + i) * kPoseSums + ct] = sum;
+      pose_part[(((size_t)w * B + i) * kPoseSums + ct) * TP.oT + T] = sum;  // [w][bin][moment][part]
     }
     ++done;
   }

@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
     const int b = i / kPoseSums, a = i % kPoseSums;
     double v = 0.0;
     for (int q = 0; q < kPxBlock / 32; ++q) v += s_red[q][b][a];  // warp order
-    pose_part[(((size_t)w * gridDim.x + blockIdx.x) * B + b) * kPoseSums + a] = v;
+    pose_part[(((size_t)w * B + b) * kPoseSums + a) * gridDim.x + blockIdx.x] = v;  // [w][bin][moment][part]
   }
 }
 
@@ -654,11 +654,12 @@ __global__ void __launch_bounds__(kPxBlock) k_flows_bwd(const double* __restrict
 __global__ void k_pose_contract(const double* __restrict__ pose_part, int n_parts, int B,
                                 const double* __restrict__ pose_tab, double* __restrict__ d_poses) {
   __shared__ double s[kPoseSums];
-  const int wb = blockIdx.x, w = wb / B, i = wb % B;
+  const int wb = blockIdx.x;  // window * B + bin
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
   if (c < kPoseSums) {
     double v = 0.0;
-    for (int p = lane; p < n_parts; p += 32) v += pose_part[(((size_t)w * n_parts + p) * B + i) * kPoseSums + c];
+    const double* src = pose_part + ((size_t)wb * kPoseSums + c) * n_parts;  // contiguous parts
+    for (int p = lane; p < n_parts; p += 32) v += src[p];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) s[c] = v;
   }
