@@ -53,7 +53,7 @@ extern "C" {
 #define EVCM_API
 #endif
 
-#define EVCM_CUDA_ABI_VERSION 1
+#define EVCM_CUDA_ABI_VERSION 2
 #define EVCM_CUDA_MAX_BINS 32
 
 /* Status codes; the C++ adapter maps them onto the evcm::Error subclasses. */
@@ -84,22 +84,24 @@ typedef struct {
 
 /* EngineOptions (engine.hpp:54-61) for the cuda backend. Fields the cuda
  * backend does not need (n_workers, batch_size, padding_fraction) have no
- * counterpart; `deterministic` keeps its meaning (run-to-run bit-stable
- * gradients, engine.hpp:60). */
+ * counterpart; `deterministic` keeps its meaning and its default (1:
+ * run-to-run bit-stable results, engine.hpp:60). */
 typedef struct {
   int device;          /* CUDA device ordinal */
-  int deterministic;   /* 1: fixed-order accumulation, bit-stable run to run */
+  int deterministic;   /* 1 (default, as engine.hpp:60): the owner-computes pipeline, exact
+                          fixed-point accumulation, bit-stable run to run; 0 allows algo 1 */
   int stack_f64;       /* 1 (default, parity): fp64 IWE stack + loss coefficients;
                           0: fp32 ("fast": loss/IWE within 1e-6, gradients NOT within
                           1e-5 on sparse windows — see DESIGN.md "Numerics") */
   int grad_f64;        /* 1: fp64 flow-gradient accumulators (default 0: fp32, which
                           keeps gradients within ~1e-7 of the reference) */
   void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
-  int algo;            /* 0: owner-computes tiles (no global atomics; the only path with
-                          deterministic = 1); 1: per-event global atomics (honours
-                          stack_f64 / grad_f64); 2 (default): auto — owner when
-                          deterministic, or when the call carries >= 1 event per pixel
-                          per window and >= 2.5e5 events in total (measured crossover) */
+  int algo;            /* 0: owner-computes tiles (no global atomics; the product path);
+                          1: per-event global atomics, an independent cross-check kept
+                          for tests (needs deterministic = 0; honours stack_f64 /
+                          grad_f64); 2 (default): auto -- the owner pipeline when
+                          deterministic, else owner from >= 1 event per pixel per window
+                          and >= 2.5e5 events per call (measured crossover) */
 } evcm_cuda_options;
 
 /* EventSlice (types.hpp:121-126). */
@@ -112,17 +114,23 @@ typedef struct {
   size_t n_events;
 } evcm_slice;
 
-/* FlowSequence (types.hpp:251-253): B+1 edges and B fields. */
+/* FlowSequence (types.hpp:251-253): B+1 edges and B fields of width x height
+ * (FlowSequence::width()/height(); a size that differs from the slice's sensor
+ * raises DimensionMismatchError, engine.hpp:218-219). */
 typedef struct {
   int n_bins;
   const uint64_t* edges_us; /* host pointer, B+1 entries */
-  const double* uv;         /* [B][2][H][W] */
+  const double* uv;         /* [B][2][height][width], contiguous f64 */
+  int width, height;
 } evcm_flows;
 
-/* LossResult (warp.hpp:292-295). */
+/* LossResult (warp.hpp:292-295) + the id of the forward that produced it:
+ * evcm_cuda_backward_of checks it, so a backward never pairs with the device
+ * state of a different (later) forward. */
 typedef struct {
   double value;
   int no_survivors;
+  uint64_t forward_id;
 } evcm_loss;
 
 typedef struct evcm_cuda_engine evcm_cuda_engine;
@@ -152,10 +160,26 @@ EVCM_API int evcm_cuda_forward_products(evcm_cuda_engine* e, double* count, doub
                                int64_t* n_active, uint8_t* alive, int32_t* bin, double* pos,
                                size_t* n_alive);
 
-/* Engine::backward for the window of the last forward (same slice/flows).
+/* The tile sort of the last forward (owner pipeline; the reference's
+ * determinism analog, engine.hpp:584-598): keys[n] the 8x8 sort-tile key of
+ * every event (0xffffffff: masked), perm[n_sorted] the window-local index of
+ * the event at each sorted slot, sorted_keys[n_sorted] the keys in sorted order;
+ * HOST arrays, any may be NULL. The sort is stable: perm equals a stable argsort
+ * of the valid keys. */
+EVCM_API int evcm_cuda_sort_products(evcm_cuda_engine* e, uint32_t* keys, uint32_t* perm,
+                                     uint32_t* sorted_keys, size_t* n_sorted);
+
+/* Engine::backward for the window of the last forward (same slice). The
+ * trajectories come from that forward (ForwardResult.traj, engine.hpp:196,
+ * 564-567) and the flow Jacobians from `flows` (engine.hpp:185-205).
  * grad: [B][2][H][W] f64, in `mem` space. */
 EVCM_API int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* slice, const evcm_flows* flows,
                        int mem, double* grad);
+/* Same, checked against the forward it belongs to: fails with EVCM_ERR_STATE
+ * unless forward_id is the id the engine's last forward returned. */
+EVCM_API int evcm_cuda_backward_of(evcm_cuda_engine* e, const evcm_slice* slice,
+                                   const evcm_flows* flows, uint64_t forward_id, int mem,
+                                   double* grad);
 
 /* Engine::loss_and_grad. */
 EVCM_API int evcm_cuda_loss_and_grad(evcm_cuda_engine* e, const evcm_slice* slice,
@@ -346,6 +370,23 @@ EVCM_API int evcm_cuda_last_launch_count(evcm_cuda_engine* e);
 /* Device memory currently held by the engine's workspaces, in bytes (the
  * PhaseStats.peak_bytes analog, memtrack.hpp:72-102). */
 EVCM_API size_t evcm_cuda_workspace_bytes(evcm_cuda_engine* e);
+/* PhaseStats (engine.hpp:63-66, 226-242) of the last evcm_cuda_forward /
+ * evcm_cuda_backward, always recorded (CUDA events on the engine stream):
+ * phases 0 warp (staging + sort + trajectories), 1 splat, 2 loss, 3 backward.
+ * time_us[4]: device time of the phase; peak_bytes[4]: device workspace held by
+ * the engine when the phase ended (the engine's buffers only grow, so this is
+ * the phase's peak). Either pointer may be NULL. */
+EVCM_API int evcm_cuda_phase_stats(evcm_cuda_engine* e, double* time_us, size_t* peak_bytes);
+
+/* ---- stream ordering ---------------------------------------------------------------- */
+
+/* Orders the engine's stream after the work already enqueued on `stream` (a
+ * cudaStream_t of the caller, e.g. the producer of device inputs): the
+ * engine's next kernels wait for it. No-op when stream is the engine's own. */
+EVCM_API int evcm_cuda_stream_wait(evcm_cuda_engine* e, void* stream);
+/* The converse: `stream` waits for the work enqueued on the engine's stream
+ * (e.g. a consumer of an asynchronous chain's outputs). */
+EVCM_API int evcm_cuda_stream_signal(evcm_cuda_engine* e, void* stream);
 
 #ifdef __cplusplus
 }

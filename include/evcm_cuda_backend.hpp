@@ -59,6 +59,10 @@ inline std::vector<double> pack_flows(const FlowSequence& f) {
   return uv;
 }
 
+inline evcm_flows c_flows(const FlowSequence& f, const std::vector<double>& uv) {
+  return evcm_flows{f.n_bins(), f.edges_us.data(), uv.data(), f.width(), f.height()};
+}
+
 inline evcm_slice c_slice(const EventSlice& s) {
   static_assert(sizeof(Event) == sizeof(evcm_event), "evcm::Event layout");
   return evcm_slice{s.width, s.height, s.t_start_us, s.t_end_us,
@@ -85,13 +89,15 @@ class Engine {
     h_.reset(h);
   }
 
-  // Engine::forward (engine.hpp:145-183): stack, trajectories and loss.
+  // Engine::forward (engine.hpp:145-183): stack, trajectories, loss and the
+  // per-phase PhaseStats (engine.hpp:154,169,179).
   ForwardResult forward(const EventSlice& slice, const FlowSequence& flows) const {
     const std::vector<double> uv = pack_flows(flows);
     const evcm_slice s = c_slice(slice);
-    const evcm_flows f{flows.n_bins(), flows.edges_us.data(), uv.data()};
+    const evcm_flows f = c_flows(flows, uv);
     evcm_loss loss{};
     check(evcm_cuda_forward(h_.get(), &s, &f, EVCM_MEM_HOST, &loss));
+    last_fwd_ = Fingerprint{loss.forward_id, loss.value, loss.no_survivors != 0};
     ForwardResult res;
     const int W = slice.width, H = slice.height, R = flows.n_bins() + 1;
     const std::size_t HW = static_cast<std::size_t>(W) * H, n = slice.events.size();
@@ -111,24 +117,39 @@ class Engine {
     res.traj.n_alive = n_alive;
     res.loss.value = loss.value;
     res.loss.no_survivors = loss.no_survivors != 0;
+    double t_us[4];
+    std::size_t bytes[4];
+    check(evcm_cuda_phase_stats(h_.get(), t_us, bytes));
+    res.warp_stats = PhaseStats{t_us[0], bytes[0]};
+    res.splat_stats = PhaseStats{t_us[1], bytes[1]};
+    res.loss_stats = PhaseStats{t_us[2], bytes[2]};
     return res;
   }
 
   // Engine::backward (engine.hpp:185-205) for the window of the last forward.
+  // The device keeps the state of the engine's LAST forward only: `fwd` must be
+  // that forward's result (matched by its loss), otherwise ConfigError.
   BackwardResult backward(const EventSlice& slice, const FlowSequence& flows,
-                          const ForwardResult&) const {
+                          const ForwardResult& fwd) const {
     const std::vector<double> uv = pack_flows(flows);
     const evcm_slice s = c_slice(slice);
-    const evcm_flows f{flows.n_bins(), flows.edges_us.data(), uv.data()};
+    const evcm_flows f = c_flows(flows, uv);
     const std::size_t HW = static_cast<std::size_t>(slice.width) * slice.height;
     std::vector<double> g(static_cast<std::size_t>(flows.n_bins()) * 2 * HW);
-    check(evcm_cuda_backward(h_.get(), &s, &f, EVCM_MEM_HOST, g.data()));
+    const bool same = std::memcmp(&fwd.loss.value, &last_fwd_.value, sizeof(double)) == 0 &&
+                      fwd.loss.no_survivors == last_fwd_.no_survivors;
+    check(evcm_cuda_backward_of(h_.get(), &s, &f, same ? last_fwd_.id : 0, EVCM_MEM_HOST,
+                                g.data()));
     BackwardResult res;
     res.grad = GradientBuffer(slice.width, slice.height, flows.n_bins());
     for (int b = 0; b < flows.n_bins(); ++b) {
       std::memcpy(&res.grad.gu[b][0], g.data() + (2 * b) * HW, HW * sizeof(double));
       std::memcpy(&res.grad.gv[b][0], g.data() + (2 * b + 1) * HW, HW * sizeof(double));
     }
+    double t_us[4];
+    std::size_t bytes[4];
+    check(evcm_cuda_phase_stats(h_.get(), t_us, bytes));
+    res.stats = PhaseStats{t_us[3], bytes[3]};
     return res;
   }
 
@@ -142,6 +163,12 @@ class Engine {
   evcm_cuda_engine* handle() const { return h_.get(); }
 
  private:
+  struct Fingerprint {
+    std::uint64_t id = 0;
+    double value = 0.0;
+    bool no_survivors = false;
+  };
+  mutable Fingerprint last_fwd_;
   struct Del {
     void operator()(evcm_cuda_engine* e) const { evcm_cuda_destroy(e); }
   };

@@ -216,7 +216,20 @@ struct evcm_cuda_engine {
     return static_cast<T*>(b.p);
   }
 
+  // PhaseStats of the last forward / backward (evcm_cuda_phase_stats)
+  double phase_us[4] = {0, 0, 0, 0};
+  size_t phase_bytes[4] = {0, 0, 0, 0};
+  size_t ws_at_mark[16] = {};
+  uint64_t fwd_id = 0;  // id of the forward whose state the engine holds (0: none)
+  uint64_t fwd_counter = 0;
+  cudaEvent_t order_ev = nullptr;  // evcm_cuda_stream_wait / signal
+  size_t ws_bytes() const {
+    size_t t = 0;
+    for (auto& kv : bufs) t += kv.second.cap;
+    return t;
+  }
   void mark(int i) {
+    if (i >= 0 && i < 16) ws_at_mark[i] = ws_bytes();
     if (!timing) return;
     while ((int)ev.size() <= i) {
       cudaEvent_t e;
@@ -294,12 +307,18 @@ void check_slice_header(const evcm_slice* s) {  // EventSlice::validate (types.h
   if (s->t_end_us < s->t_start_us) fail(EVCM_ERR_TIME_RANGE, "event slice: t_end precedes t_start");
 }
 
-void check_flows(const evcm_slice* s, const evcm_flows* f) {  // FlowSequence::validate + shape/span
+// Engine::validate_window after slice.validate() (engine.hpp:215-222): FlowSequence::validate
+// (types.hpp:268-284), then the sensor shape, then the window span.
+void check_flows(const evcm_slice* s, const evcm_flows* f) {
   if (f->n_bins < 1 || !f->edges_us)
     fail(EVCM_ERR_CONFIG, "flow sequence: need B >= 1 fields and B+1 edges");
   for (int i = 0; i < f->n_bins; ++i)
     if (f->edges_us[i] >= f->edges_us[i + 1])
       fail(EVCM_ERR_CONFIG, "flow sequence: edges must be strictly increasing");
+  if (f->width <= 0 || f->height <= 0 || !f->uv)
+    fail(EVCM_ERR_DIMENSION, "flow field: u and v must share a nonempty shape");
+  if (f->width != (int)s->width || f->height != (int)s->height)
+    fail(EVCM_ERR_DIMENSION, "engine: flow shape differs from sensor shape");
   if (f->edges_us[0] != s->t_start_us || f->edges_us[f->n_bins] != s->t_end_us)
     fail(EVCM_ERR_CONFIG, "engine: flow bin edges do not span the slice window");
   if (s->t_end_us - s->t_start_us >= (1ull << 31))
@@ -491,9 +510,12 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   const size_t nl = (size_t)nw * NS * TP.oT;
   uint32_t* lcount = e->get<uint32_t>("lcount", nl);
   // the sort's first kernel also resets the cell boxes and list counts
+  // the engine-level forward (want_stack) also keeps the sort permutation for
+  // evcm_cuda_sort_products; the batched chain does not write it
   launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
               e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
-              nullptr, e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)), bbox,
+              want_stack ? e->get<uint32_t>("perm", total) : nullptr,
+              e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)), bbox,
               (size_t)nw * NS * TP.nT, lcount, nl);
   e->mark(3);
   FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
@@ -628,7 +650,7 @@ void evcm_cuda_default_options(evcm_cuda_options* o) {
   if (!o) return;
   std::memset(o, 0, sizeof *o);
   o->device = 0;
-  o->deterministic = 0;
+  o->deterministic = 1;  // engine.hpp:60
   o->stack_f64 = 1;  // parity precision
   o->grad_f64 = 0;
   o->stream = nullptr;
@@ -644,6 +666,9 @@ int evcm_cuda_create(const evcm_cuda_options* opts, evcm_cuda_engine** out) {
     int n = 0;
     ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
     if (o.device < 0 || o.device >= n) fail(EVCM_ERR_CONFIG, "engine: no such CUDA device");
+    if (o.algo < 0 || o.algo > 2) fail(EVCM_ERR_CONFIG, "engine: unknown algo (0 owner, 1 atomic, 2 auto)");
+    if (o.algo == 1 && o.deterministic)
+      fail(EVCM_ERR_CONFIG, "deterministic mode needs algo owner or auto");
     auto* e = new evcm_cuda_engine();
     e->opt = o;
     set_device(e);
@@ -666,6 +691,7 @@ void evcm_cuda_destroy(evcm_cuda_engine* e) {
   for (auto& kv : e->pins)
     if (kv.second.p) cudaFreeHost(kv.second.p);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  if (e->order_ev) cudaEventDestroy(e->order_ev);
   for (auto& g : e->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& q : e->pending)
@@ -699,13 +725,24 @@ size_t evcm_cuda_workspace_bytes(evcm_cuda_engine* e) {
   return s;
 }
 
+// The API forward/backward always time their phases (PhaseStats, engine.hpp:226-242):
+// the stage marks are CUDA events on the engine stream, read after the call's sync.
+struct ForceTiming {
+  evcm_cuda_engine* e;
+  bool saved;
+  explicit ForceTiming(evcm_cuda_engine* x) : e(x), saved(x->timing) { e->timing = true; }
+  ~ForceTiming() { e->timing = saved; }
+};
+
 int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
                       evcm_loss* loss) {
   return guarded([&] {
     if (!e) fail(EVCM_ERR_CONFIG, "null engine");
     set_device(e);
     reset_launch_count();
+    ForceTiming ft(e);
     e->have_fwd = false;
+    e->fwd_id = 0;
     e->mark(0);
     WinParams P;
     const double2* flows = prepare_window(e, s, f, mem, &P);
@@ -716,14 +753,28 @@ int evcm_cuda_forward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows
     ck(cudaMemcpyAsync(&l, e->get<double>("loss", 1), sizeof l, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaMemcpyAsync(&ns, e->get<int>("no_surv", 1), sizeof ns, cudaMemcpyDeviceToHost, e->stream), "D2H");
     sync_and_check(e, "forward");
-    e->collect_range(0, e->owner() ? 6 : M_FWD0 + 3);
-    if (loss) {
-      loss->value = l;
-      loss->no_survivors = ns;
-    }
+    const int last = e->owner() ? 6 : M_FWD0 + 3;
+    e->collect_range(0, last);
+    // phases: warp = staging + sort + trajectory records (owner) | staging + memset
+    // (atomic, whose warp is fused into the splat kernel); splat; loss
+    const int splat = e->owner() ? 4 : M_FWD0 + 1;
+    double warp = 0;
+    for (int i = 0; i < splat; ++i) warp += e->stage_ms[i];
+    e->phase_us[0] = 1e3 * warp;
+    e->phase_us[1] = 1e3 * e->stage_ms[splat];
+    e->phase_us[2] = 1e3 * e->stage_ms[splat + 1];
+    e->phase_bytes[0] = e->ws_at_mark[splat];
+    e->phase_bytes[1] = e->ws_at_mark[splat + 1];
+    e->phase_bytes[2] = e->ws_at_mark[last];
     e->P = P;
     e->n_events = s->n_events;
     e->have_fwd = true;
+    e->fwd_id = ++e->fwd_counter;
+    if (loss) {
+      loss->value = l;
+      loss->no_survivors = ns;
+      loss->forward_id = e->fwd_id;
+    }
     e->last_launches = launch_count();
   });
 }
@@ -772,36 +823,113 @@ int evcm_cuda_forward_products(evcm_cuda_engine* e, double* count, double* tsum,
   });
 }
 
+namespace {
+void backward_impl(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
+                   double* grad, uint64_t want_id) {
+  if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+  if (!s || !f) fail(EVCM_ERR_CONFIG, "null slice or flows");
+  set_device(e);
+  reset_launch_count();
+  ForceTiming ft(e);
+  check_slice_header(s);
+  check_flows(s, f);
+  if (!e->have_fwd || e->n_events != s->n_events || e->P.W != s->width || e->P.H != s->height ||
+      e->P.B != f->n_bins || (want_id && want_id != e->fwd_id))
+    fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
+  const WinParams& P = e->P;
+  const int m0 = e->owner() ? 6 : M_FWD0 + 3;
+  e->mark(m0);
+  // the flow Jacobians come from the flows given here (engine.hpp:185-205); the
+  // trajectories from the forward (its records / packed events)
+  const double* uv = to_device(e, "flows_planar", f->uv, (size_t)f->n_bins * 2 * P.HW, mem);
+  double2* flows = e->get<double2>("flows", (size_t)f->n_bins * P.HW);
+  launch_interleave_flows(e->stream, uv, f->n_bins, P.HW, flows);
+  double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
+  if (e->owner()) {
+    run_backward_owner(e, P, flows, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
+  } else {
+    void* g = run_backward(e, P, s->n_events, flows);
+    if (e->opt.grad_f64)
+      launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
+    else
+      launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
+  }
+  from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
+  const int m1 = e->owner() ? 9 : M_FWD0 + 5;
+  e->mark(m1);
+  ck(cudaStreamSynchronize(e->stream), "backward");
+  e->collect_range(m0, m1);
+  double t = 0;
+  for (int i = m0; i < m1; ++i) t += e->stage_ms[i];
+  e->phase_us[3] = 1e3 * t;
+  e->phase_bytes[3] = e->ws_at_mark[m1];
+  ck(cudaGetLastError(), "backward kernels");
+  e->last_launches = launch_count();
+}
+}  // namespace
+
 int evcm_cuda_backward(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f, int mem,
                        double* grad) {
+  return guarded([&] { backward_impl(e, s, f, mem, grad, 0); });
+}
+
+int evcm_cuda_backward_of(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f,
+                          uint64_t forward_id, int mem, double* grad) {
+  return guarded([&] {
+    if (forward_id == 0) fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
+    backward_impl(e, s, f, mem, grad, forward_id);
+  });
+}
+
+int evcm_cuda_sort_products(evcm_cuda_engine* e, uint32_t* keys, uint32_t* perm, uint32_t* sorted_keys,
+                            size_t* n_sorted) {
+  return guarded([&] {
+    if (!e || !e->have_fwd) fail(EVCM_ERR_STATE, "engine: no forward result to read");
+    if (!e->owner()) fail(EVCM_ERR_STATE, "engine: the last forward did not sort (algo atomic)");
+    set_device(e);
+    const size_t n = e->n_events, total = e->n_total;
+    const uint32_t* kd = e->get<uint32_t>("sort_keys", 1);
+    uint32_t nv = 0;
+    from_device(e, &nv, e->get<uint32_t>("tile_ptr", 1) + e->TP.nT, sizeof nv, EVCM_MEM_HOST);
+    if (keys) from_device(e, keys, kd, n * sizeof(uint32_t), EVCM_MEM_HOST);
+    if (sorted_keys) from_device(e, sorted_keys, kd + total, n * sizeof(uint32_t), EVCM_MEM_HOST);
+    if (perm) from_device(e, perm, e->get<uint32_t>("perm", total), n * sizeof(uint32_t), EVCM_MEM_HOST);
+    ck(cudaStreamSynchronize(e->stream), "sort products");
+    if (n_sorted) *n_sorted = nv;
+  });
+}
+
+int evcm_cuda_phase_stats(evcm_cuda_engine* e, double* time_us, size_t* peak_bytes) {
   return guarded([&] {
     if (!e) fail(EVCM_ERR_CONFIG, "null engine");
-    if (!s || !f) fail(EVCM_ERR_CONFIG, "null slice or flows");
-    set_device(e);
-    reset_launch_count();
-    check_slice_header(s);
-    check_flows(s, f);
-    if (!e->have_fwd || e->n_events != s->n_events || e->P.W != s->width || e->P.H != s->height ||
-        e->P.B != f->n_bins)
-      fail(EVCM_ERR_STATE, "engine: backward needs the forward of the same window");
-    const WinParams& P = e->P;
-    e->mark(e->owner() ? 6 : M_FWD0 + 3);
-    double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
-    if (e->owner()) {
-      run_backward_owner(e, P, e->get<double2>("flows", 1), nullptr, nullptr, nullptr, nullptr,
-                         nullptr, nullptr, out);
-    } else {
-      void* g = run_backward(e, P, s->n_events, e->get<double2>("flows", 1));
-      if (e->opt.grad_f64)
-        launch_unpack_grad<double2>(e->stream, static_cast<double2*>(g), P.B, P.HW, out);
-      else
-        launch_unpack_grad<float2>(e->stream, static_cast<float2*>(g), P.B, P.HW, out);
+    for (int i = 0; i < 4; ++i) {
+      if (time_us) time_us[i] = e->phase_us[i];
+      if (peak_bytes) peak_bytes[i] = e->phase_bytes[i];
     }
-    from_device(e, grad, out, (size_t)P.B * 2 * P.HW * sizeof(double), mem);
-    ck(cudaStreamSynchronize(e->stream), "backward");
-    if (e->owner()) e->collect_range(6, 9); else e->collect_range(M_FWD0 + 3, M_FWD0 + 5);
-    ck(cudaGetLastError(), "backward kernels");
-    e->last_launches = launch_count();
+  });
+}
+
+int evcm_cuda_stream_wait(evcm_cuda_engine* e, void* stream) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st == e->stream) return;
+    set_device(e);
+    if (!e->order_ev) ck(cudaEventCreateWithFlags(&e->order_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e->order_ev, st), "event record");
+    ck(cudaStreamWaitEvent(e->stream, e->order_ev, 0), "stream wait");
+  });
+}
+
+int evcm_cuda_stream_signal(evcm_cuda_engine* e, void* stream) {
+  return guarded([&] {
+    if (!e) fail(EVCM_ERR_CONFIG, "null engine");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st == e->stream) return;
+    set_device(e);
+    if (!e->order_ev) ck(cudaEventCreateWithFlags(&e->order_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e->order_ev, e->stream), "event record");
+    ck(cudaStreamWaitEvent(st, e->order_ev, 0), "stream wait");
   });
 }
 
@@ -835,7 +963,8 @@ int evcm_cuda_depth_pose_to_flows(evcm_cuda_engine* e, int W, int H, const doubl
     const double* tab = upload_pose_table(e, ph.data(), 1, B, edges.data(), true);
     const double* dd = to_device(e, "depth", depth, (size_t)P.HW, mem);
     const uint8_t* md = mask ? to_device(e, "mask", mask, (size_t)P.HW, mem) : nullptr;
-    double2* fl = e->get<double2>("flows", (size_t)B * P.HW);
+    // its own buffer: the forward's flows stay intact for a following backward
+    double2* fl = e->get<double2>("mf_flows", (size_t)B * P.HW);
     uint8_t* vd = valid ? e->get<uint8_t>("valid", (size_t)B * P.HW) : nullptr;
     launch_motion_field(e->stream, dd, md, tab, P, K, fl, vd);
     double* planar = e->get<double>("flows_planar_out", (size_t)B * 2 * P.HW);
@@ -899,10 +1028,17 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
     if (W <= 0 || H <= 0 || W > 65535 || H > 65535) fail(EVCM_ERR_DIMENSION, "chain: bad sensor size");
     if (bt->t_end_us <= bt->t_start_us || bt->t_end_us - bt->t_start_us >= (1ull << 31))
       fail(EVCM_ERR_CONFIG, "chain: window must be nonempty and shorter than 2^31 us");
+    // event offsets: n_windows + 1 host entries from 0, non-decreasing
+    if (bt->ev_offsets[0] != 0) fail(EVCM_ERR_CONFIG, "chain: ev_offsets[0] must be 0");
+    for (int w = 0; w < nw; ++w)
+      if (bt->ev_offsets[w + 1] < bt->ev_offsets[w])
+        fail(EVCM_ERR_CONFIG, "chain: ev_offsets must be non-decreasing");
+    if (bt->ev_offsets[nw] >= (1ull << 32)) fail(EVCM_ERR_CONFIG, "chain: more than 2^32 events");
     const std::vector<uint64_t> edges = zeros_edges(bt->t_start_us, bt->t_end_us, B);
     WinParams P = make_params(W, H, edges.data(), B, nw, bt->t_start_us, bt->t_end_us);
     P.stride_us = bt->window_stride_us;
     e->have_fwd = false;
+    e->fwd_id = 0;
     e->mark(0);
     // Rotation tables: host poses -> built on the host with the reference's own
     // expression order (bit-identical flows); device poses -> k_pose_table (no
@@ -1042,6 +1178,7 @@ void chain_impl(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, int
     g->last_use = ++e->use_clock;
     ck(cudaGraphLaunch(g->exec, e->stream), "graph launch");
     e->have_fwd = false;
+    e->fwd_id = 0;
     e->last_launches = g->launches;
     if (async) {  // checked by evcm_cuda_chain_wait(slot)
       auto& q = e->pending[e->slot];

@@ -36,3 +36,45 @@ def allreduce_window_sums(buf, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return buf
+
+
+class OverlappedAllReduce:
+    """Double-buffered all-reduce of the packed window sums:
+    step i's chain writes buffer i % 2 and its reduction is issued asynchronously
+    (on NCCL's internal stream, ordered after the chain on the caller's stream),
+    so it runs while step i+1 computes into the other buffer. ``buffer(i)``
+    makes the caller's stream wait for the reduction of step i-2 before the
+    buffer is reused; ``drain()`` waits for every outstanding reduction. With one
+    rank (or no process group) it only hands out the buffers."""
+
+    def __init__(self, n: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.bufs = [torch.zeros(n, dtype=torch.float64, device=device) for _ in range(2)]
+        self.work = [None, None]
+        self.group = group
+        self.active = dist.is_available() and dist.is_initialized() and \
+            dist.get_world_size(group) > 1
+
+    def _wait(self, slot: int) -> None:
+        w = self.work[slot]
+        if w is not None:
+            w.wait()  # NCCL: the current stream waits; gloo: the host waits
+            self.work[slot] = None
+
+    def buffer(self, i: int):
+        self._wait(i % 2)
+        return self.bufs[i % 2]
+
+    def submit(self, i: int):
+        """Starts the reduction of step i's buffer; returns the buffer."""
+        import torch.distributed as dist
+        b = self.bufs[i % 2]
+        if self.active:
+            self.work[i % 2] = dist.all_reduce(b, op=dist.ReduceOp.SUM, group=self.group,
+                                               async_op=True)
+        return b
+
+    def drain(self) -> None:
+        for s in (0, 1):
+            self._wait(s)

@@ -103,11 +103,12 @@ class _Slice(C.Structure):
 
 
 class _Flows(C.Structure):
-    _fields_ = [("n_bins", C.c_int), ("edges_us", C.c_void_p), ("uv", C.c_void_p)]
+    _fields_ = [("n_bins", C.c_int), ("edges_us", C.c_void_p), ("uv", C.c_void_p),
+                ("width", C.c_int), ("height", C.c_int)]
 
 
 class _Loss(C.Structure):
-    _fields_ = [("value", C.c_double), ("no_survivors", C.c_int)]
+    _fields_ = [("value", C.c_double), ("no_survivors", C.c_int), ("forward_id", C.c_uint64)]
 
 
 class _ChainBatch(C.Structure):
@@ -150,6 +151,12 @@ def load_library(build_if_missing: bool = True):
     L.evcm_cuda_forward.argtypes = [vp, vp, vp, i32, vp]
     L.evcm_cuda_forward_products.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
     L.evcm_cuda_backward.argtypes = [vp, vp, vp, i32, vp]
+    L.evcm_cuda_backward_of.argtypes = [vp, vp, vp, u64, i32, vp]
+    L.evcm_cuda_phase_stats.argtypes = [vp, vp, vp]
+    L.evcm_cuda_sort_products.argtypes = [vp, vp, vp, vp, vp]
+    L.evcm_cuda_stream_wait.argtypes = [vp, vp]
+    L.evcm_cuda_stream_signal.argtypes = [vp, vp]
+    L.evcm_cuda_abi_version.restype = i32
     L.evcm_cuda_loss_and_grad.argtypes = [vp, vp, vp, i32, vp, vp]
     L.evcm_cuda_depth_pose_to_flows.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, u64, u64,
                                                 i32, vp, vp, vp]
@@ -309,11 +316,16 @@ class FlowSequence:
 
     def _c(self):
         self.edges_us = np.ascontiguousarray(self.edges_us, np.uint64)
-        if not _is_torch(self.uv):
+        if _is_torch(self.uv):
+            import torch
+            if self.uv.dtype != torch.float64 or not self.uv.is_contiguous():
+                raise DimensionMismatchError("flow sequence: uv must be a contiguous float64 "
+                                             "[B, 2, H, W] tensor")
+        else:
             self.uv = np.ascontiguousarray(self.uv, np.float64)
         if self.uv.ndim != 4 or self.uv.shape[0] != self.n_bins or self.uv.shape[1] != 2:
             raise DimensionMismatchError("flow sequence: uv must be [B, 2, H, W]")
-        return _Flows(self.n_bins, _ptr(self.edges_us), _ptr(self.uv))
+        return _Flows(self.n_bins, _ptr(self.edges_us), _ptr(self.uv), self.width, self.height)
 
 
 @dataclass
@@ -357,16 +369,17 @@ class ForwardResult:
     """ForwardResult (engine.hpp:99-105). The stack and trajectories stay on the
     device; ``stack`` / ``traj`` copy them back on first access."""
 
-    def __init__(self, engine: "Engine", generation: int, loss: LossResult, dims):
+    def __init__(self, engine: "Engine", generation: int, loss: LossResult, dims,
+                 forward_id: int = 0, stats=None):
         self._engine = engine
         self._gen = generation
+        self._id = forward_id
         self.loss = loss
         self._dims = dims  # (W, H, B, n)
         self._stack = None
         self._traj = None
-        self.warp_stats = PhaseStats()
-        self.splat_stats = PhaseStats()
-        self.loss_stats = PhaseStats()
+        st = stats or [PhaseStats()] * 3
+        self.warp_stats, self.splat_stats, self.loss_stats = st[0], st[1], st[2]
 
     def _check_live(self):
         if self._engine._generation != self._gen:
@@ -385,6 +398,31 @@ class ForwardResult:
                 self._engine._h, _ptr(count), _ptr(tsum), _ptr(na), None, None, None, None))
             self._stack = IweStack(W, H, R, count, tsum, na)
         return self._stack
+
+    def alive_bin(self):
+        """(alive u8 [n], bin i32 [n], n_alive) without the positions (which are
+        (B+1) x 16 B per event)."""
+        self._check_live()
+        n = self._dims[3]
+        alive = np.zeros(n, np.uint8)
+        bins = np.zeros(n, np.int32)
+        na = C.c_size_t()
+        _raise(load_library().evcm_cuda_forward_products(
+            self._engine._h, None, None, None, _ptr(alive), _ptr(bins), None, C.byref(na)))
+        return alive, bins, int(na.value)
+
+    def sort_products(self):
+        """(keys [n], perm [n_sorted], sorted_keys [n_sorted]) of the forward's
+        stable tile sort (owner pipeline), uint32."""
+        self._check_live()
+        n = self._dims[3]
+        keys = np.zeros(n, np.uint32)
+        perm = np.zeros(n, np.uint32)
+        sk = np.zeros(n, np.uint32)
+        ns = C.c_size_t()
+        _raise(load_library().evcm_cuda_sort_products(self._engine._h, _ptr(keys), _ptr(perm),
+                                                      _ptr(sk), C.byref(ns)))
+        return keys, perm[: ns.value], sk[: ns.value]
 
     @property
     def traj(self) -> Trajectories:
@@ -427,7 +465,7 @@ class EngineOptions:
     """EngineOptions (engine.hpp:54-61) for the cuda backend."""
     backend: str = "cuda"
     device: int = 0
-    deterministic: bool = False
+    deterministic: bool = True  # engine.hpp:60
     stack_f64: bool = True   # parity precision; False = fp32 "fast" stack
     grad_f64: bool = False
     stream: Optional[int] = None  # raw cudaStream_t handle, None = engine-owned
@@ -462,17 +500,37 @@ class Engine:
     def options(self) -> EngineOptions:
         return self.opts
 
+    def _order_after(self, *arrays) -> None:
+        """Device inputs produced on the caller's current torch stream: the
+        engine's stream waits for that work before its kernels read them."""
+        for a in arrays:
+            if a is not None and _is_torch(a) and a.is_cuda:
+                import torch
+                cur = torch.cuda.current_stream(a.device).cuda_stream
+                _raise(load_library().evcm_cuda_stream_wait(self._h, C.c_void_p(cur)))
+                return
+
+    def phase_stats(self):
+        """PhaseStats (engine.hpp:63-66) of the last forward's warp / splat / loss
+        and the last backward's phases."""
+        t = (C.c_double * 4)()
+        b = (C.c_size_t * 4)()
+        _raise(load_library().evcm_cuda_phase_stats(self._h, t, b))
+        return [PhaseStats(float(t[i]), int(b[i])) for i in range(4)]
+
     # -- Engine::forward (engine.hpp:145-183)
     def forward(self, slice_: EventSlice, flows: FlowSequence) -> ForwardResult:
         s, f = slice_._c(), flows._c()
         mem = _mem_of(slice_.events if slice_.n_events else None, flows.uv)
+        self._order_after(slice_.events, flows.uv)
         loss = _Loss()
         self._generation += 1
         _raise(load_library().evcm_cuda_forward(self._h, C.byref(s), C.byref(f), mem,
                                                 C.byref(loss)))
         return ForwardResult(self, self._generation,
                              LossResult(loss.value, bool(loss.no_survivors)),
-                             (slice_.width, slice_.height, flows.n_bins, slice_.n_events))
+                             (slice_.width, slice_.height, flows.n_bins, slice_.n_events),
+                             int(loss.forward_id), self.phase_stats()[:3])
 
     # -- Engine::backward (engine.hpp:185-205)
     def backward(self, slice_: EventSlice, flows: FlowSequence, fwd: ForwardResult,
@@ -480,6 +538,7 @@ class Engine:
         fwd._check_live()
         s, f = slice_._c(), flows._c()
         mem = _mem_of(slice_.events if slice_.n_events else None, flows.uv)
+        self._order_after(slice_.events, flows.uv, out)
         if out is None:
             if mem == MEM_DEVICE:
                 import torch
@@ -487,8 +546,15 @@ class Engine:
                                   dtype=torch.float64, device=flows.uv.device)
             else:
                 out = np.zeros((flows.n_bins, 2, slice_.height, slice_.width))
-        _raise(load_library().evcm_cuda_backward(self._h, C.byref(s), C.byref(f), mem, _ptr(out)))
-        return BackwardResult(out)
+        if _is_torch(out):
+            import torch
+            if out.dtype != torch.float64 or not out.is_contiguous() or \
+                    tuple(out.shape) != (flows.n_bins, 2, slice_.height, slice_.width):
+                raise DimensionMismatchError("backward: out must be a contiguous float64 "
+                                             "[B, 2, H, W] tensor")
+        _raise(load_library().evcm_cuda_backward_of(self._h, C.byref(s), C.byref(f), fwd._id, mem,
+                                                    _ptr(out)))
+        return BackwardResult(out, self.phase_stats()[3])
 
     # -- Engine::loss_and_grad (engine.hpp:208-213)
     def loss_and_grad(self, slice_: EventSlice, flows: FlowSequence):
@@ -534,6 +600,7 @@ class Engine:
         ``check_window=False`` only read_events' record checks (io.hpp:123-144)."""
         s = slice_._c()
         mem = _mem_of(slice_.events if slice_.n_events else None)
+        self._order_after(slice_.events)
         _raise(load_library().evcm_cuda_validate_slice(self._h, C.byref(s), int(check_window),
                                                        mem, None))
 
@@ -544,6 +611,7 @@ class Engine:
         if not _is_torch(events):
             events = np.ascontiguousarray(events, EVENT_DTYPE)
         n = events.numel() // 16 if _is_torch(events) else len(events)
+        self._order_after(events)
         offs = np.zeros(int(n_windows) + 1, np.uint64)
         _raise(load_library().evcm_cuda_window_offsets(
             self._h, _ptr(events) if n else None, n, int(t0_us), int(window_us), int(n_windows),
@@ -621,6 +689,17 @@ class Engine:
         out_mem = MEM_DEVICE if out_device else MEM_HOST
         K = k.as_array() if isinstance(k, CameraIntrinsics) else np.asarray(k, np.float64)
         offs = np.ascontiguousarray(ev_offsets, np.uint64)
+        n_ev = events.numel() // 16 if _is_torch(events) else len(events)
+        if offs.ndim != 1 or len(offs) != nw + 1:
+            raise ConfigError(f"chain: ev_offsets needs n_windows + 1 = {nw + 1} entries")
+        if offs[0] != 0 or np.any(offs[1:] < offs[:-1]):
+            raise ConfigError("chain: ev_offsets must start at 0 and be non-decreasing")
+        if int(offs[-1]) > n_ev:
+            raise DimensionMismatchError(f"chain: ev_offsets end at {int(offs[-1])} but only "
+                                         f"{n_ev} events were given")
+        if tuple(poses.shape) != (nw, poses.shape[1], 6):
+            raise DimensionMismatchError("chain: poses must be [n_windows, B, 6]")
+        self._order_after(depth, poses, events)
         if out is None:
             if out_mem == MEM_DEVICE:
                 import torch
@@ -676,6 +755,7 @@ def depth_pose_to_flows(depth, poses, k, t_start_us, t_end_us, mask=None, engine
     """depth_pose_to_flows (geometry.hpp:229-264). depth [H, W], poses [B, 6]."""
     e = engine or default_engine()
     mem = _mem_of(depth, poses, mask)
+    e._order_after(depth, poses, mask)
     H, W = depth.shape
     B = poses.shape[0] if len(poses.shape) == 2 else len(poses) // 6
     if mem == MEM_HOST:
@@ -700,6 +780,7 @@ def depth_pose_to_flows_backward(depth, poses, k, flows: FlowSequence, grad, mas
     """depth_pose_to_flows_backward (geometry.hpp:279-325) -> (d_depth [H, W], d_poses [B, 6])."""
     e = engine or default_engine()
     mem = _mem_of(depth, poses, grad, mask)
+    e._order_after(depth, poses, grad, mask)
     H, W = depth.shape
     B = flows.n_bins
     if grad.shape[0] != B or (len(poses.shape) == 2 and poses.shape[0] != B):

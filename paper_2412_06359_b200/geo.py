@@ -111,6 +111,7 @@ def geometry_consistency_loss_batch(d0, d1, poses, k, mask0=None, mask1=None,
     go = _GeoOut(_ptr(out.value), _ptr(out.n_valid), _ptr(out.projected), _ptr(out.interpolated),
                  _ptr(out.valid), _ptr(out.d_d0), _ptr(out.d_d1), _ptr(out.d_poses),
                  _ptr(out.d_depth_sum))
+    e._order_after(d0, d1, poses)
     _raise(load_library().evcm_cuda_geometry_consistency_loss(
         e._h, W, H, _ptr(d0), _ptr(mask0), _ptr(d1), _ptr(mask1), n, _ptr(poses),
         _ptr(_k_array(k)), float(upstream), int(want_grad), mem, C.byref(go)))

@@ -24,19 +24,23 @@ from .engine import ConfigError, Engine, _is_torch
 class ChainPipeline:
     """Double-buffered ``chain_batch`` over a stream of host batches.
 
-    ``engine`` must run on a torch CUDA stream (EngineOptions(stream=...)) or its
-    own stream; the pipeline uses ``compute_stream`` (default: the current torch
-    stream of the engine's device) for the waits and the result read-back."""
+    ``engine`` must run on an explicit CUDA stream (EngineOptions(stream=...));
+    ``compute_stream`` (default: that stream wrapped for torch) must be the
+    engine's stream: it carries the waits for the staged copies and the result
+    read-back."""
 
     def __init__(self, engine: Engine, compute_stream=None):
         import torch
         self.engine = engine
         self.dev = torch.device("cuda", engine.opts.device)
+        if engine.opts.stream is None:
+            raise ConfigError("ChainPipeline: the engine needs an explicit stream "
+                              "(EngineOptions(stream=torch_stream.cuda_stream))")
         if compute_stream is None:
-            if engine.opts.stream is None:
-                raise ConfigError("ChainPipeline: the engine needs an explicit stream "
-                                  "(EngineOptions(stream=torch_stream.cuda_stream))")
             compute_stream = torch.cuda.ExternalStream(engine.opts.stream, device=self.dev)
+        elif compute_stream.cuda_stream != engine.opts.stream:
+            # the engine's kernels must wait for the staged copies: one stream
+            raise ConfigError("ChainPipeline: compute_stream must be the engine's stream")
         self.compute = compute_stream
         self.copy = torch.cuda.Stream(self.dev)
         self.sets = [None, None]

@@ -105,6 +105,7 @@ def decode(pred: DirectPredictor, engine: Engine | None = None) -> DecodedPredic
     ph, pw = params.shape
     mem = _mem_of(params)
     depth = _zeros_like_side(params, (ph * pred.upsample, pw * pred.upsample))
+    e._order_after(params)
     _raise(load_library().evcm_cuda_decode(e._h, pw, ph, pred.upsample, _ptr(params), mem,
                                            _ptr(depth)))
     return DecodedPredictor(depth, pred.poses)
@@ -128,6 +129,7 @@ def accumulate_gradients(pred: DirectPredictor, decoded_depth, k, flows: FlowSeq
     ph, pw = params.shape
     mem = _mem_of(params, d_depth)
     out = _zeros_like_side(params, (ph, pw))
+    e._order_after(params, d_depth)
     _raise(load_library().evcm_cuda_decode_backward(e._h, pw, ph, pred.upsample, _ptr(params),
                                                     _ptr(_f64(d_depth)), mem, _ptr(out)))
     if extra_d_poses is not None:
@@ -156,6 +158,7 @@ def predictor_loss_and_gradients(pred: DirectPredictor, slice_: EventSlice, k, l
     dpar = _zeros_like_side(params, (ph, pw))
     dpos = _zeros_like_side(params, (pred.n_bins, 6))
     sl = slice_._c()
+    e._order_after(params, poses, slice_.events)
     _raise(load_library().evcm_cuda_predictor_loss_and_gradients_geo(
         e._h, pw, ph, pred.upsample, _ptr(params), pred.n_bins, _ptr(poses),
         _ptr(_k_array(k)), C.byref(sl), float(lambda_geo), mem, _ptr(losses), _ptr(dpar),
@@ -221,6 +224,7 @@ class Adam:
         self.t += 1
         n = int(slots.shape[0])
         mem = _mem_of(slots, grads, self.m)
+        e._order_after(slots, grads)
         _raise(load_library().evcm_cuda_adam_step(
             e._h, n, _ptr(slots), _ptr(_f64(grads)), _ptr(self.m), _ptr(self.v), self.t,
             cfg.learning_rate, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps, mem))

@@ -23,19 +23,19 @@ def engine():
 @pytest.fixture(scope="session")
 def engine_f64():
     import paper_2412_06359_b200 as P
-    return P.Engine(P.EngineOptions(stack_f64=True, grad_f64=True, algo="atomic"))
+    return P.Engine(P.EngineOptions(stack_f64=True, grad_f64=True, algo="atomic", deterministic=False))
 
 
 @pytest.fixture(scope="session")
 def engine_fast():
     import paper_2412_06359_b200 as P
-    return P.Engine(P.EngineOptions(stack_f64=False, algo="atomic"))
+    return P.Engine(P.EngineOptions(stack_f64=False, algo="atomic", deterministic=False))
 
 
 @pytest.fixture(scope="session")
 def engine_atomic():
     import paper_2412_06359_b200 as P
-    return P.Engine(P.EngineOptions(algo="atomic"))
+    return P.Engine(P.EngineOptions(algo="atomic", deterministic=False))
 
 
 @pytest.fixture(scope="session")

@@ -70,6 +70,36 @@ int main() {
       threw = true;
     }
     CHECK(threw, "CoordinateRangeError");
+    // flow grid of the wrong size: DimensionMismatchError (engine.hpp:218-219)
+    FdInstance small = random_fd_instance(43);
+    const FlowSequence other = FlowSequence::zeros(small.slice.width + 1, small.slice.height,
+                                                   small.slice.t_start_us, small.slice.t_end_us,
+                                                   small.flows.n_bins());
+    threw = false;
+    try {
+      gpu.forward(small.slice, other);
+    } catch (const DimensionMismatchError&) {
+      threw = true;
+    }
+    CHECK(threw, "DimensionMismatchError on a flow/sensor size mismatch");
+    // PhaseStats are filled (engine.hpp:63-66, 226-242)
+    const FdInstance a = random_fd_instance(101), b = random_fd_instance(102);
+    const ForwardResult fa = gpu.forward(a.slice, a.flows);
+    CHECK(fa.warp_stats.time_us > 0 && fa.splat_stats.time_us > 0 && fa.loss_stats.time_us > 0 &&
+              fa.splat_stats.peak_bytes > 0,
+          "forward PhaseStats");
+    const BackwardResult ba = gpu.backward(a.slice, a.flows, fa);
+    CHECK(ba.stats.time_us > 0 && ba.stats.peak_bytes > 0, "backward PhaseStats");
+    // a backward of an earlier forward is refused (the device holds the last one)
+    const ForwardResult fb = gpu.forward(b.slice, b.flows);
+    threw = false;
+    try {
+      gpu.backward(a.slice, a.flows, fa);
+    } catch (const ConfigError&) {
+      threw = true;
+    }
+    CHECK(threw, "stale forward refused");
+    (void)fb;
   }
   // motion field and its backward
   const cuda::Engine gpu;

@@ -47,7 +47,7 @@ def test_error_names_and_abi_version():
     names = {c: lib.evcm_cuda_error_name(c).decode() for c in (1, 2, 3, 4, 5, 6, 7, 20, 21)}
     assert names[1] == "ConfigError" and names[2] == "DimensionMismatchError"
     assert names[3] == "CoordinateRangeError" and names[5] == "UnsortedEventsError"
-    assert lib.evcm_cuda_abi_version() == 1
+    assert lib.evcm_cuda_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -71,7 +71,13 @@ def test_default_options():
     lib = P.load_library()
     o = E._Options()
     lib.evcm_cuda_default_options(C.byref(o))
-    assert o.stack_f64 == 1 and o.grad_f64 == 0 and o.algo == 2 and o.deterministic == 0
+    # deterministic by default, as the reference (engine.hpp:60)
+    assert o.stack_f64 == 1 and o.grad_f64 == 0 and o.algo == 2 and o.deterministic == 1
+    assert P.EngineOptions().deterministic is True
+
+
+def test_abi_version():
+    assert P.load_library().evcm_cuda_abi_version() == 2
 
 
 def test_backend_names():
