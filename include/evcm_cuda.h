@@ -93,8 +93,11 @@ typedef struct {
   int stack_f64;       /* 1 (default, parity): fp64 IWE stack + loss coefficients;
                           0: fp32 ("fast": loss/IWE within 1e-6, gradients NOT within
                           1e-5 on sparse windows — see DESIGN.md "Numerics") */
-  int grad_f64;        /* 1: fp64 flow-gradient accumulators (default 0: fp32, which
-                          keeps gradients within ~1e-7 of the reference) */
+  int grad_f64;        /* algo 1 only: fp64 flow-gradient accumulators (default 0: fp32,
+                          which keeps gradients within ~1e-7 of the reference). With
+                          stack_f64 this is the path that tracks the reference through
+                          long optimisation loops (run_window: ~1e-11 after 12 updates;
+                          DESIGN.md §3) */
   void* stream;        /* cudaStream_t to run on; NULL = engine-owned stream */
   int algo;            /* 0: owner-computes tiles (no global atomics; the product path);
                           1: per-event global atomics, an independent cross-check kept

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _slice_flows(w):
-    return P.EventSlice(w.W, w.H, 0, int(w.edges[-1]), w.events), P.FlowSequence(w.edges, w.uv)
+    return P.EventSlice(w.W, w.H, 0, int(w.edges[-1]), w.events), P.FlowSequence(w.edges, w.flows)
 
 
 def test_default_engine_is_deterministic_owner():
@@ -46,7 +46,7 @@ def test_flow_grid_must_match_sensor(engine):
     f = engine.forward(sl, fl)
     with pytest.raises(P.DimensionMismatchError):
         engine.backward(sl, bad, f)
-    dev = torch.from_numpy(w.uv).cuda()
+    dev = torch.from_numpy(w.flows).cuda()
     with pytest.raises(P.DimensionMismatchError):  # fp32 device flows
         engine.forward(sl, P.FlowSequence(w.edges, dev.float()))
     with pytest.raises(P.DimensionMismatchError):  # strided device flows
@@ -76,9 +76,9 @@ def test_backward_uses_the_flows_it_is_given(engine):
     sl, fl = _slice_flows(w)
     f = engine.forward(sl, fl)
     same = engine.backward(sl, fl, f).grad.copy()
-    want = O.backward(O.Window(w.W, w.H, w.edges, w.events, w.uv))
+    want = O.backward(O.Window(w.W, w.H, w.edges, w.events, w.flows))
     assert rel_inf(same, want) <= 1e-5
-    uv2 = (w.uv * 1.5).astype(np.float32).astype(np.float64)
+    uv2 = (w.flows * 1.5).astype(np.float32).astype(np.float64)
     other = engine.backward(sl, P.FlowSequence(w.edges, uv2), f).grad
     assert not np.array_equal(other, same)
 
@@ -127,10 +127,12 @@ def test_engine_waits_for_the_producer_stream():
         big = torch.randn(4096, 4096, device="cuda")
         for _ in range(8):
             big = big @ big * 1e-3  # keep the side stream busy
-        uv = torch.zeros(w.uv.shape, dtype=torch.float64, device="cuda")
-        uv.copy_(torch.from_numpy(w.uv), non_blocking=False)
+        uv = torch.zeros(w.flows.shape, dtype=torch.float64, device="cuda")
+        uv.copy_(torch.from_numpy(w.flows), non_blocking=False)
         uv.add_(big.sum() * 0.0)  # last writer of uv runs after the matmuls
-        got = e.forward(sl, P.FlowSequence(w.edges, uv)).loss.value
+        ev = torch.from_numpy(w.events.view(np.uint8).copy()).cuda()
+        got = e.forward(P.EventSlice(w.W, w.H, 0, int(w.edges[-1]), ev),
+                        P.FlowSequence(w.edges, uv)).loss.value
     assert got == want
 
 

@@ -38,7 +38,7 @@ def _engine_window(eng, depth, poses, K, ev, t1, B):
     """Engine-level forward / backward of one window on the reference's own
     motion field, checked against Engine::loss_and_grad of the reference."""
     H, W = depth.shape
-    flows, _ = O.ref_depth_pose_to_flows(depth, poses, K, 0, t1)
+    flows = O.ref_depth_pose_to_flows(depth, poses, K, 0, t1)[0]
     w = O.Window(W, H, O.make_edges(0, t1, B), ev, flows)
     sl = P.EventSlice(W, H, 0, t1, ev)
     fl = P.FlowSequence(w.edges.copy(), flows.copy())
@@ -106,7 +106,7 @@ def test_sweep_dense_windows(eng, n):
 def test_sort_permutation_is_stable_argsort(eng, W, H, n):
     wl = dict(bench.WORKLOADS["B"], W=W, H=H, n_events=n)
     depth, poses, K, ev, offs = bench.make_inputs(wl, 0, 1)
-    flows, _ = O.ref_depth_pose_to_flows(depth[0], poses[0], K, 0, wl["window_us"])
+    flows = O.ref_depth_pose_to_flows(depth[0], poses[0], K, 0, wl["window_us"])[0]
     edges = O.make_edges(0, wl["window_us"], wl["B"])
     fwd = eng.forward(P.EventSlice(W, H, 0, wl["window_us"], ev), P.FlowSequence(edges, flows))
     keys, perm, sorted_keys = fwd.sort_products()

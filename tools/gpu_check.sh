@@ -10,4 +10,4 @@ timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider --durations
 echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.txt
 timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 echo "bench rc=$?" >> gpurun_out/${tag}_bench.err
-tail -3 gpurun_out/${tag}_smoke.txt gpurun_out/${tag}_pytest.txt gpurun_out/${tag}_bench.err
+tail -n 3 gpurun_out/${tag}_smoke.txt gpurun_out/${tag}_pytest.txt gpurun_out/${tag}_bench.err
