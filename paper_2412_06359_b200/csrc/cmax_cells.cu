@@ -114,6 +114,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void consumer_sync(int count) {
   asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory");
 }
+// Warp sums of N components at once by transposition: each halving step trades
+// half of the remaining components with the partner lane (N - 1 + log2(32 / N)
+// double shuffles instead of 5 N); lane l returns the sum of component
+// (l >> (5 - log2 N)) & (N - 1) (lanes with l % (32 / N) == 0 hold distinct
+// components). Fixed order: deterministic.
+template <int N>
+__device__ __forceinline__ double warp_comp_sum(double (&c)[N], int lane) {
+#pragma unroll
+  for (int h = N / 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
+    const bool up = lane & off;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double mine = up ? c[h + k] : c[k], other = up ? c[k] : c[h + k];
+      c[k] = mine + __shfl_xor_sync(0xffffffffu, other, off);
+    }
+  }
+  double v = c[0];
+#pragma unroll
+  for (int off = 16 / N; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
@@ -945,35 +966,26 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   // ---------------- consumers ----------------
   const int ct = tid - 64, cw = wid - 2;
   const uint32_t acc_s = smem_u32(acc);
-  const int lxp = ct % kOwnW, lyp = ct / kOwnW;
-  const int px = ox0 + lxp, py = oy0 + lyp;
-  const bool own_px = px < W && py < H;
-  const int gq = py * W + px, op = lyp * kRowW + lxp;
-  const double dpx = own_px && depth ? depth[(size_t)w * HW + gq] : 0.0;
-  const bool dok = own_px && depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
-  // backproject(x, 1.0, k) (geometry.hpp:147-149), bin-independent
-  const double rx = 1.0 * ((double)px - cx) / fx, ry = 1.0 * ((double)py - cy) / fy;
   // fixed-point scale of this window's gradient terms: |w g| <= max|g| < 2^e,
   // scaled to 2^kbits (s_kbits is written by the producer before its first round)
   int e2 = 0;
   frexp((double)__uint_as_float(gmax[w]), &e2);
-  double gsc = 0.0, igsc = 0.0;
+  double gsc = 0.0;
   double dd = 0.0;  // d_depth of this pixel, bins summed in order
   uint32_t it = 0;
-  for (int done = 0; done < i1 - i0;) {
+  const int n_bins = i1 - i0;
+  for (int done = 0; done < n_bins;) {
     const int b = (int)(it % kBufQ);
     mbar_wait(&full[b], (it / kBufQ) & 1);
-    if (it == 0) {
-      gsc = ldexp(1.0, s_kbits - e2);
-      igsc = ldexp(1.0, e2 - s_kbits);
-    }
+    if (it == 0) gsc = ldexp(1.0, s_kbits - e2);
     const BRound d = desc[b];
     const uint4* s16 = stage16 + b * kStageQ;
     const float2* s8 = stage8 + b * kStageQ;
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[b];
     const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
-    const int lo_bin = kGrouped && d.r == prime_r ? d.r : 0;
+    // (prime group: re-formed from blockIdx.z here rather than kept live)
+    const int lo_bin = kGrouped && d.r == (int)blockIdx.z * B / (int)gridDim.z ? d.r : 0;
     // record sinks of reference d.r (slots < split)
     compacted<kCons>(
         (uint32_t)cw * 32, d.split, wq[cw],
@@ -1035,10 +1047,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     // bin i = d.r - 1 complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
     const int i = d.r - 1;
     consumer_sync(kCons);
-    // pose sums of this pixel (see kPoseSums): N = d v r^T (0..8), v (9..11)
-    double c6[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) c6[k] = 0.0;
+    // per-pixel constants, re-formed per bin (not held across the streaming loop:
+    // the register budget of two 576-thread CTAs per SM is 56)
+    const int lxp = ct % kOwnW, lyp = ct / kOwnW;
+    const int px = ox0 + lxp, py = oy0 + lyp;
+    const bool own_px = px < W && py < H;
+    const int gq = py * W + px, op = lyp * kRowW + lxp;
+    const double igsc = ldexp(1.0, e2 - s_kbits);
+    // pose sums of this pixel (see kPoseSums): N = d v r^T (0..8), v (9..11),
+    // generated from (d, v, r^) in two passes (fewer live registers than all 12)
+    double mv0 = 0.0, mv1 = 0.0, mv2 = 0.0, mdp = 0.0, mrx = 0.0, mry = 0.0;
     double ddi = 0.0;  // this bin's d_depth term
     {
       const uint32_t* at = acc + (i & 1) * 4 * kPlane;
@@ -1051,7 +1069,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
           grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
         }
+        const double dpx = depth ? depth[(size_t)w * HW + gq] : 0.0;
+        const bool dok = depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
         if (dok && (gu != 0.0 || gv != 0.0)) {
+          // backproject(x, 1.0, k) (geometry.hpp:147-149)
+          const double rx = 1.0 * ((double)px - cx) / fx, ry = 1.0 * ((double)py - cy) / fy;
           const double* ptab = pose_tab + ((size_t)w * B + i) * kPoseTab;
           const double rr0 = ptab[0] * rx + ptab[1] * ry + ptab[2];
           const double rr1 = ptab[3] * rx + ptab[4] * ry + ptab[5];
@@ -1071,38 +1093,30 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             // the add is explicitly rounded: k_depth_bins re-forms this sum from the stored terms
             ddi = v0 * rr0 + v1 * rr1 + v2 * rr2;
             dd = __dadd_rn(dd, ddi);
-            const double dv[3] = {dpx * v0, dpx * v1, dpx * v2};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              c6[3 * a] = dv[a] * rx;
-              c6[3 * a + 1] = dv[a] * ry;
-              c6[3 * a + 2] = dv[a];
-            }
-            c6[9] = v0;
-            c6[10] = v1;
-            c6[11] = v2;
+            mv0 = v0;
+            mv1 = v1;
+            mv2 = v2;
+            mdp = dpx;
+            mrx = rx;
+            mry = ry;
           }
         }
       }
     }
     if (kGrouped && dbin && own_px) dbin[((size_t)w * B + i) * HW + gq] = ddi;
     if (pose_part) {
-      // sixteen warp sums by transposition: each halving step trades half of
-      // the remaining components with the partner lane (15 double shuffles, not
-      // 60); lane 2c ends up holding component c (fixed order: deterministic)
-#pragma unroll
-      for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
-        const bool up = lane & off;
-#pragma unroll
-        for (int k = 0; k < h; ++k) {
-          const double mine = up ? c6[h + k] : c6[k], other = up ? c6[k] : c6[h + k];
-          c6[k] = mine + __shfl_xor_sync(kFull, other, off);
-        }
+      // warp sums by transposition (warp_comp_sum), fixed order: deterministic
+      {
+        const double d0 = mdp * mv0, d1 = mdp * mv1, d2 = mdp * mv2;
+        double c[8] = {d0 * mrx, d0 * mry, d0, d1 * mrx, d1 * mry, d1, d2 * mrx, d2 * mry};
+        const double v = warp_comp_sum(c, lane);
+        if ((lane & 3) == 0) s_pose[i & 1][cw][(lane >> 2) & 7] = v;
       }
-      const double v = c6[0] + __shfl_xor_sync(kFull, c6[0], 1);
-      const int comp = ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) +
-                       ((lane & 2) ? 1 : 0);
-      if ((lane & 1) == 0 && comp < kPoseSums) s_pose[i & 1][cw][comp] = v;
+      {
+        double c[4] = {mdp * mv2, mv0, mv1, mv2};
+        const double v = warp_comp_sum(c, lane);
+        if ((lane & 7) == 0) s_pose[i & 1][cw][8 + ((lane >> 3) & 3)] = v;
+      }
     }
     consumer_sync(kCons);  // also: the zeroed tile is ready for bin i + 2
     if (pose_part && ct < kPoseSums) {
@@ -1112,7 +1126,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     }
     ++done;
   }
-  if (d_depth && !(kGrouped && dbin) && own_px) d_depth[(size_t)w * HW + gq] = dd;
+  {
+    const int px = ox0 + ct % kOwnW, py = oy0 + ct / kOwnW;
+    if (d_depth && !(kGrouped && dbin) && px < W && py < H) d_depth[(size_t)w * HW + py * W + px] = dd;
+  }
   (void)H;
 }
 
