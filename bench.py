@@ -76,6 +76,22 @@ def measured_traffic(workload, kernel, world):
         return None
 
 
+def measured_ceilings(workload, kernel, world):
+    """Utilisation of the candidate ceilings (shared-memory / L1 data pipe,
+    shared atomics, L1 writeback, fp64 pipe, issue, DRAM; % of peak) of
+    `kernel` from the committed `ncu --set full` capture of this workload on
+    1 GPU (profiles/ceilings.json, tools/ncu_ceilings_json.py); `binding` names
+    the busiest one. This path is gather/atomic work, so the HBM roofline alone
+    does not say what bounds a kernel (SURVEY.md §8(d) secondary ceilings)."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ceilings.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -488,6 +504,7 @@ def cuda_arm(args, wl):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": measured_traffic(args.workload, dom, world),
+                "ceilings": measured_ceilings(args.workload, dom, world),
                 "algorithmic_bytes_per_launch": per_kernel[dom], "launch_ms": kern[dom],
                 "bytes_model": "SURVEY.md §8(d) canonical parity precision (b_ev 18 B, "
                                "b_px 1180 B at B=10), per-kernel split of bench.py "
