@@ -13,8 +13,15 @@ STAGE = {"k_motion_field": "motion_field", "k_traj_records": "traj_records",
          "k_fwd_cells": "fwd_owner", "k_bwd_event": "bwd_event", "k_bwd_cells": "bwd_owner"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
-out = {"_source": "tools/ncu_traffic.py over one `ncu --set full --clock-control none` capture "
-                  "per workload (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                    "traffic.json")
+try:  # merge: workloads not given keep their earlier capture
+    with open(path) as f:
+        out = json.load(f)
+except Exception:
+    out = {}
+out["_source"] = ("tools/ncu_traffic.py over one `ncu --set full --clock-control none` capture "
+                  "per workload (dram__bytes_read.sum + dram__bytes_write.sum per launch)")
 for arg in sys.argv[1:]:
     wl, rep = arg.split("=", 1)
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
@@ -33,8 +40,6 @@ for arg in sys.argv[1:]:
             tot += float(r[i]) * SCALE.get(units[i], 1)
         res.setdefault(STAGE[name], int(tot))
     out[wl] = res
-path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
-                    "traffic.json")
 with open(path, "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out, indent=1))
