@@ -16,7 +16,10 @@ constexpr int kOwnH = 16;
 constexpr int kChunk = 8192;       // max events per sort chunk (one CTA); TileParams.chunk adapts
 constexpr int kSortThreads = 512;  // key/histogram CTA size
 constexpr int kScatterThreads = 256;  // 8 warps x 1024 events per scatter chunk
-constexpr int kMaxTiles = 12000;   // sort scatter keeps 8 x nT u16 counters in smem
+// sort tiles per window: the scatter keeps nW x nT u16 counters in shared memory
+// (nW = 4 warps above 2048 tiles: 4 x 28000 x 2 B = 219 KB of the 227 KB), the
+// owner lists store u16 tile ids. 28000 tiles: up to 1280 x 1024 (or 1600 x 1120)
+constexpr int kMaxTiles = 28000;
 constexpr int kListCapO = 128;     // source-list capacity per (window, slot, owner tile)
 
 struct TileParams {

@@ -225,3 +225,20 @@ def test_overflowing_owner_lists(factor):
     from tests.helpers import contraction_window
     w = contraction_window(256, 192, 6, 40000, factor=factor)
     _check(P.Engine(P.EngineOptions(algo="owner")), w)
+
+
+@pytest.mark.parametrize("W,H,n", [(1280, 720, 400_000), (1280, 1024, 300_000)])
+def test_large_sensor(engine, W, H, n):
+    """Sensors beyond 12000 sort tiles (1280x720: 14400, 1280x1024: 20480), the
+    owner pipeline's 4-warp scatter at up to 28000 tiles, against the oracle."""
+    w = smooth_window(W, H, 10, n, seed=W + H)
+    _check(engine, w)
+    assert engine.last_algo() == "owner"
+
+
+def test_sensor_above_tile_limit_raises(engine):
+    """More than 28000 8x8 sort tiles (1920x1080 = 32400): ConfigError, as the
+    reference raises for invalid configurations (types.hpp:18-76)."""
+    w = smooth_window(1920, 1080, 2, 1000, seed=3)
+    with pytest.raises(P.ConfigError):
+        engine.forward(_slice(w), _flows(w))
