@@ -1046,13 +1046,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
 
     // bin i = d.r - 1 complete: fused depth_pose_to_flows_backward (geometry.hpp:300-322)
     const int i = d.r - 1;
-    consumer_sync(kCons);
     // per-pixel constants, re-formed per bin (not held across the streaming loop:
-    // the register budget of two 576-thread CTAs per SM is 56)
+    // the register budget of two 576-thread CTAs per SM is 56); the depth load is
+    // issued before the barrier so its latency overlaps the wait
     const int lxp = ct % kOwnW, lyp = ct / kOwnW;
     const int px = ox0 + lxp, py = oy0 + lyp;
     const bool own_px = px < W && py < H;
     const int gq = py * W + px, op = lyp * kRowW + lxp;
+    const double dpx = own_px && depth ? __ldg(depth + (size_t)w * HW + gq) : 0.0;
+    consumer_sync(kCons);
     const double igsc = ldexp(1.0, e2 - s_kbits);
     // pose sums of this pixel (see kPoseSums): N = d v r^T (0..8), v (9..11),
     // generated from (d, v, r^) in two passes (fewer live registers than all 12)
@@ -1069,7 +1071,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           grad_out[((size_t)w * B + i) * 2 * HW + gq] = gu;
           grad_out[(((size_t)w * B + i) * 2 + 1) * HW + gq] = gv;
         }
-        const double dpx = depth ? depth[(size_t)w * HW + gq] : 0.0;
         const bool dok = depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
         if (dok && (gu != 0.0 || gv != 0.0)) {
           // backproject(x, 1.0, k) (geometry.hpp:147-149)

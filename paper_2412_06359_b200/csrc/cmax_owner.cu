@@ -216,8 +216,10 @@ __global__ void __launch_bounds__(1024) k_sort_tilescan(const uint32_t* __restri
 // Stable scatter: warp `wid` of chunk c owns events [c*chunk + wid*chunk/nW, ...);
 // per-warp tile counts (u16) give each warp its base inside the chunk's run of
 // the tile, so the output keeps the input (time) order inside every tile.
+// (__maxnreg__: ptxas picked 32 registers for the 128-thread form and spilled;
+// 48 leaves no spill and does not limit occupancy, which shared memory sets)
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_sort_scatter(
+__global__ void __maxnreg__(48) k_sort_scatter(
     const uint2* __restrict__ packed, const uint32_t* __restrict__ keys,
     const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
     const uint32_t* __restrict__ tile_ptr, uint2* __restrict__ sorted, uint32_t* __restrict__ perm,
