@@ -13,7 +13,7 @@ import paper_2412_06359_b200 as P  # noqa: E402
 from tests.helpers import chain_inputs  # noqa: E402
 
 for algo in ("owner", "atomic"):
-    eng = P.Engine(P.EngineOptions(algo=algo))
+    eng = P.Engine(P.EngineOptions(algo=algo, deterministic=algo != "atomic"))
     depth, poses, K, ev, offs = chain_inputs(40, 30, 4, 3, 2500, seed=1)
     loss, dd, dp = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
     gf = eng.depth_pose_to_flows(depth[0], poses[0], K, 0, 100000)
