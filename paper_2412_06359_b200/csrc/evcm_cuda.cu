@@ -11,6 +11,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/evcm_cuda.h"
 #include "cmax_kernels.h"
@@ -228,7 +229,17 @@ struct evcm_cuda_engine {
     for (auto& kv : bufs) t += kv.second.cap;
     return t;
   }
+  // NVTX markers at the stage boundaries (host side; visible to nsys / ncu
+  // --nvtx): instantaneous marks, so a forward-only call leaves nothing open
+  void nvtx_stage(int i) {
+    static const char* kOwner[] = {"evcm: staging", "evcm: motion_field", "evcm: sort",
+                                   "evcm: traj_records+lists", "evcm: fwd_owner",
+                                   "evcm: loss_finalize", "evcm: bwd_event", "evcm: bwd_owner",
+                                   "evcm: pose_contract", "evcm: end"};
+    if (i >= 0 && i < 10) nvtxMarkA(use_owner || i < 2 ? kOwner[i] : "evcm: atomic stage");
+  }
   void mark(int i) {
+    nvtx_stage(i);
     if (i >= 0 && i < 16) ws_at_mark[i] = ws_bytes();
     if (!timing) return;
     while ((int)ev.size() <= i) {
