@@ -590,18 +590,21 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
           const double sx0 = ax * fsc, sx1 = wx * fsc;
           const bool inx0 = lx >= 0, inx1 = lx + ox < kOwnW, iny0 = ly >= 0, iny1 = ly + oy < kOwnH;
           const int o00 = ly * kRowW + lx;
+          // branch-free corners: a corner outside the tile adds a zero term to a
+          // padding word of row 0 (x = 32 + lane % 8, never read), so the four
+          // corners issue without divergent branches
+          const int pad = kOwnW + (lane & 7);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const bool in = ((q & 1) ? inx1 : inx0) && ((q & 2) ? iny1 : iny0);
             const double wqq = ((q & 1) ? sx1 : sx0) * ((q & 2) ? wy : ay);
-            if (in && wqq > 0.0) {
-              const int o = o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0);
-              const uint32_t a = pa + 4u * (uint32_t)o;
-              const unsigned long long qc = fx_q(wqq);  // wqq <= 2^50
-              if (qc == 0ull) flag[o] = 1u;  // w > 0 below the fixed-point resolution
-              fx_add(a, a + 4 * kPlane, qc);
-              fx_add(a + 8 * kPlane, a + 12 * kPlane, fx_q(wqq * tb));
-            }
+            const int o = in ? o00 + ((q & 2) ? oy * kRowW : 0) + ((q & 1) ? ox : 0) : pad;
+            const double wv = in ? wqq : 0.0;
+            const uint32_t a = pa + 4u * (uint32_t)o;
+            const unsigned long long qc = fx_q(wv);  // wv <= 2^50
+            if (wv > 0.0 && qc == 0ull) flag[o] = 1u;  // w > 0 below the fixed-point resolution
+            fx_add(a, a + 4 * kPlane, qc);
+            fx_add(a + 8 * kPlane, a + 12 * kPlane, fx_q(wv * tb));
           }
         });
     __syncwarp();
