@@ -203,3 +203,17 @@ def test_chain_batch_many_tiles():
         assert rel_inf(dp[w], ref[w][2]) <= 1e-5, rel_inf(dp[w], ref[w][2])
     l2, dd2, dp2 = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
     assert np.array_equal(l2, loss) and np.array_equal(dd2, dd) and np.array_equal(dp2, dp)
+
+
+def test_chain_batch_large_sensor():
+    """1280 x 720 (14400 sort tiles, beyond round 1's 12000 limit): the batched
+    chain with the fused flows backward against the oracle composition."""
+    eng = P.Engine()
+    depth, poses, K, ev, offs = chain_inputs(1280, 720, 10, 2, 500000, seed=33)
+    loss, dd, dp = eng.chain_batch(depth, poses, K, 0, 100000, ev, offs)
+    assert eng.last_algo() == "owner"
+    ref = _oracle_chain(depth, poses, K, ev, offs)
+    for w in range(2):
+        assert abs(loss[w] - ref[w][0]) <= 1e-5 * abs(ref[w][0])
+        assert rel_inf(dd[w], ref[w][1]) <= 1e-5, rel_inf(dd[w], ref[w][1])
+        assert rel_inf(dp[w], ref[w][2]) <= 1e-5, rel_inf(dp[w], ref[w][2])
