@@ -996,9 +996,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           if ((fk[v >> 5] >> (v & 31)) & 1u) return false;
           const uint32_t cell = s16[v].x;
           const int lx = (int)(cell & 0xffffu) - ox0, ly = (int)((cell >> 16) & 0x7fffu) - oy0;
-          if (cell == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH) return false;
-          const float2 g = s8[v];
-          return g.x != 0.f || g.y != 0.f;
+          // (zero sink values are not filtered here: they add zero terms, and the
+          // test would cost a second shared load per candidate slot)
+          return !(cell == kDead || lx + ox < 0 || lx >= kOwnW || ly + oy < 0 || ly >= kOwnH);
         },
         [&](uint32_t v) {
           const uint4 rec = s16[v];
