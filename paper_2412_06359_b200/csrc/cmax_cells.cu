@@ -729,10 +729,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   float2* stage8 = reinterpret_cast<float2*>(stage16 + kBufQ * kStageQ);    // [kBufQ][kStageQ] values
   uint32_t* acc = reinterpret_cast<uint32_t*>(stage8 + kBufQ * kStageQ);   // [tile][gu, gv][lo, hi][kPlane]
   __shared__ Batch bt;
-  __shared__ BRound desc[kBufQ];
+  // round metadata (descriptor, slack bitmask) in 2 kBufQ sets: the set of
+  // round it was last used by round it - 4, released before round it - 2 was
+  // staged, so the producer fills it before waiting for the buffer of round it
+  __shared__ BRound desc[2 * kBufQ];
   __shared__ uint32_t roffs[2][2 * kListCapO + 1 > kBatchCap ? 2 * kListCapO + 1 : kBatchCap];
   __shared__ uint32_t s_it;  // round counter hand-off after an overflowed group
-  __shared__ uint32_t fake[kBufQ][kStageQ / 32];  // slack slots of the staged round
+  __shared__ uint32_t fake[2 * kBufQ][kStageQ / 32];  // slack slots of the staged round
   __shared__ __align__(16) uint2 rv[2][2][kRgCap];   // prefetched ranges (reference, source)
   __shared__ __align__(16) uint2 fb[kBatchCap + 1];  // overflow-path ranges
   __shared__ __align__(8) uint64_t full[kBufQ], empty[kBufQ], rbar[2];
@@ -813,7 +816,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         // kind 1 packed events: upper half of the record buffer (slot v at byte
         // 8 * (kStageQ + v) > 16 * v for every record slot v < split)
         uint2* s8e = reinterpret_cast<uint2*>(s16) + kStageQ;
-        uint32_t* fk = fake[b];
+        const int ms = (int)(it % (2 * kBufQ));  // metadata set of this round
+        uint32_t* fk = fake[ms];
         // the ranges that intersect this round: [la, lb) (prefixes are monotone)
         int la = 0, lb = nl;
         {
@@ -859,7 +863,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           bytes += (uint32_t)((a1 - a0) * 8);
         }
         bytes = warp_sum_u32(bytes);
-        if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
         for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
         __syncwarp();
         for (int l = la + lane; l < lb; l += 32) {
@@ -874,11 +877,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             atomicOr(fk + (q >> 5), 1u << (q & 31));
         }
         if (lane == 0) {
-          desc[b].n = nslots;
-          desc[b].split = n0 < la ? 0u : (n0 < lb ? roff[n0] : nslots);
-          desc[b].r = g;
-          desc[b].last = (final && rb + capv >= total) ? 1 : 0;
+          desc[ms].n = nslots;
+          desc[ms].split = n0 < la ? 0u : (n0 < lb ? roff[n0] : nslots);
+          desc[ms].r = g;
+          desc[ms].last = (final && rb + capv >= total) ? 1 : 0;
         }
+        __syncwarp();
+        // only now wait for the buffer itself (consumers done with round it - 2)
+        if (it >= kBufQ) mbar_wait(&empty[b], ((it / kBufQ) - 1) & 1);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive_expect_tx(&full[b], bytes);
@@ -986,11 +992,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const int b = (int)(it % kBufQ);
     mbar_wait(&full[b], (it / kBufQ) & 1);
     if (it == 0) gsc = ldexp(1.0, s_kbits - e2);
-    const BRound d = desc[b];
+    const int ms = (int)(it % (2 * kBufQ));  // metadata set of this round
+    const BRound d = desc[ms];
     const uint4* s16 = stage16 + b * kStageQ;
     const float2* s8 = stage8 + b * kStageQ;
     const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
-    const uint32_t* fk = fake[b];
+    const uint32_t* fk = fake[ms];
     const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
     // (prime group: re-formed from blockIdx.z here rather than kept live)
     const int lo_bin = kGrouped && d.r == (int)blockIdx.z * B / (int)gridDim.z ? d.r : 0;
