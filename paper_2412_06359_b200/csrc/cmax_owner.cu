@@ -397,10 +397,15 @@ __device__ __forceinline__ uint4 make_rec(const Cell& c, uint32_t dt, int pol) {
 // of the interior references 1..B-1 are the ones the flow sampling of the next
 // step computes anyway, so only references 0 and B need their own bilin_cell.
 // rec[r * stride] receives the record of reference r. Returns alive.
+// Records go straight to global memory (plane r of `grec`, stride n_total; a
+// warp's lanes mostly share j, so the stores of a step mostly share a plane) and
+// the cell of every reference to shared memory (scell[r * stride], for the box
+// reduction that needs all lanes at the same reference).
 __device__ __forceinline__ bool trajectory_records(double x0, double y0, double t, int j,
                                                    const double2* __restrict__ flows,
                                                    const WinParams& P, const double* es,
-                                                   uint4* rec, int stride, uint32_t dtu, int pol) {
+                                                   uint4* grec, uint64_t gstride, uint32_t* scell,
+                                                   int stride, uint32_t dtu, int pol) {
   const int W = P.W, H = P.H, B = P.B, HW = P.HW;
   const Cell c0 = bilin_cell(x0, y0, W, H);
   const double2 u0 = sample_flow(flows + (size_t)j * HW, c0);
@@ -416,14 +421,21 @@ __device__ __forceinline__ bool trajectory_records(double x0, double y0, double 
     const double2 p = back ? pb : pf;
     const double dt = back ? ds(es[i], es[i + 1]) : ds(es[i + 1], es[i]);
     const Cell c = bilin_cell(p.x, p.y, W, H);
-    rec[(back ? i + 1 : i) * stride] = make_rec(c, dtu, pol);
+    const int rr = back ? i + 1 : i;
+    const uint4 rv = make_rec(c, dtu, pol);
+    grec[rr * gstride] = rv;
+    scell[rr * stride] = rv.x;
     const double2 u = sample_flow(flows + (size_t)i * HW, c);
     const double2 q = make_double2(da(p.x, dm(dt, u.x)), da(p.y, dm(dt, u.y)));
     ok = ok && in_bounds(q.x, q.y, W, H);
     if (back) pb = q; else pf = q;
   }
-  rec[0] = make_rec(bilin_cell(pb.x, pb.y, W, H), dtu, pol);  // pb = pos[0]
-  rec[B * stride] = make_rec(bilin_cell(pf.x, pf.y, W, H), dtu, pol);  // pf = pos[B]
+  const uint4 r0 = make_rec(bilin_cell(pb.x, pb.y, W, H), dtu, pol);  // pb = pos[0]
+  const uint4 rB = make_rec(bilin_cell(pf.x, pf.y, W, H), dtu, pol);  // pf = pos[B]
+  grec[0] = r0;
+  scell[0] = r0.x;
+  grec[B * gstride] = rB;
+  scell[B * stride] = rB.x;
   return ok;
 }
 
@@ -435,7 +447,7 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
   extern __shared__ __align__(16) unsigned char smem[];
   double* es = reinterpret_cast<double*>(smem);
   uint32_t* erel = reinterpret_cast<uint32_t*>(es + kMaxRefs);
-  uint4* srec = reinterpret_cast<uint4*>(smem + kEvSmemHeader) + threadIdx.x;  // [r][thread]
+  uint32_t* scell = reinterpret_cast<uint32_t*>(smem + kEvSmemHeader) + threadIdx.x;  // [r][thread]
   for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
     es[i] = P.es[i];
     erel[i] = P.erel[i];
@@ -457,8 +469,9 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
     const double t = dm((double)dt, 1e-6);
     j = bin_of(dt, erel, P.B);
     alive = trajectory_records((double)ev_x(e), (double)ev_y(e), t, j,
-                               flows + (size_t)w * P.B * P.HW, P, es, srec, blockDim.x, dt,
-                               ev_pol(e));
+                               flows + (size_t)w * P.B * P.HW, P, es,
+                               reinterpret_cast<uint4*>(recs) + base + k, n_total, scell,
+                               blockDim.x, dt, ev_pol(e));
     S = (int)sorted_keys[base + k];  // sort tile of this slot
   }
   const unsigned amask = __ballot_sync(kFull, alive);
@@ -477,11 +490,14 @@ __global__ void __launch_bounds__(kEvBlock) k_traj_records(
       atomicMin(&b->w, cmy);
     }
   };
+  // a dead (left the sensor) event's records are rewritten dead
   const uint4 dead = make_uint4(kDead, 0u, 0u, 0u);
   for (int r = 0; r < R; ++r) {
-    const uint4 rv = alive ? srec[r * blockDim.x] : dead;
-    if (valid) reinterpret_cast<uint4*>(recs)[(size_t)r * n_total + base + k] = rv;
-    if (alive) box_update(peers, leader, r, rv.x & 0xffffu, (rv.x >> 16) & 0x7fffu);
+    if (valid && !alive) reinterpret_cast<uint4*>(recs)[(size_t)r * n_total + base + k] = dead;
+    if (alive) {
+      const uint32_t cell = scell[r * blockDim.x];
+      box_update(peers, leader, r, cell & 0xffffu, (cell >> 16) & 0x7fffu);
+    }
   }
   // source-pixel boxes per bin (the partial steps of the backward sink at x0)
   if (alive) {
@@ -700,7 +716,7 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                          uint64_t n_total, FwdRec* recs, uint4* bbox, uint32_t* lcount,
                          uint16_t* lists) {
   static size_t a = 0;
-  const size_t smem = kEvSmemHeader + sizeof(uint4) * (size_t)(P.B + 1) * kEvBlock;
+  const size_t smem = kEvSmemHeader + sizeof(uint32_t) * (size_t)(P.B + 1) * kEvBlock;
   set_smem(reinterpret_cast<const void*>(k_traj_records), smem, &a);
   if (max_n > 0) {
     count_launch();
