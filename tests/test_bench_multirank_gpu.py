@@ -28,3 +28,29 @@ def test_two_ranks_on_one_gpu():
     assert d["config"]["windows_per_gpu_per_step"] == 2
     # the all-reduced loss sums both ranks' windows; rank 0's own sum is smaller
     assert d["check"]["reduced_loss"] > d["check"]["sum_loss_last_step"] > 0
+
+
+def test_bench_line_contract():
+    """One rank, small workload: the JSON line carries the contract's keys --
+    roofline (bound/achieved/peak/unit/frac/traffic + the ceilings entry),
+    cpu_baseline (the reference compiled here, on this box's cores), e2e with the
+    copied bytes, gpu_launches, clocks -- and the values are consistent."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "B",
+                        "--steps", "3", "--warmup", "3", "--cpu-budget-s", "2"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= d["steps"] * 10  # the owner chain's kernels, every step
+    assert d["value"] > 100 * d["cpu_baseline"]["value"]
