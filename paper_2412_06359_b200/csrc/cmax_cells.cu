@@ -301,6 +301,18 @@ __device__ __forceinline__ void fx_add(uint32_t a_lo, uint32_t a_hi, unsigned lo
       "r"(a_hi), "l"(q)
       : "memory");
 }
+// 1 / x to within 1 ulp (MUFU.RCP64H seed + two Newton steps), for x > 0 normal:
+// the epilogues' reciprocals feed the loss, coefficients and gradients, which are
+// tolerance-checked (1e-5), so they need not be the correctly rounded 1.0 / x
+// (__drcp_rn is a longer sequence with a slow path)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 // round-to-nearest-even integer conversions by the 2^52 "magic number": adding
 // 2^52 (1.5 * 2^52) to x leaves round(x) in the low mantissa bits -- one DADD and
 // an integer subtract instead of the F2I.64 conversion (a quarter-rate pipe).
@@ -635,7 +647,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         const int g = py * W + px;
         actv += (flag[o] || C0 > 0.0 || C1 > 0.0) ? 1u : 0u;  // refresh_active: some w > 0
         // correctly rounded reciprocals (== 1.0 / x, without the general divide)
-        const double i0 = __drcp_rn(C0 + kLossEps), i1 = __drcp_rn(C1 + kLossEps);
+        const double i0 = rcp_fast(C0 + kLossEps), i1 = rcp_fast(C1 + kLossEps);
         const double c0 = S0 * i0, c1 = S1 * i1;
         lsum += c0 * c0 + c1 * c1;
         double2* cwp = coef + ((size_t)w * R + r) * 2 * HW;
@@ -721,9 +733,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
     const uint2* __restrict__ ranges, const int* __restrict__ no_surv,
     const double* __restrict__ depth, const uint8_t* __restrict__ mask,
-    const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy,
-    double* __restrict__ d_depth, double* __restrict__ dbin, double* __restrict__ pose_part,
-    double* __restrict__ grad_out) {
+    const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy, double ifx,
+    double ify, double* __restrict__ d_depth, double* __restrict__ dbin,
+    double* __restrict__ pose_part, double* __restrict__ grad_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* stage16 = reinterpret_cast<uint4*>(smem);                          // [kBufQ][kStageQ] records
   float2* stage8 = reinterpret_cast<float2*>(stage16 + kBufQ * kStageQ);    // [kBufQ][kStageQ] values
@@ -753,9 +765,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
   const bool run = !no_surv[w];
   // this CTA's bins [i0, i1); group gs = max(i0, 1) primes bin i0 when i0 > 0
-  const int i0 = kGrouped ? (int)blockIdx.z * B / (int)gridDim.z : 0;
-  const int i1 = kGrouped ? ((int)blockIdx.z + 1) * B / (int)gridDim.z : B;
-  const int gs = i0 > 0 ? i0 : 1, prime_r = kGrouped && i0 > 0 ? i0 : -1;
+  // (functions of blockIdx, re-formed where used rather than kept live)
+  auto bin_lo = [&]() { return kGrouped ? (int)blockIdx.z * P.B / (int)gridDim.z : 0; };
+  auto bin_hi = [&]() { return kGrouped ? ((int)blockIdx.z + 1) * P.B / (int)gridDim.z : P.B; };
+  auto first_group = [&]() { return bin_lo() > 0 ? bin_lo() : 1; };
+  auto prime_group = [&]() { return kGrouped && bin_lo() > 0 ? bin_lo() : -1; };
 
   for (int i = tid; i < 8 * kPlane; i += kBwdThreads) acc[i] = 0u;
   if (tid == 0) {
@@ -782,7 +796,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     auto prefetch = [&](int g) {  // warp 0 only
       const size_t gref = ((size_t)w * NS + g) * TP.oT + T;
       const size_t gsrc = ((size_t)w * NS + R + g - 1) * TP.oT + T;
-      const int q = (g - gs) & 1;
+      const int q = (g - first_group()) & 1;
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
@@ -943,13 +957,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
       __syncwarp();
     }
     if (run) {
-      if (pw == 0) prefetch(gs);
-      for (int g = gs; g <= i1; ++g) {
+      if (pw == 0) prefetch(first_group());
+      for (int g = first_group(); g <= bin_hi(); ++g) {
         pair_sync();  // both producers are done with the ranges of group g - 1
-        if (pw == 0 && g + 1 <= i1) prefetch(g + 1);
-        const int q = (g - gs) & 1;
-        mbar_wait(&rbar[q], ((g - gs) >> 1) & 1);
-        const bool prime = g == prime_r;  // record sinks of reference g only, bin g not complete
+        if (pw == 0 && g + 1 <= bin_hi()) prefetch(g + 1);
+        const int q = (g - first_group()) & 1;
+        mbar_wait(&rbar[q], ((g - first_group()) >> 1) & 1);
+        const bool prime = g == prime_group();  // record sinks of reference g only, bin g not complete
         const uint2* va = g < B ? rv[q][0] : nullptr;
         const uint2* vb = prime ? nullptr : rv[q][1];
         const bool oa = va && va[0].x == kOverflow, ob = vb && vb[0].x == kOverflow;
@@ -972,7 +986,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         }
       }
     } else {  // no survivors: every bin is zero, still finish each one
-      for (int g = i0 + 1; g <= i1; ++g) rounds(make_cat(nullptr, nullptr), g, true, false);
+      for (int g = bin_lo() + 1; g <= bin_hi(); ++g) rounds(make_cat(nullptr, nullptr), g, true, false);
     }
     return;
   }
@@ -987,7 +1001,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
   double gsc = 0.0;
   double dd = 0.0;  // d_depth of this pixel, bins summed in order
   uint32_t it = 0;
-  const int n_bins = i1 - i0;
+  const int n_bins = bin_hi() - bin_lo();
   for (int done = 0; done < n_bins;) {
     const int b = (int)(it % kBufQ);
     mbar_wait(&full[b], (it / kBufQ) & 1);
@@ -1089,14 +1103,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         const bool dok = depth && pose_tab && (!mask || mask[(size_t)w * HW + gq]) && dpx > 0.0;
         if (dok && (gu != 0.0 || gv != 0.0)) {
           // backproject(x, 1.0, k) (geometry.hpp:147-149)
-          const double rx = 1.0 * ((double)px - cx) / fx, ry = 1.0 * ((double)py - cy) / fy;
+          // (times the reciprocal focal lengths: within 1 ulp of the division)
+          const double rx = ((double)px - cx) * ifx, ry = ((double)py - cy) * ify;
           const double* ptab = pose_tab + ((size_t)w * B + i) * kPoseTab;
           const double rr0 = ptab[0] * rx + ptab[1] * ry + ptab[2];
           const double rr1 = ptab[3] * rx + ptab[4] * ry + ptab[5];
           const double rr2 = ptab[6] * rx + ptab[7] * ry + ptab[8];
           const double p0 = dpx * rr0 + ptab[36], p1 = dpx * rr1 + ptab[37], p2 = dpx * rr2 + ptab[38];
           if (p2 > 0.0) {
-            const double inv_dt = ptab[39], iz = __drcp_rn(p2);  // == 1.0 / p2 (correctly rounded)
+            const double inv_dt = ptab[39], iz = rcp_fast(p2);  // 1 / p2 to 1 ulp
             // reproject_with_grads (geometry.hpp:185-209) folded into the adjoint:
             // v = (gu du/dX, gv dv/dY, gu du/dZ + gv dv/dZ) / dt with du/dX = fx/Z,
             // du/dZ = -fx X/Z^2 (dv alike) -- the translation gradient; d_depth adds
@@ -1215,7 +1230,8 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
   auto* kern = groups > 1 ? k_bwd_cells<true> : k_bwd_cells<false>;
   kern<<<dim3(TP.oT, P.n_windows, groups), kBwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
-      no_surv, depth, mask, pose_tab, k0, k1, k2, k3, d_depth, dbin, pose_part, grad_out);
+      no_surv, depth, mask, pose_tab, k0, k1, k2, k3, 1.0 / k0, 1.0 / k1, d_depth, dbin, pose_part,
+      grad_out);
   if (dbin) {
     count_launch();
     const size_t n = (size_t)P.n_windows * P.HW;
