@@ -587,6 +587,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
     const FwdRec* sb = stage + b * kStageP;
     const double esr = P.es[d.r], iwin = P.inv_window;
     const double fsc = ldexp(1.0, d.fb);  // 2^fb, exact scaling
+    const double ifsc = ldexp(1.0, -d.fb);  // 2^-fb (exact; the epilogue's scale back)
     // splat_bilinear corners (warp.hpp:147-160) as exact fixed-point sums
     compacted<kFwdCons>(
         (uint32_t)cw * 32, d.n, wq[cw],
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
       const int px = ox0 + lx, py = oy0 + ly;
       const int o = ly * kRowW + lx;
       if (px < W && py < H) {
-        const double ifs = 1.0 / fsc;  // 2^-fb
+        const double ifs = ifsc;  // 2^-fb
         const double C0 = (double)fx_read(acc + o, acc + kPlane + o) * ifs;
         const double S0 = (double)fx_read(acc + 2 * kPlane + o, acc + 3 * kPlane + o) * ifs;
         const double C1 = (double)fx_read(acc + 4 * kPlane + o, acc + 5 * kPlane + o) * ifs;
