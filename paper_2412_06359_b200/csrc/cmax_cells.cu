@@ -397,6 +397,46 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
   }
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (P.B + 1);
+  if (slot < R && cnt <= 32u) {
+    // reference slot: the records of consecutive sort tiles are contiguous
+    // (tile_ptr order), so the list is sorted (rank by counting, ids are
+    // distinct) and every run S, S+1, ... becomes ONE range -- an owner tile's
+    // row of sort tiles is one bulk copy instead of one per tile
+    const uint32_t S = lane < (int)cnt ? lists[gid * kListCapO + lane] : 0xffffffffu;
+    uint32_t rank = 0;
+    for (uint32_t m = 0; m < cnt; ++m) rank += __shfl_sync(kFull, S, (int)m) < S ? 1u : 0u;
+    // lane k gets the k-th smallest id: the lane whose rank is k
+    uint32_t sk = 0xffffffffu;
+    for (uint32_t m = 0; m < cnt; ++m) {
+      const uint32_t rm = __shfl_sync(kFull, rank, (int)m), vm = __shfl_sync(kFull, S, (int)m);
+      if (rm == (uint32_t)lane) sk = vm;
+    }
+    const uint32_t prev = __shfl_up_sync(kFull, sk, 1);
+    const bool valid = lane < (int)cnt;
+    const bool start = valid && (lane == 0 || sk != prev + 1u);
+    const unsigned starts = __ballot_sync(kFull, start);
+    const int nr = __popc(starts);
+    // run of this start lane: [sk, last] with last = the id before the next start
+    const int ridx = __popc(starts & ((1u << lane) - 1u));
+    const unsigned later = starts & ~((2u << lane) - 1u);  // starts after this lane
+    const int next_start = later ? __ffs(later) - 1 : (int)cnt;
+    const uint32_t last = __shfl_sync(kFull, sk, max(next_start - 1, 0));
+    uint32_t lo = 0, len = 0;
+    if (start) {
+      lo = tp[sk];
+      len = tp[last + 1] - lo;
+    }
+    // prefix of the run lengths in run order (runs are in increasing lane order)
+    uint32_t x = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (start) out[1 + ridx] = make_uint2(lo, x - len);
+    const uint32_t tot = __shfl_sync(kFull, x, 31);
+    if (lane == 0) out[0] = make_uint2((uint32_t)nr, tot);
+    return;
+  }
   uint32_t carry = 0;
   for (uint32_t l0 = 0; l0 < cnt; l0 += 32) {
     const uint32_t l = l0 + lane;
