@@ -382,7 +382,8 @@ __device__ __forceinline__ void batch_to_view(const Batch& bt, uint2* fb) {
 
 __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
                          const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ bin_ptr,
-                         WinParams P, TileParams TP, uint2* __restrict__ ranges) {
+                         const uint32_t* __restrict__ srcbase, WinParams P, TileParams TP,
+                         uint2* __restrict__ ranges) {
   const int lane = threadIdx.x & 31;
   const size_t gid = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int NS = 2 * P.B + 1, R = P.B + 1;
@@ -397,11 +398,21 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
   }
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (P.B + 1);
-  if (slot < R && cnt <= 32u) {
-    // reference slot: the records of consecutive sort tiles are contiguous
-    // (tile_ptr order), so the list is sorted (rank by counting, ids are
-    // distinct) and every run S, S+1, ... becomes ONE range -- an owner tile's
-    // row of sort tiles is one bulk copy instead of one per tile
+  const int sb = slot - R;  // source slot: bin
+  const uint32_t* src_b = srcbase + ((size_t)w * P.B + (sb >= 0 ? sb : 0)) * TP.nT;
+  // first position and length of sort tile S's candidates: its records at the
+  // reference (tile order), or the source sinks of its events of bin sb in the
+  // (bin, tile, time) layout (k_src_base)
+  auto lo_of = [&](uint32_t S) { return slot < R ? tp[S] : src_b[S]; };
+  auto len_of = [&](uint32_t S) {
+    return slot < R ? tp[S + 1] - tp[S]
+                    : bp[(size_t)S * (P.B + 1) + sb + 1] - bp[(size_t)S * (P.B + 1) + sb];
+  };
+  if (cnt <= 32u) {
+    // the candidates of consecutive sort tiles are contiguous (tile order in
+    // both layouts), so the list is sorted (rank by counting, ids are distinct)
+    // and every run S, S+1, ... becomes ONE range -- an owner tile's row of
+    // sort tiles is one bulk copy instead of one per tile
     const uint32_t S = lane < (int)cnt ? lists[gid * kListCapO + lane] : 0xffffffffu;
     uint32_t rank = 0;
     for (uint32_t m = 0; m < cnt; ++m) rank += __shfl_sync(kFull, S, (int)m) < S ? 1u : 0u;
@@ -423,8 +434,8 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
     const uint32_t last = __shfl_sync(kFull, sk, max(next_start - 1, 0));
     uint32_t lo = 0, len = 0;
     if (start) {
-      lo = tp[sk];
-      len = tp[last + 1] - lo;
+      lo = lo_of(sk);
+      len = lo_of(last) + len_of(last) - lo;
     }
     // prefix of the run lengths in run order (runs are in increasing lane order)
     uint32_t x = len;
@@ -442,17 +453,9 @@ __global__ void k_ranges(const uint32_t* __restrict__ lcount, const uint16_t* __
     const uint32_t l = l0 + lane;
     uint32_t lo = 0, len = 0;
     if (l < cnt) {
-      const int S = lists[gid * kListCapO + l];
-      uint32_t hi;
-      if (slot < R) {  // reference slot: every event of the sort tile
-        lo = tp[S];
-        hi = tp[S + 1];
-      } else {  // source slot of bin i: the tile's events of bin i (time-sorted)
-        const uint32_t* b = bp + (size_t)S * (P.B + 1);
-        lo = b[slot - R];
-        hi = b[slot - R + 1];
-      }
-      len = hi - lo;
+      const uint32_t S = lists[gid * kListCapO + l];
+      lo = lo_of(S);
+      len = len_of(S);
     }
     uint32_t x = len;
     for (int o = 1; o < 32; o <<= 1) {
@@ -772,7 +775,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const FwdRec* __restrict__ recs, const float2* __restrict__ vals, uint64_t n_total,
     const uint32_t* __restrict__ gmax, const uint4* __restrict__ bbox,
     const uint32_t* __restrict__ lcount, const uint16_t* __restrict__ lists,
-    const uint2* __restrict__ ranges, const int* __restrict__ no_surv,
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ srcbase,
+    const uint4* __restrict__ srcrec, const int* __restrict__ no_surv,
     const double* __restrict__ depth, const uint8_t* __restrict__ mask,
     const double* __restrict__ pose_tab, double fx, double fy, double cx, double cy, double ifx,
     double ify, double* __restrict__ d_depth, double* __restrict__ dbin,
@@ -851,7 +855,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     auto rounds = [&](const Cat& cv, int g, bool final, bool all) {
       const FwdRec* rr = recs + (size_t)min(g, B) * n_total + base;
       const float2* v0 = vals + (size_t)(g - 1) * n_total;  // sinks at reference g
-      const float2* v1 = vals + (size_t)(B - 1) * n_total;  // source-pixel sinks
+      const uint4* v1 = srcrec + base;  // source-pixel sinks with their events ((bin, tile) order)
       const int nl = cv.nl(), n0 = cv.n0;
       const uint32_t total = cv.total();
       // virtual candidates per round, leaving room for <= 3 slack slots per range
@@ -868,9 +872,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
         uint32_t* const roff = roffs[pw];
         uint4* s16 = stage16 + b * kStageQ;
         float2* s8 = stage8 + b * kStageQ;
-        // kind 1 packed events: upper half of the record buffer (slot v at byte
-        // 8 * (kStageQ + v) > 16 * v for every record slot v < split)
-        uint2* s8e = reinterpret_cast<uint2*>(s16) + kStageQ;
         const int ms = (int)(it % (2 * kBufQ));  // metadata set of this round
         uint32_t* fk = fake[ms];
         // the ranges that intersect this round: [la, lb) (prefixes are monotone)
@@ -889,14 +890,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           }
           lb = a;
         }
-        // region offsets: exclusive scan of roundup2(len + 2) over the ranges
+        // region offsets: exclusive scan of roundup2(len + 2) over the record
+        // ranges (their 8 B values are copied as 16 B-aligned supersets) and of
+        // len over the source ranges (16 B records, no slack)
         uint32_t carry = 0;
         for (int l0 = la; l0 < lb; l0 += 32) {
           const int l = l0 + lane;
           uint32_t sz = 0;
           if (l < lb) {
             const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
-            sz = lo < hi ? ((hi - lo + 3) & ~1u) : 0u;
+            sz = lo < hi ? (l < n0 ? ((hi - lo + 3) & ~1u) : hi - lo) : 0u;
           }
           uint32_t x = sz;
           for (int o = 1; o < 32; o <<= 1) {
@@ -914,13 +917,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
           const uint64_t a0 = (base + k0) & ~1ull, a1 = (base + k0 + len + 1) & ~1ull;
-          bytes += (uint32_t)(l < n0 ? len * sizeof(FwdRec) : (a1 - a0) * 8);
-          bytes += (uint32_t)((a1 - a0) * 8);
+          bytes += (uint32_t)(len * 16) + (l < n0 ? (uint32_t)((a1 - a0) * 8) : 0u);
         }
         bytes = warp_sum_u32(bytes);
         for (int q = lane; q < kStageQ / 32; q += 32) fk[q] = 0u;
         __syncwarp();
-        for (int l = la + lane; l < lb; l += 32) {
+        for (int l = la + lane; l < min(lb, n0); l += 32) {
           const uint32_t lo = max(cv.pre(l), rb), hi = min(cv.pre(l + 1), rb + capv);
           if (lo >= hi) continue;
           const uint64_t k0 = cv.rng(l) + (lo - cv.pre(l)), len = hi - lo;
@@ -955,8 +957,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             bulk_g2s(s8 + s0, v0 + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
             bulk_g2s(s16 + s0 + par, rr + k0, (uint32_t)(len * sizeof(FwdRec)), &full[b]);
           } else {
-            bulk_g2s(s8 + s0, v1 + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
-            bulk_g2s(s8e + s0, sorted + a0, (uint32_t)((a1 - a0) * 8), &full[b]);
+            bulk_g2s(s16 + s0, v1 + k0, (uint32_t)(len * 16), &full[b]);
           }
         }
         ++it;
@@ -976,7 +977,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
                       [&](int, int S) {
                         if (kind == 0) return make_uint2(tp[S], tp[S + 1]);
                         const uint32_t* b = bp + (size_t)S * (B + 1);
-                        return make_uint2(b[g - 1], b[g]);
+                        const uint32_t lo = srcbase[((size_t)w * B + g - 1) * TP.nT + S];
+                        return make_uint2(lo, lo + b[g] - b[g - 1]);
                       });
         more = bt.more;
         batch_to_view(bt, fb);
@@ -1051,7 +1053,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
     const BRound d = desc[ms];
     const uint4* s16 = stage16 + b * kStageQ;
     const float2* s8 = stage8 + b * kStageQ;
-    const uint2* s8e = reinterpret_cast<const uint2*>(s16) + kStageQ;
     const uint32_t* fk = fake[ms];
     const uint32_t er = P.erel[d.r < B ? d.r : B];  // the sink test's threshold for this round
     // (prime group: re-formed from blockIdx.z here rather than kept live)
@@ -1094,15 +1095,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2) k_bwd_cells(
             }
           }
         });
-    // source-pixel sinks of bin d.r - 1 (slots >= split): weight 1 at the event's pixel
+    // source-pixel sinks of bin d.r - 1 (slots >= split): weight 1 at the event's
+    // pixel; each slot a 16 B {packed event, gx, gy} record, no slack slots
     {
       const uint32_t pt = acc_s + (uint32_t)((d.r - 1) & 1) * (4 * kPlane * 4);
       for (uint32_t v = d.split + ct; v < d.n; v += kCons) {
-        if ((fk[v >> 5] >> (v & 31)) & 1u) continue;
-        const uint2 e = s8e[v];
+        const uint4 sr = s16[v];
+        const uint2 e = make_uint2(sr.x, sr.y);
         const int lx = ev_x(e) - ox0, ly = ev_y(e) - oy0;
         if (lx < 0 || lx >= kOwnW || ly < 0 || ly >= kOwnH) continue;
-        const float2 g = s8[v];
+        const float2 g = make_float2(__uint_as_float(sr.z), __uint_as_float(sr.w));
         if (g.x == 0.f && g.y == 0.f) continue;
         const uint32_t a = pt + 4u * (uint32_t)(ly * kRowW + lx);
         fx_add(a, a + 4 * kPlane, fx_qs((double)g.x * gsc));
@@ -1255,9 +1257,10 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
                       const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
-                      const int* no_surv, const double* depth, const uint8_t* mask,
-                      const double* pose_tab, const double* K, double* d_depth, double* pose_part,
-                      double* grad_out, int groups, double* dbin) {
+                      const uint32_t* srcbase, const uint4* srcrec, const int* no_surv,
+                      const double* depth, const uint8_t* mask, const double* pose_tab,
+                      const double* K, double* d_depth, double* pose_part, double* grad_out,
+                      int groups, double* dbin) {
   const double k0 = K ? K[0] : 1.0, k1 = K ? K[1] : 1.0, k2 = K ? K[2] : 0.0, k3 = K ? K[3] : 0.0;
   static bool attr = false;
   if (!attr) {
@@ -1271,7 +1274,7 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
   auto* kern = groups > 1 ? k_bwd_cells<true> : k_bwd_cells<false>;
   kern<<<dim3(TP.oT, P.n_windows, groups), kBwdThreads, bwd_cells_smem(), s>>>(
       sorted, ev_off, P, TP, tile_ptr, bin_ptr, recs, bwd, n_total, gmax, bbox, lcount, lists, ranges,
-      no_surv, depth, mask, pose_tab, k0, k1, k2, k3, 1.0 / k0, 1.0 / k1, d_depth, dbin, pose_part,
+      srcbase, srcrec, no_surv, depth, mask, pose_tab, k0, k1, k2, k3, 1.0 / k0, 1.0 / k1, d_depth, dbin, pose_part,
       grad_out);
   if (dbin) {
     count_launch();
@@ -1299,12 +1302,12 @@ int owner_groups(const TileParams& TP, const WinParams& P, bool backward) {
 }
 
 void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,
-                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const WinParams& P,
-                   const TileParams& TP, uint2* ranges) {
+                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const uint32_t* srcbase,
+                   const WinParams& P, const TileParams& TP, uint2* ranges) {
   const size_t lists_n = (size_t)P.n_windows * (2 * P.B + 1) * TP.oT;
   count_launch();
-  k_ranges<<<(unsigned)((lists_n * 32 + 255) / 256), 256, 0, s>>>(lcount, lists, tile_ptr, bin_ptr, P,
-                                                                  TP, ranges);
+  k_ranges<<<(unsigned)((lists_n * 32 + 255) / 256), 256, 0, s>>>(lcount, lists, tile_ptr, bin_ptr,
+                                                                  srcbase, P, TP, ranges);
 }
 
 }  // namespace evcm_b200

@@ -384,6 +384,51 @@ __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __re
   }
 }
 
+// Source-sink layout (bin, tile, time): srcbase[w][b][S] = window-relative
+// position of the first source sink of sort tile S's events of bin b, so that
+// the events of bin b of consecutive sort tiles are contiguous and the backward
+// owner's source ranges merge like its record ranges (k_ranges). One CTA per
+// window, the bins one after another, each an exclusive scan over the tiles of
+// the per-(tile, bin) counts from bin_ptr.
+__global__ void __launch_bounds__(1024) k_src_base(const uint32_t* __restrict__ bin_ptr,
+                                                   WinParams P, TileParams TP,
+                                                   uint32_t* __restrict__ srcbase) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t s_carry;
+  const int w = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, B = P.B;
+  const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int b = 0; b < B; ++b) {
+    uint32_t* out = srcbase + ((size_t)w * B + b) * TP.nT;
+    for (int c = 0; c < TP.nT; c += blockDim.x) {
+      const int S = c + threadIdx.x;
+      const uint32_t v = S < TP.nT ? bp[(size_t)S * (B + 1) + b + 1] - bp[(size_t)S * (B + 1) + b] : 0u;
+      uint32_t x = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) warp_tot[wid] = x;
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t q = warp_tot[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, q, o);
+          if (lane >= o) q += y;
+        }
+        warp_tot[lane] = q;
+      }
+      __syncthreads();
+      const uint32_t excl = s_carry + x - v + (wid > 0 ? warp_tot[wid - 1] : 0u);
+      if (S < TP.nT) out[S] = excl;
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+      __syncthreads();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // trajectories -> splat records + per-(sort tile, slot) cell boxes
 
@@ -553,7 +598,9 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
     const FwdRec* __restrict__ recs, uint64_t n_total, const double2* __restrict__ coef,
     const double* __restrict__ scale_tab, const int* __restrict__ no_surv,
-    float2* __restrict__ bwd, uint32_t* __restrict__ gmax) {
+    const uint32_t* __restrict__ sorted_keys, const uint32_t* __restrict__ bin_ptr,
+    const uint32_t* __restrict__ srcbase, uint4* __restrict__ srcrec, float2* __restrict__ bwd,
+    uint32_t* __restrict__ gmax) {
   __shared__ double es[kMaxRefs];
   __shared__ uint32_t erel[kMaxRefs];
   for (int i = threadIdx.x; i <= P.B; i += blockDim.x) {
@@ -569,18 +616,25 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
   if (k >= n) return;
   const FwdRec* rk = recs + base + k;  // + r * n_total
   // sink values: bwd[(r - 1) * n_total + slot] for the sink at reference r in
-  // 1..B-1 (each is the sink of exactly one bin: r - 1 if r <= j, else r), and
-  // bwd[(B - 1) * n_total + slot] for the source-pixel sink of bin j
-  if (rk[0].cell == kDead) {  // masked event: contributes nothing (engine.hpp:564)
-    bwd[(size_t)(P.B - 1) * n_total + base + k] = make_float2(0.f, 0.f);
-    return;
-  }
+  // 1..B-1 (each is the sink of exactly one bin: r - 1 if r <= j, else r); the
+  // source-pixel sink of bin j goes with the packed event to srcrec at its
+  // (bin, tile, time) position (k_src_base)
   const int B = P.B, R = B + 1, W = P.W, H = P.H, HW = P.HW;
-  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const uint2 e = sorted[base + k];
   const uint32_t dt_us = ev_dt(e);
-  const double t = dm((double)dt_us, 1e-6);
   const int j = bin_of(dt_us, erel, B);
+  uint4* src_out;
+  {
+    const uint32_t S = sorted_keys[base + k];
+    const uint32_t b0 = bin_ptr[((size_t)w * TP.nT + S) * (B + 1) + j];
+    src_out = srcrec + base + srcbase[((size_t)w * B + j) * TP.nT + S] + ((uint32_t)k - b0);
+  }
+  if (rk[0].cell == kDead) {  // masked event: contributes nothing (engine.hpp:564)
+    *src_out = make_uint4(e.x, e.y, 0u, 0u);
+    return;
+  }
+  const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
+  const double t = dm((double)dt_us, 1e-6);
   const int pol = ev_pol(e);
   const double2* cpw = coef + ((size_t)w * R * 2 + pol) * HW;  // + r*2*HW
   const double* sc = scale_tab + (size_t)w * R;
@@ -625,7 +679,7 @@ __global__ void __launch_bounds__(kEvBlock) k_bwd_event(
   }
   const double cb = es[j] - t, cf = es[j + 1] - t;
   const float2 o = make_float2((float)(cb * gb.x + cf * gf.x), (float)(cb * gb.y + cf * gf.y));
-  bo[(size_t)(B - 1) * n_total] = o;
+  *src_out = make_uint4(e.x, e.y, __float_as_uint(o.x), __float_as_uint(o.y));
   gm = fmaxf(gm, fmaxf(fabsf(o.x), fabsf(o.y)));
   // window max |value|: the fixed-point scale of the backward owner (cmax_cells.cu)
   const unsigned am = __activemask();
@@ -674,7 +728,8 @@ void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
                  const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
-                 uint32_t* bin_ptr, uint4* bbox, size_t n_bbox, uint32_t* lcount, size_t n_lcount) {
+                 uint32_t* bin_ptr, uint32_t* srcbase, uint4* bbox, size_t n_bbox,
+                 uint32_t* lcount, size_t n_lcount) {
   static size_t a1 = 0, a2 = 0;
   // many sort tiles: 4 warps per CTA, so the per-warp tile counts (2 B per tile)
   // leave room for more resident CTAs (measured: -9 % sort at 640x480)
@@ -708,6 +763,10 @@ if (sc_threads == kScatterThreads)
   count_launch();
   k_bin_ptr<<<dim3((TP.nT + 7) / 8, P.n_windows), 256, 0, s>>>(sorted, ev_off, P, TP,
                                                                     tile_ptr, bin_ptr);
+  if (srcbase) {
+    count_launch();
+    k_src_base<<<P.n_windows, 1024, 0, s>>>(bin_ptr, P, TP, srcbase);
+  }
 }
 
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
@@ -732,13 +791,15 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
-                      const double2* coef, const double* scale, const int* no_surv, float2* bwd,
-                      uint32_t* gmax) {
+                      const double2* coef, const double* scale, const int* no_surv,
+                      const uint32_t* sorted_keys, const uint32_t* bin_ptr, const uint32_t* srcbase,
+                      uint4* srcrec, float2* bwd, uint32_t* gmax) {
   cudaMemsetAsync(gmax, 0, (size_t)P.n_windows * sizeof(uint32_t), s);
   if (max_n == 0) return;
   count_launch();
   k_bwd_event<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, 0, s>>>(
-      sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, bwd, gmax);
+      sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, sorted_keys,
+      bin_ptr, srcbase, srcrec, bwd, gmax);
 }
 
 }  // namespace evcm_b200

@@ -46,8 +46,8 @@ void launch_stage_pack(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_
 void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, const WinParams& P,
                  const TileParams& TP, const double2* flows, uint64_t n_total, uint32_t* keys,
                  uint32_t* counts, uint32_t* tile_ptr, uint2* sorted, uint32_t* perm,
-                 uint32_t* bin_ptr, uint4* bbox = nullptr, size_t n_bbox = 0,
-                 uint32_t* lcount = nullptr, size_t n_lcount = 0);
+                 uint32_t* bin_ptr, uint32_t* srcbase = nullptr, uint4* bbox = nullptr,
+                 size_t n_bbox = 0, uint32_t* lcount = nullptr, size_t n_lcount = 0);
 void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                          const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                          const uint32_t* sorted_keys, uint64_t max_n, const double2* flows,
@@ -56,8 +56,9 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
                       uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
-                      const double2* coef, const double* scale, const int* no_surv, float2* bwd,
-                      uint32_t* gmax);
+                      const double2* coef, const double* scale, const int* no_surv,
+                      const uint32_t* sorted_keys, const uint32_t* bin_ptr, const uint32_t* srcbase,
+                      uint4* srcrec, float2* bwd, uint32_t* gmax);
 // Owner kernels with exact fixed-point shared-memory accumulation (cmax_cells.cu).
 void launch_fwd_cells(cudaStream_t s, const uint64_t* ev_off, const WinParams& P,
                       const TileParams& TP, const uint32_t* tile_ptr, const FwdRec* recs,
@@ -74,13 +75,14 @@ void launch_bwd_cells(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
                       const uint32_t* bin_ptr, const FwdRec* recs, const float2* bwd,
                       uint64_t n_total, const uint32_t* gmax, const uint4* bbox,
                       const uint32_t* lcount, const uint16_t* lists, const uint2* ranges,
-                      const int* no_surv, const double* depth, const uint8_t* mask,
-                      const double* pose_tab, const double* K, double* d_depth, double* pose_part,
-                      double* grad_out, int groups, double* dbin);
+                      const uint32_t* srcbase, const uint4* srcrec, const int* no_surv,
+                      const double* depth, const uint8_t* mask, const double* pose_tab,
+                      const double* K, double* d_depth, double* pose_part, double* grad_out,
+                      int groups, double* dbin);
 // Per (window, slot, owner tile) list: precomputed candidate ranges (kListCapO + 2
 // uint2 entries; see cmax_cells.cu)
 void launch_ranges(cudaStream_t s, const uint32_t* lcount, const uint16_t* lists,
-                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const WinParams& P,
-                   const TileParams& TP, uint2* ranges);
+                   const uint32_t* tile_ptr, const uint32_t* bin_ptr, const uint32_t* srcbase,
+                   const WinParams& P, const TileParams& TP, uint2* ranges);
 
 }  // namespace evcm_b200

@@ -526,7 +526,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   launch_sort(e->stream, e->get<uint2>("packed", 1), ev_off, P, TP, flows, total, keys,
               e->get<uint32_t>("sort_counts", (size_t)nw * TP.nT * TP.nchunks), tile_ptr, sorted,
               want_stack ? e->get<uint32_t>("perm", total) : nullptr,
-              e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)), bbox,
+              e->get<uint32_t>("bin_ptr", (size_t)nw * TP.nT * (P.B + 1)),
+              e->get<uint32_t>("srcbase", (size_t)nw * P.B * TP.nT), bbox,
               (size_t)nw * NS * TP.nT, lcount, nl);
   e->mark(3);
   FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
@@ -534,7 +535,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
   launch_traj_records(e->stream, sorted, ev_off, P, TP, tile_ptr, keys + total, e->max_n, flows,
                       total, recs, bbox, lcount, lists);
   uint2* ranges = e->get<uint2>("ranges", nl * (kListCapO + 2));
-  launch_ranges(e->stream, lcount, lists, tile_ptr, e->get<uint32_t>("bin_ptr", 1), P, TP, ranges);
+  launch_ranges(e->stream, lcount, lists, tile_ptr, e->get<uint32_t>("bin_ptr", 1),
+                e->get<uint32_t>("srcbase", 1), P, TP, ranges);
   e->mark(4);
   const size_t np = (size_t)nw * R * TP.oT;
   double2* stack = want_stack ? e->get<double2>("stack", (size_t)nw * R * 2 * P.HW) : nullptr;
@@ -565,18 +567,22 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   const uint2* sorted = e->get<uint2>("sorted", 1);
   const uint32_t* tile_ptr = e->get<uint32_t>("tile_ptr", 1);
   const FwdRec* recs = e->get<FwdRec>("recs", (size_t)R * total);
-  float2* bwd = e->get<float2>("bwdrec", (size_t)P.B * total);
+  float2* bwd = e->get<float2>("bwdrec", (size_t)std::max(1, P.B - 1) * total);  // record-sink values
   uint32_t* gmax = e->get<uint32_t>("gmax", (size_t)nw);
+  // source-pixel sinks with their packed events, (bin, tile, time) order
+  uint4* srcrec = e->get<uint4>("srcrec", total);
   launch_bwd_event(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, recs, total,
                    e->get<double2>("coef", 1), e->get<double>("scale", 1), e->get<int>("no_surv", 1),
-                   bwd, gmax);
+                   e->get<uint32_t>("sort_keys", 1) + total, e->get<uint32_t>("bin_ptr", 1),
+                   e->get<uint32_t>("srcbase", 1), srcrec, bwd, gmax);
   e->mark(7);
   double* pose_part =
       depth ? e->get<double>("pose_part_owner", (size_t)nw * TP.oT * P.B * kPoseSums) : nullptr;
   const int bgroups = owner_groups(TP, P, true);
   launch_bwd_cells(e->stream, sorted, ev_off, P, TP, tile_ptr, e->get<uint32_t>("bin_ptr", 1), recs,
                    bwd, total, gmax, e->get<uint4>("bbox", 1), e->get<uint32_t>("lcount", 1),
-                   e->get<uint16_t>("lists", 1), e->get<uint2>("ranges", 1), e->get<int>("no_surv", 1),
+                   e->get<uint16_t>("lists", 1), e->get<uint2>("ranges", 1),
+                   e->get<uint32_t>("srcbase", 1), srcrec, e->get<int>("no_surv", 1),
                    depth, mask, pose_tab,
                    K, depth ? d_depth : nullptr, pose_part, grad_out, bgroups,
                    bgroups > 1 && depth ? e->get<double>("dbin", (size_t)nw * P.B * P.HW) : nullptr);
