@@ -384,48 +384,60 @@ __global__ void k_bin_ptr(const uint2* __restrict__ sorted, const uint64_t* __re
   }
 }
 
+constexpr int kSrcBaseThreads = 512;
+
 // Source-sink layout (bin, tile, time): srcbase[w][b][S] = window-relative
 // position of the first source sink of sort tile S's events of bin b, so that
 // the events of bin b of consecutive sort tiles are contiguous and the backward
 // owner's source ranges merge like its record ranges (k_ranges). One CTA per
-// window, the bins one after another, each an exclusive scan over the tiles of
-// the per-(tile, bin) counts from bin_ptr.
-__global__ void __launch_bounds__(1024) k_src_base(const uint32_t* __restrict__ bin_ptr,
-                                                   WinParams P, TileParams TP,
-                                                   uint32_t* __restrict__ srcbase) {
-  __shared__ uint32_t warp_tot[32];
+// (bin, window): the bin's offset is the number of the window's events in
+// earlier bins (bin_ptr is cumulative per tile: sum over S of bp[S][b] - bp[S][0]),
+// then an exclusive scan over the tiles of the per-(tile, bin) counts.
+__global__ void __launch_bounds__(kSrcBaseThreads) k_src_base(const uint32_t* __restrict__ bin_ptr,
+                                                              WinParams P, TileParams TP,
+                                                              uint32_t* __restrict__ srcbase) {
+  __shared__ uint32_t warp_tot[kSrcBaseThreads / 32];
   __shared__ uint32_t s_carry;
-  const int w = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, B = P.B;
+  const int b = blockIdx.x, w = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int B = P.B, nw = kSrcBaseThreads / 32;
   const uint32_t* bp = bin_ptr + (size_t)w * TP.nT * (B + 1);
-  if (threadIdx.x == 0) s_carry = 0;
+  uint32_t before = 0;
+  for (int S = threadIdx.x; S < TP.nT; S += kSrcBaseThreads)
+    before += bp[(size_t)S * (B + 1) + b] - bp[(size_t)S * (B + 1)];
+  before = __reduce_add_sync(kFull, before);
+  if (lane == 0) warp_tot[wid] = before;
   __syncthreads();
-  for (int b = 0; b < B; ++b) {
-    uint32_t* out = srcbase + ((size_t)w * B + b) * TP.nT;
-    for (int c = 0; c < TP.nT; c += blockDim.x) {
-      const int S = c + threadIdx.x;
-      const uint32_t v = S < TP.nT ? bp[(size_t)S * (B + 1) + b + 1] - bp[(size_t)S * (B + 1) + b] : 0u;
-      uint32_t x = v;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) warp_tot[wid] = x;
-      __syncthreads();
-      if (wid == 0) {
-        uint32_t q = warp_tot[lane];
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFull, q, o);
-          if (lane >= o) q += y;
-        }
-        warp_tot[lane] = q;
-      }
-      __syncthreads();
-      const uint32_t excl = s_carry + x - v + (wid > 0 ? warp_tot[wid - 1] : 0u);
-      if (S < TP.nT) out[S] = excl;
-      __syncthreads();
-      if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
-      __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (int i = 0; i < nw; ++i) c += warp_tot[i];
+    s_carry = c;
+  }
+  __syncthreads();
+  uint32_t* out = srcbase + ((size_t)w * B + b) * TP.nT;
+  for (int c = 0; c < TP.nT; c += kSrcBaseThreads) {
+    const int S = c + threadIdx.x;
+    const uint32_t v = S < TP.nT ? bp[(size_t)S * (B + 1) + b + 1] - bp[(size_t)S * (B + 1) + b] : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
     }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t q = lane < nw ? warp_tot[lane] : 0u;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, q, o);
+        if (lane >= o) q += y;
+      }
+      if (lane < nw) warp_tot[lane] = q;
+    }
+    __syncthreads();
+    const uint32_t excl = s_carry + x - v + (wid > 0 ? warp_tot[wid - 1] : 0u);
+    if (S < TP.nT) out[S] = excl;
+    __syncthreads();
+    if (threadIdx.x == kSrcBaseThreads - 1) s_carry = excl + v;
+    __syncthreads();
   }
 }
 
@@ -593,7 +605,7 @@ __device__ __forceinline__ double2 pos_grad_w(const double2* __restrict__ cp, in
                       -c.ax * g00 - c.wx * g10 + c.ax * g01 + c.wx * g11);
 }
 
-__global__ void __launch_bounds__(kEvBlock) k_bwd_event(
+__global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
     TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
     const FwdRec* __restrict__ recs, uint64_t n_total, const double2* __restrict__ coef,
@@ -765,7 +777,7 @@ if (sc_threads == kScatterThreads)
                                                                     tile_ptr, bin_ptr);
   if (srcbase) {
     count_launch();
-    k_src_base<<<P.n_windows, 1024, 0, s>>>(bin_ptr, P, TP, srcbase);
+    k_src_base<<<dim3(P.B, P.n_windows), kSrcBaseThreads, 0, s>>>(bin_ptr, P, TP, srcbase);
   }
 }
 
