@@ -224,16 +224,18 @@ __global__ void __maxnreg__(48) k_sort_scatter(
     const uint64_t* __restrict__ ev_off, TileParams TP, const uint32_t* __restrict__ offsets,
     const uint32_t* __restrict__ tile_ptr, uint2* __restrict__ sorted, uint32_t* __restrict__ perm,
     uint32_t* __restrict__ sorted_keys) {
-  extern __shared__ uint16_t whist[];  // [nW warps][nT]
+  extern __shared__ __align__(16) uint16_t whist[];  // [nW warps][ws]
   constexpr int nW = NW;  // 8 warps, or 4 for many tiles (launch_sort)
   const int per = TP.chunk / nW;
-  for (int i = threadIdx.x; i < nW * TP.nT; i += blockDim.x) whist[i] = 0;
+  const int ws = (TP.nT + 7) & ~7;  // row stride: 8 tiles per 16 B word
+  for (int i = threadIdx.x; i < nW * ws / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(whist)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   const int w = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t base = ev_off[w];
   const uint64_t n = ev_off[w + 1] - base;
   const uint64_t k0 = (uint64_t)blockIdx.x * TP.chunk + (uint64_t)wid * per;
-  uint16_t* mine = whist + wid * TP.nT;
+  uint16_t* mine = whist + wid * ws;
   // pass 1: per-warp counts. Many-tile chunks (NW = 4, e.g. 640x480) pipeline
   // the key loads by hand (see pass 3); the 8-warp form measured faster as is.
   if constexpr (NW <= 4) {
@@ -281,12 +283,19 @@ __global__ void __maxnreg__(48) k_sort_scatter(
   __syncthreads();
   const uint32_t* off = offsets + ((size_t)w * TP.nchunks + blockIdx.x) * TP.nT;
   const uint32_t* tp = tile_ptr + (size_t)w * (TP.nT + 1);
-  for (int t = threadIdx.x; t < TP.nT; t += blockDim.x) {  // pass 2: prefix over warps
-    uint32_t run = 0;
+  // pass 2: prefix over warps, 8 tiles per thread as u16 pairs in u32 words
+  // (every partial sum is <= chunk < 2^16: no carry between the halves)
+  for (int i = threadIdx.x; i < ws / 8; i += blockDim.x) {
+    uint4 run = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
     for (int q = 0; q < nW; ++q) {
-      const uint32_t v = whist[q * TP.nT + t];
-      whist[q * TP.nT + t] = (uint16_t)run;
-      run += v;
+      uint4* p = reinterpret_cast<uint4*>(whist + q * ws) + i;
+      const uint4 v = *p;
+      *p = run;
+      run.x += v.x;
+      run.y += v.y;
+      run.z += v.z;
+      run.w += v.w;
     }
   }
   __syncthreads();
@@ -746,7 +755,7 @@ void launch_sort(cudaStream_t s, const uint2* packed, const uint64_t* ev_off, co
   // many sort tiles: 4 warps per CTA, so the per-warp tile counts (2 B per tile)
   // leave room for more resident CTAs (measured: -9 % sort at 640x480)
   const int sc_threads = TP.nT > 2048 ? kScatterThreads / 2 : kScatterThreads;
-  const size_t sc_smem = (size_t)(sc_threads / 32) * TP.nT * 2;
+  const size_t sc_smem = (size_t)(sc_threads / 32) * ((TP.nT + 7) & ~7) * 2;
   set_smem(reinterpret_cast<const void*>(k_key_hist), TP.nT * sizeof(uint32_t), &a1);
   static size_t a3 = 0;
   if (sc_threads == kScatterThreads)
