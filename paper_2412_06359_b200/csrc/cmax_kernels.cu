@@ -93,13 +93,16 @@ __global__ void k_stage(const evcm_event* __restrict__ ev, const uint64_t* __res
 }
 
 // flows [B][2][HW] f64 planes -> interleaved double2 [B][HW]
+// (out32: optional fp32 copy, the owner backward's flow-Jacobian operand)
 __global__ void k_interleave_flows(const double* __restrict__ uv, int B, int HW,
-                                   double2* __restrict__ out) {
+                                   double2* __restrict__ out, float2* __restrict__ out32) {
   const size_t total = (size_t)B * HW;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t b = i / HW, p = i % HW;
-    out[i] = make_double2(uv[(2 * b) * HW + p], uv[(2 * b + 1) * HW + p]);
+    const double2 f = make_double2(uv[(2 * b) * HW + p], uv[(2 * b + 1) * HW + p]);
+    out[i] = f;
+    if (out32) out32[i] = make_float2((float)f.x, (float)f.y);
   }
 }
 
@@ -256,7 +259,7 @@ void launch_chain_init(cudaStream_t s, const ChainInit& a, const WinParams& P) {
 __global__ void k_motion_field(const double* __restrict__ depth, const uint8_t* __restrict__ mask,
                                const double* __restrict__ pose_tab, WinParams P, double fx,
                                double fy, double cx, double cy, double2* __restrict__ flows,
-                               uint8_t* __restrict__ valid) {
+                               uint8_t* __restrict__ valid, float2* __restrict__ flows32) {
   const int w = blockIdx.y;
   const int HW = P.HW, B = P.B;
   const double* dep = depth + (size_t)w * HW;
@@ -290,6 +293,7 @@ __global__ void k_motion_field(const double* __restrict__ depth, const uint8_t* 
         }
       }
       flows[((size_t)w * B + b) * HW + q] = f;
+      if (flows32) flows32[((size_t)w * B + b) * HW + q] = make_float2((float)f.x, (float)f.y);
       if (valid) valid[((size_t)w * B + b) * HW + q] = ok;
     }
   }
@@ -766,20 +770,21 @@ void launch_stage(cudaStream_t s, const evcm_event* ev, const uint64_t* ev_off, 
   k_stage<<<dim3(blocks, P.n_windows), 256, 0, s>>>(ev, ev_off, P, packed, err);
 }
 
-void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out) {
+void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out,
+                             float2* out32) {
   const size_t total = (size_t)B * HW;
   const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
   ++g_launches;
-  k_interleave_flows<<<blocks, 256, 0, s>>>(uv, B, HW, out);
+  k_interleave_flows<<<blocks, 256, 0, s>>>(uv, B, HW, out, out32);
 }
 
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,
-                         double2* flows, uint8_t* valid) {
+                         double2* flows, uint8_t* valid, float2* flows32) {
   const int bx = (P.HW + 255) / 256;
   ++g_launches;
   k_motion_field<<<dim3(bx, P.n_windows), 256, 0, s>>>(depth, mask, pose_tab, P, K[0], K[1], K[2],
-                                                      K[3], flows, valid);
+                                                      K[3], flows, valid, flows32);
 }
 
 template <typename S2>

@@ -49,10 +49,11 @@ struct ChainInit {
 void launch_chain_init(cudaStream_t s, const ChainInit& a, const WinParams& P);
 void launch_window_sums(cudaStream_t s, const double* loss, const double* d_depth,
                         const double* d_poses, int nw, int HW, int B6, double* out);
-void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out);
+void launch_interleave_flows(cudaStream_t s, const double* uv, int B, int HW, double2* out,
+                             float2* out32 = nullptr);
 void launch_motion_field(cudaStream_t s, const double* depth, const uint8_t* mask,
                          const double* pose_tab, const WinParams& P, const double* K,
-                         double2* flows, uint8_t* valid);
+                         double2* flows, uint8_t* valid, float2* flows32 = nullptr);
 template <typename S2>
 void launch_fwd_splat(cudaStream_t s, const uint2* packed, const uint64_t* ev_off,
                       const WinParams& P, uint64_t max_n, const double2* flows, S2* stack);

@@ -616,7 +616,7 @@ __device__ __forceinline__ double2 pos_grad_w(const double2* __restrict__ cp, in
 
 __global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
     const uint2* __restrict__ sorted, const uint64_t* __restrict__ ev_off, WinParams P,
-    TileParams TP, const uint32_t* __restrict__ tile_ptr, const double2* __restrict__ flows,
+    TileParams TP, const uint32_t* __restrict__ tile_ptr, const float2* __restrict__ flows32,
     const FwdRec* __restrict__ recs, uint64_t n_total, const double2* __restrict__ coef,
     const double* __restrict__ scale_tab, const int* __restrict__ no_surv,
     const uint32_t* __restrict__ sorted_keys, const uint32_t* __restrict__ bin_ptr,
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
   const int pol = ev_pol(e);
   const double2* cpw = coef + ((size_t)w * R * 2 + pol) * HW;  // + r*2*HW
   const double* sc = scale_tab + (size_t)w * R;
-  const double2* fl = flows + (size_t)w * B * HW;
+  const float2* fl = flows32 + (size_t)w * B * HW;
   float2* bo = bwd + base + k;  // + i * n_total
   const double iwin = P.inv_window;  // same tb formula as k_fwd_owner
   auto tb_of = [&](int r) { return fabs(t - es[r]) * iwin; };
@@ -684,15 +684,18 @@ __global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
     const float2 o = make_float2((float)(dt * g.x), (float)(dt * g.y));
     bo[(size_t)(r - 1) * n_total] = o;
     gm = fmaxf(gm, fmaxf(fabsf(o.x), fabsf(o.y)));
-    // (I + dt J_i)^T g + d[r]   (warp.hpp:91-94, engine.hpp:490-491)
+    // (I + dt J_i)^T g + d[r]   (warp.hpp:91-94, engine.hpp:490-491); the flow
+    // Jacobian from the fp32 copy of the flows: dt J enters next to the identity,
+    // so its 2^-24 relative error stays ~1e-7 of the adjoint, within the
+    // gradient tolerance, and the 8 B pixel halves the gathers' sectors
     const int i00 = c.y0 * W + c.x0;
-    const double2* f = fl + (size_t)i * HW;
-    const double2 a = __ldg(f + i00), b = __ldg(f + i00 + ox);
-    const double2 d0 = __ldg(f + i00 + oy * W), d1 = __ldg(f + i00 + oy * W + ox);
-    const double dux = c.ay * (b.x - a.x) + c.wy * (d1.x - d0.x);
-    const double duy = c.ax * (d0.x - a.x) + c.wx * (d1.x - b.x);
-    const double dvx = c.ay * (b.y - a.y) + c.wy * (d1.y - d0.y);
-    const double dvy = c.ax * (d0.y - a.y) + c.wx * (d1.y - b.y);
+    const float2* f = fl + (size_t)i * HW;
+    const float2 a = __ldg(f + i00), b = __ldg(f + i00 + ox);
+    const float2 d0 = __ldg(f + i00 + oy * W), d1 = __ldg(f + i00 + oy * W + ox);
+    const double dux = c.ay * ((double)b.x - a.x) + c.wy * ((double)d1.x - d0.x);
+    const double duy = c.ax * ((double)d0.x - a.x) + c.wx * ((double)d1.x - b.x);
+    const double dvx = c.ay * ((double)b.y - a.y) + c.wy * ((double)d1.y - d0.y);
+    const double dvy = c.ax * ((double)d0.y - a.y) + c.wx * ((double)d1.y - b.y);
     const double2 d = pos_grad_w(cpw + (size_t)r * 2 * HW, W, ox, oy, c, tb_of(r), sc[r]);
     const double nx = g.x * (1.0 + dt * dux) + g.y * dt * dvx + d.x;
     const double ny = g.y * (1.0 + dt * dvy) + g.x * dt * duy + d.y;
@@ -811,7 +814,7 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
 
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                      uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
+                      uint64_t max_n, const float2* flows32, const FwdRec* recs, uint64_t n_total,
                       const double2* coef, const double* scale, const int* no_surv,
                       const uint32_t* sorted_keys, const uint32_t* bin_ptr, const uint32_t* srcbase,
                       uint4* srcrec, float2* bwd, uint32_t* gmax) {
@@ -819,7 +822,7 @@ void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_of
   if (max_n == 0) return;
   count_launch();
   k_bwd_event<<<dim3((unsigned)((max_n + kEvBlock - 1) / kEvBlock), P.n_windows), kEvBlock, 0, s>>>(
-      sorted, ev_off, P, TP, tile_ptr, flows, recs, n_total, coef, scale, no_surv, sorted_keys,
+      sorted, ev_off, P, TP, tile_ptr, flows32, recs, n_total, coef, scale, no_surv, sorted_keys,
       bin_ptr, srcbase, srcrec, bwd, gmax);
 }
 

@@ -55,7 +55,7 @@ void launch_traj_records(cudaStream_t s, const uint2* sorted, const uint64_t* ev
                          uint16_t* lists);
 void launch_bwd_event(cudaStream_t s, const uint2* sorted, const uint64_t* ev_off,
                       const WinParams& P, const TileParams& TP, const uint32_t* tile_ptr,
-                      uint64_t max_n, const double2* flows, const FwdRec* recs, uint64_t n_total,
+                      uint64_t max_n, const float2* flows32, const FwdRec* recs, uint64_t n_total,
                       const double2* coef, const double* scale, const int* no_surv,
                       const uint32_t* sorted_keys, const uint32_t* bin_ptr, const uint32_t* srcbase,
                       uint4* srcrec, float2* bwd, uint32_t* gmax);

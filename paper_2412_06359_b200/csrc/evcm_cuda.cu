@@ -557,7 +557,8 @@ void run_forward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* f
 // Owner-computes backward: per-event adjoint -> per-bin (gx, gy), then the
 // per-tile gradient gather with the fused flows backward (when depth is given)
 // and/or the f64 gradient planes (grad_out, [w][B][2][HW]). Marks 7..9.
-void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* flows,
+// flows32: fp32 copy of the window's flows (the flow-Jacobian operand of k_bwd_event)
+void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const float2* flows32,
                         const double* depth, const uint8_t* mask, const double* pose_tab,
                         const double* K, double* d_depth, double* d_poses, double* grad_out) {
   const TileParams& TP = e->TP;
@@ -571,7 +572,7 @@ void run_backward_owner(evcm_cuda_engine* e, const WinParams& P, const double2* 
   uint32_t* gmax = e->get<uint32_t>("gmax", (size_t)nw);
   // source-pixel sinks with their packed events, (bin, tile, time) order
   uint4* srcrec = e->get<uint4>("srcrec", total);
-  launch_bwd_event(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows, recs, total,
+  launch_bwd_event(e->stream, sorted, ev_off, P, TP, tile_ptr, e->max_n, flows32, recs, total,
                    e->get<double2>("coef", 1), e->get<double>("scale", 1), e->get<int>("no_surv", 1),
                    e->get<uint32_t>("sort_keys", 1) + total, e->get<uint32_t>("bin_ptr", 1),
                    e->get<uint32_t>("srcbase", 1), srcrec, bwd, gmax);
@@ -860,10 +861,11 @@ void backward_impl(evcm_cuda_engine* e, const evcm_slice* s, const evcm_flows* f
   // trajectories from the forward (its records / packed events)
   const double* uv = to_device(e, "flows_planar", f->uv, (size_t)f->n_bins * 2 * P.HW, mem);
   double2* flows = e->get<double2>("flows", (size_t)f->n_bins * P.HW);
-  launch_interleave_flows(e->stream, uv, f->n_bins, P.HW, flows);
+  float2* flows32 = e->owner() ? e->get<float2>("flows32", (size_t)f->n_bins * P.HW) : nullptr;
+  launch_interleave_flows(e->stream, uv, f->n_bins, P.HW, flows, flows32);
   double* out = e->get<double>("grad_f64", (size_t)P.B * 2 * P.HW);
   if (e->owner()) {
-    run_backward_owner(e, P, flows, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
+    run_backward_owner(e, P, flows32, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, out);
   } else {
     void* g = run_backward(e, P, s->n_events, flows);
     if (e->opt.grad_f64)
@@ -1108,14 +1110,15 @@ void chain_enqueue(evcm_cuda_engine* e, const evcm_chain_batch* bt, int in_mem, 
     const double* depth =
         depth_dev ? depth_dev : to_device(e, "depth", bt->depth, (size_t)nw * P.HW, in_mem);
     double2* flows = e->get<double2>("flows", (size_t)nw * B * P.HW);
+    float2* flows32 = e->owner() ? e->get<float2>("flows32", (size_t)nw * B * P.HW) : nullptr;
     e->mark(1);
-    launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr);
+    launch_motion_field(e->stream, depth, nullptr, tab, P, bt->K, flows, nullptr, flows32);
     run_forward(e, P, max_n, flows);
     const bool direct = out_mem == EVCM_MEM_DEVICE;
     double* ddo = (direct && out->d_depth) ? out->d_depth : e->get<double>("d_depth", (size_t)nw * P.HW);
     double* dpo = (direct && out->d_poses) ? out->d_poses : e->get<double>("d_poses", (size_t)nw * B * 6);
     if (e->owner()) {
-      run_backward_owner(e, P, flows, depth, nullptr, tab, bt->K, ddo, dpo, nullptr);
+      run_backward_owner(e, P, flows32, depth, nullptr, tab, bt->K, ddo, dpo, nullptr);
     } else {
       void* g = run_backward(e, P, max_n, flows);
       double* pp = e->get<double>("pose_part", (size_t)nw * flows_bwd_parts(P) * B * kPoseSums);
