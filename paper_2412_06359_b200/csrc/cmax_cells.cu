@@ -742,11 +742,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
 // depth_pose_to_flows_backward (geometry.hpp:300-322); d_depth sums the bins
 // in order in registers.
 //
-// Staging layout: every range gets an even-aligned slot region of
-// roundup2(len + 2) slots; its 8 B values (sink values, packed events) are
-// bulk-copied as the 16 B-aligned superset starting at the region, and its
-// records at the same slot offset, so slot s holds the record, value and event
-// of one candidate; the slack slots of every region are flagged in a bitmask.
+// Staging layout: every record range gets an even-aligned slot region of
+// roundup2(len + 2) slots; its 8 B sink values are bulk-copied as the 16 B-aligned
+// superset starting at the region, and its records at the same slot offset, so
+// slot s holds the record and value of one candidate; the slack slots of every
+// region are flagged in a bitmask. Source ranges are 16 B {packed event, gx, gy}
+// records in (bin, tile, time) order (k_bwd_event, k_src_base): one bulk copy
+// each, no slack.
 //
 // Bin groups (gridDim.z > 1, owner_groups): CTA z owns bins [i0, i1) and
 // streams groups i0..i1, where group i0 (i0 > 0) only primes bin i0 with the
