@@ -694,9 +694,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_fwd_cells(
         const double i0 = rcp_fast(C0 + kLossEps), i1 = rcp_fast(C1 + kLossEps);
         const double c0 = S0 * i0, c1 = S1 * i1;
         lsum += c0 * c0 + c1 * c1;
-        double2* cwp = coef + ((size_t)w * R + r) * 2 * HW;
-        cwp[g] = make_double2(c0, c0 * i0);
-        cwp[HW + g] = make_double2(c1, c1 * i1);
+        // polarity-interleaved [w][r][px][pol]: the two polarities of a pixel
+        // share a 32 B sector, so k_bwd_event's lanes of both polarities
+        // gather from the same cache lines
+        double2* cwp = coef + (((size_t)w * R + r) * HW + g) * 2;
+        // one 32 B store per pixel (a warp's row of pixels stays one contiguous run)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(cwp), "d"(c0), "d"(c0 * i0),
+                     "d"(c1), "d"(c1 * i1)
+                     : "memory");
         if (stack_out) {
           double2* so = stack_out + ((size_t)w * R + r) * 2 * HW;
           so[g] = make_double2(C0, S0);

@@ -602,11 +602,12 @@ __global__ void k_build_lists(const uint4* __restrict__ bbox, WinParams P, TileP
 // ---------------------------------------------------------------------------
 // backward, per event: d[r] at every reference + adjoint sweep -> (gx, gy) per bin
 
+// cp: the event's polarity in a polarity-interleaved plane (pixel stride 2)
 __device__ __forceinline__ double2 pos_grad_w(const double2* __restrict__ cp, int W, int ox, int oy,
                                               const CellW& c, double tb, double scale) {
-  const int i00 = c.y0 * W + c.x0;
-  const double2 k00 = __ldg(cp + i00), k10 = __ldg(cp + i00 + ox);
-  const double2 k01 = __ldg(cp + i00 + oy * W), k11 = __ldg(cp + i00 + oy * W + ox);
+  const int i00 = 2 * (c.y0 * W + c.x0);
+  const double2 k00 = __ldg(cp + i00), k10 = __ldg(cp + i00 + 2 * ox);
+  const double2 k01 = __ldg(cp + i00 + 2 * oy * W), k11 = __ldg(cp + i00 + 2 * (oy * W + ox));
   const double g00 = scale * k00.y * (tb - k00.x);
   const double g10 = scale * k10.y * (tb - k10.x);
   const double g01 = scale * k01.y * (tb - k01.x);
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
   const int ox = W >= 2 ? 1 : 0, oy = H >= 2 ? 1 : 0;
   const double t = dm((double)dt_us, 1e-6);
   const int pol = ev_pol(e);
-  const double2* cpw = coef + ((size_t)w * R * 2 + pol) * HW;  // + r*2*HW
+  const double2* cpw = coef + (size_t)w * R * 2 * HW + pol;  // + r*2*HW, [px][pol]
   const double* sc = scale_tab + (size_t)w * R;
   const float2* fl = flows32 + (size_t)w * B * HW;
   float2* bo = bwd + base + k;  // + i * n_total
