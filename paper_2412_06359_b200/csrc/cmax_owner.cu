@@ -676,7 +676,13 @@ __global__ void __launch_bounds__(kEvBlock, 8) k_bwd_event(
     const CellW c = decode(rk[(size_t)B * n_total]);
     gf = pos_grad_w(cpw + (size_t)B * 2 * HW, W, ox, oy, c, tb_of(B), sc[B]);
   }
+  // the records stream from HBM and each step starts by decoding its record:
+  // pull the next step's record into L2 one step ahead (no registers held)
+  auto ref_at = [&](int s) { return s < j ? s + 1 : B - 1 - (s - j); };
+  if (B > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(rk + (size_t)ref_at(0) * n_total));
   for (int s = 0; s < B - 1; ++s) {
+    if (s + 1 < B - 1)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rk + (size_t)ref_at(s + 1) * n_total));
     const bool back = s < j;
     const int i = back ? s : B - 1 - (s - j);
     const int r = back ? i + 1 : i;
